@@ -1,0 +1,24 @@
+"""Build the CPU oracle shared library (test infrastructure only).
+
+gcc -O2 -ffp-contract=off -fno-fast-math: every fp32 op rounds where it is
+written; the only FMA is the explicit fmaf() the oracle's definition calls for.
+"""
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "oracle_mlp.c")
+LIB = os.path.join(HERE, "liboracle_mlp.so")
+
+
+def build(force: bool = False) -> str:
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= os.path.getmtime(SRC):
+        return LIB
+    cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fno-builtin-rint",
+           "-fopenmp", "-shared", "-fPIC", "-Wall", "-Wextra", "-o", LIB, SRC, "-lm"]
+    subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True))

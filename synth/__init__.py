@@ -1,0 +1,156 @@
+"""Seeded synthetic inputs for the INT8 Swin MLP sub-layer (shared by the CUDA
+path's tests/bench and by the oracle's tests).
+
+This module holds NONE of the method's arithmetic (no GEMM, no epilogue, no
+LayerNorm): it only draws random numbers and applies the input recipe of
+DESIGN.md §4, which mirrors the paper's workload — Swin-T/S/B/L MLP layers
+(C -> 4C -> C, mlp_ratio 4) whose weights and input activations were
+quantized to int8 by FasterTransformer-style max-abs post-training
+quantization.  Calibration of the hidden and output
+scales is analytic (a distributional choice of this recipe), so the generator
+never needs the method to pick its own parameters.
+
+Seeds: base 240201169; layer seed = base + 1000*config + 100*stage + layer.
+"""
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+BASE_SEED = 240201169
+ACT_RELU = 0
+ACT_GELU = 1
+
+# Swin stage channel widths and the BASELINE.json configs.
+SWIN = {
+    "T": {"C": 96, "depths": (2, 2, 6, 2)},
+    "S": {"C": 96, "depths": (2, 2, 18, 2)},
+    "B": {"C": 128, "depths": (2, 2, 18, 2)},
+    "L": {"C": 192, "depths": (2, 2, 18, 2)},
+}
+
+
+def stage_tokens(batch: int, img: int = 224, patch: int = 4):
+    """Tokens per stage for a batch of img x img images (patch 4, 2x merge per stage)."""
+    side = img // patch
+    return [batch * (side >> s) ** 2 for s in range(4)]
+
+
+@dataclass
+class Layer:
+    """One quantized MLP layer: int8 weights [out][in] + fp32 scales/biases.
+    Field names match swin_mlp_int8_desc_t (include/swin_mlp_int8.h)."""
+    C: int
+    H: int
+    act: int
+    s_x: float
+    z_x: int
+    w1: np.ndarray              # int8 [H][C]
+    s_w1: np.ndarray            # fp32 [H]
+    b1: Optional[np.ndarray]    # fp32 [H] or None (paper mode)
+    s_h: float
+    z_h: int
+    w2: np.ndarray              # int8 [C][H]
+    s_w2: np.ndarray            # fp32 [C]
+    b2: Optional[np.ndarray]    # fp32 [C] or None
+    gamma: np.ndarray           # fp32 [C]
+    beta: np.ndarray            # fp32 [C]
+    eps: float
+    s_y: float
+    z_y: int
+    seed: int = 0
+    meta: dict = field(default_factory=dict)
+
+
+def _quant_weights(rng, n_out, n_in, std=0.02):
+    """FT-style per-output-channel symmetric PTQ of N(0, std^2) weights (recipe)."""
+    w = rng.standard_normal((n_out, n_in), dtype=np.float32) * np.float32(std)
+    amax = np.abs(w).max(axis=1)
+    amax = np.where(amax > 0, amax, np.float32(1.0)).astype(np.float32)
+    s = (amax / np.float32(127.0)).astype(np.float32)
+    q = np.clip(np.rint(w / s[:, None]), -127, 127).astype(np.int8)
+    return q, s
+
+
+def make_layer(C: int, seed: int, act: int = ACT_RELU, fc1_bias: bool = False,
+               z_x: int = 0, z_h: int = 0, z_y: int = 0, H: Optional[int] = None,
+               x_std_est: float = 1.0) -> Layer:
+    """Weights, scales and LN params of one layer (the recipe of DESIGN.md §4).
+
+    s_x is fixed by make_activations' recipe (max-abs of an N(0,1) tensor with
+    2% x6 outlier channels ~ 6*4.5 sigma); s_h and s_y are analytic 4-sigma
+    clip points of the hidden pre-activation and the LayerNorm output.
+    z_h = -128 selects the asymmetric hidden grid (s_h halves, range 0..255)."""
+    H = 4 * C if H is None else H
+    rng = np.random.Generator(np.random.PCG64(seed))
+    w1, s_w1 = _quant_weights(rng, H, C)
+    w2, s_w2 = _quant_weights(rng, C, H)
+    b1 = (rng.standard_normal(H, dtype=np.float32) * np.float32(0.02)) if fc1_bias else None
+    b2 = rng.standard_normal(C, dtype=np.float32) * np.float32(0.02)
+    gamma = (np.float32(1.0) + np.float32(0.1) * rng.standard_normal(C, dtype=np.float32)).astype(np.float32)
+    beta = (np.float32(0.1) * rng.standard_normal(C, dtype=np.float32)).astype(np.float32)
+    # activation scale: the input recipe's max-abs (outlier channels x6, ~4.5 sigma)
+    s_x = np.float32(6.0 * 4.5 * x_std_est / 127.0)
+    # hidden pre-activation std: 0.02 * sqrt(C * E[x^2]), E[x^2] = 0.98 + 0.02*36
+    sig_h = 0.02 * np.sqrt(C * 1.70) * x_std_est
+    levels = 255.0 if z_h == -128 else 127.0
+    s_h = np.float32(4.0 * sig_h / levels)
+    s_y = np.float32(5.0 / 127.0)
+    return Layer(C=C, H=H, act=act, s_x=float(s_x), z_x=z_x, w1=w1, s_w1=s_w1, b1=b1,
+                 s_h=float(s_h), z_h=z_h, w2=w2, s_w2=s_w2, b2=b2, gamma=gamma, beta=beta,
+                 eps=1e-5, s_y=float(s_y), z_y=z_y, seed=seed)
+
+
+def make_activations(layer: Layer, T: int, seed: int, outlier_frac: float = 0.02,
+                     outlier_gain: float = 6.0) -> np.ndarray:
+    """int8 [T][C] input tokens: N(0,1) with `outlier_frac` of the channels
+    scaled by `outlier_gain` (ViT-like outlier channels), quantized with the
+    layer's s_x and z_x (RNE, saturating)."""
+    C = layer.C
+    rng = np.random.Generator(np.random.PCG64(seed))
+    gain = np.ones(C, np.float32)
+    n_out = max(1, int(round(outlier_frac * C)))
+    gain[rng.choice(C, n_out, replace=False)] = np.float32(outlier_gain)
+    out = np.empty((T, C), np.int8)
+    inv = np.float32(1.0 / layer.s_x)
+    step = 1 << 16
+    for t0 in range(0, T, step):
+        t1 = min(T, t0 + step)
+        x = rng.standard_normal((t1 - t0, C), dtype=np.float32) * gain
+        out[t0:t1] = np.clip(np.rint(x * inv) + layer.z_x, -128, 127).astype(np.int8)
+    return out
+
+
+def make_residual(T: int, C: int, seed: int) -> np.ndarray:
+    """fp32 [T][C] residual stream for the fp32-residual mode: 2*N(0,1)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return (np.float32(2.0) * rng.standard_normal((T, C), dtype=np.float32)).astype(np.float32)
+
+
+def layer_seed(config: int, stage: int, layer: int) -> int:
+    return BASE_SEED + 1000 * config + 100 * stage + layer
+
+
+def swin_t_batch64_layers(act: int = ACT_RELU):
+    """BASELINE configs[1]: Swin-T, all four stage MLPs, batch 64 (one layer per stage).
+    Returns [(layer, T, x_seed)]."""
+    toks = stage_tokens(64)
+    out = []
+    for s in range(4):
+        C = 96 << s
+        L = make_layer(C, layer_seed(2, s, 0), act=act)
+        out.append((L, toks[s], layer_seed(2, s, 0) + 50))
+    return out
+
+
+def config_layers(config: int, act: int = ACT_RELU, batch: Optional[int] = None):
+    """Per-stage (C, T, n_layers) for BASELINE configs 1..5 (1-based)."""
+    if config == 1:
+        return [(768, 49 * (batch or 1), 1)]
+    name, b, img, win = {2: ("T", 64, 224, 7), 3: ("S", 256, 224, 7), 4: ("B", 1024, 224, 7),
+                         5: ("L", 512, 384, 12)}[config]
+    b = batch or b
+    C0 = SWIN[name]["C"]
+    depths = (1, 1, 1, 1) if config == 2 else SWIN[name]["depths"]
+    toks = stage_tokens(b, img=img)
+    return [(C0 << s, toks[s], depths[s]) for s in range(4)]
