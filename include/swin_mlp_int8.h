@@ -1,0 +1,154 @@
+/*
+ * swin_mlp_int8.h — C ABI of the B200-native (sm_100a) fully-integer Swin
+ * MLP sub-layer of arXiv 2402.01169, "GELU-less quantized SWIN".
+ *
+ * The layer (Fig. 1, lines 72-86; "GELU-less SWIN", lines 244-247,
+ * 326-328), for T tokens of C channels, hidden width H (= 4C in Swin):
+ *
+ *   FC1 GEMM   A1[t][n] = sum_k (X[t][k] - z_x) * W1[n][k]        int32
+ *   op #5      Hq[t][n] = Q_h(act(dQ(A1) + b1[n]))                 int8
+ *              act = ReLU (the paper's replacement, fused
+ *              into the GEMM epilogue) or GELU (control)
+ *   FC2 GEMM   A2[t][c] = sum_j (Hq[t][j] - z_h) * W2[c][j]        int32
+ *   op #6      z = dQ(A2) + b2[c] + residual;  Y = Q_y(LayerNorm(z))
+ *
+ * Exact arithmetic (what "bit-exact" in the tests means) — fl() = fp32
+ * round-to-nearest-even, rne() = round half to even:
+ *   a  = fl(A1);  y = fmaf(a, m1[n], b1[n] or 0),  m1[n] = fl(x_scale*w1_scale[n])
+ *   ReLU: v = fl(max(y,0) * inv_h)         GELU: v = fl(gelu_erf(y) * inv_h)
+ *   Hq = clamp(rne(v) + h_zero_point, -128, 127),  inv_h = fl(1/h_scale)
+ *   d  = fmaf(fl(A2), m2[c], b2[c] or 0),  m2[c] = fl(h_scale*w2_scale[c])
+ *   r  = residual[t][c]  or, when residual == NULL, fl(fl(X[t][c] - z_x) * x_scale)
+ *   z  = fl(d + r); mu, var (biased), rstd = 1/sqrt(var+eps) in double;
+ *   yhat = fl(((z-mu)*rstd)*gamma[c] + beta[c])  (double ops);
+ *   Y  = clamp(rne(fl(yhat * inv_y)) + y_zero_point, -128, 127),  inv_y = fl(1/y_scale)
+ * The readings behind these choices (rounding, zero points, residual
+ * operand, trailing Q, eps) are listed in DESIGN.md §3.
+ *
+ * Layout: row-major.  X, Y: [T][C] int8.  W1: [H][C] int8, W2: [C][H] int8
+ * (nn.Linear [out][in], i.e. both GEMMs are K-major "TN").  Weights are
+ * symmetric (zero point 0), per-output-channel scales.
+ *
+ * Errors: every entry point returns a swin_mlp_status_t; no exception or
+ * abort crosses the ABI.  Validation happens synchronously before any
+ * launch; on error nothing is launched, outputs are untouched and
+ * swin_mlp_int8_last_error() (thread-local) describes the failure.
+ */
+#ifndef SWIN_MLP_INT8_H_
+#define SWIN_MLP_INT8_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct swin_mlp_int8_s* swin_mlp_int8_t;
+
+typedef enum {
+    SWIN_MLP_OK = 0,
+    SWIN_MLP_EINVAL = 1,        /* bad argument (message in last_error)                 */
+    SWIN_MLP_EUNSUPPORTED = 2,  /* valid but not supported by this build (e.g. C > 1536)   */
+    SWIN_MLP_ENOMEM = 3,        /* device allocation failed                                */
+    SWIN_MLP_ECUDA = 4          /* a CUDA runtime/driver call failed (message has the code) */
+} swin_mlp_status_t;
+
+typedef enum {
+    SWIN_MLP_ACT_RELU = 0,      /* the paper's GELU-less block             */
+    SWIN_MLP_ACT_GELU_ERF = 1   /* control: exact erf GELU, 0.5*y*(1+erf(y/sqrt 2))       */
+} swin_mlp_act_t;
+
+/* Layer description passed to swin_mlp_int8_create.  All pointers may be
+ * host or device memory (detected); they are read during create only —
+ * the handle keeps its own device copies. */
+typedef struct {
+    int32_t C;                  /* channels; C % 32 == 0, 32 <= C <= 1536                  */
+    int32_t H;                  /* hidden width; H % 32 == 0, C <= H <= 6144 (Swin: 4*C)   */
+    swin_mlp_act_t act;
+    float   x_scale;            /* input activation scale s_x > 0 (finite, normal)         */
+    int32_t x_zero_point;       /* z_x in [-128, 127]                                      */
+    const int8_t* w1;           /* [H][C]                                                  */
+    const float*  w1_scale;     /* [H], > 0                                                */
+    const float*  b1;           /* [H] or NULL (NULL = the paper's bias-free FC1) */
+    float   h_scale;            /* hidden (post-activation) scale s_h > 0                  */
+    int32_t h_zero_point;       /* z_h in [-128, 127]                                      */
+    const int8_t* w2;           /* [C][H]                                                  */
+    const float*  w2_scale;     /* [C], > 0                                                */
+    const float*  b2;           /* [C] or NULL                                             */
+    const float*  ln_gamma;     /* [C]                                                     */
+    const float*  ln_beta;      /* [C]                                                     */
+    float   ln_eps;             /* > 0 (1e-5)                                              */
+    float   y_scale;            /* output scale s_y > 0                                    */
+    int32_t y_zero_point;       /* z_y in [-128, 127]                                      */
+    int32_t device;             /* CUDA device ordinal the handle lives on                 */
+} swin_mlp_int8_desc_t;
+
+/* Create a layer handle: validates the description, folds the fp32
+ * constants m1, inv_h, m2, inv_y, computes the int32 zero-point
+ * corrections sum_k W1[n][k] and sum_j W2[c][j], uploads everything to
+ * handle-owned device memory and encodes the weight TMA descriptors.
+ * No device compute beyond copies.  *out is set only on SWIN_MLP_OK. */
+swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_mlp_int8_t* out);
+
+/* Bytes of caller-provided device workspace `run` needs for T tokens
+ * (the int8 hidden tensor Hq, [T][H], 128-byte aligned).  Returns 0 for a
+ * NULL handle or T <= 0. */
+size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T);
+
+/* The hot path: Y = layer(X) for T tokens, stream-ordered, asynchronous.
+ *   x            [T][C] int8, device, 16-byte aligned
+ *   residual     [T][C] fp32, device, 16-byte aligned, or NULL (NULL: r = dQ(X), reading R3)
+ *   y            [T][C] int8, device, 16-byte aligned (may not alias x)
+ *   residual_out [T][C] fp32, device, or NULL: receives z (pre-LN sum) for pre-norm chaining
+ *   T >= 0 (T == 0: no launch, SWIN_MLP_OK)
+ *   workspace    >= swin_mlp_int8_workspace_bytes(h, T) bytes, device, 128-byte aligned
+ *   stream       cudaStream_t (NULL = legacy default stream)
+ * Ownership: all buffers are the caller's; nothing is retained after return. */
+swin_mlp_status_t swin_mlp_int8_run(swin_mlp_int8_t h, const int8_t* x, const float* residual,
+                                    int8_t* y, float* residual_out, int64_t T,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same as run, plus debug taps (any may be NULL), all device memory:
+ *   acc1 [T][H] int32 (FC1 accumulators incl. zero-point term), hidden [T][H] int8 (Hq),
+ *   acc2 [T][C] int32, ln_out [T][C] fp32 (yhat, the pre-quant LayerNorm output).
+ * Runs the same kernels as `run` with their tap-writing variants. */
+swin_mlp_status_t swin_mlp_int8_run_debug(swin_mlp_int8_t h, const int8_t* x, const float* residual,
+                                          int8_t* y, float* residual_out, int64_t T,
+                                          void* workspace, size_t workspace_bytes, void* stream,
+                                          int32_t* acc1, int8_t* hidden, int32_t* acc2, float* ln_out);
+
+/* End-to-end convenience: x, residual (or NULL) and y are HOST buffers
+ * (pinned for full bandwidth); device staging is taken from `workspace`,
+ * which must hold swin_mlp_int8_host_workspace_bytes(h, T, residual != NULL).
+ * Copies H2D, runs, copies D2H, all on `stream`; returns after enqueueing
+ * (synchronize the stream before reading y). */
+size_t swin_mlp_int8_host_workspace_bytes(swin_mlp_int8_t h, int64_t T, int32_t with_residual);
+swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host, const float* residual_host,
+                                         int8_t* y_host, int64_t T, void* workspace, size_t workspace_bytes,
+                                         void* stream);
+
+/* Debug getter: the folded fp32 constants exactly as the kernels use them
+ * (host arrays m1[H], m2[C]; scalars inv_h, inv_y), and the int32
+ * zero-point corrections wsum1[H], wsum2[C].  Any pointer may be NULL. */
+swin_mlp_status_t swin_mlp_int8_get_constants(swin_mlp_int8_t h, float* m1, float* inv_h, float* m2,
+                                              float* inv_y, int32_t* wsum1, int32_t* wsum2);
+
+/* Number of kernel launches one `run` enqueues (for the bench's launch count). */
+int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h);
+
+/* Introspection: the launch plan of this layer, out8[8] = {FC1 BN, FC1 cluster size,
+ * FC1 stages, FC1 max co-resident clusters, FC2 BN, FC2 cluster size, FC2 stages,
+ * FC2 max clusters}.  Returns 0, or -1 on a NULL argument. */
+int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out8);
+
+/* Release the handle's device memory.  No run may be in flight. NULL is OK. */
+swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* swin_mlp_int8_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWIN_MLP_INT8_H_ */

@@ -1,0 +1,248 @@
+"""paper_2402_01169_b200 — B200-native (sm_100a) fully-integer Swin MLP sub-layer
+of arXiv 2402.01169 ("GELU-less quantized SWIN").
+
+A thin ctypes binding over the C ABI in include/swin_mlp_int8.h (same names,
+argument marshalling only).  Every step of the layer — FC1 GEMM, fused op #5
+(ReLU or the GELU control), FC2 GEMM, fused op #6 (bias, residual, LayerNorm,
+requantize) — runs in the CUDA kernels of libswin_mlp_int8.so.  There is no
+CPU fallback: if the library is missing or was built for another target the
+import of `lib()` raises.
+
+PyTorch is used only for device memory and streams (see SwinMlpInt8Layer).
+"""
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libswin_mlp_int8.so")
+
+SWIN_MLP_OK = 0
+SWIN_MLP_EINVAL = 1
+SWIN_MLP_EUNSUPPORTED = 2
+SWIN_MLP_ENOMEM = 3
+SWIN_MLP_ECUDA = 4
+SWIN_MLP_ACT_RELU = 0
+SWIN_MLP_ACT_GELU_ERF = 1
+
+# every symbol include/swin_mlp_int8.h declares
+EXPORTS = [
+    "swin_mlp_int8_create", "swin_mlp_int8_workspace_bytes", "swin_mlp_int8_run",
+    "swin_mlp_int8_run_debug", "swin_mlp_int8_host_workspace_bytes", "swin_mlp_int8_run_host",
+    "swin_mlp_int8_get_constants", "swin_mlp_int8_launches_per_run", "swin_mlp_int8_plan",
+    "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
+]
+
+
+class swin_mlp_int8_desc_t(ctypes.Structure):
+    _fields_ = [
+        ("C", ctypes.c_int32), ("H", ctypes.c_int32), ("act", ctypes.c_int32),
+        ("x_scale", ctypes.c_float), ("x_zero_point", ctypes.c_int32),
+        ("w1", ctypes.c_void_p), ("w1_scale", ctypes.c_void_p), ("b1", ctypes.c_void_p),
+        ("h_scale", ctypes.c_float), ("h_zero_point", ctypes.c_int32),
+        ("w2", ctypes.c_void_p), ("w2_scale", ctypes.c_void_p), ("b2", ctypes.c_void_p),
+        ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
+        ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+    ]
+
+
+class SwinMlpError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"swin_mlp_int8 status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library (fails loudly if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    L.swin_mlp_int8_create.argtypes = [ctypes.POINTER(swin_mlp_int8_desc_t), ctypes.POINTER(P)]
+    L.swin_mlp_int8_create.restype = i32
+    L.swin_mlp_int8_workspace_bytes.argtypes = [P, i64]
+    L.swin_mlp_int8_workspace_bytes.restype = sz
+    L.swin_mlp_int8_run.argtypes = [P, P, P, P, P, i64, P, sz, P]
+    L.swin_mlp_int8_run.restype = i32
+    L.swin_mlp_int8_run_debug.argtypes = [P, P, P, P, P, i64, P, sz, P, P, P, P, P]
+    L.swin_mlp_int8_run_debug.restype = i32
+    L.swin_mlp_int8_host_workspace_bytes.argtypes = [P, i64, i32]
+    L.swin_mlp_int8_host_workspace_bytes.restype = sz
+    L.swin_mlp_int8_run_host.argtypes = [P, P, P, P, i64, P, sz, P]
+    L.swin_mlp_int8_run_host.restype = i32
+    L.swin_mlp_int8_get_constants.argtypes = [P, P, P, P, P, P, P]
+    L.swin_mlp_int8_get_constants.restype = i32
+    L.swin_mlp_int8_launches_per_run.argtypes = [P]
+    L.swin_mlp_int8_launches_per_run.restype = i32
+    L.swin_mlp_int8_plan.argtypes = [P, P]
+    L.swin_mlp_int8_plan.restype = i32
+    L.swin_mlp_int8_destroy.argtypes = [P]
+    L.swin_mlp_int8_destroy.restype = i32
+    L.swin_mlp_int8_last_error.argtypes = []
+    L.swin_mlp_int8_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().swin_mlp_int8_last_error().decode()
+
+
+def _check(st):
+    if st != SWIN_MLP_OK:
+        raise SwinMlpError(st, last_error())
+
+
+# ---- same-name thin wrappers over the C ABI (raw pointers as ints) -------------
+def swin_mlp_int8_create(desc: swin_mlp_int8_desc_t) -> int:
+    h = ctypes.c_void_p()
+    _check(lib().swin_mlp_int8_create(ctypes.byref(desc), ctypes.byref(h)))
+    return h.value
+
+
+def swin_mlp_int8_workspace_bytes(h, T) -> int:
+    return int(lib().swin_mlp_int8_workspace_bytes(h, T))
+
+
+def swin_mlp_int8_run(h, x, residual, y, residual_out, T, workspace, workspace_bytes, stream):
+    _check(lib().swin_mlp_int8_run(h, x, residual, y, residual_out, T, workspace, workspace_bytes, stream))
+
+
+def swin_mlp_int8_run_debug(h, x, residual, y, residual_out, T, workspace, workspace_bytes, stream,
+                            acc1, hidden, acc2, ln_out):
+    _check(lib().swin_mlp_int8_run_debug(h, x, residual, y, residual_out, T, workspace, workspace_bytes,
+                                         stream, acc1, hidden, acc2, ln_out))
+
+
+def swin_mlp_int8_host_workspace_bytes(h, T, with_residual) -> int:
+    return int(lib().swin_mlp_int8_host_workspace_bytes(h, T, int(with_residual)))
+
+
+def swin_mlp_int8_run_host(h, x_host, residual_host, y_host, T, workspace, workspace_bytes, stream):
+    _check(lib().swin_mlp_int8_run_host(h, x_host, residual_host, y_host, T, workspace, workspace_bytes, stream))
+
+
+def swin_mlp_int8_destroy(h):
+    _check(lib().swin_mlp_int8_destroy(h))
+
+
+def swin_mlp_int8_launches_per_run(h) -> int:
+    return int(lib().swin_mlp_int8_launches_per_run(h))
+
+
+def swin_mlp_int8_last_error() -> str:
+    return last_error()
+
+
+# ---- torch-facing convenience (device memory + streams only) ---------------------
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class SwinMlpInt8Layer:
+    """One layer handle.  `layer` is any object with the fields of
+    swin_mlp_int8_desc_t (e.g. synth.Layer); numpy arrays are passed as host
+    pointers and copied by swin_mlp_int8_create."""
+
+    def __init__(self, layer, device: int = 0):
+        import numpy as np
+        import torch
+        self._keep = []
+
+        def hp(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return a.ctypes.data_as(ctypes.c_void_p).value
+
+        d = swin_mlp_int8_desc_t()
+        d.C, d.H, d.act = int(layer.C), int(layer.H), int(layer.act)
+        d.x_scale, d.x_zero_point = float(layer.s_x), int(layer.z_x)
+        d.w1, d.w1_scale, d.b1 = hp(layer.w1, np.int8), hp(layer.s_w1, np.float32), hp(layer.b1, np.float32)
+        d.h_scale, d.h_zero_point = float(layer.s_h), int(layer.z_h)
+        d.w2, d.w2_scale, d.b2 = hp(layer.w2, np.int8), hp(layer.s_w2, np.float32), hp(layer.b2, np.float32)
+        d.ln_gamma, d.ln_beta, d.ln_eps = hp(layer.gamma, np.float32), hp(layer.beta, np.float32), float(layer.eps)
+        d.y_scale, d.y_zero_point = float(layer.s_y), int(layer.z_y)
+        d.device = int(device)
+        self.C, self.H, self.device = d.C, d.H, device
+        self.handle = swin_mlp_int8_create(d)
+        self._keep = []
+        self._ws = None
+        self._torch = torch
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                lib().swin_mlp_int8_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def plan(self):
+        out = (ctypes.c_int32 * 8)()
+        lib().swin_mlp_int8_plan(self.handle, out)
+        return {"fc1_bn": out[0], "fc1_cs": out[1], "fc1_stages": out[2], "fc1_max_clusters": out[3],
+                "fc2_bn": out[4], "fc2_cs": out[5], "fc2_stages": out[6], "fc2_max_clusters": out[7]}
+
+    def constants(self):
+        import numpy as np
+        m1 = np.empty(self.H, np.float32); m2 = np.empty(self.C, np.float32)
+        w1 = np.empty(self.H, np.int32); w2 = np.empty(self.C, np.int32)
+        ih = ctypes.c_float(); iy = ctypes.c_float()
+        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        _check(lib().swin_mlp_int8_get_constants(self.handle, P(m1), ctypes.byref(ih), P(m2), ctypes.byref(iy),
+                                                 P(w1), P(w2)))
+        return m1, ih.value, m2, iy.value, w1, w2
+
+    def workspace(self, T):
+        torch = self._torch
+        n = swin_mlp_int8_workspace_bytes(self.handle, T)
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.empty(max(n, 128), dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    def __call__(self, x, residual=None, y=None, residual_out=None, stream=None, workspace=None):
+        torch = self._torch
+        T = x.shape[0]
+        if y is None:
+            y = torch.empty((T, self.C), dtype=torch.int8, device=x.device)
+        ws = self.workspace(T) if workspace is None else workspace
+        s = torch.cuda.current_stream(x.device).cuda_stream if stream is None else stream
+        swin_mlp_int8_run(self.handle, _ptr(x), _ptr(residual), _ptr(y), _ptr(residual_out), T,
+                          _ptr(ws), ws.numel(), ctypes.c_void_p(s))
+        return y
+
+    def run_debug(self, x, residual=None, residual_out=None):
+        torch = self._torch
+        T = x.shape[0]
+        dev = x.device
+        y = torch.empty((T, self.C), dtype=torch.int8, device=dev)
+        acc1 = torch.empty((T, self.H), dtype=torch.int32, device=dev)
+        hid = torch.empty((T, self.H), dtype=torch.int8, device=dev)
+        acc2 = torch.empty((T, self.C), dtype=torch.int32, device=dev)
+        ln = torch.empty((T, self.C), dtype=torch.float32, device=dev)
+        ws = self.workspace(T)
+        s = torch.cuda.current_stream(dev).cuda_stream
+        swin_mlp_int8_run_debug(self.handle, _ptr(x), _ptr(residual), _ptr(y), _ptr(residual_out), T,
+                                _ptr(ws), ws.numel(), ctypes.c_void_p(s),
+                                _ptr(acc1), _ptr(hid), _ptr(acc2), _ptr(ln))
+        return {"y": y, "acc1": acc1, "hidden": hid, "acc2": acc2, "yhat": ln}
+
+    def run_host(self, x_host, y_host, residual_host=None, workspace=None, stream=None):
+        """x_host/y_host/residual_host: pinned CPU tensors (host pointers into the C ABI)."""
+        torch = self._torch
+        T = x_host.shape[0]
+        n = swin_mlp_int8_host_workspace_bytes(self.handle, T, residual_host is not None)
+        ws = workspace if workspace is not None else torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}")
+        s = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        swin_mlp_int8_run_host(self.handle, _ptr(x_host), _ptr(residual_host), _ptr(y_host), T,
+                               _ptr(ws), ws.numel(), ctypes.c_void_p(s))
+        return y_host

@@ -1,0 +1,37 @@
+"""Build the sm_100a C-ABI library in-tree (the .so travels to the GPU box).
+
+nvcc -gencode arch=compute_100a,code=sm_100a: tcgen05.mma.kind::i8 only
+assembles for sm_100a (not sm_100f / sm_103a).  -fmad=false: no implicit
+contraction — every FMA in the epilogues is an explicit __fmaf_rn, so the
+fp32 operation order is exactly the one the oracle defines.
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SRC_DIR = os.path.join(HERE, "csrc")
+SOURCES = [os.path.join(SRC_DIR, "swin_mlp_int8.cu")]
+DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("mlp_kernels.cuh", "sm100_ptx.cuh")] + \
+    [os.path.join(ROOT, "include", "swin_mlp_int8.h")]
+LIB = os.path.join(HERE, "libswin_mlp_int8.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "-fmad=false", "-Xcompiler", "-fPIC",
+         "-shared", "-cudart", "static", "-I" + os.path.join(ROOT, "include")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and os.path.exists(LIB):
+        t = os.path.getmtime(LIB)
+        if all(os.path.getmtime(d) <= t for d in DEPS):
+            return LIB
+    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SOURCES
+    subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose="-v" in sys.argv))

@@ -1,0 +1,499 @@
+// swin_mlp_int8.cu — host side of the C ABI declared in include/swin_mlp_int8.h:
+// validation, constant folding, weight upload, tile/cluster planning, TMA
+// descriptor encoding and stream-ordered launches of the sm_100a kernels in
+// mlp_kernels.cuh.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
+// (tcgen05.mma.kind::i8 exists only on sm_100a).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/swin_mlp_int8.h"
+#include "mlp_kernels.cuh"
+
+using namespace swinmlp;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (expr);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(e_ == cudaErrorMemoryAllocation ? SWIN_MLP_ENOMEM : SWIN_MLP_ECUDA,     \
+                        "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+// One GEMM+epilogue launch plan.
+struct Plan {
+    int BN = 0, CS = 1, stages = 0, n_groups = 1;
+    uint32_t smem = 0;
+    int max_clusters = 0;
+};
+
+bool normal_positive(float v) { return std::isfinite(v) && std::fpclassify(v) == FP_NORMAL && v > 0.0f; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// 2-D int8 tensor [rows][cols] (row stride `ld` bytes) as a TMA map with a
+// {128 B along K, box_rows} box and 128-byte swizzle; out-of-range rows and
+// columns read as zero (ragged T and K tails).
+swin_mlp_status_t encode_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                            uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return fail(SWIN_MLP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(SWIN_MLP_ECUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld box_rows=%u", (int)r,
+                    (long long)rows, (long long)cols, box_rows);
+    return SWIN_MLP_OK;
+}
+
+constexpr uint32_t kSmemBudget = 227 * 1024;
+
+template <int EPI, bool DBG>
+swin_mlp_status_t prepare_kernel(const Plan& pl) {
+    auto k = mlp_gemm_kernel<EPI, DBG>;
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    return SWIN_MLP_OK;
+}
+
+template <int EPI>
+swin_mlp_status_t prepare_all(Plan& pl, int num_sms) {
+    swin_mlp_status_t st;
+    if ((st = prepare_kernel<EPI, false>(pl)) != SWIN_MLP_OK) return st;
+    if ((st = prepare_kernel<EPI, true>(pl)) != SWIN_MLP_OK) return st;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)pl.CS);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pl.CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, mlp_gemm_kernel<EPI, false>, &cfg);
+    if (e != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = num_sms / pl.CS;
+    }
+    pl.max_clusters = n;
+    return SWIN_MLP_OK;
+}
+
+// Columns per CTA tile, CTAs per cluster, ring depth for one GEMM.
+// full_row: the epilogue needs whole rows (LayerNorm) -> the cluster must
+// cover all N columns (CS * BN == N); otherwise column groups are independent.
+bool make_plan(int N, bool full_row, Plan& pl) {
+    pl = Plan();
+    if (full_row) {
+        for (int cs : {1, 2, 4, 8}) {
+            if (N % cs) continue;
+            const int bn = N / cs;
+            if (bn <= 256 && bn % 16 == 0) { pl.BN = bn; pl.CS = cs; break; }
+        }
+        if (!pl.BN) return false;
+        pl.n_groups = 1;
+    } else {
+        for (int bn : {256, 192, 128, 96, 64, 32}) {
+            if (N % bn == 0) { pl.BN = bn; break; }
+        }
+        if (!pl.BN) return false;
+        pl.CS = 1;
+        pl.n_groups = N / pl.BN;
+    }
+    const uint32_t stage = (uint32_t)(kBM * kBK + pl.BN * kBK);
+    const uint32_t extra = smem_layout(pl.BN, pl.CS, 0).total + 1024;
+    int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
+    if (stages > 8) stages = 8;
+    if (stages < 2) return false;
+    pl.stages = stages;
+    pl.smem = smem_layout(pl.BN, pl.CS, stages).total + 1024;
+    return pl.smem <= kSmemBudget;
+}
+
+template <int EPI, bool DBG>
+swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                         cudaStream_t stream) {
+    const int64_t units = a.num_units;
+    int64_t clusters = units < pl.max_clusters ? units : pl.max_clusters;
+    if (clusters < 1) clusters = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(clusters * pl.CS));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pl.CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, mlp_gemm_kernel<EPI, DBG>, ta, tb, a));
+    return SWIN_MLP_OK;
+}
+
+}  // namespace
+
+struct swin_mlp_int8_s {
+    swin_mlp_int8_desc_t d;   // scalars; pointers not retained
+    int device = 0, num_sms = 0;
+    Plan p1, p2;
+    // device copies (handle-owned)
+    int8_t *w1 = nullptr, *w2 = nullptr;
+    float *m1 = nullptr, *b1 = nullptr, *m2 = nullptr, *b2 = nullptr, *gamma = nullptr, *beta = nullptr;
+    int32_t *zc1 = nullptr, *zc2 = nullptr;
+    // host copies of the folded constants (debug getter)
+    std::vector<float> hm1, hm2;
+    std::vector<int32_t> hws1, hws2;
+    float inv_h = 0.f, inv_y = 0.f;
+    CUtensorMap tm_w1, tm_w2;
+    std::vector<void*> allocs;
+    ~swin_mlp_int8_s() {
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+swin_mlp_status_t fetch(const T* src, size_t n, std::vector<T>& out, const char* name) {
+    if (!src) return fail(SWIN_MLP_EINVAL, "%s is NULL", name);
+    out.resize(n);
+    CUDA_TRY(cudaMemcpy(out.data(), src, n * sizeof(T), cudaMemcpyDefault));
+    return SWIN_MLP_OK;
+}
+
+template <typename T>
+swin_mlp_status_t upload(swin_mlp_int8_s* h, const std::vector<T>& v, T** dst) {
+    void* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, v.size() * sizeof(T) + 16));
+    h->allocs.push_back(p);
+    CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    *dst = static_cast<T*>(p);
+    return SWIN_MLP_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+#define ST_TRY(...)                                 \
+    do {                                            \
+        swin_mlp_status_t s_ = (__VA_ARGS__);       \
+        if (s_ != SWIN_MLP_OK) return s_;           \
+    } while (0)
+
+extern "C" {
+
+const char* swin_mlp_int8_last_error(void) { return g_last_error.c_str(); }
+
+swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_mlp_int8_t* out) {
+    g_last_error.clear();
+    if (!desc || !out) return fail(SWIN_MLP_EINVAL, "desc and out must be non-NULL");
+    const swin_mlp_int8_desc_t& d = *desc;
+    if (d.C < 32 || d.C % 32) return fail(SWIN_MLP_EINVAL, "C=%d must be a multiple of 32 and >= 32", d.C);
+    if (d.H < d.C || d.H % 32) return fail(SWIN_MLP_EINVAL, "H=%d must be a multiple of 32 and >= C", d.H);
+    if (d.C > 1536 || d.H > 6144) return fail(SWIN_MLP_EUNSUPPORTED, "C=%d H=%d exceed 1536/6144", d.C, d.H);
+    if (d.act != SWIN_MLP_ACT_RELU && d.act != SWIN_MLP_ACT_GELU_ERF)
+        return fail(SWIN_MLP_EINVAL, "unknown activation %d", (int)d.act);
+    if (!normal_positive(d.x_scale) || !normal_positive(d.h_scale) || !normal_positive(d.y_scale))
+        return fail(SWIN_MLP_EINVAL, "activation scales must be finite, normal and > 0");
+    if (!(d.ln_eps > 0.0f) || !std::isfinite(d.ln_eps)) return fail(SWIN_MLP_EINVAL, "ln_eps must be > 0");
+    for (int32_t z : {d.x_zero_point, d.h_zero_point, d.y_zero_point})
+        if (z < -128 || z > 127) return fail(SWIN_MLP_EINVAL, "zero point %d outside [-128, 127]", z);
+    if (!d.w1 || !d.w2 || !d.w1_scale || !d.w2_scale || !d.ln_gamma || !d.ln_beta)
+        return fail(SWIN_MLP_EINVAL, "w1, w2, w1_scale, w2_scale, ln_gamma, ln_beta are required");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (d.device < 0 || d.device >= ndev) return fail(SWIN_MLP_EINVAL, "device %d of %d", d.device, ndev);
+    DeviceGuard guard(d.device);
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, d.device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(SWIN_MLP_EUNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)", d.device,
+                    prop.major, prop.minor);
+
+    const int C = d.C, H = d.H;
+    std::vector<int8_t> w1, w2;
+    std::vector<float> sw1, sw2, b1, b2, g, bt;
+    ST_TRY(fetch(d.w1, (size_t)H * C, w1, "w1"));
+    ST_TRY(fetch(d.w2, (size_t)C * H, w2, "w2"));
+    ST_TRY(fetch(d.w1_scale, (size_t)H, sw1, "w1_scale"));
+    ST_TRY(fetch(d.w2_scale, (size_t)C, sw2, "w2_scale"));
+    ST_TRY(fetch(d.ln_gamma, (size_t)C, g, "ln_gamma"));
+    ST_TRY(fetch(d.ln_beta, (size_t)C, bt, "ln_beta"));
+    if (d.b1) ST_TRY(fetch(d.b1, (size_t)H, b1, "b1"));
+    if (d.b2) ST_TRY(fetch(d.b2, (size_t)C, b2, "b2"));
+
+    auto h = new swin_mlp_int8_s();
+    h->d = d;
+    h->d.w1 = h->d.w2 = nullptr;
+    h->d.w1_scale = h->d.w2_scale = h->d.b1 = h->d.b2 = h->d.ln_gamma = h->d.ln_beta = nullptr;
+    h->device = d.device;
+    h->num_sms = prop.multiProcessorCount;
+    auto bail = [&](swin_mlp_status_t st) {
+        delete h;
+        return st;
+    };
+
+    // O0: folded constants, literal fp32 formulas (one rounding each).
+    h->hm1.resize(H);
+    h->hm2.resize(C);
+    for (int n = 0; n < H; ++n) {
+        if (!normal_positive(sw1[n])) return bail(fail(SWIN_MLP_EINVAL, "w1_scale[%d] not finite/normal/positive", n));
+        volatile float m = d.x_scale * sw1[n];
+        h->hm1[n] = m;
+        if (!normal_positive(h->hm1[n])) return bail(fail(SWIN_MLP_EINVAL, "x_scale*w1_scale[%d] not normal", n));
+    }
+    for (int c = 0; c < C; ++c) {
+        if (!normal_positive(sw2[c])) return bail(fail(SWIN_MLP_EINVAL, "w2_scale[%d] not finite/normal/positive", c));
+        volatile float m = d.h_scale * sw2[c];
+        h->hm2[c] = m;
+        if (!normal_positive(h->hm2[c])) return bail(fail(SWIN_MLP_EINVAL, "h_scale*w2_scale[%d] not normal", c));
+    }
+    {
+        volatile float one = 1.0f;
+        h->inv_h = one / d.h_scale;
+        h->inv_y = one / d.y_scale;
+    }
+    if (!normal_positive(h->inv_h) || !normal_positive(h->inv_y))
+        return bail(fail(SWIN_MLP_EINVAL, "1/h_scale or 1/y_scale not normal"));
+    // int32 zero-point corrections z * sum_k W[n][k]
+    h->hws1.assign(H, 0);
+    h->hws2.assign(C, 0);
+    std::vector<int32_t> zc1(H), zc2(C);
+    for (int n = 0; n < H; ++n) {
+        int64_t s = 0;
+        for (int k = 0; k < C; ++k) {
+            if (w1[(size_t)n * C + k] == -128) return bail(fail(SWIN_MLP_EINVAL, "w1 must be symmetric (-128 not allowed)"));
+            s += w1[(size_t)n * C + k];
+        }
+        h->hws1[n] = (int32_t)s;
+        zc1[n] = (int32_t)(s * d.x_zero_point);
+    }
+    for (int c = 0; c < C; ++c) {
+        int64_t s = 0;
+        for (int k = 0; k < H; ++k) {
+            if (w2[(size_t)c * H + k] == -128) return bail(fail(SWIN_MLP_EINVAL, "w2 must be symmetric (-128 not allowed)"));
+            s += w2[(size_t)c * H + k];
+        }
+        h->hws2[c] = (int32_t)s;
+        zc2[c] = (int32_t)(s * d.h_zero_point);
+    }
+
+    // tile / cluster plans
+    if (!make_plan(H, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
+    if (!make_plan(C, true, h->p2))
+        return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC2 tile plan for C=%d (needs C = CS*BN, BN%%16==0, BN<=256, CS in 1,2,4,8)", C));
+
+    swin_mlp_status_t st;
+#define H_TRY(expr)                                   \
+    do {                                              \
+        if ((st = (expr)) != SWIN_MLP_OK) return bail(st); \
+    } while (0)
+    H_TRY(upload(h, w1, &h->w1));
+    H_TRY(upload(h, w2, &h->w2));
+    H_TRY(upload(h, h->hm1, &h->m1));
+    H_TRY(upload(h, h->hm2, &h->m2));
+    H_TRY(upload(h, g, &h->gamma));
+    H_TRY(upload(h, bt, &h->beta));
+    if (d.b1) H_TRY(upload(h, b1, &h->b1));
+    if (d.b2) H_TRY(upload(h, b2, &h->b2));
+    if (d.x_zero_point) H_TRY(upload(h, zc1, &h->zc1));
+    if (d.h_zero_point) H_TRY(upload(h, zc2, &h->zc2));
+    H_TRY(encode_2d(&h->tm_w1, h->w1, H, C, C, (uint32_t)h->p1.BN));
+    H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H, (uint32_t)h->p2.BN));
+    if (d.act == SWIN_MLP_ACT_RELU) H_TRY(prepare_all<EP5_RELU>(h->p1, h->num_sms));
+    else H_TRY(prepare_all<EP5_GELU>(h->p1, h->num_sms));
+    H_TRY(prepare_all<EP6_LN>(h->p2, h->num_sms));
+#undef H_TRY
+    *out = h;
+    return SWIN_MLP_OK;
+}
+
+size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T) {
+    if (!h || T <= 0) return 0;
+    return (size_t)(((T * h->d.H) + 127) / 128 * 128);
+}
+
+static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const float* residual, int8_t* y,
+                                  float* residual_out, int64_t T, void* workspace, size_t ws_bytes, void* stream,
+                                  int32_t* acc1, int8_t* hidden, int32_t* acc2, float* ln_out, bool dbg) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (T < 0) return fail(SWIN_MLP_EINVAL, "T=%lld < 0", (long long)T);
+    if (T == 0) return SWIN_MLP_OK;
+    if (T > (int64_t)1 << 31) return fail(SWIN_MLP_EUNSUPPORTED, "T=%lld too large", (long long)T);
+    if (!x || !y || !workspace) return fail(SWIN_MLP_EINVAL, "x, y and workspace are required");
+    if (!aligned16(x) || !aligned16(y) || (residual && !aligned16(residual)) ||
+        (residual_out && !aligned16(residual_out)) || (reinterpret_cast<uintptr_t>(workspace) & 127u))
+        return fail(SWIN_MLP_EINVAL, "x/y/residual/residual_out must be 16-byte aligned, workspace 128-byte aligned");
+    if (ws_bytes < swin_mlp_int8_workspace_bytes(h, T))
+        return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", ws_bytes, swin_mlp_int8_workspace_bytes(h, T));
+    if ((const void*)x == (const void*)y) return fail(SWIN_MLP_EINVAL, "y may not alias x");
+    const int C = h->d.C, H = h->d.H;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int8_t* hq = static_cast<int8_t*>(workspace);
+
+    CUtensorMap tm_x, tm_h;
+    ST_TRY(encode_2d(&tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
+    ST_TRY(encode_2d(&tm_h, hq, T, H, H, (uint32_t)(kBM / h->p2.CS)));
+    const int64_t m_tiles = (T + kBM - 1) / kBM;
+
+    GemmArgs a1 = {};
+    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages;
+    a1.n_groups = h->p1.n_groups; a1.num_units = m_tiles * h->p1.n_groups; a1.ldo = H;
+    a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
+    a1.out = hq; a1.acc_tap = acc1;
+
+    GemmArgs a2 = {};
+    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages;
+    a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
+    a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
+    a2.out = y; a2.x = x; a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
+    a2.resid = residual; a2.resid_out = residual_out;
+    a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = (double)h->d.ln_eps;
+    a2.acc_tap = acc2; a2.ln_tap = ln_out;
+
+    const bool dbg1 = dbg && acc1, dbg2 = dbg && (acc2 || ln_out);
+    if (h->d.act == SWIN_MLP_ACT_RELU) {
+        ST_TRY(dbg1 ? launch<EP5_RELU, true>(h->p1, tm_x, h->tm_w1, a1, s)
+                    : launch<EP5_RELU, false>(h->p1, tm_x, h->tm_w1, a1, s));
+    } else {
+        ST_TRY(dbg1 ? launch<EP5_GELU, true>(h->p1, tm_x, h->tm_w1, a1, s)
+                    : launch<EP5_GELU, false>(h->p1, tm_x, h->tm_w1, a1, s));
+    }
+    if (dbg && hidden) CUDA_TRY(cudaMemcpyAsync(hidden, hq, (size_t)T * H, cudaMemcpyDeviceToDevice, s));
+    ST_TRY(dbg2 ? launch<EP6_LN, true>(h->p2, tm_h, h->tm_w2, a2, s)
+                : launch<EP6_LN, false>(h->p2, tm_h, h->tm_w2, a2, s));
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_mlp_int8_run(swin_mlp_int8_t h, const int8_t* x, const float* residual, int8_t* y,
+                                    float* residual_out, int64_t T, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+    return run_impl(h, x, residual, y, residual_out, T, workspace, workspace_bytes, stream, nullptr, nullptr,
+                    nullptr, nullptr, false);
+}
+
+swin_mlp_status_t swin_mlp_int8_run_debug(swin_mlp_int8_t h, const int8_t* x, const float* residual, int8_t* y,
+                                          float* residual_out, int64_t T, void* workspace, size_t workspace_bytes,
+                                          void* stream, int32_t* acc1, int8_t* hidden, int32_t* acc2,
+                                          float* ln_out) {
+    return run_impl(h, x, residual, y, residual_out, T, workspace, workspace_bytes, stream, acc1, hidden, acc2,
+                    ln_out, true);
+}
+
+static size_t align128(size_t v) { return (v + 127) / 128 * 128; }
+
+size_t swin_mlp_int8_host_workspace_bytes(swin_mlp_int8_t h, int64_t T, int32_t with_residual) {
+    if (!h || T <= 0) return 0;
+    const size_t tc = (size_t)T * h->d.C;
+    return swin_mlp_int8_workspace_bytes(h, T) + align128(tc) + align128(tc) + (with_residual ? align128(tc * 4) : 0);
+}
+
+swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host, const float* residual_host,
+                                         int8_t* y_host, int64_t T, void* workspace, size_t workspace_bytes,
+                                         void* stream) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (T < 0) return fail(SWIN_MLP_EINVAL, "T=%lld < 0", (long long)T);
+    if (T == 0) return SWIN_MLP_OK;
+    if (!x_host || !y_host || !workspace) return fail(SWIN_MLP_EINVAL, "x_host, y_host and workspace are required");
+    const size_t need = swin_mlp_int8_host_workspace_bytes(h, T, residual_host != nullptr);
+    if (workspace_bytes < need) return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", workspace_bytes, need);
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t tc = (size_t)T * h->d.C;
+    uint8_t* w = static_cast<uint8_t*>(workspace);
+    const size_t ws = swin_mlp_int8_workspace_bytes(h, T);
+    int8_t* xd = reinterpret_cast<int8_t*>(w + ws);
+    int8_t* yd = reinterpret_cast<int8_t*>(w + ws + align128(tc));
+    float* rd = residual_host ? reinterpret_cast<float*>(w + ws + 2 * align128(tc)) : nullptr;
+    CUDA_TRY(cudaMemcpyAsync(xd, x_host, tc, cudaMemcpyHostToDevice, s));
+    if (rd) CUDA_TRY(cudaMemcpyAsync(rd, residual_host, tc * 4, cudaMemcpyHostToDevice, s));
+    ST_TRY(swin_mlp_int8_run(h, xd, rd, yd, nullptr, T, w, ws, stream));
+    CUDA_TRY(cudaMemcpyAsync(y_host, yd, tc, cudaMemcpyDeviceToHost, s));
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_mlp_int8_get_constants(swin_mlp_int8_t h, float* m1, float* inv_h, float* m2, float* inv_y,
+                                              int32_t* wsum1, int32_t* wsum2) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (m1) std::memcpy(m1, h->hm1.data(), h->hm1.size() * sizeof(float));
+    if (m2) std::memcpy(m2, h->hm2.data(), h->hm2.size() * sizeof(float));
+    if (wsum1) std::memcpy(wsum1, h->hws1.data(), h->hws1.size() * sizeof(int32_t));
+    if (wsum2) std::memcpy(wsum2, h->hws2.data(), h->hws2.size() * sizeof(int32_t));
+    if (inv_h) *inv_h = h->inv_h;
+    if (inv_y) *inv_y = h->inv_y;
+    return SWIN_MLP_OK;
+}
+
+int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h) { return h ? 2 : 0; }
+
+swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
+    if (!h) return SWIN_MLP_OK;
+    {
+        DeviceGuard guard(h->device);
+        delete h;
+    }
+    return SWIN_MLP_OK;
+}
+
+// Test/bench introspection: the launch plan chosen for this layer.
+int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out8) {
+    if (!h || !out8) return -1;
+    out8[0] = h->p1.BN; out8[1] = h->p1.CS; out8[2] = h->p1.stages; out8[3] = h->p1.max_clusters;
+    out8[4] = h->p2.BN; out8[5] = h->p2.CS; out8[6] = h->p2.stages; out8[7] = h->p2.max_clusters;
+    return 0;
+}
+
+}  // extern "C"

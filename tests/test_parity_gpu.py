@@ -1,0 +1,191 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
+on the same seeded inputs (synth/).  Run on a B200 with -m gpu.
+
+Tiers (BASELINE.json north_star):
+  acc1, acc2 (int32)                      bit-exact
+  Hq, ReLU, canonical fp32 order          bit-exact
+  Hq, GELU control                        <= 1 LSB on <= 0.01 % of elements
+  Y (int8)                                <= 1 LSB on <= 0.01 % of elements
+  yhat (pre-quant LayerNorm, fp32)        |gpu - ref| <= 1e-5 * max(1, |ref|)
+Each stage is checked on the GPU's own input to that stage (oracle step
+applied to the previous GPU tap), plus end to end against oracle.mlp.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2402_01169_b200 as P
+    P.lib()  # fails loudly if the extension is missing
+    return torch.device("cuda:0")
+
+
+def _layer(C, seed, act=0, bias=False, zx=0, zh=0, zy=0):
+    return synth.make_layer(C, seed, act=act, fc1_bias=bias, z_x=zx, z_h=zh, z_y=zy)
+
+
+def _tier_int8(got, ref, frac=1e-4, what=""):
+    d = np.abs(got.astype(np.int32) - ref.astype(np.int32))
+    assert d.max(initial=0) <= 1, f"{what}: max |diff| {d.max()} > 1 LSB"
+    n_bad = int((d > 0).sum())
+    assert n_bad <= max(0, int(frac * d.size)), f"{what}: {n_bad} of {d.size} elements differ (> {frac:%})"
+    return n_bad
+
+
+def _tier_yhat(got, ref, what="yhat"):
+    err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+    tol = 1e-5 * np.maximum(1.0, np.abs(ref.astype(np.float64)))
+    assert (err <= tol).all(), f"{what}: max rel err {(err / tol).max() * 1e-5:.3e}"
+
+
+def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True):
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    X = synth.make_activations(L, T, x_seed)
+    R = synth.make_residual(T, L.C, x_seed + 1) if resid else None
+    layer = SwinMlpInt8Layer(L, device=0)
+    xd = torch.from_numpy(X).to(dev)
+    rd = torch.from_numpy(R).to(dev) if resid else None
+    zo = torch.empty((T, L.C), dtype=torch.float32, device=dev)
+    taps = layer.run_debug(xd, residual=rd, residual_out=zo)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in taps.items()}
+    g["z"] = zo.cpu().numpy()
+    # stage-wise
+    m1, ih, m2, iy = oracle.fold_constants(L.s_x, L.s_w1, L.s_h, L.s_w2, L.s_y)
+    a1 = oracle.gemm_i8(X, L.w1, L.z_x, nthreads=0)
+    np.testing.assert_array_equal(g["acc1"], a1, err_msg="acc1 (FC1 int32) not bit-exact")
+    h = oracle.ep5(g["acc1"], m1, L.b1, ih, L.z_h, act=L.act)
+    if L.act == synth.ACT_RELU:
+        np.testing.assert_array_equal(g["hidden"], h, err_msg="Hq (ReLU) not bit-exact")
+    else:
+        _tier_int8(g["hidden"], h, what="Hq (GELU)")
+    a2 = oracle.gemm_i8(g["hidden"], L.w2, L.z_h)
+    np.testing.assert_array_equal(g["acc2"], a2, err_msg="acc2 (FC2 int32) not bit-exact")
+    Y, yh, z = oracle.ep6(g["acc2"], m2, L.b2, X, L.s_x, L.z_x, L.gamma, L.beta, L.eps, iy, L.z_y, R=R)
+    np.testing.assert_array_equal(g["z"], z, err_msg="z (pre-LN sum) not bit-exact")
+    _tier_yhat(g["yhat"], yh)
+    flips = _tier_int8(g["y"], Y, what="Y")
+    # the production (non-debug) kernels give the same Y
+    y2 = layer(xd, residual=rd)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y2.cpu().numpy(), g["y"], err_msg="run != run_debug")
+    if e2e:
+        ref = oracle.mlp(L, X, R=R)
+        _tier_int8(g["y"], ref, frac=1e-4 if L.act == synth.ACT_RELU else 1e-3, what="Y end-to-end")
+    return flips
+
+
+@pytest.mark.parametrize("C,T", [(96, 1000), (128, 300), (192, 257), (256, 129), (384, 200),
+                                 (512, 131), (768, 257), (1024, 100), (1536, 129)])
+def test_parity_relu_paper_mode(dev, C, T):
+    """The paper's GELU-less block: ReLU, no FC1 bias, symmetric zero points."""
+    _run_and_check(dev, _layer(C, 1000 + C), T)
+
+
+@pytest.mark.parametrize("C,T", [(96, 513), (384, 130), (768, 129)])
+def test_parity_gelu_control(dev, C, T):
+    """GELU control epilogue (the fused op the paper removes)."""
+    _run_and_check(dev, _layer(C, 2000 + C, act=1, bias=True), T)
+
+
+@pytest.mark.parametrize("C,T,zx,zh,zy", [(96, 300, -7, 0, 3), (192, 200, 0, -128, 0), (384, 150, 5, -7, -2)])
+def test_parity_zero_points_and_bias(dev, C, T, zx, zh, zy):
+    """Asymmetric activation zero points (reading R5) and an FC1 bias (north-star op #5)."""
+    _run_and_check(dev, _layer(C, 3000 + C, bias=True, zx=zx, zh=zh, zy=zy), T)
+
+
+@pytest.mark.parametrize("C,T", [(96, 200), (768, 131)])
+def test_parity_fp32_residual(dev, C, T):
+    """fp32 residual operand of op #6 (reading R3) and the residual_out tap."""
+    _run_and_check(dev, _layer(C, 4000 + C), T, resid=True)
+
+
+@pytest.mark.parametrize("T", [1, 2, 127, 128, 129, 255, 256])
+def test_parity_tile_edges(dev, T):
+    """Ragged token tails around the 128-row tile."""
+    _run_and_check(dev, _layer(192, 5000), T)
+
+
+def test_t_zero_is_noop(dev):
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    layer = SwinMlpInt8Layer(_layer(96, 1), device=0)
+    x = torch.empty((0, 96), dtype=torch.int8, device=dev)
+    y = layer(x)
+    torch.cuda.synchronize()
+    assert y.shape == (0, 96)
+
+
+def test_folded_constants_match_oracle(dev):
+    """O0 on the device side: the library's folded fp32 constants equal the oracle's bit for bit."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(384, 6000, zx=-3, zh=-128)
+    layer = SwinMlpInt8Layer(L, device=0)
+    m1, ih, m2, iy, w1, w2 = layer.constants()
+    om1, oih, om2, oiy = oracle.fold_constants(L.s_x, L.s_w1, L.s_h, L.s_w2, L.s_y)
+    np.testing.assert_array_equal(m1, om1)
+    np.testing.assert_array_equal(m2, om2)
+    assert np.float32(ih) == np.float32(oih) and np.float32(iy) == np.float32(oiy)
+    np.testing.assert_array_equal(w1, L.w1.astype(np.int64).sum(1))
+    np.testing.assert_array_equal(w2, L.w2.astype(np.int64).sum(1))
+
+
+def test_shard_concat_equals_unsharded(dev):
+    """Tokens are independent rows: running shards separately and
+    concatenating equals the unsharded run bit-exactly (the multi-GPU invariant)."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(384, 7000)
+    T = 1000
+    X = torch.from_numpy(synth.make_activations(L, T, 9)).to(dev)
+    layer = SwinMlpInt8Layer(L, device=0)
+    full = layer(X).cpu()
+    parts = [layer(X[a:b].contiguous()).cpu() for a, b in ((0, 384), (384, 513), (513, 1000))]
+    torch.cuda.synchronize()
+    assert torch.equal(full, torch.cat(parts))
+    # row permutation equivariance
+    perm = torch.randperm(T, generator=torch.Generator().manual_seed(1))
+    yp = layer(X[perm.to(dev)].contiguous()).cpu()
+    assert torch.equal(yp, full[perm])
+
+
+def test_run_host_matches_device(dev):
+    """The end-to-end host-buffer entry point (H2D, run, D2H inside the library)."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(192, 8000)
+    T = 700
+    Xn = synth.make_activations(L, T, 3)
+    layer = SwinMlpInt8Layer(L, device=0)
+    xh = torch.from_numpy(Xn).pin_memory()
+    yh = torch.empty((T, 192), dtype=torch.int8).pin_memory()
+    layer.run_host(xh, yh)
+    torch.cuda.synchronize()
+    yd = layer(xh.to(dev)).cpu()
+    torch.cuda.synchronize()
+    assert torch.equal(yh, yd)
+
+
+def test_full_size_config2_sampled(dev):
+    """BASELINE configs[1] (Swin-T, four stage MLPs, batch 64) at full size, in the
+    bench's launch configuration: sampled rows (first/last tile, tile boundaries,
+    random) against the oracle computed row by row."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    rng = np.random.default_rng(11)
+    for L, T, xs in synth.swin_t_batch64_layers():
+        X = synth.make_activations(L, T, xs)
+        layer = SwinMlpInt8Layer(L, device=0)
+        y = layer(torch.from_numpy(X).to(dev)).cpu().numpy()
+        torch.cuda.synchronize()
+        rows = np.unique(np.concatenate([np.arange(0, 128), np.arange(T - 128, T),
+                                         np.arange(127, T, 128)[:200], np.arange(128, T, 128)[:200],
+                                         rng.integers(0, T, 1500)]))
+        ref = oracle.mlp(L, X, rows=rows)
+        _tier_int8(y[rows], ref, what=f"config2 C={L.C} sampled rows")
