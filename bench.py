@@ -1,0 +1,357 @@
+"""Benchmark of the B200-native GELU-less INT8 Swin MLP sub-layer.
+
+`python bench.py --gpus N --steps K --warmup W [--impl reference]`
+
+Workload (BASELINE.json configs[1], the configuration the metric is quoted on
+that fits one GPU): Swin-T, all four stage MLPs (C = 96/192/384/768, H = 4C)
+at batch 64 -> T = 200704 / 50176 / 12544 / 3136 tokens.  One step = one pass
+of the whole hot path (FC1 -> op #5 ReLU -> FC2 -> op #6 LN+Q) over all four
+layers.  Multi-GPU: one process per GPU (torchrun), weights broadcast once from
+rank 0 over NCCL, every rank runs its own batch of 64 images (weak scaling, no
+collective on the hot path).  L2 is flushed (256 MiB write, untimed) before
+every timed step; each step is timed with CUDA events on the launching stream;
+the job time is the max over ranks.
+
+Rank 0 prints ONE JSON line (see README/DESIGN.md §6 for every key).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s per Swin MLP layer at 1/2/4/8 B200; % INT8 TC peak; ReLU vs GELU us"
+WORKLOAD = ("configs[1]: Swin-T all four stage MLPs (C=96/192/384/768 -> 4C -> C; "
+            "T=200704/50176/12544/3136 tokens), batch 64 per GPU, int8")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--pairs", type=int, default=30, help="interleaved ReLU/GELU paired trials")
+    ap.add_argument("--cpu-stride", type=int, default=8, help="cpu_baseline samples every n-th token")
+    ap.add_argument("--ref-stride", type=int, default=64, help="--impl reference samples every n-th token")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def layers_spec(batch, act):
+    import synth
+    toks = synth.stage_tokens(batch)
+    out = []
+    for s in range(4):
+        C = 96 << s
+        out.append((synth.make_layer(C, synth.layer_seed(2, s, 0), act=act), toks[s], synth.layer_seed(2, s, 0) + 50))
+    return out
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"bf16_burst": d["bf16_tflops"], "bf16_sustained": d.get("bf16_tflops_sustained"),
+                "hbm_gbs": d["hbm_gbs"], "src": "MEASURED_PEAKS.json", "sm_max_mhz": d.get("sm_max_mhz")}
+    return {"bf16_burst": 1590.0, "bf16_sustained": 1400.0, "hbm_gbs": 6650.0,
+            "src": "B200_PROFILING.md fallback", "sm_max_mhz": 1965.0}
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampling during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index, period=0.002):
+        self.samples, self.reasons, self.period = [], set(), period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            self.max = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_oracle_rate(spec, stride, offset=0, nthreads=0):
+    """Oracle tokens/s on every `stride`-th token of each layer (bounded sample)."""
+    import numpy as np
+    import oracle
+    import synth
+    nthreads = nthreads or os.cpu_count()
+    tok = 0
+    t_total = 0.0
+    for L, T, xs in spec:
+        X = synth.make_activations(L, T, xs)
+        rows = np.arange(offset % stride, T, stride, dtype=np.int64)
+        t0 = time.perf_counter()
+        oracle.mlp(L, X, rows=rows, nthreads=nthreads)
+        t_total += time.perf_counter() - t0
+        tok += rows.size
+    return tok / t_total, tok, t_total, nthreads
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import synth
+    spec = layers_spec(args.batch, synth.ACT_RELU)
+    total_tok, total_t = 0, 0.0
+    for i in range(args.warmup):
+        cpu_oracle_rate(spec, args.ref_stride * 4, offset=i)
+    nth = os.cpu_count()
+    for k in range(args.steps):
+        _, tok, t, nth = cpu_oracle_rate(spec, args.ref_stride, offset=k)
+        total_tok += tok
+        total_t += t
+    v = total_tok / total_t
+    sample = f"every {args.ref_stride}th token of each of the 4 layers per step ({total_tok // max(1, args.steps)} tokens/step)"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "s8",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": nth, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2402_01169_b200 as P
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P.lib()
+
+    # ---- layers: rank 0 generates, weights broadcast once over NCCL --------------------------------
+    spec = layers_spec(args.batch, synth.ACT_RELU)
+    names = ["w1", "s_w1", "w2", "s_w2", "b2", "gamma", "beta"]
+    relu_layers, gelu_layers, xs_dev, xs_host, ys, T_list = [], [], [], [], [], []
+    for li, (L, T, xseed) in enumerate(spec):
+        dev_arrays = {}
+        for n in names:
+            a = getattr(L, n)
+            t = torch.from_numpy(np.ascontiguousarray(a)).to(dev) if rank == 0 else \
+                torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
+            if ws > 1:
+                dist.broadcast(t, 0)
+            dev_arrays[n] = t
+        for n, t in dev_arrays.items():
+            setattr(L, n, t)          # create() copies from device pointers
+        relu_layers.append(SwinMlpInt8Layer(L, device=local))
+        L.act = synth.ACT_GELU
+        gelu_layers.append(SwinMlpInt8Layer(L, device=local))
+        L.act = synth.ACT_RELU
+        X = synth.make_activations(L, T, xseed + 7919 * rank)
+        xh = torch.from_numpy(X).pin_memory()
+        xs_host.append(xh)
+        xs_dev.append(xh.to(dev))
+        ys.append(torch.empty((T, L.C), dtype=torch.int8, device=dev))
+        T_list.append(T)
+    ws_bytes = max(P.swin_mlp_int8_workspace_bytes(l.handle, T) for l, T in zip(relu_layers, T_list))
+    host_ws = max(P.swin_mlp_int8_host_workspace_bytes(l.handle, T, 0) for l, T in zip(relu_layers, T_list))
+    workspace = torch.empty(max(ws_bytes, host_ws), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    tokens_per_step = sum(T_list)
+
+    def step(layers):
+        for l, x, y in zip(layers, xs_dev, ys):
+            l(x, y=y, workspace=workspace)
+
+    def timed(fn, n, flush_l2=True):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for k in range(n):
+            if flush_l2:
+                flush.fill_(k & 0xff)
+            evs[k][0].record(stream)
+            fn()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        return [a.elapsed_time(b) for a, b in evs]
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v):
+        if ws == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up ---------------------------------------------------------------------------------
+    for _ in range(max(args.warmup, 0)):
+        step(relu_layers)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: exactly K steps --------------------------------------------------------------
+    for l in relu_layers:
+        l.profile_begin(args.steps)
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        per_step = timed(lambda: step(relu_layers), args.steps)
+    barrier()
+    prof = [l.profile_end() for l in relu_layers]
+    t_ms = max_over_ranks(sum(per_step))
+    value = ws * tokens_per_step * args.steps / (t_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (per-launch CUDA events, native) -------------------------
+    peaks = load_peaks()
+    int8_peak_tops = 2.0 * peaks["bf16_burst"]      # nominal int8/bf16 dense ratio 4.5/2.25 = 2
+    kernels = []
+    for (L, T, _), (f1, f2, n) in zip(spec, prof):
+        ops = 2.0 * T * L.C * L.H
+        for name, ms in (("fc1_relu_q", f1), ("fc2_ln_q", f2)):
+            avg_s = ms / max(n, 1) / 1e3
+            kernels.append({"kernel": f"{name}[C={L.C},T={T}]", "avg_us": avg_s * 1e6,
+                            "tops": ops / avg_s / 1e12 if avg_s > 0 else None, "ops": ops})
+    dom = max(kernels, key=lambda k: k["avg_us"])
+    step_us = 1e3 * sum(per_step) / args.steps
+    share = dom["avg_us"] / step_us
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom["kernel"])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": dom["kernel"], "achieved": dom["tops"], "peak": int8_peak_tops,
+                "unit": "TOPS", "frac": dom["tops"] / int8_peak_tops, "traffic": traffic,
+                "share_of_step": share,
+                "peak_source": f"{peaks['src']} bf16_tflops {peaks['bf16_burst']} x 2 (int8:bf16 nominal 4.5:2.25), burst",
+                "algorithmic": "2*T*C*H int8 MACs-as-ops per launch (SURVEY §8(d): 16*C^2 ops per token per layer)",
+                "step_frac": (sum(k["ops"] for k in kernels) / (step_us / 1e6) / 1e12) / int8_peak_tops,
+                "kernels": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in kk.items() if k != "ops"}
+                            for kk in kernels]}
+
+    # ---- end to end through the C ABI with host buffers (H2D + run + D2H per step) ----------------
+    ys_host = [torch.empty((T, L.C), dtype=torch.int8).pin_memory() for (L, T, _) in spec]
+
+    def step_host():
+        for l, xh, yh in zip(relu_layers, xs_host, ys_host):
+            l.run_host(xh, yh, workspace=workspace)
+
+    for _ in range(2):
+        step_host()
+    barrier()
+    e2e_steps = max(3, min(args.steps, 20))
+    e2e_ms = max_over_ranks(sum(timed(step_host, e2e_steps)))
+    barrier()
+    e2e_val = ws * tokens_per_step * e2e_steps / (e2e_ms / 1e3)
+    h2d = sum(int(x.numel()) for x in xs_host)
+    d2h = sum(int(y.numel()) for y in ys_host)
+
+    # ---- ReLU vs GELU epilogue: interleaved paired trials (SPEC.md:525 style) ---------------------
+    for _ in range(3):
+        step(gelu_layers)
+    relu_us, gelu_us, wins = [], [], 0
+    for i in range(args.pairs):
+        order = (relu_layers, gelu_layers) if i % 2 == 0 else (gelu_layers, relu_layers)
+        res = {}
+        for layers in order:
+            res[id(layers)] = 1e3 * timed(lambda: step(layers), 1)[0]
+        r, g = res[id(relu_layers)], res[id(gelu_layers)]
+        relu_us.append(r)
+        gelu_us.append(g)
+        wins += r < g
+    relu_gelu = {"relu_us_median": statistics.median(relu_us), "gelu_us_median": statistics.median(gelu_us),
+                 "gelu_over_relu": statistics.median(gelu_us) / statistics.median(relu_us),
+                 "pairs": args.pairs, "relu_wins": wins,
+                 "unit": "us per step (4 layers)"}
+
+    # ---- CPU baseline: the oracle as it stands on this host (rank 0, N=1 only) ----------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        rate, tok, t, nth = cpu_oracle_rate(layers_spec(args.batch, synth.ACT_RELU), args.cpu_stride)
+        cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
+               "sample": f"every {args.cpu_stride}th token of each of the 4 layers ({tok} tokens, {t:.1f} s)"}
+
+    plan = relu_layers[-1].plan()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "s8", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "layers": [{"C": L.C, "H": L.H, "T": T} for (L, T, _) in spec],
+                           "act": "relu (GELU-less, b1=None)", "parallelism": f"token-shard weak x{ws}",
+                           "l2": "flushed between steps (256 MiB write, untimed)", "plan_C768": plan},
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "swin_mlp_int8_run_host"},
+                "gpu_launches": sum(n for (_, _, n) in prof) * 2,
+                "relu_vs_gelu": relu_gelu,
+                "tensor_frac_of_step": roofline["step_frac"],
+                "clocks": sampler.result()}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -20,7 +20,8 @@
  *   d  = fmaf(fl(A2), m2[c], b2[c] or 0),  m2[c] = fl(h_scale*w2_scale[c])
  *   r  = residual[t][c]  or, when residual == NULL, fl(fl(X[t][c] - z_x) * x_scale)
  *   z  = fl(d + r); mu, var (biased), rstd = 1/sqrt(var+eps) in double;
- *   yhat = fl(((z-mu)*rstd)*gamma[c] + beta[c])  (double ops);
+ *   yhat = fl(((z-mu)*rstd)*gamma[c] + beta[c])  (double ops; desc.ln_fp64 = 1 —
+ *   with ln_fp64 = 0 the same formula is evaluated in fp32 with one fmaf);
  *   Y  = clamp(rne(fl(yhat * inv_y)) + y_zero_point, -128, 127),  inv_y = fl(1/y_scale)
  * The readings behind these choices (rounding, zero points, residual
  * operand, trailing Q, eps) are listed in DESIGN.md §3.
@@ -82,6 +83,10 @@ typedef struct {
     float   y_scale;            /* output scale s_y > 0                                    */
     int32_t y_zero_point;       /* z_y in [-128, 127]                                      */
     int32_t device;             /* CUDA device ordinal the handle lives on                 */
+    int32_t ln_fp64;            /* LayerNorm statistics/normalisation precision:
+                                 *   1: fp64 in the oracle's operation order (Y, yhat bit-exact
+                                 *      up to the order of the row sums)
+                                 *   0: fp32 (faster; Y within 1 LSB on <= 0.01 % of elements) */
 } swin_mlp_int8_desc_t;
 
 /* Create a layer handle: validates the description, folds the fp32
@@ -136,6 +141,15 @@ swin_mlp_status_t swin_mlp_int8_get_constants(swin_mlp_int8_t h, float* m1, floa
 
 /* Number of kernel launches one `run` enqueues (for the bench's launch count). */
 int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h);
+
+/* Native per-kernel timing for the bench's roofline: after profile_begin,
+ * every run/run_debug records CUDA events before FC1, between FC1 and FC2
+ * and after FC2 on its stream (at most max_runs runs are recorded; later
+ * runs are not).  profile_end synchronizes those events, returns the summed
+ * FC1+ep5 and FC2+ep6 kernel durations in ms and the number of recorded runs,
+ * and stops recording.  Any output pointer may be NULL. */
+swin_mlp_status_t swin_mlp_int8_profile_begin(swin_mlp_int8_t h, int32_t max_runs);
+swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, float* fc2_ms, int32_t* runs);
 
 /* Introspection: the launch plan of this layer, out8[8] = {FC1 BN, FC1 cluster size,
  * FC1 stages, FC1 max co-resident clusters, FC2 BN, FC2 cluster size, FC2 stages,

@@ -29,6 +29,7 @@ EXPORTS = [
     "swin_mlp_int8_create", "swin_mlp_int8_workspace_bytes", "swin_mlp_int8_run",
     "swin_mlp_int8_run_debug", "swin_mlp_int8_host_workspace_bytes", "swin_mlp_int8_run_host",
     "swin_mlp_int8_get_constants", "swin_mlp_int8_launches_per_run", "swin_mlp_int8_plan",
+    "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end",
     "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
 ]
 
@@ -42,7 +43,7 @@ class swin_mlp_int8_desc_t(ctypes.Structure):
         ("w2", ctypes.c_void_p), ("w2_scale", ctypes.c_void_p), ("b2", ctypes.c_void_p),
         ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
         ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32),
-        ("device", ctypes.c_int32),
+        ("device", ctypes.c_int32), ("ln_fp64", ctypes.c_int32),
     ]
 
 
@@ -82,6 +83,10 @@ def lib():
     L.swin_mlp_int8_launches_per_run.restype = i32
     L.swin_mlp_int8_plan.argtypes = [P, P]
     L.swin_mlp_int8_plan.restype = i32
+    L.swin_mlp_int8_profile_begin.argtypes = [P, i32]
+    L.swin_mlp_int8_profile_begin.restype = i32
+    L.swin_mlp_int8_profile_end.argtypes = [P, P, P, P]
+    L.swin_mlp_int8_profile_end.restype = i32
     L.swin_mlp_int8_destroy.argtypes = [P]
     L.swin_mlp_int8_destroy.restype = i32
     L.swin_mlp_int8_last_error.argtypes = []
@@ -150,7 +155,7 @@ class SwinMlpInt8Layer:
     swin_mlp_int8_desc_t (e.g. synth.Layer); numpy arrays are passed as host
     pointers and copied by swin_mlp_int8_create."""
 
-    def __init__(self, layer, device: int = 0):
+    def __init__(self, layer, device: int = 0, ln_fp64: bool = False):
         import numpy as np
         import torch
         self._keep = []
@@ -158,6 +163,10 @@ class SwinMlpInt8Layer:
         def hp(a, dt):
             if a is None:
                 return None
+            if isinstance(a, torch.Tensor):      # host or device tensor: create() detects which
+                a = a.contiguous()
+                self._keep.append(a)
+                return a.data_ptr()
             a = np.ascontiguousarray(a, dtype=dt)
             self._keep.append(a)
             return a.ctypes.data_as(ctypes.c_void_p).value
@@ -171,6 +180,7 @@ class SwinMlpInt8Layer:
         d.ln_gamma, d.ln_beta, d.ln_eps = hp(layer.gamma, np.float32), hp(layer.beta, np.float32), float(layer.eps)
         d.y_scale, d.y_zero_point = float(layer.s_y), int(layer.z_y)
         d.device = int(device)
+        d.ln_fp64 = int(bool(ln_fp64))
         self.C, self.H, self.device = d.C, d.H, device
         self.handle = swin_mlp_int8_create(d)
         self._keep = []
@@ -191,6 +201,15 @@ class SwinMlpInt8Layer:
         lib().swin_mlp_int8_plan(self.handle, out)
         return {"fc1_bn": out[0], "fc1_cs": out[1], "fc1_stages": out[2], "fc1_max_clusters": out[3],
                 "fc2_bn": out[4], "fc2_cs": out[5], "fc2_stages": out[6], "fc2_max_clusters": out[7]}
+
+    def profile_begin(self, max_runs):
+        _check(lib().swin_mlp_int8_profile_begin(self.handle, int(max_runs)))
+
+    def profile_end(self):
+        """Returns (fc1_ms_total, fc2_ms_total, runs) of the runs recorded since profile_begin."""
+        a, b, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
+        _check(lib().swin_mlp_int8_profile_end(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
+        return a.value, b.value, n.value
 
     def constants(self):
         import numpy as np

@@ -19,8 +19,15 @@
 //               instruction, int32 accumulators in TMEM, 2 accumulator buffers so
 //               the epilogue of tile i overlaps the MMAs of tile i+1.
 //   warp 2      TMEM allocator.
+//   warp 3      column-constant loader: per tile, copies the tile's per-column
+//               constants (dequant multiplier, bias, zero-point correction,
+//               LN gamma/beta) from global into a 2-deep shared-memory ring.
 //   warps 4-11  epilogue: warp w drains TMEM lane quadrant (w % 4) — thread = one
-//               token row — over half of the tile's columns ((w-4)/4 picks the half).
+//               token row — over half of the tile's columns ((w-4)/4 picks the half),
+//               16 columns per tcgen05.ld, next load in flight while the current
+//               chunk is processed.  Each warp stages its int8 output chunk
+//               [32 rows][16 B] in a private smem ring and writes it with a TMA
+//               bulk tensor store (rows >= T are clipped by the TMA unit).
 //
 // EP6 row statistics: each thread owns one row of its half; the two halves are
 // combined through shared memory, the CS CTAs of the cluster (which split the
@@ -28,9 +35,16 @@
 // st.async + mbarrier complete_tx, always summed in rank order, so every CTA
 // of the cluster derives bit-identical mean and rstd.  z is parked in TMEM
 // between the three passes (sum, centred sum of squares, normalise).
+// Template flags F (so the hot loop carries no predicated-off work):
+//   kHasB  bias present, kHasZc activation zero point != 0 (int32 correction),
+//   kZqNz  output zero point != 0, kS64 LayerNorm in fp64.
+// kS64 = true computes the statistics and the normalisation in fp64 in the
+// oracle's operation order (bit-exact up to summation order); false uses fp32
+// (cheaper; the <= 1 LSB on <= 0.01 % tier).
 #pragma once
 #include <cuda.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "sm100_ptx.cuh"
 
@@ -43,7 +57,13 @@ constexpr int kBK = 128;             // K bytes per pipeline stage (one 128-B sw
 constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiThreads = 256;
+constexpr int kEpiWarps = 8;
 constexpr int kChunk = 16;           // columns per tcgen05.ld (32x32b.x16)
+constexpr int kRing = 4;             // output staging chunks per epilogue warp
+constexpr int kRingBytes = 32 * kChunk;   // [32 rows][16 B] = one chunk
+constexpr int kSlotBytes = 2 * kRingBytes; // a ring slot holds 2 chunks (one fence + bulk group)
+constexpr int kHasB = 1, kHasZc = 2, kZqNz = 4, kS64 = 8;
+constexpr int kNConst = 5;           // m, b, zc, gamma, beta
 
 struct GemmArgs {
     int64_t M;             // token rows
@@ -59,7 +79,6 @@ struct GemmArgs {
     const int32_t* zc;     // [N] zero-point correction z*sum_k W[n][k], or nullptr
     float inv_q;           // 1/s of the output quantizer (inv_h or inv_y)
     int32_t zq;            // output zero point (z_h or z_y)
-    int8_t* out;           // [M][ldo] int8 output (Hq or Y)
     // EP6 only
     const int8_t* x;       // [M][ldo] layer input (residual = dQ(x) when resid == nullptr)
     float s_x;
@@ -68,22 +87,24 @@ struct GemmArgs {
     float* resid_out;      // [M][ldo] fp32 z or nullptr
     const float* gamma;
     const float* beta;
-    double eps;
+    float eps;
     // debug taps
     int32_t* acc_tap;      // [M][ldo] int32 accumulators (incl. zero-point term)
     float* ln_tap;         // [M][ldo] fp32 yhat (EP6)
 };
 
 struct SmemLayout {
-    uint32_t a, b, bars, tmem_slot, red, xbuf, total;
+    uint32_t a, b, ring, consts, bars, tmem_slot, red, xbuf, total;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(int BN, int CS, int stages) {
     SmemLayout L;
     L.a = 0;
     L.b = L.a + (uint32_t)stages * kBM * kBK;
-    L.bars = L.b + (uint32_t)stages * (uint32_t)BN * kBK;
-    const uint32_t nbars = 2u * stages + 2 + 2 + 2;
+    L.ring = L.b + (uint32_t)stages * (uint32_t)BN * kBK;
+    L.consts = L.ring + (uint32_t)kEpiWarps * kRing * kSlotBytes;
+    L.bars = L.consts + 2u * kNConst * (uint32_t)BN * 4u;
+    const uint32_t nbars = 2u * stages + 2 + 2 + 2 + 2;
     L.tmem_slot = L.bars + 8u * nbars;
     L.red = (L.tmem_slot + 8 + 15) & ~15u;
     L.xbuf = L.red + 2u * 2u * kBM * 8u;
@@ -97,30 +118,48 @@ __host__ __device__ inline uint32_t tmem_cols_for(int BN) {
     return c;
 }
 
-// Q of the fused ops: clamp(rne(v) + zp, -128, 127); rne = cvt.rni (half to even),
-// which saturates out-of-range values; the +-1024 clamp keeps the add exact.
-__device__ __forceinline__ int32_t quant_rne(float v, int32_t zp) {
-    int32_t r = __float2int_rn(v);
-    r = min(max(r, -1024), 1024) + zp;
-    return min(max(r, -128), 127);
-}
-
-__device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
-    return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
-           ((uint32_t)(d & 0xff) << 24);
-}
-
 // Exact-erf GELU in fp32 (the control's activation; reading R8).
 __device__ __forceinline__ float gelu_erf_f32(float y) {
     const float t = erff(__fmul_rn(y, 0.70710678118654752440f));
     return __fmul_rn(__fmul_rn(0.5f, y), __fadd_rn(1.0f, t));
 }
 
-template <int EPI, bool DBG>
+// Q of 16 scaled values v (already multiplied by 1/s): clamp(rne(v) + zq, -128, 127),
+// packed little-endian into 4 words.  zq == 0: F2IP (rne + saturate + pack 2 per
+// instruction; with RELU the max(.,0) folds in as well).  zq != 0: rne saturated to
+// int16, + zq, saturating pack (the zero point is added after rounding, reading R5).
+template <bool RELU, bool ZQNZ>
+__device__ __forceinline__ void quant_pack16(const float (&v)[16], int32_t zq, uint32_t (&w)[4]) {
+    using namespace sm100;
+    if constexpr (!ZQNZ) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int32_t q[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) q[j] = __float2int_rn(RELU ? fmaxf(v[4 * k + j], 0.0f) : v[4 * k + j]);
+            w[k] = pack_sat_s8(q[1], q[0], pack_sat_s8(q[3], q[2], 0u));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int32_t q[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                q[j] = f2i_rn_sat16(v[4 * k + j]) + zq;
+                if (RELU) q[j] = max(q[j], zq);
+            }
+            w[k] = pack_sat_s8(q[1], q[0], pack_sat_s8(q[3], q[2], 0u));
+        }
+    }
+}
+
+template <int EPI, int F>
 __global__ void __launch_bounds__(kThreads, 1)
 mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ GemmArgs p) {
+                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ GemmArgs p) {
     using namespace sm100;
+    constexpr bool HAS_B = (F & kHasB) != 0, HAS_ZC = (F & kHasZc) != 0, ZQNZ = (F & kZqNz) != 0;
+    constexpr bool STATS64 = (F & kS64) != 0;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -136,7 +175,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t bar_tfull = bar_empty + 8u * stages;
     const uint32_t bar_tempty = bar_tfull + 16u;
     const uint32_t bar_x = bar_tempty + 16u;
+    const uint32_t bar_cfull = bar_x + 16u;
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
+    float* consts = reinterpret_cast<float*>(gbase + L.consts);   // [2][kNConst][BN]
     double* red = reinterpret_cast<double*>(gbase + L.red);
     double* xbuf = reinterpret_cast<double*>(gbase + L.xbuf);
 
@@ -147,6 +188,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmO);
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -155,8 +197,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar_tfull + 8u * i, 1);
-            mbar_init(bar_tempty + 8u * i, kEpiThreads / 32);
+            mbar_init(bar_tempty + 8u * i, kEpiWarps);
             mbar_init(bar_x + 8u * i, 1);
+            mbar_init(bar_cfull + 8u * i, 32);
         }
         fence_mbar_init();
     }
@@ -228,6 +271,27 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 mma_commit(bar_tfull + 8u * buf);
             }
         }
+    } else if (warp == 3) {
+        // ============================ column constants ========================
+        uint32_t it = 0;
+        for (int64_t u = cid; u < p.num_units; u += nclus, ++it) {
+            const int ng = (int)(u % p.n_groups);
+            const int n0 = (ng * (int)CS + (int)rank) * BN;
+            const uint32_t buf = it & 1u, aph = (it >> 1) & 1u;
+            mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);     // epilogue done with this buffer
+            float* cb = consts + (size_t)buf * kNConst * BN;
+            for (int c = (int)lane; c < BN; c += 32) {
+                const int n = n0 + c;
+                cb[0 * BN + c] = __ldg(p.m + n);
+                cb[1 * BN + c] = p.b ? __ldg(p.b + n) : 0.0f;
+                cb[2 * BN + c] = p.zc ? __int_as_float(__ldg(p.zc + n)) : __int_as_float(0);
+                if (EPI == EP6_LN) {
+                    cb[3 * BN + c] = __ldg(p.gamma + n);
+                    cb[4 * BN + c] = __ldg(p.beta + n);
+                }
+            }
+            mbar_arrive(bar_cfull + 8u * buf);
+        }
     } else if (warp >= kEpiWarp0) {
         // ============================ epilogue ================================
         const uint32_t ew = warp - kEpiWarp0;
@@ -237,82 +301,136 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int nch = BN / kChunk;
         const int split = (nch + 1) / 2;
         const int ch_lo = half ? split : 0, ch_hi = half ? nch : split;
+        const uint32_t ring = base + L.ring + ew * (kRing * kSlotBytes);
+        uint32_t g = 0;      // ring slots (bulk groups) issued by this warp
+        uint32_t pend = 0;   // chunks staged in the current slot
+        int pend_col0 = 0, pend_col1 = 0;
+        int64_t pend_row = 0;
+
+        // Write the staged chunks ([32 rows][16 B] each) with TMA bulk tensor stores:
+        // one proxy fence and one bulk group per slot of 2 chunks.
+        auto flush = [&]() {
+            if (!pend) return;
+            const uint32_t slot = ring + (g % kRing) * kSlotBytes;
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&tmO, slot, pend_col0, (int32_t)pend_row);
+                if (pend == 2) tma_store_2d(&tmO, slot + kRingBytes, pend_col1, (int32_t)pend_row);
+                bulk_commit();
+            }
+            ++g;
+            pend = 0;
+        };
+        // stage 16 packed int8 columns of this warp's 32 rows
+        auto store_chunk = [&](const uint32_t (&w)[4], int col, int64_t row0) {
+            const uint32_t slot = ring + (g % kRing) * kSlotBytes;
+            if (pend == 0 && g >= (uint32_t)kRing) {
+                if (lane == 0) bulk_wait_read<kRing - 1>();   // the slot's previous stores have read smem
+                __syncwarp();
+            }
+            st_shared_v4(slot + pend * kRingBytes + lane * 16u, w[0], w[1], w[2], w[3]);
+            if (pend == 0) pend_col0 = col; else pend_col1 = col;
+            pend_row = row0;
+            if (++pend == 2) flush();
+        };
+
         uint32_t it = 0;
         for (int64_t u = cid; u < p.num_units; u += nclus, ++it) {
             const int64_t m_tile = u / p.n_groups;
             const int ng = (int)(u % p.n_groups);
             const int n0 = (ng * (int)CS + (int)rank) * BN;
             const uint32_t buf = it & 1u, aph = (it >> 1) & 1u;
+            mbar_wait(bar_cfull + 8u * buf, aph);
             mbar_wait(bar_tfull + 8u * buf, aph);
             tc_fence_after();
             const int64_t row = m_tile * kBM + rit;
+            const int64_t wrow0 = m_tile * kBM + quad * 32u;
             const bool valid = row < p.M;
             const uint32_t tb = tmem_base + ((quad * 32u) << 16) + buf * (uint32_t)BN;
+            const float* cm = consts + (size_t)buf * kNConst * BN;
+            const float* cbias = cm + BN;
+            const int32_t* czc = reinterpret_cast<const int32_t*>(cm + 2 * BN);
+
+            // z (or y) for one 16-column chunk: fl(fmaf(fl(acc - zc), m, b))
+            auto dequant16 = [&](uint32_t (&r)[16], int cl, float (&y)[16]) {
+#pragma unroll
+                for (int j4 = 0; j4 < 4; ++j4) {
+                    const float4 mv = *reinterpret_cast<const float4*>(cm + cl + 4 * j4);
+                    const float mm[4] = {mv.x, mv.y, mv.z, mv.w};
+                    float bb[4] = {0.f, 0.f, 0.f, 0.f};
+                    if constexpr (HAS_B) {
+                        const float4 bv = *reinterpret_cast<const float4*>(cbias + cl + 4 * j4);
+                        bb[0] = bv.x; bb[1] = bv.y; bb[2] = bv.z; bb[3] = bv.w;
+                    }
+                    if constexpr (HAS_ZC) {
+                        const int4 zv = *reinterpret_cast<const int4*>(czc + cl + 4 * j4);
+                        r[4 * j4 + 0] -= (uint32_t)zv.x; r[4 * j4 + 1] -= (uint32_t)zv.y;
+                        r[4 * j4 + 2] -= (uint32_t)zv.z; r[4 * j4 + 3] -= (uint32_t)zv.w;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float a = __int2float_rn((int32_t)r[4 * j4 + j]);
+                        y[4 * j4 + j] = HAS_B ? __fmaf_rn(a, mm[j], bb[j]) : __fmul_rn(a, mm[j]);
+                    }
+                }
+            };
+            auto tap_acc = [&](const uint32_t (&r)[16], int col) {
+                if (p.acc_tap && valid) {
+                    int32_t* trow = p.acc_tap + row * (int64_t)p.ldo + col;
+#pragma unroll
+                    for (int j4 = 0; j4 < 4; ++j4)
+                        st_v4(trow + 4 * j4, make_int4((int)r[4 * j4], (int)r[4 * j4 + 1], (int)r[4 * j4 + 2],
+                                                       (int)r[4 * j4 + 3]));
+                }
+            };
 
             if constexpr (EPI == EP5_RELU || EPI == EP5_GELU) {
-                int8_t* orow = p.out + row * (int64_t)p.ldo + n0;
-                for (int ch = ch_lo; ch < ch_hi; ++ch) {
-                    uint32_t r[16];
-                    tmem_ld16(tb + (uint32_t)(ch * kChunk), r);
-                    tmem_wait_ld();
-                    const int c0 = n0 + ch * kChunk;
-                    int32_t q[16];
+                auto process = [&](uint32_t (&r)[16], int ch) {
+                    const int cl = ch * kChunk;
+                    float y[16];
+                    dequant16(r, cl, y);
+                    tap_acc(r, n0 + cl);
+                    float v[16];
 #pragma unroll
-                    for (int j4 = 0; j4 < 4; ++j4) {
-                        const float4 mv = __ldg(reinterpret_cast<const float4*>(p.m + c0) + j4);
-                        const float4 bv = p.b ? __ldg(reinterpret_cast<const float4*>(p.b + c0) + j4)
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
-                        const int4 zv = p.zc ? __ldg(reinterpret_cast<const int4*>(p.zc + c0) + j4)
-                                             : make_int4(0, 0, 0, 0);
-                        const float mm[4] = {mv.x, mv.y, mv.z, mv.w};
-                        const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
-                        const int32_t zz[4] = {zv.x, zv.y, zv.z, zv.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int32_t acc = (int32_t)r[j4 * 4 + j] - zz[j];
-                            r[j4 * 4 + j] = (uint32_t)acc;
-                            const float y = __fmaf_rn(__int2float_rn(acc), mm[j], bb[j]);
-                            float v;
-                            if constexpr (EPI == EP5_RELU) v = __fmul_rn(fmaxf(y, 0.0f), p.inv_q);
-                            else v = __fmul_rn(gelu_erf_f32(y), p.inv_q);
-                            q[j4 * 4 + j] = quant_rne(v, p.zq);
-                        }
+                    for (int j = 0; j < 16; ++j) {
+                        if constexpr (EPI == EP5_RELU) v[j] = __fmul_rn(y[j], p.inv_q);   // ReLU folded into the pack
+                        else v[j] = __fmul_rn(gelu_erf_f32(y[j]), p.inv_q);
                     }
-                    if (valid) {
-                        int4 pk;
-                        pk.x = (int)pack4(q[0], q[1], q[2], q[3]);
-                        pk.y = (int)pack4(q[4], q[5], q[6], q[7]);
-                        pk.z = (int)pack4(q[8], q[9], q[10], q[11]);
-                        pk.w = (int)pack4(q[12], q[13], q[14], q[15]);
-                        st_v4(orow + ch * kChunk, pk);
-                        if (DBG && p.acc_tap) {
-                            int32_t* trow = p.acc_tap + row * (int64_t)p.ldo + c0;
-#pragma unroll
-                            for (int j4 = 0; j4 < 4; ++j4)
-                                st_v4(trow + 4 * j4, make_int4((int)r[4 * j4], (int)r[4 * j4 + 1],
-                                                               (int)r[4 * j4 + 2], (int)r[4 * j4 + 3]));
-                        }
-                    }
+                    uint32_t w[4];
+                    quant_pack16<EPI == EP5_RELU, ZQNZ>(v, p.zq, w);
+                    store_chunk(w, n0 + cl, wrow0);
+                };
+                uint32_t ra[16], rb[16];
+                int ch = ch_lo;
+                if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
+                while (ch < ch_hi) {
+                    tmem_wait_ld_dep(ra);
+                    if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
+                    process(ra, ch);
+                    if (++ch >= ch_hi) break;
+                    tmem_wait_ld_dep(rb);
+                    if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
+                    process(rb, ch);
+                    ++ch;
                 }
             } else {
                 // ---------------- fused op #6: dQ, bias, +residual, LayerNorm, Q ----------------
                 const int C = p.ldo;
-                // pass 1: z = fl(fmaf(fl(A2), m2, b2) + r); park z in TMEM; row sum in double
-                double s1 = 0.0;
-                for (int ch = ch_lo; ch < ch_hi; ++ch) {
-                    uint32_t r[16];
-                    tmem_ld16(tb + (uint32_t)(ch * kChunk), r);
-                    const int c0 = n0 + ch * kChunk;
-                    float rr[16];
+                using acc_t = typename std::conditional<STATS64, double, float>::type;
+                // pass 1: z = fl(fl(fmaf(fl(A2), m2, b2)) + r); park z in TMEM; row sum
+                acc_t s1 = 0;
+                auto load_resid = [&](int ch, float (&rr)[16]) {
+                    const int col = n0 + ch * kChunk;
                     if (p.resid) {
 #pragma unroll
                         for (int j4 = 0; j4 < 4; ++j4) {
-                            float4 v = valid ? __ldg(reinterpret_cast<const float4*>(p.resid + row * C + c0) + j4)
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                            const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(p.resid + row * C + col) + j4)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
                             rr[4 * j4] = v.x; rr[4 * j4 + 1] = v.y; rr[4 * j4 + 2] = v.z; rr[4 * j4 + 3] = v.w;
                         }
                     } else {
-                        int4 xv = valid ? ld_nc_v4(p.x + row * C + c0) : make_int4(0, 0, 0, 0);
+                        const int4 xv = valid ? ld_nc_v4(p.x + row * C + col) : make_int4(0, 0, 0, 0);
                         const uint32_t xw[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
@@ -320,132 +438,162 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             rr[j] = __fmul_rn(__int2float_rn(xi - p.z_x), p.s_x);
                         }
                     }
-                    tmem_wait_ld();
+                };
+                auto pass1 = [&](uint32_t (&r)[16], int ch) {
+                    const int cl = ch * kChunk;
+                    float rr[16];
+                    load_resid(ch, rr);
                     float z[16];
+                    dequant16(r, cl, z);
+                    tap_acc(r, n0 + cl);
 #pragma unroll
-                    for (int j4 = 0; j4 < 4; ++j4) {
-                        const float4 mv = __ldg(reinterpret_cast<const float4*>(p.m + c0) + j4);
-                        const float4 bv = p.b ? __ldg(reinterpret_cast<const float4*>(p.b + c0) + j4)
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
-                        const int4 zv = p.zc ? __ldg(reinterpret_cast<const int4*>(p.zc + c0) + j4)
-                                             : make_int4(0, 0, 0, 0);
-                        const float mm[4] = {mv.x, mv.y, mv.z, mv.w};
-                        const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
-                        const int32_t zz[4] = {zv.x, zv.y, zv.z, zv.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int jj = j4 * 4 + j;
-                            const int32_t acc = (int32_t)r[jj] - zz[j];
-                            r[jj] = (uint32_t)acc;
-                            const float d = __fmaf_rn(__int2float_rn(acc), mm[j], bb[j]);
-                            z[jj] = __fadd_rn(d, rr[jj]);
-                            s1 = __dadd_rn(s1, (double)z[jj]);
-                        }
-                    }
-                    if (DBG && p.acc_tap) {
-                        if (valid) {
-                            int32_t* trow = p.acc_tap + row * (int64_t)C + c0;
-#pragma unroll
-                            for (int j4 = 0; j4 < 4; ++j4)
-                                st_v4(trow + 4 * j4, make_int4((int)r[4 * j4], (int)r[4 * j4 + 1],
-                                                               (int)r[4 * j4 + 2], (int)r[4 * j4 + 3]));
-                        }
+                    for (int j = 0; j < 16; ++j) {
+                        z[j] = __fadd_rn(z[j], rr[j]);
+                        if constexpr (STATS64) s1 = __dadd_rn(s1, (double)z[j]);
+                        else s1 = __fadd_rn(s1, z[j]);
+                        r[j] = __float_as_uint(z[j]);
                     }
                     if (p.resid_out && valid) {
-                        float* zrow = p.resid_out + row * (int64_t)C + c0;
+                        float* zrow = p.resid_out + row * (int64_t)C + n0 + cl;
 #pragma unroll
                         for (int j4 = 0; j4 < 4; ++j4)
                             *reinterpret_cast<float4*>(zrow + 4 * j4) =
                                 make_float4(z[4 * j4], z[4 * j4 + 1], z[4 * j4 + 2], z[4 * j4 + 3]);
                     }
-                    uint32_t zb[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) zb[j] = __float_as_uint(z[j]);
-                    tmem_st16(tb + (uint32_t)(ch * kChunk), zb);
+                    tmem_st16(tb + (uint32_t)cl, r);
+                };
+                {
+                    uint32_t ra[16], rb[16];
+                    int ch = ch_lo;
+                    if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
+                    while (ch < ch_hi) {
+                        tmem_wait_ld_dep(ra);
+                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
+                        pass1(ra, ch);
+                        if (++ch >= ch_hi) break;
+                        tmem_wait_ld_dep(rb);
+                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
+                        pass1(rb, ch);
+                        ++ch;
+                    }
                 }
                 tmem_wait_st();
 
                 // row statistics: halves via smem, CTAs of the cluster via DSMEM (rank order)
-                auto combine = [&](double v, int pass) -> double {
-                    red[(pass * 2 + (int)half) * kBM + rit] = v;
+                auto combine = [&](acc_t v, int pass) -> acc_t {
+                    red[(pass * 2 + (int)half) * kBM + rit] = (double)v;
                     named_bar_sync(1, kEpiThreads);
-                    const double t = __dadd_rn(red[(pass * 2 + 0) * kBM + rit], red[(pass * 2 + 1) * kBM + rit]);
+                    const acc_t t = (acc_t)red[(pass * 2 + 0) * kBM + rit] + (acc_t)red[(pass * 2 + 1) * kBM + rit];
                     if (CS == 1) return t;
                     const uint32_t xb = bar_x + 8u * (uint32_t)pass;
                     if (half == 0) {
                         if (ew == 0 && lane == 0) mbar_arrive_expect_tx(xb, CS * kBM * 8u);
                         const uint32_t slot = smem_u32(xbuf + ((size_t)pass * CS + rank) * kBM + rit);
-                        for (uint32_t r = 0; r < CS; ++r) st_async_f64(mapa(slot, r), t, mapa(xb, r));
+                        for (uint32_t r = 0; r < CS; ++r) st_async_f64(mapa(slot, r), (double)t, mapa(xb, r));
                     }
                     mbar_wait_cluster(xb, it & 1u);
-                    double S = 0.0;
-                    for (uint32_t r = 0; r < CS; ++r) S = __dadd_rn(S, xbuf[((size_t)pass * CS + r) * kBM + rit]);
+                    acc_t S = 0;
+                    for (uint32_t r = 0; r < CS; ++r) S = S + (acc_t)xbuf[((size_t)pass * CS + r) * kBM + rit];
                     return S;
                 };
-                const double S = combine(s1, 0);
-                const double mu = __ddiv_rn(S, (double)C);
+                const acc_t S = combine(s1, 0);
+                const acc_t mu = S / (acc_t)C;
 
                 // pass 2: centred sum of squares
-                double s2 = 0.0;
-                for (int ch = ch_lo; ch < ch_hi; ++ch) {
-                    uint32_t r[16];
-                    tmem_ld16(tb + (uint32_t)(ch * kChunk), r);
-                    tmem_wait_ld();
+                acc_t s2 = 0;
+                {
+                    auto pass2 = [&](const uint32_t (&r)[16]) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const double dz = __dsub_rn((double)__uint_as_float(r[j]), mu);
-                        s2 = __dadd_rn(s2, __dmul_rn(dz, dz));
+                        for (int j = 0; j < 16; ++j) {
+                            if constexpr (STATS64) {
+                                const double dz = __dsub_rn((double)__uint_as_float(r[j]), mu);
+                                s2 = __dadd_rn(s2, __dmul_rn(dz, dz));
+                            } else {
+                                const float dz = __fsub_rn(__uint_as_float(r[j]), mu);
+                                s2 = __fmaf_rn(dz, dz, s2);
+                            }
+                        }
+                    };
+                    uint32_t ra[16], rb[16];
+                    int ch = ch_lo;
+                    if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
+                    while (ch < ch_hi) {
+                        tmem_wait_ld_dep(ra);
+                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
+                        pass2(ra);
+                        if (++ch >= ch_hi) break;
+                        tmem_wait_ld_dep(rb);
+                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
+                        pass2(rb);
+                        ++ch;
                     }
                 }
-                const double SS = combine(s2, 1);
-                const double var = __ddiv_rn(SS, (double)C);
-                const double rstd = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, p.eps)));
+                const acc_t SS = combine(s2, 1);
+                acc_t rstd;
+                if constexpr (STATS64) rstd = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(SS, (double)C), (double)p.eps)));
+                else rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(SS, (float)C), p.eps)));
 
                 // pass 3: yhat = fl(((z-mu)*rstd)*gamma + beta); Y = Q_y(yhat)
-                int8_t* orow = p.out + row * (int64_t)C;
-                for (int ch = ch_lo; ch < ch_hi; ++ch) {
-                    uint32_t r[16];
-                    tmem_ld16(tb + (uint32_t)(ch * kChunk), r);
-                    const int c0 = n0 + ch * kChunk;
-                    float gm[16], bt[16];
-#pragma unroll
-                    for (int j4 = 0; j4 < 4; ++j4) {
-                        const float4 g = __ldg(reinterpret_cast<const float4*>(p.gamma + c0) + j4);
-                        const float4 b = __ldg(reinterpret_cast<const float4*>(p.beta + c0) + j4);
-                        gm[4 * j4] = g.x; gm[4 * j4 + 1] = g.y; gm[4 * j4 + 2] = g.z; gm[4 * j4 + 3] = g.w;
-                        bt[4 * j4] = b.x; bt[4 * j4 + 1] = b.y; bt[4 * j4 + 2] = b.z; bt[4 * j4 + 3] = b.w;
-                    }
-                    tmem_wait_ld();
-                    int32_t q[16];
+                const float* cg = cm + 3 * BN;
+                const float* cbt = cm + 4 * BN;
+                auto pass3 = [&](const uint32_t (&r)[16], int ch) {
+                    const int cl = ch * kChunk;
                     float yh[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const double xh = __dmul_rn(__dsub_rn((double)__uint_as_float(r[j]), mu), rstd);
-                        const double yv = __dadd_rn(__dmul_rn(xh, (double)gm[j]), (double)bt[j]);
-                        yh[j] = __double2float_rn(yv);
-                        q[j] = quant_rne(__fmul_rn(yh[j], p.inv_q), p.zq);
-                    }
-                    if (valid) {
-                        int4 pk;
-                        pk.x = (int)pack4(q[0], q[1], q[2], q[3]);
-                        pk.y = (int)pack4(q[4], q[5], q[6], q[7]);
-                        pk.z = (int)pack4(q[8], q[9], q[10], q[11]);
-                        pk.w = (int)pack4(q[12], q[13], q[14], q[15]);
-                        st_v4(orow + c0, pk);
-                        if (DBG && p.ln_tap) {
-                            float* lrow = p.ln_tap + row * (int64_t)C + c0;
+                    for (int j4 = 0; j4 < 4; ++j4) {
+                        const float4 gv = *reinterpret_cast<const float4*>(cg + cl + 4 * j4);
+                        const float4 bv = *reinterpret_cast<const float4*>(cbt + cl + 4 * j4);
+                        const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+                        const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-                            for (int j4 = 0; j4 < 4; ++j4)
-                                *reinterpret_cast<float4*>(lrow + 4 * j4) =
-                                    make_float4(yh[4 * j4], yh[4 * j4 + 1], yh[4 * j4 + 2], yh[4 * j4 + 3]);
+                        for (int j = 0; j < 4; ++j) {
+                            const float zf = __uint_as_float(r[4 * j4 + j]);
+                            if constexpr (STATS64) {
+                                const double xh = __dmul_rn(__dsub_rn((double)zf, mu), rstd);
+                                yh[4 * j4 + j] = __double2float_rn(__dadd_rn(__dmul_rn(xh, (double)gg[j]), (double)bb[j]));
+                            } else {
+                                const float xh = __fmul_rn(__fsub_rn(zf, mu), rstd);
+                                yh[4 * j4 + j] = __fmaf_rn(xh, gg[j], bb[j]);
+                            }
                         }
+                    }
+                    float v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(yh[j], p.inv_q);
+                    uint32_t w[4];
+                    quant_pack16<false, ZQNZ>(v, p.zq, w);
+                    store_chunk(w, n0 + cl, wrow0);
+                    if (p.ln_tap && valid) {
+                        float* lrow = p.ln_tap + row * (int64_t)C + n0 + cl;
+#pragma unroll
+                        for (int j4 = 0; j4 < 4; ++j4)
+                            *reinterpret_cast<float4*>(lrow + 4 * j4) =
+                                make_float4(yh[4 * j4], yh[4 * j4 + 1], yh[4 * j4 + 2], yh[4 * j4 + 3]);
+                    }
+                };
+                {
+                    uint32_t ra[16], rb[16];
+                    int ch = ch_lo;
+                    if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
+                    while (ch < ch_hi) {
+                        tmem_wait_ld_dep(ra);
+                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
+                        pass3(ra, ch);
+                        if (++ch >= ch_hi) break;
+                        tmem_wait_ld_dep(rb);
+                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
+                        pass3(rb, ch);
+                        ++ch;
                     }
                 }
             }
+            flush();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_tempty + 8u * buf);
         }
+        if (lane == 0) bulk_wait_all();   // output stores complete before the CTA retires
+        __syncwarp();
     }
 
     // teardown: no CTA leaves while a peer may still address its shared memory

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/swin_mlp_int8.h"
@@ -41,8 +42,10 @@ swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
                         "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
     } while (0)
 
+
 // One GEMM+epilogue launch plan.
 struct Plan {
+    void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
     int BN = 0, CS = 1, stages = 0, n_groups = 1;
     uint32_t smem = 0;
     int max_clusters = 0;
@@ -66,15 +69,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // {128 B along K, box_rows} box and 128-byte swizzle; out-of-range rows and
 // columns read as zero (ragged T and K tails).
 swin_mlp_status_t encode_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
-                            uint32_t box_rows) {
+                            uint32_t box_rows, uint32_t box_cols = kBK,
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto fn = encode_fn();
     if (!fn) return fail(SWIN_MLP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld};
-    cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t es[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(SWIN_MLP_ECUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld box_rows=%u", (int)r,
@@ -84,18 +88,28 @@ swin_mlp_status_t encode_2d(CUtensorMap* map, const void* ptr, int64_t rows, int
 
 constexpr uint32_t kSmemBudget = 227 * 1024;
 
-template <int EPI, bool DBG>
-swin_mlp_status_t prepare_kernel(const Plan& pl) {
-    auto k = mlp_gemm_kernel<EPI, DBG>;
-    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    return SWIN_MLP_OK;
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
+
+template <int EPI, int... Fs>
+KernelFn pick(int f, std::integer_sequence<int, Fs...>) {
+    static const KernelFn table[] = {mlp_gemm_kernel<EPI, Fs>...};
+    return table[f];
 }
 
-template <int EPI>
-swin_mlp_status_t prepare_all(Plan& pl, int num_sms) {
-    swin_mlp_status_t st;
-    if ((st = prepare_kernel<EPI, false>(pl)) != SWIN_MLP_OK) return st;
-    if ((st = prepare_kernel<EPI, true>(pl)) != SWIN_MLP_OK) return st;
+// The kernel specialised for one layer's flags (bias present, activation zero
+// point, output zero point, LN precision) — no predicated-off work in the hot loop.
+KernelFn kernel_for(int epi, int flags) {
+    switch (epi) {
+        case EP5_RELU: return pick<EP5_RELU>(flags & 7, std::make_integer_sequence<int, 8>{});
+        case EP5_GELU: return pick<EP5_GELU>(flags & 7, std::make_integer_sequence<int, 8>{});
+        default: return pick<EP6_LN>(flags & 15, std::make_integer_sequence<int, 16>{});
+    }
+}
+
+swin_mlp_status_t prepare(Plan& pl, int num_sms) {
+    // The attribute is per kernel function (process-wide), shared by every handle:
+    // always grant the full budget so one layer's plan never shrinks another's.
+    CUDA_TRY(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.CS);
     cfg.blockDim = dim3(kThreads);
@@ -108,7 +122,7 @@ swin_mlp_status_t prepare_all(Plan& pl, int num_sms) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, mlp_gemm_kernel<EPI, false>, &cfg);
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, pl.fn, &cfg);
     if (e != cudaSuccess || n <= 0) {
         cudaGetLastError();
         n = num_sms / pl.CS;
@@ -148,9 +162,8 @@ bool make_plan(int N, bool full_row, Plan& pl) {
     return pl.smem <= kSmemBudget;
 }
 
-template <int EPI, bool DBG>
-swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
-                         cudaStream_t stream) {
+swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
+                         const GemmArgs& a, cudaStream_t stream) {
     const int64_t units = a.num_units;
     int64_t clusters = units < pl.max_clusters ? units : pl.max_clusters;
     if (clusters < 1) clusters = 1;
@@ -166,7 +179,7 @@ swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMa
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, mlp_gemm_kernel<EPI, DBG>, ta, tb, a));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, pl.fn, ta, tb, to, a));
     return SWIN_MLP_OK;
 }
 
@@ -186,8 +199,13 @@ struct swin_mlp_int8_s {
     float inv_h = 0.f, inv_y = 0.f;
     CUtensorMap tm_w1, tm_w2;
     std::vector<void*> allocs;
+    // native profiling (bench roofline): event triples per recorded run
+    bool prof_on = false;
+    int prof_max = 0, prof_n = 0;
+    std::vector<cudaEvent_t> prof_ev;
     ~swin_mlp_int8_s() {
         for (void* p : allocs) cudaFree(p);
+        for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     }
 };
 
@@ -352,9 +370,12 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     if (d.h_zero_point) H_TRY(upload(h, zc2, &h->zc2));
     H_TRY(encode_2d(&h->tm_w1, h->w1, H, C, C, (uint32_t)h->p1.BN));
     H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H, (uint32_t)h->p2.BN));
-    if (d.act == SWIN_MLP_ACT_RELU) H_TRY(prepare_all<EP5_RELU>(h->p1, h->num_sms));
-    else H_TRY(prepare_all<EP5_GELU>(h->p1, h->num_sms));
-    H_TRY(prepare_all<EP6_LN>(h->p2, h->num_sms));
+    h->p1.fn = kernel_for(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU,
+                          (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (d.h_zero_point ? kZqNz : 0));
+    h->p2.fn = kernel_for(EP6_LN, (d.b2 ? kHasB : 0) | (d.h_zero_point ? kHasZc : 0) |
+                                      (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0));
+    H_TRY(prepare(h->p1, h->num_sms));
+    H_TRY(prepare(h->p2, h->num_sms));
 #undef H_TRY
     *out = h;
     return SWIN_MLP_OK;
@@ -384,37 +405,37 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int8_t* hq = static_cast<int8_t*>(workspace);
 
-    CUtensorMap tm_x, tm_h;
+    CUtensorMap tm_x, tm_h, tm_ho, tm_y;
     ST_TRY(encode_2d(&tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
     ST_TRY(encode_2d(&tm_h, hq, T, H, H, (uint32_t)(kBM / h->p2.CS)));
+    // epilogue output maps: [32 rows][16 B] boxes, no swizzle (one warp's chunk)
+    ST_TRY(encode_2d(&tm_ho, hq, T, H, H, 32, kChunk, CU_TENSOR_MAP_SWIZZLE_NONE));
+    ST_TRY(encode_2d(&tm_y, y, T, C, C, 32, kChunk, CU_TENSOR_MAP_SWIZZLE_NONE));
     const int64_t m_tiles = (T + kBM - 1) / kBM;
 
     GemmArgs a1 = {};
     a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages;
     a1.n_groups = h->p1.n_groups; a1.num_units = m_tiles * h->p1.n_groups; a1.ldo = H;
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
-    a1.out = hq; a1.acc_tap = acc1;
+    a1.acc_tap = dbg ? acc1 : nullptr;
 
     GemmArgs a2 = {};
     a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages;
     a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
-    a2.out = y; a2.x = x; a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
+    a2.x = x; a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
     a2.resid = residual; a2.resid_out = residual_out;
-    a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = (double)h->d.ln_eps;
-    a2.acc_tap = acc2; a2.ln_tap = ln_out;
+    a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
+    a2.acc_tap = dbg ? acc2 : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
 
-    const bool dbg1 = dbg && acc1, dbg2 = dbg && (acc2 || ln_out);
-    if (h->d.act == SWIN_MLP_ACT_RELU) {
-        ST_TRY(dbg1 ? launch<EP5_RELU, true>(h->p1, tm_x, h->tm_w1, a1, s)
-                    : launch<EP5_RELU, false>(h->p1, tm_x, h->tm_w1, a1, s));
-    } else {
-        ST_TRY(dbg1 ? launch<EP5_GELU, true>(h->p1, tm_x, h->tm_w1, a1, s)
-                    : launch<EP5_GELU, false>(h->p1, tm_x, h->tm_w1, a1, s));
-    }
+    cudaEvent_t* ev = nullptr;
+    if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+    ST_TRY(launch(h->p1, tm_x, h->tm_w1, tm_ho, a1, s));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
     if (dbg && hidden) CUDA_TRY(cudaMemcpyAsync(hidden, hq, (size_t)T * H, cudaMemcpyDeviceToDevice, s));
-    ST_TRY(dbg2 ? launch<EP6_LN, true>(h->p2, tm_h, h->tm_w2, a2, s)
-                : launch<EP6_LN, false>(h->p2, tm_h, h->tm_w2, a2, s));
+    ST_TRY(launch(h->p2, tm_h, h->tm_w2, tm_y, a2, s));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
     return SWIN_MLP_OK;
 }
 
@@ -474,6 +495,42 @@ swin_mlp_status_t swin_mlp_int8_get_constants(swin_mlp_int8_t h, float* m1, floa
     if (wsum2) std::memcpy(wsum2, h->hws2.data(), h->hws2.size() * sizeof(int32_t));
     if (inv_h) *inv_h = h->inv_h;
     if (inv_y) *inv_y = h->inv_y;
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_mlp_int8_profile_begin(swin_mlp_int8_t h, int32_t max_runs) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (max_runs < 0) return fail(SWIN_MLP_EINVAL, "max_runs < 0");
+    DeviceGuard guard(h->device);
+    while ((int)h->prof_ev.size() < 3 * max_runs) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        h->prof_ev.push_back(e);
+    }
+    h->prof_max = max_runs;
+    h->prof_n = 0;
+    h->prof_on = true;
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, float* fc2_ms, int32_t* runs) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    DeviceGuard guard(h->device);
+    float t1 = 0.f, t2 = 0.f;
+    for (int i = 0; i < h->prof_n; ++i) {
+        cudaEvent_t* ev = &h->prof_ev[3 * (size_t)i];
+        CUDA_TRY(cudaEventSynchronize(ev[2]));
+        float a = 0.f, b = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        CUDA_TRY(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        t1 += a;
+        t2 += b;
+    }
+    if (fc1_ms) *fc1_ms = t1;
+    if (fc2_ms) *fc2_ms = t2;
+    if (runs) *runs = h->prof_n;
+    h->prof_on = false;
+    h->prof_n = 0;
     return SWIN_MLP_OK;
 }
 

@@ -48,11 +48,11 @@ def _tier_yhat(got, ref, what="yhat"):
     assert (err <= tol).all(), f"{what}: max rel err {(err / tol).max() * 1e-5:.3e}"
 
 
-def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True):
+def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True, ln_fp64=False):
     from paper_2402_01169_b200 import SwinMlpInt8Layer
     X = synth.make_activations(L, T, x_seed)
     R = synth.make_residual(T, L.C, x_seed + 1) if resid else None
-    layer = SwinMlpInt8Layer(L, device=0)
+    layer = SwinMlpInt8Layer(L, device=0, ln_fp64=ln_fp64)
     xd = torch.from_numpy(X).to(dev)
     rd = torch.from_numpy(R).to(dev) if resid else None
     zo = torch.empty((T, L.C), dtype=torch.float32, device=dev)
@@ -75,6 +75,9 @@ def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True):
     np.testing.assert_array_equal(g["z"], z, err_msg="z (pre-LN sum) not bit-exact")
     _tier_yhat(g["yhat"], yh)
     flips = _tier_int8(g["y"], Y, what="Y")
+    if ln_fp64:
+        # fp64 statistics in the oracle's op order: only the row-sum order differs
+        np.testing.assert_array_equal(g["y"], Y, err_msg="Y (ln_fp64) not bit-exact")
     # the production (non-debug) kernels give the same Y
     y2 = layer(xd, residual=rd)
     torch.cuda.synchronize()
@@ -90,6 +93,12 @@ def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True):
 def test_parity_relu_paper_mode(dev, C, T):
     """The paper's GELU-less block: ReLU, no FC1 bias, symmetric zero points."""
     _run_and_check(dev, _layer(C, 1000 + C), T)
+
+
+@pytest.mark.parametrize("C,T", [(96, 1000), (256, 129), (384, 200), (768, 257), (1536, 129)])
+def test_parity_relu_ln_fp64(dev, C, T):
+    """ln_fp64 = 1: LayerNorm statistics and normalisation in fp64, the oracle's order (O5)."""
+    _run_and_check(dev, _layer(C, 1000 + C), T, ln_fp64=True)
 
 
 @pytest.mark.parametrize("C,T", [(96, 513), (384, 130), (768, 129)])
@@ -189,3 +198,16 @@ def test_full_size_config2_sampled(dev):
                                          rng.integers(0, T, 1500)]))
         ref = oracle.mlp(L, X, rows=rows)
         _tier_int8(y[rows], ref, what=f"config2 C={L.C} sampled rows")
+
+
+def test_multiple_handles_interleaved(dev):
+    """Handles of different shapes coexist: create all first, then run in any order
+    (regression: a per-kernel launch attribute set by one handle must not break another)."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    Ls = [_layer(C, 9000 + C) for C in (768, 96, 1536, 192)]
+    layers = [SwinMlpInt8Layer(L, device=0) for L in Ls]
+    for L, layer in list(zip(Ls, layers))[::-1]:
+        X = synth.make_activations(L, 150, 4)
+        y = layer(torch.from_numpy(X).to(dev)).cpu().numpy()
+        torch.cuda.synchronize()
+        _tier_int8(y, oracle.mlp(L, X), what=f"C={L.C}")
