@@ -151,6 +151,15 @@ int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h);
 swin_mlp_status_t swin_mlp_int8_profile_begin(swin_mlp_int8_t h, int32_t max_runs);
 swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, float* fc2_ms, int32_t* runs);
 
+/* Pipeline tracing (debug): while set, every run makes CTA `cta` of each
+ * kernel record %globaltimer stamps (ns) into the device buffer `trace`
+ * (8192 uint64: FC1 at [0, 4096), FC2 at [4096, 8192); within a kernel
+ * trace[role*1024 + 2*i + {0,1}] for its i-th tile, roles 0 TMA producer
+ * (first stage acquired, last k-block issued), 1 MMA (accumulator acquired,
+ * tile committed), 2 epilogue (accumulator ready, tile stored), 3 constant
+ * loader (buffer acquired, constants published)).  trace = NULL disables. */
+swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_t cta);
+
 /* Introspection: the launch plan of this layer, out8[8] = {FC1 BN, FC1 cluster size,
  * FC1 stages, FC1 max co-resident clusters, FC2 BN, FC2 cluster size, FC2 stages,
  * FC2 max clusters}.  Returns 0, or -1 on a NULL argument. */

@@ -29,7 +29,7 @@ EXPORTS = [
     "swin_mlp_int8_create", "swin_mlp_int8_workspace_bytes", "swin_mlp_int8_run",
     "swin_mlp_int8_run_debug", "swin_mlp_int8_host_workspace_bytes", "swin_mlp_int8_run_host",
     "swin_mlp_int8_get_constants", "swin_mlp_int8_launches_per_run", "swin_mlp_int8_plan",
-    "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end",
+    "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end", "swin_mlp_int8_set_trace",
     "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
 ]
 
@@ -87,6 +87,8 @@ def lib():
     L.swin_mlp_int8_profile_begin.restype = i32
     L.swin_mlp_int8_profile_end.argtypes = [P, P, P, P]
     L.swin_mlp_int8_profile_end.restype = i32
+    L.swin_mlp_int8_set_trace.argtypes = [P, P, i32]
+    L.swin_mlp_int8_set_trace.restype = i32
     L.swin_mlp_int8_destroy.argtypes = [P]
     L.swin_mlp_int8_destroy.restype = i32
     L.swin_mlp_int8_last_error.argtypes = []
@@ -201,6 +203,10 @@ class SwinMlpInt8Layer:
         lib().swin_mlp_int8_plan(self.handle, out)
         return {"fc1_bn": out[0], "fc1_cs": out[1], "fc1_stages": out[2], "fc1_max_clusters": out[3],
                 "fc2_bn": out[4], "fc2_cs": out[5], "fc2_stages": out[6], "fc2_max_clusters": out[7]}
+
+    def set_trace(self, buf=None, cta=0):
+        """buf: int64 device tensor of >= 8192 elements (see swin_mlp_int8_set_trace), or None."""
+        _check(lib().swin_mlp_int8_set_trace(self.handle, _ptr(buf), int(cta)))
 
     def profile_begin(self, max_runs):
         _check(lib().swin_mlp_int8_profile_begin(self.handle, int(max_runs)))

@@ -54,14 +54,15 @@ enum Epi : int { EP5_RELU = 0, EP5_GELU = 1, EP6_LN = 2 };
 
 constexpr int kBM = 128;             // rows per tile (UMMA M, TMEM lanes)
 constexpr int kBK = 128;             // K bytes per pipeline stage (one 128-B swizzle row)
-constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
-constexpr int kEpiThreads = 256;
-constexpr int kEpiWarps = 8;
+// Epilogue width per kernel: the op-#5 epilogue is light (few registers), so it
+// runs 16 warps (4 per SMSP, 4 column parts per TMEM lane quadrant); op #6 keeps
+// 8 warps (2 parts) for its register-heavy LayerNorm passes.
+__host__ __device__ constexpr int epi_warps(int epi) { return epi == 2 ? 8 : 16; }
+__host__ __device__ constexpr int kernel_threads(int epi) { return 32 * (kEpiWarp0 + epi_warps(epi)); }
 constexpr int kChunk = 16;           // columns per tcgen05.ld (32x32b.x16)
-constexpr int kRing = 4;             // output staging chunks per epilogue warp
-constexpr int kRingBytes = 32 * kChunk;   // [32 rows][16 B] = one chunk
-constexpr int kSlotBytes = 2 * kRingBytes; // a ring slot holds 2 chunks (one fence + bulk group)
+constexpr int kChunkBytes = 32 * kChunk;        // [32 rows][16 B] = one warp's output chunk
+
 constexpr int kHasB = 1, kHasZc = 2, kZqNz = 4, kS64 = 8;
 constexpr int kNConst = 5;           // m, b, zc, gamma, beta
 
@@ -71,6 +72,8 @@ struct GemmArgs {
     int32_t BN;            // columns per CTA tile (UMMA N)
     int32_t CS;            // CTAs per cluster (share one m-tile, A multicast)
     int32_t stages;        // smem ring depth
+    int32_t nbuf;          // output staging tiles (1 or 2)
+    int32_t out_w;         // output TMA box width in bytes (128/64/32/16; swizzle of the same width)
     int32_t n_groups;      // column groups of CS*BN columns
     int64_t num_units;     // m_tiles * n_groups
     int32_t ldo;           // columns of the output (= N total)
@@ -91,20 +94,34 @@ struct GemmArgs {
     // debug taps
     int32_t* acc_tap;      // [M][ldo] int32 accumulators (incl. zero-point term)
     float* ln_tap;         // [M][ldo] fp32 yhat (EP6)
+    // pipeline trace (debug): when non-null, CTA `trace_cta` records %globaltimer
+    // stamps: trace[role*1024 + 2*i + {0,1}] for its i-th tile, roles 0 producer
+    // (first stage acquired, last k-block issued), 1 MMA (accumulator acquired,
+    // tile committed), 2 epilogue warp 4 (accumulator ready, tile stored), 3 the
+    // constant loader (buffer acquired, constants published).
+    unsigned long long* trace;
+    int32_t trace_cta;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct SmemLayout {
     uint32_t a, b, ring, consts, bars, tmem_slot, red, xbuf, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(int BN, int CS, int stages) {
+// nbuf: output staging buffers per epilogue warp (1 or 2 tiles in flight)
+__host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int stages, int nbuf) {
     SmemLayout L;
     L.a = 0;
     L.b = L.a + (uint32_t)stages * kBM * kBK;
     L.ring = L.b + (uint32_t)stages * (uint32_t)BN * kBK;
-    L.consts = L.ring + (uint32_t)kEpiWarps * kRing * kSlotBytes;
+    L.consts = L.ring + (uint32_t)nbuf * (uint32_t)BN * kBM;
     L.bars = L.consts + 2u * kNConst * (uint32_t)BN * 4u;
-    const uint32_t nbars = 2u * stages + 2 + 2 + 2 + 2;
+    const uint32_t nbars = 2u * stages + 2 + 2 + 2 + 2 + 2 + 2;
     L.tmem_slot = L.bars + 8u * nbars;
     L.red = (L.tmem_slot + 8 + 15) & ~15u;
     L.xbuf = L.red + 2u * 2u * kBM * 8u;
@@ -154,9 +171,10 @@ __device__ __forceinline__ void quant_pack16(const float (&v)[16], int32_t zq, u
 }
 
 template <int EPI, int F>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kernel_threads(EPI), 1)
 mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ GemmArgs p) {
+                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ GemmArgs p) {
     using namespace sm100;
     constexpr bool HAS_B = (F & kHasB) != 0, HAS_ZC = (F & kHasZc) != 0, ZQNZ = (F & kZqNz) != 0;
     constexpr bool STATS64 = (F & kS64) != 0;
@@ -168,7 +186,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int BN = p.BN;
     const uint32_t CS = (uint32_t)p.CS;
     const int stages = p.stages;
-    const SmemLayout L = smem_layout(BN, p.CS, stages);
+    constexpr int kEpiWarps = epi_warps(EPI), kEpiThreads = 32 * kEpiWarps, kParts = kEpiWarps / 4;
+    const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.nbuf);
     const uint32_t sA = base + L.a, sB = base + L.b;
     const uint32_t bar_full = base + L.bars;
     const uint32_t bar_empty = bar_full + 8u * stages;
@@ -176,6 +195,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t bar_tempty = bar_tfull + 16u;
     const uint32_t bar_x = bar_tempty + 16u;
     const uint32_t bar_cfull = bar_x + 16u;
+    const uint32_t bar_sfull = bar_cfull + 16u;     // output tile staged (count: epilogue warps)
+    const uint32_t bar_sfree = bar_sfull + 16u;     // staging buffer reusable (count 1)
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
     float* consts = reinterpret_cast<float*>(gbase + L.consts);   // [2][kNConst][BN]
     double* red = reinterpret_cast<double*>(gbase + L.red);
@@ -183,12 +204,14 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
+    unsigned long long* trc = (p.trace && (int)blockIdx.x == p.trace_cta) ? p.trace : nullptr;
     const uint32_t tmem_cols = tmem_cols_for(BN);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmO);
+        if (EPI == EP6_LN) tma_prefetch_desc(&tmX);
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -200,6 +223,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_init(bar_tempty + 8u * i, kEpiWarps);
             mbar_init(bar_x + 8u * i, 1);
             mbar_init(bar_cfull + 8u * i, 32);
+            mbar_init(bar_sfull + 8u * i, kEpiWarps);
+            mbar_init(bar_sfree + 8u * i, 1);
         }
         fence_mbar_init();
     }
@@ -214,19 +239,23 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t a_bytes = kBM * kBK, b_bytes = (uint32_t)BN * kBK;
     const uint16_t cmask = (uint16_t)((1u << CS) - 1u);
 
+    // Producer, MMA and store roles run on the whole warp with warp-uniform control
+    // flow (so addresses and descriptors live in uniform registers); one elected
+    // lane issues the TMA / tcgen05 instructions.
     if (warp == 0) {
         // ============================ TMA producer ============================
-        if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            const int a_rows = kBM / (int)CS;
-            for (int64_t u = cid; u < p.num_units; u += nclus) {
-                const int64_t m_tile = u / p.n_groups;
-                const int ng = (int)(u % p.n_groups);
-                const int n0 = (ng * (int)CS + (int)rank) * BN;
-                const int row0 = (int)(m_tile * kBM);
-                for (int kb = 0; kb < num_kb; ++kb) {
-                    mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+        int s = 0;
+        uint32_t ph = 0, tu = 0;
+        const int a_rows = kBM / (int)CS;
+        for (uint32_t u = cid; u < (uint32_t)p.num_units; u += nclus) {
+            const uint32_t m_tile = u / (uint32_t)p.n_groups;
+            const int ng = (int)(u % (uint32_t)p.n_groups);
+            const int n0 = (ng * (int)CS + (int)rank) * BN;
+            const int row0 = (int)(m_tile * kBM);
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+                if (elect_one()) {
+                    if (trc && kb == 0 && tu < 512) trc[2 * tu] = gtimer();
                     mbar_arrive_expect_tx(bar_full + 8u * s, a_bytes + b_bytes);
                     tma_load_2d(&tmB, sB + (uint32_t)s * b_bytes, bar_full + 8u * s, kb * kBK, n0);
                     if (CS == 1)
@@ -234,51 +263,111 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     else
                         tma_load_2d_mc(&tmA, sA + (uint32_t)s * a_bytes + rank * (uint32_t)a_rows * kBK,
                                        bar_full + 8u * s, kb * kBK, row0 + (int)rank * a_rows, cmask);
-                    if (++s == stages) { s = 0; ph ^= 1u; }
                 }
-            }
-            // Drain: every stage's last fill released by all consumers of the cluster,
-            // so no multicast commit can still target this CTA after it exits.
-            for (int i = 0; i < stages; ++i) {
-                mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+                __syncwarp();
                 if (++s == stages) { s = 0; ph ^= 1u; }
             }
+            if (trc && lane == 0 && tu < 512) trc[2 * tu + 1] = gtimer();
+            ++tu;
+        }
+        // Drain: every stage's last fill released by all consumers of the cluster,
+        // so no multicast commit can still target this CTA after it exits.
+        for (int i = 0; i < stages; ++i) {
+            mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+            if (++s == stages) { s = 0; ph ^= 1u; }
         }
     } else if (warp == 1) {
         // ============================ MMA issuer ==============================
-        if (lane == 0) {
-            const uint32_t idesc = idesc_i8(kBM, (uint32_t)BN);
-            int s = 0;
-            uint32_t ph = 0, it = 0;
-            for (int64_t u = cid; u < p.num_units; u += nclus, ++it) {
-                const uint32_t buf = it & 1u, aph = (it >> 1) & 1u;
-                mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);
+        const uint32_t idesc = idesc_i8(kBM, (uint32_t)BN);
+        int s = 0;
+        uint32_t ph = 0, it = 0;
+        for (uint32_t u = cid; u < (uint32_t)p.num_units; u += nclus, ++it) {
+            const uint32_t buf = it & 1u, aph = (it >> 1) & 1u;
+            mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);
+            tc_fence_after();
+            if (trc && lane == 0 && it < 256) trc[1024 + 4 * it] = gtimer();
+            const uint32_t d = tmem_base + buf * (uint32_t)BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(bar_full + 8u * s, ph);
                 tc_fence_after();
-                const uint32_t d = tmem_base + buf * (uint32_t)BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
-                    mbar_wait(bar_full + 8u * s, ph);
-                    tc_fence_after();
-                    const uint64_t ad = umma_desc_k128(sA + (uint32_t)s * a_bytes);
-                    const uint64_t bd = umma_desc_k128(sB + (uint32_t)s * b_bytes);
-                    const int rem = p.K - kb * kBK;
-                    const int nk = rem >= kBK ? 4 : rem / 32;
+                if (trc && lane == 0 && it < 256 && kb == 0) trc[1024 + 4 * it + 1] = gtimer();
+                const uint64_t ad = umma_desc_k128(sA + (uint32_t)s * a_bytes);
+                const uint64_t bd = umma_desc_k128(sB + (uint32_t)s * b_bytes);
+                const int rem = p.K - kb * kBK;
+                const int nk = rem >= kBK ? 4 : rem / 32;
+                if (elect_one()) {
                     for (int k = 0; k < nk; ++k)
                         mma_i8(d, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                    if (trc && it < 256 && kb == 0) trc[1024 + 4 * it + 2] = gtimer();
                     if (CS == 1) mma_commit(bar_empty + 8u * s);
                     else mma_commit_mc(bar_empty + 8u * s, cmask);
-                    if (++s == stages) { s = 0; ph ^= 1u; }
                 }
-                mma_commit(bar_tfull + 8u * buf);
+                __syncwarp();
+                if (++s == stages) { s = 0; ph ^= 1u; }
             }
+            if (elect_one()) mma_commit(bar_tfull + 8u * buf);
+            __syncwarp();
+            if (trc && lane == 0 && it < 256) trc[1024 + 4 * it + 3] = gtimer();
+        }
+    } else if (warp == 2) {
+        // ============================ output store warp =========================
+        // Writes each staged output tile with BN/W TMA tensor stores, and re-arms
+        // the staging buffer (sfree): for op #6 with the int8 residual it first
+        // TMA-loads the residual tile x[rows][cols] into the buffer (the epilogue
+        // reads x there in pass 1 and overwrites it in place with Y in pass 3).
+        {
+            const uint32_t W = (uint32_t)p.out_w;
+            const uint32_t nb = (uint32_t)p.nbuf;
+            const bool load_x = (EPI == EP6_LN) && (p.resid == nullptr);
+            auto make_ready = [&](uint32_t u, uint32_t sbuf) {   // called by one elected lane
+                const uint32_t bar = bar_sfree + 8u * sbuf;
+                if (load_x) {
+                    const uint32_t m_tile = u / (uint32_t)p.n_groups;
+                    const int ng = (int)(u % (uint32_t)p.n_groups);
+                    const int n0 = (ng * (int)CS + (int)rank) * BN;
+                    const uint32_t dst = base + L.ring + sbuf * (uint32_t)BN * kBM;
+                    mbar_arrive_expect_tx(bar, (uint32_t)BN * kBM);
+                    for (uint32_t sub = 0; sub < (uint32_t)BN / W; ++sub)
+                        tma_load_2d(&tmX, dst + sub * (kBM * W), bar, n0 + (int)(sub * W), (int32_t)(m_tile * kBM));
+                } else {
+                    mbar_arrive(bar);
+                }
+            };
+            if (lane == 0)
+                for (uint32_t j = 0; j < nb && cid + j * nclus < (uint32_t)p.num_units; ++j)
+                    make_ready(cid + j * nclus, j);
+            __syncwarp();
+            uint32_t it = 0;
+            for (uint32_t u = cid; u < (uint32_t)p.num_units; u += nclus, ++it) {
+                const uint32_t m_tile = u / (uint32_t)p.n_groups;
+                const int ng = (int)(u % (uint32_t)p.n_groups);
+                const int n0 = (ng * (int)CS + (int)rank) * BN;
+                const uint32_t sbuf = nb == 2 ? (it & 1u) : 0u;
+                const uint32_t sph = nb == 2 ? ((it >> 1) & 1u) : (it & 1u);
+                mbar_wait(bar_sfull + 8u * sbuf, sph);
+                const uint32_t src = base + L.ring + sbuf * (uint32_t)BN * kBM;
+                if (lane == 0) {
+                    for (uint32_t sub = 0; sub < (uint32_t)BN / W; ++sub)
+                        tma_store_2d(&tmO, src + sub * (kBM * W), n0 + (int)(sub * W), (int32_t)(m_tile * kBM));
+                    bulk_commit();
+                    bulk_wait_read<0>();              // smem read: the buffer may be refilled
+                    const uint32_t nxt = u + nb * nclus;
+                    if (nxt < (uint32_t)p.num_units) make_ready(nxt, sbuf);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) bulk_wait_all();           // output writes complete before the CTA retires
+            __syncwarp();
         }
     } else if (warp == 3) {
         // ============================ column constants ========================
         uint32_t it = 0;
-        for (int64_t u = cid; u < p.num_units; u += nclus, ++it) {
-            const int ng = (int)(u % p.n_groups);
+        for (uint32_t u = cid; u < (uint32_t)p.num_units; u += nclus, ++it) {
+            const int ng = (int)(u % (uint32_t)p.n_groups);
             const int n0 = (ng * (int)CS + (int)rank) * BN;
             const uint32_t buf = it & 1u, aph = (it >> 1) & 1u;
             mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);     // epilogue done with this buffer
+            if (trc && lane == 0 && it < 512) trc[3072 + 2 * it] = gtimer();
             float* cb = consts + (size_t)buf * kNConst * BN;
             for (int c = (int)lane; c < BN; c += 32) {
                 const int n = n0 + c;
@@ -290,62 +379,56 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     cb[4 * BN + c] = __ldg(p.beta + n);
                 }
             }
+            if (trc && lane == 0 && it < 512) trc[3072 + 2 * it + 1] = gtimer();
             mbar_arrive(bar_cfull + 8u * buf);
         }
     } else if (warp >= kEpiWarp0) {
         // ============================ epilogue ================================
         const uint32_t ew = warp - kEpiWarp0;
         const uint32_t quad = warp & 3u;          // TMEM lane quadrant this warp may access
-        const uint32_t half = ew >> 2;
+        const uint32_t half = ew >> 2;            // column part (0 .. kParts-1)
         const uint32_t rit = quad * 32u + lane;   // row in tile
         const int nch = BN / kChunk;
-        const int split = (nch + 1) / 2;
-        const int ch_lo = half ? split : 0, ch_hi = half ? nch : split;
-        const uint32_t ring = base + L.ring + ew * (kRing * kSlotBytes);
-        uint32_t g = 0;      // ring slots (bulk groups) issued by this warp
-        uint32_t pend = 0;   // chunks staged in the current slot
-        int pend_col0 = 0, pend_col1 = 0;
-        int64_t pend_row = 0;
-
-        // Write the staged chunks ([32 rows][16 B] each) with TMA bulk tensor stores:
-        // one proxy fence and one bulk group per slot of 2 chunks.
-        auto flush = [&]() {
-            if (!pend) return;
-            const uint32_t slot = ring + (g % kRing) * kSlotBytes;
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&tmO, slot, pend_col0, (int32_t)pend_row);
-                if (pend == 2) tma_store_2d(&tmO, slot + kRingBytes, pend_col1, (int32_t)pend_row);
-                bulk_commit();
-            }
-            ++g;
-            pend = 0;
-        };
-        // stage 16 packed int8 columns of this warp's 32 rows
-        auto store_chunk = [&](const uint32_t (&w)[4], int col, int64_t row0) {
-            const uint32_t slot = ring + (g % kRing) * kSlotBytes;
-            if (pend == 0 && g >= (uint32_t)kRing) {
-                if (lane == 0) bulk_wait_read<kRing - 1>();   // the slot's previous stores have read smem
-                __syncwarp();
-            }
-            st_shared_v4(slot + pend * kRingBytes + lane * 16u, w[0], w[1], w[2], w[3]);
-            if (pend == 0) pend_col0 = col; else pend_col1 = col;
-            pend_row = row0;
-            if (++pend == 2) flush();
-        };
-
+        const int per = (nch + kParts - 1) / kParts;
+        const int ch_lo = min((int)half * per, nch), ch_hi = min(ch_lo + per, nch);
+        // Output staging: the whole tile [128 rows][BN] in sub-boxes of W bytes
+        // ([BN/W][128][W], 16-byte granules XOR-swizzled exactly like the TMA
+        // SWIZZLE_{W}B mode, so the 16-B writes of a warp are bank-conflict free).
+        // The store warp (warp 2) writes it with BN/W TMA tensor stores of [128][W]
+        // once all epilogue warps arrived on sfull[buf]; it re-arms sfree[buf] when
+        // the stores have read the buffer.  Epilogue warps never wait on each other.
+        const uint32_t W = (uint32_t)p.out_w;
+        const uint32_t tile_bytes = (uint32_t)BN * kBM;
+        const uint32_t swz_shift = W == 128 ? 0u : W == 64 ? 1u : 2u;
+        const uint32_t swz_mask = W == 128 ? 7u : W == 64 ? 3u : W == 32 ? 1u : 0u;
+        const uint32_t row_swz = (rit >> swz_shift) & swz_mask;
+        uint32_t ubuf = base + L.ring;
+        const bool elected = (ew == 0 && lane == 0);
         uint32_t it = 0;
-        for (int64_t u = cid; u < p.num_units; u += nclus, ++it) {
-            const int64_t m_tile = u / p.n_groups;
-            const int ng = (int)(u % p.n_groups);
+
+        // stage 16 packed int8 columns (chunk ch) of this thread's row
+        auto store_chunk = [&](const uint32_t (&w)[4], int ch) {
+            const uint32_t col = (uint32_t)ch * kChunk;
+            const uint32_t sub = col / W, g16 = (col % W) >> 4;
+            st_shared_v4(ubuf + sub * (kBM * W) + rit * W + ((g16 ^ row_swz) << 4), w[0], w[1], w[2], w[3]);
+        };
+
+        for (uint32_t u = cid; u < (uint32_t)p.num_units; u += nclus, ++it) {
+            const uint32_t m_tile = u / (uint32_t)p.n_groups;
+            const int ng = (int)(u % (uint32_t)p.n_groups);
             const int n0 = (ng * (int)CS + (int)rank) * BN;
             const uint32_t buf = it & 1u, aph = (it >> 1) & 1u;
+            const uint32_t sbuf = p.nbuf == 2 ? buf : 0u, sph = p.nbuf == 2 ? aph : (it & 1u);
+            ubuf = base + L.ring + sbuf * tile_bytes;
+            if (trc && elected && it < 64) trc[2048 + 16 * it + 0] = gtimer();
+            mbar_wait(bar_sfree + 8u * sbuf, sph);   // staging buffer free (and residual x tile landed)
+            if (trc && elected && it < 64) trc[2048 + 16 * it + 1] = gtimer();
             mbar_wait(bar_cfull + 8u * buf, aph);
+            if (trc && elected && it < 64) trc[2048 + 16 * it + 8] = gtimer();
             mbar_wait(bar_tfull + 8u * buf, aph);
+            if (trc && elected && it < 64) trc[2048 + 16 * it + 2] = gtimer();
             tc_fence_after();
-            const int64_t row = m_tile * kBM + rit;
-            const int64_t wrow0 = m_tile * kBM + quad * 32u;
+            const int64_t row = (int64_t)m_tile * kBM + rit;
             const bool valid = row < p.M;
             const uint32_t tb = tmem_base + ((quad * 32u) << 16) + buf * (uint32_t)BN;
             const float* cm = consts + (size_t)buf * kNConst * BN;
@@ -399,7 +482,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                     uint32_t w[4];
                     quant_pack16<EPI == EP5_RELU, ZQNZ>(v, p.zq, w);
-                    store_chunk(w, n0 + cl, wrow0);
+                    store_chunk(w, ch);
                 };
                 uint32_t ra[16], rb[16];
                 int ch = ch_lo;
@@ -430,8 +513,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             rr[4 * j4] = v.x; rr[4 * j4 + 1] = v.y; rr[4 * j4 + 2] = v.z; rr[4 * j4 + 3] = v.w;
                         }
                     } else {
-                        const int4 xv = valid ? ld_nc_v4(p.x + row * C + col) : make_int4(0, 0, 0, 0);
-                        const uint32_t xw[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
+                        // the x tile was TMA-staged (swizzled) in this tile's output buffer
+                        const uint32_t cc = (uint32_t)ch * kChunk;
+                        const uint32_t sub = cc / W, g16 = (cc % W) >> 4;
+                        uint32_t xw[4];
+                        ld_shared_v4(ubuf + sub * (kBM * W) + rit * W + ((g16 ^ row_swz) << 4), xw);
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const int32_t xi = (int32_t)(int8_t)((xw[j >> 2] >> (8 * (j & 3))) & 0xff);
@@ -481,6 +567,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
                 // row statistics: halves via smem, CTAs of the cluster via DSMEM (rank order)
                 auto combine = [&](acc_t v, int pass) -> acc_t {
+                    static_assert(kParts == 2, "op-#6 epilogue combines two column parts");
                     red[(pass * 2 + (int)half) * kBM + rit] = (double)v;
                     named_bar_sync(1, kEpiThreads);
                     const acc_t t = (acc_t)red[(pass * 2 + 0) * kBM + rit] + (acc_t)red[(pass * 2 + 1) * kBM + rit];
@@ -562,7 +649,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(yh[j], p.inv_q);
                     uint32_t w[4];
                     quant_pack16<false, ZQNZ>(v, p.zq, w);
-                    store_chunk(w, n0 + cl, wrow0);
+                    store_chunk(w, ch);
                     if (p.ln_tap && valid) {
                         float* lrow = p.ln_tap + row * (int64_t)C + n0 + cl;
 #pragma unroll
@@ -587,13 +674,15 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                 }
             }
-            flush();
             tc_fence_before();
+            fence_proxy_async_smem();   // staged bytes visible to the TMA (async proxy)
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty + 8u * buf);
+            if (lane == 0) {
+                mbar_arrive(bar_tempty + 8u * buf);   // TMEM free: next MMA may start
+                mbar_arrive(bar_sfull + 8u * sbuf);   // this warp's part of the tile is staged
+            }
+            if (trc && elected && it < 64) trc[2048 + 16 * it + 7] = gtimer();
         }
-        if (lane == 0) bulk_wait_all();   // output stores complete before the CTA retires
-        __syncwarp();
     }
 
     // teardown: no CTA leaves while a peer may still address its shared memory

@@ -26,6 +26,12 @@ __device__ __forceinline__ uint32_t cluster_nctarank() {
     asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
     return r;
 }
+// One lane of the (converged) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
 // All threads of all CTAs of the cluster.
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -49,17 +55,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 }
 // Bounded wait: a lost arrival traps (kernel error) after ~2^34 cycles
 // instead of hanging the GPU.
-// try_wait carries a suspend-time hint so a waiting warp sleeps in hardware
-// until the phase completes instead of spinning on issue slots.
+// (try_wait without a suspend-time hint: with the hint ptxas emits
+// NANOSLEEP.SYNCS after a failed probe, which delayed wake-ups by 100s of ns.)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t done;
     long long t0 = 0;
     for (uint32_t it = 0;; ++it) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done) : "r"(bar), "r"(parity), "r"(0x989680) : "memory");
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
         if (done) return;
         if (it == 64) t0 = clock64();
         if (it > 64 && ((it & 1023) == 0) && clock64() - t0 > (1ll << 34)) __trap();
@@ -72,9 +78,9 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
     for (uint32_t it = 0;; ++it) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done) : "r"(bar), "r"(parity), "r"(0x989680) : "memory");
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
         if (done) return;
         if (it == 64) t0 = clock64();
         if (it > 64 && ((it & 1023) == 0) && clock64() - t0 > (1ll << 34)) __trap();
@@ -220,6 +226,9 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t (&v)[4]) {
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr) : "memory");
 }
 // d = {c[15:0], sat_s8(a), sat_s8(b)}  (byte0 = b, byte1 = a; probed on sm_100a)
 __device__ __forceinline__ uint32_t pack_sat_s8(int32_t a, int32_t b, uint32_t c) {

@@ -45,8 +45,9 @@ swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
 
 // One GEMM+epilogue launch plan.
 struct Plan {
-    void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
-    int BN = 0, CS = 1, stages = 0, n_groups = 1;
+    void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
+    int epi = 0, threads = 0;
+    int BN = 0, CS = 1, stages = 0, n_groups = 1, nbuf = 1, out_w = 16;
     uint32_t smem = 0;
     int max_clusters = 0;
 };
@@ -88,7 +89,7 @@ swin_mlp_status_t encode_2d(CUtensorMap* map, const void* ptr, int64_t rows, int
 
 constexpr uint32_t kSmemBudget = 227 * 1024;
 
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
 
 template <int EPI, int... Fs>
 KernelFn pick(int f, std::integer_sequence<int, Fs...>) {
@@ -112,7 +113,7 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
     CUDA_TRY(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.CS);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3((unsigned)pl.threads);
     cfg.dynamicSmemBytes = pl.smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -134,8 +135,10 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
 // Columns per CTA tile, CTAs per cluster, ring depth for one GEMM.
 // full_row: the epilogue needs whole rows (LayerNorm) -> the cluster must
 // cover all N columns (CS * BN == N); otherwise column groups are independent.
-bool make_plan(int N, bool full_row, Plan& pl) {
+bool make_plan(int epi, int N, bool full_row, Plan& pl) {
     pl = Plan();
+    pl.epi = epi;
+    pl.threads = kernel_threads(epi);
     if (full_row) {
         for (int cs : {1, 2, 4, 8}) {
             if (N % cs) continue;
@@ -145,31 +148,39 @@ bool make_plan(int N, bool full_row, Plan& pl) {
         if (!pl.BN) return false;
         pl.n_groups = 1;
     } else {
-        for (int bn : {256, 192, 128, 96, 64, 32}) {
+        for (int bn : {256, 128, 192, 96, 64, 32}) {
             if (N % bn == 0) { pl.BN = bn; break; }
         }
         if (!pl.BN) return false;
         pl.CS = 1;
         pl.n_groups = N / pl.BN;
     }
+    // output TMA box width: widest swizzle span dividing BN (full 128-B lines when possible)
+    pl.out_w = pl.BN % 128 == 0 ? 128 : pl.BN % 64 == 0 ? 64 : pl.BN % 32 == 0 ? 32 : 16;
+    // ring depth vs. output staging: prefer 2 staged tiles while
+    // the operand ring keeps >= 3 stages, else 1
     const uint32_t stage = (uint32_t)(kBM * kBK + pl.BN * kBK);
-    const uint32_t extra = smem_layout(pl.BN, pl.CS, 0).total + 1024;
-    int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
-    if (stages > 8) stages = 8;
-    if (stages < 2) return false;
-    pl.stages = stages;
-    pl.smem = smem_layout(pl.BN, pl.CS, stages).total + 1024;
-    return pl.smem <= kSmemBudget;
+    for (int nbuf : {2, 1}) {
+        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, nbuf).total + 1024;
+        int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
+        if (stages > 8) stages = 8;
+        if (stages < (nbuf == 2 ? 3 : 2)) continue;
+        pl.stages = stages;
+        pl.nbuf = nbuf;
+        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, nbuf).total + 1024;
+        return pl.smem <= kSmemBudget;
+    }
+    return false;
 }
 
 swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
-                         const GemmArgs& a, cudaStream_t stream) {
+                         const CUtensorMap& tx, const GemmArgs& a, cudaStream_t stream) {
     const int64_t units = a.num_units;
     int64_t clusters = units < pl.max_clusters ? units : pl.max_clusters;
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(clusters * pl.CS));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3((unsigned)pl.threads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
@@ -179,7 +190,7 @@ swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMa
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, pl.fn, ta, tb, to, a));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, pl.fn, ta, tb, to, tx, a));
     return SWIN_MLP_OK;
 }
 
@@ -203,6 +214,8 @@ struct swin_mlp_int8_s {
     bool prof_on = false;
     int prof_max = 0, prof_n = 0;
     std::vector<cudaEvent_t> prof_ev;
+    unsigned long long* trace = nullptr;
+    int trace_cta = 0;
     ~swin_mlp_int8_s() {
         for (void* p : allocs) cudaFree(p);
         for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
@@ -349,8 +362,8 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     }
 
     // tile / cluster plans
-    if (!make_plan(H, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
-    if (!make_plan(C, true, h->p2))
+    if (!make_plan(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU, H, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
+    if (!make_plan(EP6_LN, C, true, h->p2))
         return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC2 tile plan for C=%d (needs C = CS*BN, BN%%16==0, BN<=256, CS in 1,2,4,8)", C));
 
     swin_mlp_status_t st;
@@ -405,36 +418,44 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int8_t* hq = static_cast<int8_t*>(workspace);
 
-    CUtensorMap tm_x, tm_h, tm_ho, tm_y;
+    CUtensorMap tm_x, tm_h, tm_ho, tm_y, tm_xr;
     ST_TRY(encode_2d(&tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
     ST_TRY(encode_2d(&tm_h, hq, T, H, H, (uint32_t)(kBM / h->p2.CS)));
-    // epilogue output maps: [32 rows][16 B] boxes, no swizzle (one warp's chunk)
-    ST_TRY(encode_2d(&tm_ho, hq, T, H, H, 32, kChunk, CU_TENSOR_MAP_SWIZZLE_NONE));
-    ST_TRY(encode_2d(&tm_y, y, T, C, C, 32, kChunk, CU_TENSOR_MAP_SWIZZLE_NONE));
+    // epilogue output maps: [128 rows][W B] boxes with the W-byte swizzle the staging uses
+    auto swz = [](int w) {
+        return w == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : w == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+             : w == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    };
+    ST_TRY(encode_2d(&tm_ho, hq, T, H, H, kBM, (uint32_t)h->p1.out_w, swz(h->p1.out_w)));
+    ST_TRY(encode_2d(&tm_y, y, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
+    // op #6 residual source x, staged by TMA with the output tile's box and swizzle
+    ST_TRY(encode_2d(&tm_xr, x, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
     const int64_t m_tiles = (T + kBM - 1) / kBM;
 
     GemmArgs a1 = {};
-    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages;
+    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.nbuf = h->p1.nbuf; a1.out_w = h->p1.out_w;
     a1.n_groups = h->p1.n_groups; a1.num_units = m_tiles * h->p1.n_groups; a1.ldo = H;
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
     a1.acc_tap = dbg ? acc1 : nullptr;
+    a1.trace = h->trace; a1.trace_cta = h->trace_cta;
 
     GemmArgs a2 = {};
-    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages;
+    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.nbuf = h->p2.nbuf; a2.out_w = h->p2.out_w;
     a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
     a2.x = x; a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
     a2.resid = residual; a2.resid_out = residual_out;
     a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
     a2.acc_tap = dbg ? acc2 : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
+    a2.trace = h->trace ? h->trace + 4096 : nullptr; a2.trace_cta = h->trace_cta;
 
     cudaEvent_t* ev = nullptr;
     if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
-    ST_TRY(launch(h->p1, tm_x, h->tm_w1, tm_ho, a1, s));
+    ST_TRY(launch(h->p1, tm_x, h->tm_w1, tm_ho, tm_ho, a1, s));
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
     if (dbg && hidden) CUDA_TRY(cudaMemcpyAsync(hidden, hq, (size_t)T * H, cudaMemcpyDeviceToDevice, s));
-    ST_TRY(launch(h->p2, tm_h, h->tm_w2, tm_y, a2, s));
+    ST_TRY(launch(h->p2, tm_h, h->tm_w2, tm_y, tm_xr, a2, s));
     if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
     return SWIN_MLP_OK;
 }
@@ -531,6 +552,14 @@ swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, fl
     if (runs) *runs = h->prof_n;
     h->prof_on = false;
     h->prof_n = 0;
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_t cta) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (cta < 0) return fail(SWIN_MLP_EINVAL, "cta < 0");
+    h->trace = static_cast<unsigned long long*>(trace);
+    h->trace_cta = cta;
     return SWIN_MLP_OK;
 }
 

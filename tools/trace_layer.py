@@ -1,0 +1,46 @@
+"""Pipeline timeline of one CTA (debug trace) for a Swin-T batch-64 stage MLP.
+usage: python tools/trace_layer.py <stage> [cta]"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import synth
+from paper_2402_01169_b200 import SwinMlpInt8Layer
+
+stage = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+cta = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+L, T, xs = synth.swin_t_batch64_layers()[stage]
+layer = SwinMlpInt8Layer(L, device=0)
+x = torch.from_numpy(synth.make_activations(L, T, xs)).cuda()
+y = torch.empty((T, L.C), dtype=torch.int8, device="cuda")
+for _ in range(3):
+    layer(x, y=y)
+buf = torch.zeros(8192, dtype=torch.int64, device="cuda")
+layer.set_trace(buf, cta)
+layer(x, y=y)
+torch.cuda.synchronize()
+layer.set_trace(None)
+t = buf.cpu().numpy().astype(np.int64)
+print("C", L.C, "T", T, layer.plan())
+EPI = ["top", "bufok", "tfull", "fence", "pre_flush", "flush_bar", "committed", "end", "cfull"]
+for k, name in ((0, "FC1"), (1, "FC2")):
+    base = t[k * 4096:(k + 1) * 4096]
+    nz = base[base > 0]
+    if nz.size == 0:
+        continue
+    t0 = nz.min()
+    prod = base[0:1024].reshape(512, 2)
+    mma4 = base[1024:2048].reshape(256, 4)
+    mma = mma4[:, [0, 3]]
+    epi = base[2048:3072].reshape(64, 16)
+    cst = base[3072:4096].reshape(512, 2)
+    print(f"== {name}: ns from first stamp")
+    print("tile  prod[s,e]       mma[s,full,issued,e]            const[s,e]      epi: " + " ".join(f"{e:>9s}" for e in EPI))
+    n = int((mma[:, 0] > 0).sum())
+    f = lambda v: (v - t0) if v else -1
+    for i in range(min(n, 40)):
+        ep = " ".join(f"{f(epi[i, j]) if i < 64 else -1:9d}" for j in range(len(EPI)))
+        print(f"{i:3d} {f(prod[i,0]):7d},{f(prod[i,1]):7d} {f(mma4[i,0]):7d},{f(mma4[i,1]):7d},{f(mma4[i,2]):7d},{f(mma4[i,3]):7d} "
+              f"{f(cst[i,0]):7d},{f(cst[i,1]):7d}  {ep}")
