@@ -14,7 +14,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libswin_mlp_int8.so")
+LIB_PATH = os.environ.get("SWIN_MLP_LIB") or os.path.join(HERE, "libswin_mlp_int8.so")
 
 SWIN_MLP_OK = 0
 SWIN_MLP_EINVAL = 1

@@ -58,7 +58,7 @@ constexpr int kEpiWarp0 = 4;
 // Epilogue width per kernel: the op-#5 epilogue is light (few registers), so it
 // runs 16 warps (4 per SMSP, 4 column parts per TMEM lane quadrant); op #6 keeps
 // 8 warps (2 parts) for its register-heavy LayerNorm passes.
-__host__ __device__ constexpr int epi_warps(int epi) { return epi == 2 ? 8 : 16; }
+__host__ __device__ constexpr int epi_warps(int epi) { return 16; }
 __host__ __device__ constexpr int kernel_threads(int epi) { return 32 * (kEpiWarp0 + epi_warps(epi)); }
 constexpr int kChunk = 16;           // columns per tcgen05.ld (32x32b.x16)
 constexpr int kChunkBytes = 32 * kChunk;        // [32 rows][16 B] = one warp's output chunk
@@ -110,7 +110,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 struct SmemLayout {
-    uint32_t a, b, ring, consts, bars, tmem_slot, red, xbuf, total;
+    uint32_t a, b, ring, xres, consts, bars, tmem_slot, red, xbuf, total;
 };
 
 // nbuf: output staging buffers per epilogue warp (1 or 2 tiles in flight)
@@ -119,13 +119,14 @@ __host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int s
     L.a = 0;
     L.b = L.a + (uint32_t)stages * kBM * kBK;
     L.ring = L.b + (uint32_t)stages * (uint32_t)BN * kBK;
-    L.consts = L.ring + (uint32_t)nbuf * (uint32_t)BN * kBM;
+    L.xres = L.ring + (uint32_t)nbuf * (uint32_t)BN * kBM;            // op #6: residual x tiles [2]
+    L.consts = L.xres + (epi == 2 ? 2u : 0u) * (uint32_t)BN * kBM;
     L.bars = L.consts + 2u * kNConst * (uint32_t)BN * 4u;
-    const uint32_t nbars = 2u * stages + 2 + 2 + 2 + 2 + 2 + 2;
+    const uint32_t nbars = 2u * stages + 2 + 2 + 4 + 2 + 2 + 2 + 2 + 2;
     L.tmem_slot = L.bars + 8u * nbars;
     L.red = (L.tmem_slot + 8 + 15) & ~15u;
-    L.xbuf = L.red + 2u * 2u * kBM * 8u;
-    L.total = L.xbuf + 2u * (uint32_t)CS * kBM * 8u;
+    L.xbuf = L.red + 2u * 2u * 2u * kBM * 8u;
+    L.total = L.xbuf + 4u * (uint32_t)CS * kBM * 8u;   // [group][pass][rank][row] doubles
     return L;
 }
 
@@ -186,7 +187,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int BN = p.BN;
     const uint32_t CS = (uint32_t)p.CS;
     const int stages = p.stages;
-    constexpr int kEpiWarps = epi_warps(EPI), kEpiThreads = 32 * kEpiWarps, kParts = kEpiWarps / 4;
+    constexpr int kEpiWarps = epi_warps(EPI), kParts = kEpiWarps / 4;
+    // warps that work on one tile: all epilogue warps (op #5), one ping-pong group (op #6)
+    constexpr int kTileWarps = (EPI == EP6_LN) ? 8 : kEpiWarps;
     const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.nbuf);
     const uint32_t sA = base + L.a, sB = base + L.b;
     const uint32_t bar_full = base + L.bars;
@@ -194,12 +197,14 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t bar_tfull = bar_empty + 8u * stages;
     const uint32_t bar_tempty = bar_tfull + 16u;
     const uint32_t bar_x = bar_tempty + 16u;
-    const uint32_t bar_cfull = bar_x + 16u;
+    const uint32_t bar_cfull = bar_x + 32u;         // bar_x: [group][pass] DSMEM row-stat exchange
     const uint32_t bar_sfull = bar_cfull + 16u;     // output tile staged (count: epilogue warps)
     const uint32_t bar_sfree = bar_sfull + 16u;     // staging buffer reusable (count 1)
+    const uint32_t bar_xfull = bar_sfree + 16u;     // op #6 residual x tile landed (count 1 + tx)
+    const uint32_t bar_xfree = bar_xfull + 16u;     // op #6 pass 1 done with the x tile (tile warps)
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
     float* consts = reinterpret_cast<float*>(gbase + L.consts);   // [2][kNConst][BN]
-    double* red = reinterpret_cast<double*>(gbase + L.red);
+    double* red = reinterpret_cast<double*>(gbase + L.red);   // [group][pass][half][row] partial row sums
     double* xbuf = reinterpret_cast<double*>(gbase + L.xbuf);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -220,11 +225,14 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(bar_tfull + 8u * i, 1);
-            mbar_init(bar_tempty + 8u * i, kEpiWarps);
+            mbar_init(bar_tempty + 8u * i, kTileWarps);
             mbar_init(bar_x + 8u * i, 1);
+            mbar_init(bar_x + 16u + 8u * i, 1);
             mbar_init(bar_cfull + 8u * i, 32);
-            mbar_init(bar_sfull + 8u * i, kEpiWarps);
+            mbar_init(bar_sfull + 8u * i, kTileWarps);
             mbar_init(bar_sfree + 8u * i, 1);
+            mbar_init(bar_xfull + 8u * i, 1);
+            mbar_init(bar_xfree + 8u * i, kTileWarps);
         }
         fence_mbar_init();
     }
@@ -318,7 +326,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         {
             const uint32_t W = (uint32_t)p.out_w;
             const uint32_t nb = (uint32_t)p.nbuf;
-            const bool load_x = (EPI == EP6_LN) && (p.resid == nullptr);
+            const bool load_x = false;   // (op #6 residual tiles are loaded by warp 3 into xres)
             auto make_ready = [&](uint32_t u, uint32_t sbuf) {   // called by one elected lane
                 const uint32_t bar = bar_sfree + 8u * sbuf;
                 if (load_x) {
@@ -361,11 +369,28 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp == 3) {
         // ============================ column constants ========================
+        // Per tile: (op #6) TMA the residual x[rows][cols] tile into xres[buf] as soon
+        // as the previous user of that buffer finished pass 1 (xfree), then copy the
+        // per-column constants once the buffer's previous tile is fully drained (tempty).
+        const bool load_x = (EPI == EP6_LN) && (p.resid == nullptr);
         uint32_t it = 0;
         for (uint32_t u = cid; u < (uint32_t)p.num_units; u += nclus, ++it) {
             const int ng = (int)(u % (uint32_t)p.n_groups);
             const int n0 = (ng * (int)CS + (int)rank) * BN;
             const uint32_t buf = it & 1u, aph = (it >> 1) & 1u;
+            if (load_x) {
+                mbar_wait(bar_xfree + 8u * buf, aph ^ 1u);
+                if (lane == 0) {
+                    const uint32_t W = (uint32_t)p.out_w;
+                    const uint32_t m_tile = u / (uint32_t)p.n_groups;
+                    const uint32_t dst = base + L.xres + buf * (uint32_t)BN * kBM;
+                    mbar_arrive_expect_tx(bar_xfull + 8u * buf, (uint32_t)BN * kBM);
+                    for (uint32_t sub = 0; sub < (uint32_t)BN / W; ++sub)
+                        tma_load_2d(&tmX, dst + sub * (kBM * W), bar_xfull + 8u * buf, n0 + (int)(sub * W),
+                                    (int32_t)(m_tile * kBM));
+                }
+                __syncwarp();
+            }
             mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);     // epilogue done with this buffer
             if (trc && lane == 0 && it < 512) trc[3072 + 2 * it] = gtimer();
             float* cb = consts + (size_t)buf * kNConst * BN;
@@ -384,19 +409,31 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp >= kEpiWarp0) {
         // ============================ epilogue ================================
+        // op #5: 16 warps; warp w drains TMEM lane quadrant (w % 4) over column part
+        //        (w-4)/4 of every tile.
+        // op #6: two ping-pong groups of 4 warps; group g = (w-4)/4 takes the tiles
+        //        with local index it % 2 == g (accumulator buffer g) and each thread
+        //        owns a whole row of its CTA's columns, so row statistics are
+        //        thread-local (plus the cluster exchange when C spans CTAs).
         const uint32_t ew = warp - kEpiWarp0;
         const uint32_t quad = warp & 3u;          // TMEM lane quadrant this warp may access
-        const uint32_t half = ew >> 2;            // column part (0 .. kParts-1)
+        const uint32_t grp = ew >> 2;             // column part (op #5) / ping-pong group (op #6)
         const uint32_t rit = quad * 32u + lane;   // row in tile
         const int nch = BN / kChunk;
-        const int per = (nch + kParts - 1) / kParts;
-        const int ch_lo = min((int)half * per, nch), ch_hi = min(ch_lo + per, nch);
+        constexpr bool kPingPong = (EPI == EP6_LN);
+        // op #6: group = (w-4)/8 (ping-pong), column half = ((w-4)/4) & 1
+        const uint32_t pgrp = kPingPong ? (ew >> 3) : 0u;
+        const uint32_t part = kPingPong ? ((ew >> 2) & 1u) : grp;
+        const int nparts = kPingPong ? 2 : kParts;
+        const int per = (nch + nparts - 1) / nparts;
+        const int ch_lo = min((int)part * per, nch);
+        const int ch_hi = min(ch_lo + per, nch);
         // Output staging: the whole tile [128 rows][BN] in sub-boxes of W bytes
         // ([BN/W][128][W], 16-byte granules XOR-swizzled exactly like the TMA
         // SWIZZLE_{W}B mode, so the 16-B writes of a warp are bank-conflict free).
         // The store warp (warp 2) writes it with BN/W TMA tensor stores of [128][W]
-        // once all epilogue warps arrived on sfull[buf]; it re-arms sfree[buf] when
-        // the stores have read the buffer.  Epilogue warps never wait on each other.
+        // once the tile's epilogue warps arrived on sfull[buf]; it re-arms
+        // sfree[buf] when the stores have read the buffer.
         const uint32_t W = (uint32_t)p.out_w;
         const uint32_t tile_bytes = (uint32_t)BN * kBM;
         const uint32_t swz_shift = W == 128 ? 0u : W == 64 ? 1u : 2u;
@@ -404,16 +441,22 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t row_swz = (rit >> swz_shift) & swz_mask;
         uint32_t ubuf = base + L.ring;
         const bool elected = (ew == 0 && lane == 0);
+        const bool grp_leader = ((ew & 7u) == 0 && lane == 0);
+        const float2 inv2 = make_float2(p.inv_q, p.inv_q);
         uint32_t it = 0;
 
-        // stage 16 packed int8 columns (chunk ch) of this thread's row
-        auto store_chunk = [&](const uint32_t (&w)[4], int ch) {
-            const uint32_t col = (uint32_t)ch * kChunk;
-            const uint32_t sub = col / W, g16 = (col % W) >> 4;
-            st_shared_v4(ubuf + sub * (kBM * W) + rit * W + ((g16 ^ row_swz) << 4), w[0], w[1], w[2], w[3]);
+        // W is a power of two: chunk ch (16 columns = one 16-B granule) lives in
+        // sub-box ch >> lg, granule ch & gm of this row
+        const uint32_t lgW = 31u - (uint32_t)__clz((int)W);            // log2(W)
+        const uint32_t lg = lgW - 4u, gm = (W >> 4) - 1u;
+        const uint32_t row_base = rit << lgW;
+        auto granule = [&](int ch) -> uint32_t {   // smem address of this row's 16-B granule of chunk ch
+            const uint32_t c = (uint32_t)ch;
+            return ubuf + ((c >> lg) << (lgW + 7u)) + row_base + (((c & gm) ^ row_swz) << 4);
         };
 
         for (uint32_t u = cid; u < (uint32_t)p.num_units; u += nclus, ++it) {
+            if (kPingPong && (it & 1u) != pgrp) continue;
             const uint32_t m_tile = u / (uint32_t)p.n_groups;
             const int ng = (int)(u % (uint32_t)p.n_groups);
             const int n0 = (ng * (int)CS + (int)rank) * BN;
@@ -435,26 +478,27 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const float* cbias = cm + BN;
             const int32_t* czc = reinterpret_cast<const int32_t*>(cm + 2 * BN);
 
-            // z (or y) for one 16-column chunk: fl(fmaf(fl(acc - zc), m, b))
-            auto dequant16 = [&](uint32_t (&r)[16], int cl, float (&y)[16]) {
+            // dQ (+bias) of one 16-column chunk, two columns per f32x2 op:
+            // y = fl(fmaf(fl(acc - zc), m, b))  (bit-identical to the scalar form)
+            auto dequant16 = [&](uint32_t (&r)[16], int cl, float2 (&y)[8]) {
 #pragma unroll
                 for (int j4 = 0; j4 < 4; ++j4) {
                     const float4 mv = *reinterpret_cast<const float4*>(cm + cl + 4 * j4);
-                    const float mm[4] = {mv.x, mv.y, mv.z, mv.w};
-                    float bb[4] = {0.f, 0.f, 0.f, 0.f};
-                    if constexpr (HAS_B) {
-                        const float4 bv = *reinterpret_cast<const float4*>(cbias + cl + 4 * j4);
-                        bb[0] = bv.x; bb[1] = bv.y; bb[2] = bv.z; bb[3] = bv.w;
-                    }
+                    float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if constexpr (HAS_B) bv = *reinterpret_cast<const float4*>(cbias + cl + 4 * j4);
                     if constexpr (HAS_ZC) {
                         const int4 zv = *reinterpret_cast<const int4*>(czc + cl + 4 * j4);
                         r[4 * j4 + 0] -= (uint32_t)zv.x; r[4 * j4 + 1] -= (uint32_t)zv.y;
                         r[4 * j4 + 2] -= (uint32_t)zv.z; r[4 * j4 + 3] -= (uint32_t)zv.w;
                     }
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float a = __int2float_rn((int32_t)r[4 * j4 + j]);
-                        y[4 * j4 + j] = HAS_B ? __fmaf_rn(a, mm[j], bb[j]) : __fmul_rn(a, mm[j]);
+                    const float2 a0 = make_float2(__int2float_rn((int32_t)r[4 * j4 + 0]), __int2float_rn((int32_t)r[4 * j4 + 1]));
+                    const float2 a1 = make_float2(__int2float_rn((int32_t)r[4 * j4 + 2]), __int2float_rn((int32_t)r[4 * j4 + 3]));
+                    if constexpr (HAS_B) {
+                        y[2 * j4] = f2_fma(a0, make_float2(mv.x, mv.y), make_float2(bv.x, bv.y));
+                        y[2 * j4 + 1] = f2_fma(a1, make_float2(mv.z, mv.w), make_float2(bv.z, bv.w));
+                    } else {
+                        y[2 * j4] = f2_mul(a0, make_float2(mv.x, mv.y));
+                        y[2 * j4 + 1] = f2_mul(a1, make_float2(mv.z, mv.w));
                     }
                 }
             };
@@ -467,189 +511,220 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                                        (int)r[4 * j4 + 3]));
                 }
             };
-
-            if constexpr (EPI == EP5_RELU || EPI == EP5_GELU) {
-                auto process = [&](uint32_t (&r)[16], int ch) {
-                    const int cl = ch * kChunk;
-                    float y[16];
-                    dequant16(r, cl, y);
-                    tap_acc(r, n0 + cl);
-                    float v[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        if constexpr (EPI == EP5_RELU) v[j] = __fmul_rn(y[j], p.inv_q);   // ReLU folded into the pack
-                        else v[j] = __fmul_rn(gelu_erf_f32(y[j]), p.inv_q);
+            // chunk loop with the next tcgen05.ld in flight while the current chunk is processed
+            // (op #6, register-bound at 16 warps, issues one load at a time and relies
+            // on its 4 warps per SMSP for latency hiding)
+            auto for_chunks = [&](auto&& fn) {
+                if constexpr (EPI == EP6_LN) {
+                    for (int ch = ch_lo; ch < ch_hi; ++ch) {
+                        uint32_t ra[16];
+                        tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
+                        tmem_wait_ld_dep(ra);
+                        fn(ra, ch);
                     }
-                    uint32_t w[4];
-                    quant_pack16<EPI == EP5_RELU, ZQNZ>(v, p.zq, w);
-                    store_chunk(w, ch);
-                };
+                    return;
+                }
                 uint32_t ra[16], rb[16];
                 int ch = ch_lo;
                 if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
                 while (ch < ch_hi) {
                     tmem_wait_ld_dep(ra);
                     if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
-                    process(ra, ch);
+                    fn(ra, ch);
                     if (++ch >= ch_hi) break;
                     tmem_wait_ld_dep(rb);
                     if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
-                    process(rb, ch);
+                    fn(rb, ch);
                     ++ch;
                 }
+            };
+
+            if constexpr (EPI == EP5_RELU || EPI == EP5_GELU) {
+                for_chunks([&](uint32_t (&r)[16], int ch) {
+                    const int cl = ch * kChunk;
+                    float2 y[8];
+                    dequant16(r, cl, y);
+                    tap_acc(r, n0 + cl);
+                    float v[16];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float2 t;
+                        if constexpr (EPI == EP5_RELU) t = f2_mul(y[j], inv2);   // ReLU folds into the pack
+                        else t = f2_mul(make_float2(gelu_erf_f32(y[j].x), gelu_erf_f32(y[j].y)), inv2);
+                        v[2 * j] = t.x;
+                        v[2 * j + 1] = t.y;
+                    }
+                    uint32_t w[4];
+                    quant_pack16<EPI == EP5_RELU, ZQNZ>(v, p.zq, w);
+                    st_shared_v4(granule(ch), w[0], w[1], w[2], w[3]);
+                });
             } else {
                 // ---------------- fused op #6: dQ, bias, +residual, LayerNorm, Q ----------------
                 const int C = p.ldo;
                 using acc_t = typename std::conditional<STATS64, double, float>::type;
+                if (!p.resid) mbar_wait(bar_xfull + 8u * buf, aph);   // residual x tile landed
+                const float2 sx2 = make_float2(p.s_x, p.s_x);
+                const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
+                const float2 xoff2 = make_float2(xoff, xoff);
                 // pass 1: z = fl(fl(fmaf(fl(A2), m2, b2)) + r); park z in TMEM; row sum
-                acc_t s1 = 0;
-                auto load_resid = [&](int ch, float (&rr)[16]) {
-                    const int col = n0 + ch * kChunk;
+                double s1d = 0.0;
+                float2 s1f = make_float2(0.f, 0.f);
+                for_chunks([&](uint32_t (&r)[16], int ch) {
+                    const int cl = ch * kChunk;
+                    float2 rr[8];
                     if (p.resid) {
 #pragma unroll
                         for (int j4 = 0; j4 < 4; ++j4) {
-                            const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(p.resid + row * C + col) + j4)
+                            const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(p.resid + row * C + n0 + cl) + j4)
                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                            rr[4 * j4] = v.x; rr[4 * j4 + 1] = v.y; rr[4 * j4 + 2] = v.z; rr[4 * j4 + 3] = v.w;
+                            rr[2 * j4] = make_float2(v.x, v.y);
+                            rr[2 * j4 + 1] = make_float2(v.z, v.w);
                         }
                     } else {
-                        // the x tile was TMA-staged (swizzled) in this tile's output buffer
-                        const uint32_t cc = (uint32_t)ch * kChunk;
-                        const uint32_t sub = cc / W, g16 = (cc % W) >> 4;
+                        // r = fl(fl(x - z_x) * s_x); the x tile was TMA-staged in this tile's buffer
                         uint32_t xw[4];
-                        ld_shared_v4(ubuf + sub * (kBM * W) + rit * W + ((g16 ^ row_swz) << 4), xw);
+#ifndef SWIN_EXP_NO_X
+                        ld_shared_v4(granule(ch) - ubuf + base + L.xres + buf * tile_bytes, xw);
+#else
+                        xw[0] = xw[1] = xw[2] = xw[3] = 0x01020304u;
+#endif
+                        // exact int8 -> float without the 1/8-rate I2F.S8: with u = x ^ 0x80
+                        // (offset binary), bits 0x4B0000uu are the float 2^23 + u, and
+                        // (2^23 + u) - (2^23 + 128 + z_x) = x - z_x exactly (small integers).
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const int32_t xi = (int32_t)(int8_t)((xw[j >> 2] >> (8 * (j & 3))) & 0xff);
-                            rr[j] = __fmul_rn(__int2float_rn(xi - p.z_x), p.s_x);
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t ob = xw[q] ^ 0x80808080u;
+                            const float2 f01 = make_float2(__uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7650)),
+                                                           __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7651)));
+                            const float2 f23 = make_float2(__uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7652)),
+                                                           __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7653)));
+                            rr[2 * q] = f2_mul(f2_sub(f01, xoff2), sx2);
+                            rr[2 * q + 1] = f2_mul(f2_sub(f23, xoff2), sx2);
                         }
                     }
-                };
-                auto pass1 = [&](uint32_t (&r)[16], int ch) {
-                    const int cl = ch * kChunk;
-                    float rr[16];
-                    load_resid(ch, rr);
-                    float z[16];
+                    float2 z[8];
                     dequant16(r, cl, z);
                     tap_acc(r, n0 + cl);
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        z[j] = __fadd_rn(z[j], rr[j]);
-                        if constexpr (STATS64) s1 = __dadd_rn(s1, (double)z[j]);
-                        else s1 = __fadd_rn(s1, z[j]);
-                        r[j] = __float_as_uint(z[j]);
+                    for (int j = 0; j < 8; ++j) {
+                        z[j] = f2_add(z[j], rr[j]);
+                        if constexpr (STATS64) {
+                            s1d = __dadd_rn(s1d, (double)z[j].x);
+                            s1d = __dadd_rn(s1d, (double)z[j].y);
+                        } else {
+                            s1f = f2_add(s1f, z[j]);
+                        }
+                        r[2 * j] = __float_as_uint(z[j].x);
+                        r[2 * j + 1] = __float_as_uint(z[j].y);
                     }
                     if (p.resid_out && valid) {
                         float* zrow = p.resid_out + row * (int64_t)C + n0 + cl;
 #pragma unroll
                         for (int j4 = 0; j4 < 4; ++j4)
                             *reinterpret_cast<float4*>(zrow + 4 * j4) =
-                                make_float4(z[4 * j4], z[4 * j4 + 1], z[4 * j4 + 2], z[4 * j4 + 3]);
+                                make_float4(z[2 * j4].x, z[2 * j4].y, z[2 * j4 + 1].x, z[2 * j4 + 1].y);
                     }
+#ifndef SWIN_EXP_NO_STTM
                     tmem_st16(tb + (uint32_t)cl, r);
-                };
-                {
-                    uint32_t ra[16], rb[16];
-                    int ch = ch_lo;
-                    if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
-                    while (ch < ch_hi) {
-                        tmem_wait_ld_dep(ra);
-                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
-                        pass1(ra, ch);
-                        if (++ch >= ch_hi) break;
-                        tmem_wait_ld_dep(rb);
-                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
-                        pass1(rb, ch);
-                        ++ch;
-                    }
-                }
+#endif
+                });
                 tmem_wait_st();
+                if (!p.resid) {   // the x tile has been consumed: let warp 3 prefetch the next one
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_xfree + 8u * buf);
+                }
+                if (trc && elected && it < 64) trc[2048 + 16 * it + 3] = gtimer();
 
-                // row statistics: halves via smem, CTAs of the cluster via DSMEM (rank order)
-                auto combine = [&](acc_t v, int pass) -> acc_t {
-                    static_assert(kParts == 2, "op-#6 epilogue combines two column parts");
-                    red[(pass * 2 + (int)half) * kBM + rit] = (double)v;
-                    named_bar_sync(1, kEpiThreads);
-                    const acc_t t = (acc_t)red[(pass * 2 + 0) * kBM + rit] + (acc_t)red[(pass * 2 + 1) * kBM + rit];
+                // row statistics across the CS CTAs of the cluster (DSMEM, summed in rank order)
+                // row statistics: the two column halves via smem (named barrier of the
+                // group's 256 threads), the CS CTAs of the cluster via DSMEM, always
+                // summed in the same order so every thread/CTA derives identical stats
+                auto cluster_sum = [&](acc_t v, int pass) -> acc_t {
+                    const uint32_t slot_id = pgrp * 2u + (uint32_t)pass;
+                    red[(slot_id * 2u + part) * kBM + rit] = (double)v;
+                    named_bar_sync(1u + pgrp, 256);
+                    const acc_t t = (acc_t)red[(slot_id * 2u + 0u) * kBM + rit] + (acc_t)red[(slot_id * 2u + 1u) * kBM + rit];
                     if (CS == 1) return t;
-                    const uint32_t xb = bar_x + 8u * (uint32_t)pass;
-                    if (half == 0) {
-                        if (ew == 0 && lane == 0) mbar_arrive_expect_tx(xb, CS * kBM * 8u);
-                        const uint32_t slot = smem_u32(xbuf + ((size_t)pass * CS + rank) * kBM + rit);
+                    const uint32_t xb = bar_x + 8u * slot_id;
+                    if (part == 0) {
+                        if (grp_leader) mbar_arrive_expect_tx(xb, CS * kBM * 8u);
+                        const uint32_t slot = smem_u32(xbuf + ((size_t)slot_id * CS + rank) * kBM + rit);
                         for (uint32_t r = 0; r < CS; ++r) st_async_f64(mapa(slot, r), (double)t, mapa(xb, r));
                     }
-                    mbar_wait_cluster(xb, it & 1u);
+                    mbar_wait_cluster(xb, (it >> 1) & 1u);
                     acc_t S = 0;
-                    for (uint32_t r = 0; r < CS; ++r) S = S + (acc_t)xbuf[((size_t)pass * CS + r) * kBM + rit];
+                    for (uint32_t r = 0; r < CS; ++r) S = S + (acc_t)xbuf[((size_t)slot_id * CS + r) * kBM + rit];
                     return S;
                 };
-                const acc_t S = combine(s1, 0);
+                acc_t s1;
+                if constexpr (STATS64) s1 = s1d; else s1 = __fadd_rn(s1f.x, s1f.y);
+                const acc_t S = cluster_sum(s1, 0);
                 const acc_t mu = S / (acc_t)C;
+                if (trc && elected && it < 64) trc[2048 + 16 * it + 4] = gtimer();
 
                 // pass 2: centred sum of squares
-                acc_t s2 = 0;
-                {
-                    auto pass2 = [&](const uint32_t (&r)[16]) {
+                double s2d = 0.0;
+                float2 s2f = make_float2(0.f, 0.f);
+                const float2 mu2 = make_float2((float)mu, (float)mu);
+                for_chunks([&](uint32_t (&r)[16], int) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            if constexpr (STATS64) {
-                                const double dz = __dsub_rn((double)__uint_as_float(r[j]), mu);
-                                s2 = __dadd_rn(s2, __dmul_rn(dz, dz));
-                            } else {
-                                const float dz = __fsub_rn(__uint_as_float(r[j]), mu);
-                                s2 = __fmaf_rn(dz, dz, s2);
-                            }
+                    for (int j = 0; j < 8; ++j) {
+                        const float2 zz = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                        if constexpr (STATS64) {
+                            const double d0 = __dsub_rn((double)zz.x, (double)mu), d1 = __dsub_rn((double)zz.y, (double)mu);
+                            s2d = __dadd_rn(s2d, __dmul_rn(d0, d0));
+                            s2d = __dadd_rn(s2d, __dmul_rn(d1, d1));
+                        } else {
+                            const float2 dz = f2_sub(zz, mu2);
+                            s2f = f2_fma(dz, dz, s2f);
                         }
-                    };
-                    uint32_t ra[16], rb[16];
-                    int ch = ch_lo;
-                    if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
-                    while (ch < ch_hi) {
-                        tmem_wait_ld_dep(ra);
-                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
-                        pass2(ra);
-                        if (++ch >= ch_hi) break;
-                        tmem_wait_ld_dep(rb);
-                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
-                        pass2(rb);
-                        ++ch;
                     }
-                }
-                const acc_t SS = combine(s2, 1);
+                });
+                acc_t s2;
+                if constexpr (STATS64) s2 = s2d; else s2 = __fadd_rn(s2f.x, s2f.y);
+                const acc_t SS = cluster_sum(s2, 1);
                 acc_t rstd;
                 if constexpr (STATS64) rstd = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(SS, (double)C), (double)p.eps)));
                 else rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(SS, (float)C), p.eps)));
+                const float2 rstd2 = make_float2((float)rstd, (float)rstd);
+                if (trc && elected && it < 64) trc[2048 + 16 * it + 5] = gtimer();
 
-                // pass 3: yhat = fl(((z-mu)*rstd)*gamma + beta); Y = Q_y(yhat)
+                // pass 3: yhat = fl(((z-mu)*rstd)*gamma + beta); Y = Q_y(yhat), staged over x in place
                 const float* cg = cm + 3 * BN;
                 const float* cbt = cm + 4 * BN;
-                auto pass3 = [&](const uint32_t (&r)[16], int ch) {
+                for_chunks([&](uint32_t (&r)[16], int ch) {
                     const int cl = ch * kChunk;
                     float yh[16];
 #pragma unroll
                     for (int j4 = 0; j4 < 4; ++j4) {
                         const float4 gv = *reinterpret_cast<const float4*>(cg + cl + 4 * j4);
                         const float4 bv = *reinterpret_cast<const float4*>(cbt + cl + 4 * j4);
-                        const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
-                        const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
+                        if constexpr (STATS64) {
+                            const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+                            const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const float zf = __uint_as_float(r[4 * j4 + j]);
-                            if constexpr (STATS64) {
-                                const double xh = __dmul_rn(__dsub_rn((double)zf, mu), rstd);
+                            for (int j = 0; j < 4; ++j) {
+                                const double xh = __dmul_rn(__dsub_rn((double)__uint_as_float(r[4 * j4 + j]), mu), rstd);
                                 yh[4 * j4 + j] = __double2float_rn(__dadd_rn(__dmul_rn(xh, (double)gg[j]), (double)bb[j]));
-                            } else {
-                                const float xh = __fmul_rn(__fsub_rn(zf, mu), rstd);
-                                yh[4 * j4 + j] = __fmaf_rn(xh, gg[j], bb[j]);
                             }
+                        } else {
+                            const float2 z0 = make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]));
+                            const float2 z1 = make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3]));
+                            const float2 y0 = f2_fma(f2_mul(f2_sub(z0, mu2), rstd2), make_float2(gv.x, gv.y), make_float2(bv.x, bv.y));
+                            const float2 y1 = f2_fma(f2_mul(f2_sub(z1, mu2), rstd2), make_float2(gv.z, gv.w), make_float2(bv.z, bv.w));
+                            yh[4 * j4] = y0.x; yh[4 * j4 + 1] = y0.y; yh[4 * j4 + 2] = y1.x; yh[4 * j4 + 3] = y1.y;
                         }
                     }
                     float v[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(yh[j], p.inv_q);
+                    for (int j = 0; j < 8; ++j) {
+                        const float2 t = f2_mul(make_float2(yh[2 * j], yh[2 * j + 1]), inv2);
+                        v[2 * j] = t.x;
+                        v[2 * j + 1] = t.y;
+                    }
                     uint32_t w[4];
                     quant_pack16<false, ZQNZ>(v, p.zq, w);
-                    store_chunk(w, ch);
+                    st_shared_v4(granule(ch), w[0], w[1], w[2], w[3]);
                     if (p.ln_tap && valid) {
                         float* lrow = p.ln_tap + row * (int64_t)C + n0 + cl;
 #pragma unroll
@@ -657,22 +732,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             *reinterpret_cast<float4*>(lrow + 4 * j4) =
                                 make_float4(yh[4 * j4], yh[4 * j4 + 1], yh[4 * j4 + 2], yh[4 * j4 + 3]);
                     }
-                };
-                {
-                    uint32_t ra[16], rb[16];
-                    int ch = ch_lo;
-                    if (ch < ch_hi) tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
-                    while (ch < ch_hi) {
-                        tmem_wait_ld_dep(ra);
-                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), rb);
-                        pass3(ra, ch);
-                        if (++ch >= ch_hi) break;
-                        tmem_wait_ld_dep(rb);
-                        if (ch + 1 < ch_hi) tmem_ld16(tb + (uint32_t)((ch + 1) * kChunk), ra);
-                        pass3(rb, ch);
-                        ++ch;
-                    }
-                }
+                });
             }
             tc_fence_before();
             fence_proxy_async_smem();   // staged bytes visible to the TMA (async proxy)

@@ -230,6 +230,22 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 __device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t (&v)[4]) {
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr) : "memory");
 }
+// ---- packed fp32x2 arithmetic (FMUL2/FADD2/FFMA2): two IEEE round-to-nearest
+// fp32 operations per instruction, bit-identical to the scalar ones.
+__device__ __forceinline__ uint64_t f2u(float2 a) { return *reinterpret_cast<uint64_t*>(&a); }
+__device__ __forceinline__ float2 u2f(uint64_t a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+    uint64_t r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b))); return u2f(r);
+}
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+    uint64_t r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b))); return u2f(r);
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+    uint64_t r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b))); return u2f(r);
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+    uint64_t r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c))); return u2f(r);
+}
 // d = {c[15:0], sat_s8(a), sat_s8(b)}  (byte0 = b, byte1 = a; probed on sm_100a)
 __device__ __forceinline__ uint32_t pack_sat_s8(int32_t a, int32_t b, uint32_t c) {
     uint32_t d;

@@ -135,6 +135,28 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
 // Columns per CTA tile, CTAs per cluster, ring depth for one GEMM.
 // full_row: the epilogue needs whole rows (LayerNorm) -> the cluster must
 // cover all N columns (CS * BN == N); otherwise column groups are independent.
+// The first candidate whose shared-memory plan fits wins.
+bool fit_smem(int epi, Plan& pl, int min_stages) {
+    // output TMA box width: widest swizzle span dividing BN (full 128-B lines when possible)
+    pl.out_w = pl.BN % 128 == 0 ? 128 : pl.BN % 64 == 0 ? 64 : pl.BN % 32 == 0 ? 32 : 16;
+    // ring depth vs. output staging: prefer 2 staged tiles while the operand ring
+    // keeps >= 3 stages, else 1 (op #6 always stages 2: one per ping-pong group)
+    const uint32_t stage = (uint32_t)(kBM * kBK + pl.BN * kBK);
+    for (int nbuf : {2, 1}) {
+        if (epi == EP6_LN && nbuf != 2) continue;
+        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, nbuf).total + 1024;
+        if (extra >= kSmemBudget) continue;
+        int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
+        if (stages > 8) stages = 8;
+        if (stages < min_stages) continue;
+        pl.stages = stages;
+        pl.nbuf = nbuf;
+        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, nbuf).total + 1024;
+        if (pl.smem <= kSmemBudget) return true;
+    }
+    return false;
+}
+
 bool make_plan(int epi, int N, bool full_row, Plan& pl) {
     pl = Plan();
     pl.epi = epi;
@@ -143,32 +165,23 @@ bool make_plan(int epi, int N, bool full_row, Plan& pl) {
         for (int cs : {1, 2, 4, 8}) {
             if (N % cs) continue;
             const int bn = N / cs;
-            if (bn <= 256 && bn % 16 == 0) { pl.BN = bn; pl.CS = cs; break; }
+            if (bn > 256 || bn % 16) continue;
+            pl.BN = bn; pl.CS = cs; pl.n_groups = 1;
+            if (fit_smem(epi, pl, 3)) return true;   // prefer a >= 3-deep operand ring
         }
-        if (!pl.BN) return false;
-        pl.n_groups = 1;
-    } else {
-        for (int bn : {256, 128, 192, 96, 64, 32}) {
-            if (N % bn == 0) { pl.BN = bn; break; }
+        for (int cs : {1, 2, 4, 8}) {
+            if (N % cs) continue;
+            const int bn = N / cs;
+            if (bn > 256 || bn % 16) continue;
+            pl.BN = bn; pl.CS = cs; pl.n_groups = 1;
+            if (fit_smem(epi, pl, 2)) return true;
         }
-        if (!pl.BN) return false;
-        pl.CS = 1;
-        pl.n_groups = N / pl.BN;
+        return false;
     }
-    // output TMA box width: widest swizzle span dividing BN (full 128-B lines when possible)
-    pl.out_w = pl.BN % 128 == 0 ? 128 : pl.BN % 64 == 0 ? 64 : pl.BN % 32 == 0 ? 32 : 16;
-    // ring depth vs. output staging: prefer 2 staged tiles while
-    // the operand ring keeps >= 3 stages, else 1
-    const uint32_t stage = (uint32_t)(kBM * kBK + pl.BN * kBK);
-    for (int nbuf : {2, 1}) {
-        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, nbuf).total + 1024;
-        int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
-        if (stages > 8) stages = 8;
-        if (stages < (nbuf == 2 ? 3 : 2)) continue;
-        pl.stages = stages;
-        pl.nbuf = nbuf;
-        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, nbuf).total + 1024;
-        return pl.smem <= kSmemBudget;
+    for (int bn : {256, 128, 192, 96, 64, 32}) {
+        if (N % bn) continue;
+        pl.BN = bn; pl.CS = 1; pl.n_groups = N / bn;
+        if (fit_smem(epi, pl, 3) || fit_smem(epi, pl, 2)) return true;
     }
     return false;
 }

@@ -24,7 +24,7 @@ torch.cuda.synchronize()
 layer.set_trace(None)
 t = buf.cpu().numpy().astype(np.int64)
 print("C", L.C, "T", T, layer.plan())
-EPI = ["top", "bufok", "tfull", "fence", "pre_flush", "flush_bar", "committed", "end", "cfull"]
+EPI = ["top", "bufok", "tfull", "pass1", "mean", "var", "-", "end", "cfull"]
 for k, name in ((0, "FC1"), (1, "FC2")):
     base = t[k * 4096:(k + 1) * 4096]
     nz = base[base > 0]
