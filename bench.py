@@ -248,6 +248,13 @@ def main():
     for _ in range(max(args.warmup, 0)):
         step(relu_layers)
     torch.cuda.synchronize(dev)
+    # guard against timing a no-op: every layer's output must be a live LayerNorm
+    # output (non-constant rows, spread over the int8 grid); parity itself is the
+    # tests' job (tests/test_parity_gpu.py), not the bench's
+    for (L, T, _), y in zip(spec, ys):
+        yf = y[: min(T, 4096)].float()
+        if not (yf.std(dim=1).min().item() > 1.0 and yf.abs().max().item() > 16):
+            raise RuntimeError(f"layer C={L.C}: output looks dead (kernel not executed?)")
 
     # ---- timed region: exactly K steps --------------------------------------------------------------
     for l in relu_layers:
@@ -332,14 +339,14 @@ def main():
         cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
                "sample": f"every {args.cpu_stride}th token of each of the 4 layers ({tok} tokens, {t:.1f} s)"}
 
-    plan = relu_layers[-1].plan()
+    plans = [l.plan() for l in relu_layers]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "s8", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "layers": [{"C": L.C, "H": L.H, "T": T} for (L, T, _) in spec],
                            "act": "relu (GELU-less, b1=None)", "parallelism": f"token-shard weak x{ws}",
-                           "l2": "flushed between steps (256 MiB write, untimed)", "plan_C768": plan},
+                           "l2": "flushed between steps (256 MiB write, untimed)", "plans": plans},
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "swin_mlp_int8_run_host"},

@@ -190,6 +190,14 @@ __device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uin
                  ::"r"(remote_addr), "l"(__double_as_longlong(v)), "r"(remote_bar) : "memory");
 }
 
+__device__ __forceinline__ void st_async_val(uint32_t remote_addr, double v, uint32_t remote_bar) {
+    st_async_f64(remote_addr, v, remote_bar);
+}
+__device__ __forceinline__ void st_async_val(uint32_t remote_addr, float v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 ::"r"(remote_addr), "r"(__float_as_uint(v)), "r"(remote_bar) : "memory");
+}
+
 // ------------------------------------------------------------------ global
 __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
     int4 r;

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -47,7 +48,7 @@ swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
 struct Plan {
     void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
     int epi = 0, threads = 0;
-    int BN = 0, CS = 1, stages = 0, n_groups = 1, nbuf = 1, out_w = 16;
+    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1;
     uint32_t smem = 0;
     int max_clusters = 0;
 };
@@ -91,9 +92,12 @@ constexpr uint32_t kSmemBudget = 227 * 1024;
 
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
 
-template <int EPI, int... Fs>
-KernelFn pick(int f, std::integer_sequence<int, Fs...>) {
-    static const KernelFn table[] = {mlp_gemm_kernel<EPI, Fs>...};
+// table index bit 3 means kSmallK for op #5 and kS64 for op #6
+template <int EPI, int I>
+constexpr int flags_of() { return (I & 7) | ((I & 8) ? (EPI == EP6_LN ? kS64 : kSmallK) : 0); }
+template <int EPI, int... Is>
+KernelFn pick(int f, std::integer_sequence<int, Is...>, bool) {
+    static const KernelFn table[] = {mlp_gemm_kernel<EPI, flags_of<EPI, Is>()>...};
     return table[f];
 }
 
@@ -101,9 +105,13 @@ KernelFn pick(int f, std::integer_sequence<int, Fs...>) {
 // point, output zero point, LN precision) — no predicated-off work in the hot loop.
 KernelFn kernel_for(int epi, int flags) {
     switch (epi) {
-        case EP5_RELU: return pick<EP5_RELU>(flags & 7, std::make_integer_sequence<int, 8>{});
-        case EP5_GELU: return pick<EP5_GELU>(flags & 7, std::make_integer_sequence<int, 8>{});
-        default: return pick<EP6_LN>(flags & 15, std::make_integer_sequence<int, 16>{});
+        // op #5: bias, zero points, small-K conversion (no fp64 LN); op #6: bias, zero
+        // points, fp64 LN (its K = H is never small)
+        case EP5_RELU: return pick<EP5_RELU>((flags & 7) | ((flags & kSmallK) ? 8 : 0),
+                                             std::make_integer_sequence<int, 16>{}, true);
+        case EP5_GELU: return pick<EP5_GELU>((flags & 7) | ((flags & kSmallK) ? 8 : 0),
+                                             std::make_integer_sequence<int, 16>{}, true);
+        default: return pick<EP6_LN>(flags & 15, std::make_integer_sequence<int, 16>{}, false);
     }
 }
 
@@ -142,24 +150,31 @@ bool fit_smem(int epi, Plan& pl, int min_stages) {
     // ring depth vs. output staging: prefer 2 staged tiles while the operand ring
     // keeps >= 3 stages, else 1 (op #6 always stages 2: one per ping-pong group)
     const uint32_t stage = (uint32_t)(kBM * kBK + pl.BN * kBK);
-    for (int nbuf : {2, 1}) {
-        if (epi == EP6_LN && nbuf != 2) continue;
-        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, nbuf).total + 1024;
+    // G ping-pong groups / accumulator buffers / staging tiles: 4 when 4*BN TMEM
+    // columns fit (smaller tiles -> more in flight), else 2
+    for (int xs : {1, 0}) {
+    if (epi != EP6_LN && xs == 0) continue;
+    for (int G : {4, 2}) {
+        if (G * pl.BN > 512) continue;
+        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs).total + 1024;
         if (extra >= kSmemBudget) continue;
         int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
         if (stages > 8) stages = 8;
         if (stages < min_stages) continue;
         pl.stages = stages;
-        pl.nbuf = nbuf;
-        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, nbuf).total + 1024;
+        pl.G = G;
+        pl.xstage = xs;
+        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs).total + 1024;
         if (pl.smem <= kSmemBudget) return true;
+    }
     }
     return false;
 }
 
-bool make_plan(int epi, int N, bool full_row, Plan& pl) {
+bool make_plan(int epi, int N, bool full_row, Plan& pl, int ebytes = 4) {
     pl = Plan();
     pl.epi = epi;
+    pl.ebytes = ebytes;
     pl.threads = kernel_threads(epi);
     if (full_row) {
         for (int cs : {1, 2, 4, 8}) {
@@ -204,6 +219,11 @@ swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMa
     cfg.attrs = at;
     cfg.numAttrs = 1;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, pl.fn, ta, tb, to, tx, a));
+    static const bool sync_check = std::getenv("SWIN_MLP_SYNC_CHECK") != nullptr;
+    if (sync_check) {   // debug: surface asynchronous kernel faults at the launch that caused them
+        CUDA_TRY(cudaStreamSynchronize(stream));
+        CUDA_TRY(cudaGetLastError());
+    }
     return SWIN_MLP_OK;
 }
 
@@ -376,7 +396,7 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
 
     // tile / cluster plans
     if (!make_plan(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU, H, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
-    if (!make_plan(EP6_LN, C, true, h->p2))
+    if (!make_plan(EP6_LN, C, true, h->p2, d.ln_fp64 ? 8 : 4))
         return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC2 tile plan for C=%d (needs C = CS*BN, BN%%16==0, BN<=256, CS in 1,2,4,8)", C));
 
     swin_mlp_status_t st;
@@ -396,8 +416,11 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     if (d.h_zero_point) H_TRY(upload(h, zc2, &h->zc2));
     H_TRY(encode_2d(&h->tm_w1, h->w1, H, C, C, (uint32_t)h->p1.BN));
     H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H, (uint32_t)h->p2.BN));
+    // |A1| <= (128 + |z_x|) * 127 * C: below 2^22 the exact magic-number int->float applies
+    const bool small_k1 = (int64_t)(128 + std::abs(d.x_zero_point)) * 127 * C < (int64_t(1) << 22);
     h->p1.fn = kernel_for(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU,
-                          (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (d.h_zero_point ? kZqNz : 0));
+                          (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (d.h_zero_point ? kZqNz : 0) |
+                          (small_k1 ? kSmallK : 0));
     h->p2.fn = kernel_for(EP6_LN, (d.b2 ? kHasB : 0) | (d.h_zero_point ? kHasZc : 0) |
                                       (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0));
     H_TRY(prepare(h->p1, h->num_sms));
@@ -446,17 +469,17 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     const int64_t m_tiles = (T + kBM - 1) / kBM;
 
     GemmArgs a1 = {};
-    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.nbuf = h->p1.nbuf; a1.out_w = h->p1.out_w;
+    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.G = h->p1.G; a1.out_w = h->p1.out_w;
     a1.n_groups = h->p1.n_groups; a1.num_units = m_tiles * h->p1.n_groups; a1.ldo = H;
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
     a1.acc_tap = dbg ? acc1 : nullptr;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
 
     GemmArgs a2 = {};
-    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.nbuf = h->p2.nbuf; a2.out_w = h->p2.out_w;
+    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.xstage = h->p2.xstage; a2.x = x; a2.out_w = h->p2.out_w;
     a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
-    a2.x = x; a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
+    a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
     a2.resid = residual; a2.resid_out = residual_out;
     a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
     a2.acc_tap = dbg ? acc2 : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
@@ -588,10 +611,11 @@ swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
 }
 
 // Test/bench introspection: the launch plan chosen for this layer.
-int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out8) {
-    if (!h || !out8) return -1;
-    out8[0] = h->p1.BN; out8[1] = h->p1.CS; out8[2] = h->p1.stages; out8[3] = h->p1.max_clusters;
-    out8[4] = h->p2.BN; out8[5] = h->p2.CS; out8[6] = h->p2.stages; out8[7] = h->p2.max_clusters;
+int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
+    if (!h || !out10) return -1;
+    out10[0] = h->p1.BN; out10[1] = h->p1.CS; out10[2] = h->p1.stages; out10[3] = h->p1.max_clusters;
+    out10[4] = h->p2.BN; out10[5] = h->p2.CS; out10[6] = h->p2.stages; out10[7] = h->p2.max_clusters;
+    out10[8] = h->p1.G; out10[9] = h->p2.G;
     return 0;
 }
 

@@ -47,6 +47,12 @@ def test_sm100a_code_only():
     out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     assert "UTCIMMA" in out and "UTMALDG" in out and "LDTM" in out
+    # every kernel instantiation carries the tcgen05 main loop (none folded to EXIT)
+    funcs = out.split("Function : ")[1:]
+    assert len(funcs) >= 16
+    for f in funcs:
+        name = f.split()[0]
+        assert "UTCIMMA" in f and "LDTM" in f and "UTMASTG" in f, name
 
 
 def _desc(P, **kw):

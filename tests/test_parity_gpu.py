@@ -211,3 +211,28 @@ def test_multiple_handles_interleaved(dev):
         y = layer(torch.from_numpy(X).to(dev)).cpu().numpy()
         torch.cuda.synchronize()
         _tier_int8(y, oracle.mlp(L, X), what=f"C={L.C}")
+
+
+@pytest.mark.parametrize("C", [96, 256, 384])
+def test_parity_extreme_accumulators(dev, C):
+    """Saturated inputs drive |A1| to its bound (128*127*C: 4.16e6 at C=256, just under
+    the 2^22 limit of the exact small-K int->float path) and saturate Hq and Y."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(C, 9100 + C)
+    rng = np.random.default_rng(C)
+    L.w1 = np.where(rng.random(L.w1.shape) < 0.5, 127, -127).astype(np.int8)
+    L.w1[: L.H // 2] = 127                       # half the hidden units see +127 everywhere
+    L.w2 = np.where(rng.random(L.w2.shape) < 0.5, 127, -127).astype(np.int8)
+    T = 300
+    X = np.full((T, C), -128, np.int8)
+    X[T // 2:] = 127
+    # near-constant LayerNorm rows (|mean| >> std): exercises the corrected two-pass fp32 variance
+    layer = SwinMlpInt8Layer(L, device=0)
+    taps = layer.run_debug(torch.from_numpy(X).to(dev))
+    torch.cuda.synchronize()
+    a1 = oracle.gemm_i8(X, L.w1, L.z_x)
+    assert np.abs(a1).max() >= 128 * 127 * C * 0.99
+    np.testing.assert_array_equal(taps["acc1"].cpu().numpy(), a1)
+    m1, ih, m2, iy = oracle.fold_constants(L.s_x, L.s_w1, L.s_h, L.s_w2, L.s_y)
+    np.testing.assert_array_equal(taps["hidden"].cpu().numpy(), oracle.ep5(a1, m1, L.b1, ih, L.z_h))
+    _tier_int8(taps["y"].cpu().numpy(), oracle.mlp(L, X), what="Y extreme")

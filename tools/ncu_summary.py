@@ -1,0 +1,115 @@
+"""Summarise the round's ncu evidence into profiles/.
+
+  python tools/ncu_summary.py <round-tag>
+
+Reads gpurun_out/launches_<tag>.csv (the gpu__time_duration launch list of
+`bench.py --steps 2 --warmup 1 --pairs 1 --no-cpu`) and gpurun_out/full_stage{0..3}.ncu-rep
+(`ncu --set full` of tools/prof_layer.py <stage>: FC1 then FC2 of the 2nd run),
+writes profiles/<tag>_launches.csv, profiles/<tag>_ncu_summary.md and
+profiles/ncu_traffic.json (DRAM bytes per launch, keyed like bench.py's kernels).
+"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+
+tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+out = os.path.join(ROOT, "profiles")
+os.makedirs(out, exist_ok=True)
+lines = []
+
+# ---- launch list
+src = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
+if os.path.exists(src):
+    shutil.copy(src, os.path.join(out, f"{tag}_launches.csv"))
+    txt = open(src).read()
+    body = txt[txt.index('"ID"'):] if '"ID"' in txt else txt
+    rows = list(csv.DictReader(io.StringIO(body)))
+    per = {}
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"]
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "")
+        us = v / 1000.0 if unit == "ns" else v if unit == "us" else v * 1000.0 if unit == "ms" else v
+        key = "mlp_gemm_kernel" if "mlp_gemm_kernel" in name else name[:60]
+        per.setdefault(key, []).append(us)
+    lines.append(f"## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, {tag})\n")
+    lines.append("Cold-cache, serialised per-launch times: compare shares, not absolutes.\n")
+    lines.append("| kernel | launches | total us | mean us |")
+    lines.append("|---|---|---|---|")
+    tot = sum(sum(v) for v in per.values())
+    for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.2f} |")
+    ours = per.get("mlp_gemm_kernel", [])
+    if ours:
+        # the bench's timed steps: 8 launches per step; the last 16 mlp launches before e2e are 2 steps
+        lines.append(f"\nOur kernels: {len(ours)} launches, {sum(ours):.1f} us of {tot:.1f} us listed "
+                     f"({sum(ours)/tot:.1%}; the rest is the L2-flush fill, copies and torch setup).\n")
+        step = ours[8:16] if len(ours) >= 16 else ours[:8]
+        names = []
+        for L, T, _ in synth.swin_t_batch64_layers():
+            names += [f"fc1_relu_q[C={L.C},T={T}]", f"fc2_ln_q[C={L.C},T={T}]"]
+        lines.append("Per-launch share of one timed step (launches 9-16):\n")
+        lines.append("| launch | us | share |")
+        lines.append("|---|---|---|")
+        for n, us in zip(names, step):
+            lines.append(f"| {n} | {us:.2f} | {us/sum(step):.1%} |")
+
+# ---- full captures
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+           "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "lts__t_bytes.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+           "launch__grid_size", "launch__cluster_dim_x"]
+traffic = {}
+lines.append("\n## `ncu --set full` captures (tools/prof_layer.py <stage>, 2nd run; one launch each)\n")
+lines.append("| kernel | us | DRAM read MB | DRAM write MB | L2 bytes MB | tensor(imma) % active | issue % | L2 % | regs | grid | cluster |")
+lines.append("|---|---|---|---|---|---|---|---|---|---|---|")
+specs = synth.swin_t_batch64_layers()
+for st in range(4):
+    rep = os.path.join(ROOT, "gpurun_out", f"full_stage{st}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    shutil.copy(rep, os.path.join(out, f"{tag}_full_stage{st}.ncu-rep"))
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rr[0], rr[1], rr[2:]
+    L, T, _ = specs[st]
+    for j, row in enumerate(data):
+        d = {h: row[i] for i, h in enumerate(hdr)}
+        u = {h: units[i] for i, h in enumerate(hdr)}
+
+        def val(m, scale_to=None):
+            v = float(d.get(m, "nan").replace(",", "") or "nan")
+            un = u.get(m, "")
+            if scale_to == "MB":
+                f = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1, "Gbyte": 1e3}.get(un, 1)
+                return v * f
+            if scale_to == "us":
+                f = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(un, 1)
+                return v * f
+            return v
+        name = f"{'fc1_relu_q' if j == 0 else 'fc2_ln_q'}[C={L.C},T={T}]"
+        rd, wr = val("dram__bytes_read.sum", "MB"), val("dram__bytes_write.sum", "MB")
+        traffic[name] = (rd + wr) * 1e6
+        lines.append(f"| {name} | {val('gpu__time_duration.sum', 'us'):.1f} | {rd:.1f} | {wr:.1f} | "
+                     f"{val('lts__t_bytes.sum', 'MB'):.1f} | "
+                     f"{val('sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active'):.1f} | "
+                     f"{val('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
+                     f"{val('lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
+                     f"{d.get('launch__registers_per_thread', '')} | {d.get('launch__grid_size', '')} | "
+                     f"{d.get('launch__cluster_dim_x', '')} |")
+json.dump(traffic, open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
+open(os.path.join(out, f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
