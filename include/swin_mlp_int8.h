@@ -160,10 +160,10 @@ swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, fl
  * loader (buffer acquired, constants published)).  trace = NULL disables. */
 swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_t cta);
 
-/* Introspection: the launch plan of this layer, out10[10] = {FC1 BN, FC1 cluster size,
+/* Introspection: the launch plan of this layer, out10[12] = {FC1 BN, FC1 cluster size,
  * FC1 stages, FC1 max co-resident clusters, FC2 BN, FC2 cluster size, FC2 stages,
- * FC2 max clusters, FC1 epilogue groups, FC2 epilogue groups}.  Returns 0, or -1
- * on a NULL argument. */
+ * FC2 max clusters, FC1 epilogue groups, FC2 epilogue groups, FC1 resident weights,
+ * FC2 resident weights}.  Returns 0, or -1 on a NULL argument. */
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
 
 /* Release the handle's device memory.  No run may be in flight. NULL is OK. */

@@ -73,6 +73,8 @@ struct GemmArgs {
     int32_t stages;        // smem ring depth
     int32_t G;             // ping-pong groups = accumulator buffers = staging tiles (2 or 4)
     int32_t xstage;        // op #6: residual x tiles staged in smem by TMA (else read from x)
+    int32_t resb;          // B (weights) resident in smem for the whole kernel (requires mt_major)
+    int32_t mt_major;      // tile order: the cluster's m-tiles with the n-groups innermost
     int32_t out_w;         // output TMA box width in bytes (128/64/32/16; swizzle of the same width)
     int32_t n_groups;      // column groups of CS*BN columns
     int64_t num_units;     // m_tiles * n_groups
@@ -107,19 +109,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 struct SmemLayout {
-    uint32_t a, b, out, xres, consts, bars, tmem_slot, red, xbuf, total;
+    uint32_t a, b, bres, out, xres, consts, bars, tmem_slot, red, xbuf, total;
 };
-__host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages + 7u * kGMax + 2u * kGMax; }
+__host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages + 7u * kGMax + 2u * kGMax + 1u; }
 
 // ebytes: size of one exchanged row statistic (4: fp32 LN, 8: fp64 LN);
 // xstage: op #6 stages the residual x tiles in smem (else pass 1 reads x from global)
+// resb_bytes: resident-B region (0 when B streams through the ring with A)
 __host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int stages, int G, int ebytes = 4,
-                                                  int xstage = 1) {
+                                                  int xstage = 1, uint32_t resb_bytes = 0) {
     SmemLayout L;
     const uint32_t tile = (uint32_t)BN * kBM;
     L.a = 0;
     L.b = L.a + (uint32_t)stages * kBM * kBK;
-    L.out = L.b + (uint32_t)stages * (uint32_t)BN * kBK;          // [G] output staging tiles
+    L.bres = L.b + (resb_bytes ? 0u : (uint32_t)stages * (uint32_t)BN * kBK);
+    L.out = L.bres + resb_bytes;                                   // [G] output staging tiles
     L.xres = L.out + (uint32_t)G * tile;                           // op #6: [G] residual x tiles
     L.consts = L.xres + (epi == EP6_LN && xstage ? (uint32_t)G * tile : 0u); // [G][kNConst][BN] fp32
     L.bars = L.consts + (uint32_t)G * kNConst * (uint32_t)BN * 4u;
@@ -207,7 +211,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t lgG = G == 4 ? 2u : 1u;
     const uint32_t tile_warps = kEpiWarps / G;
     using acc_t = typename std::conditional<STATS64, double, float>::type;   // LN statistics type
-    const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage);
+    const uint32_t resb_bytes = p.resb ? (uint32_t)p.n_groups * (uint32_t)((p.K + kBK - 1) / kBK) * (uint32_t)BN * kBK : 0u;
+    const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage, resb_bytes);
     const uint32_t tile_bytes = (uint32_t)BN * kBM;
     const uint32_t sA = base + L.a, sB = base + L.b;
     const uint32_t bar_full = base + L.bars;              // [stages] operands landed (count 1 + tx)
@@ -220,6 +225,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t bar_xfull = bar_sfree + 8u * kGMax;    // [G] op #6 x tile landed (count 1 + tx)
     const uint32_t bar_xfree = bar_xfull + 8u * kGMax;    // [G] op #6 x tile consumed (tile warps)
     const uint32_t bar_xst = bar_xfree + 8u * kGMax;      // [G][pass] op #6 DSMEM row stats (1 + tx)
+    const uint32_t bar_bfull = bar_xst + 16u * kGMax;     // resident B landed (count 1 + tx)
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
     float* consts = reinterpret_cast<float*>(gbase + L.consts);
     acc_t* red = reinterpret_cast<acc_t*>(gbase + L.red);
@@ -252,6 +258,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_init(bar_xst + 16u * i, 1);
             mbar_init(bar_xst + 16u * i + 8u, 1);
         }
+        mbar_init(bar_bfull, 1);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), tmem_cols);
@@ -262,12 +269,31 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     const uint32_t cid = blockIdx.x / CS, nclus = gridDim.x / CS;
     const uint32_t num_units = (uint32_t)p.num_units, n_groups = (uint32_t)p.n_groups;
+    const uint32_t m_tiles = num_units / n_groups;
     const int num_kb = (p.K + kBK - 1) / kBK;
     const uint32_t a_bytes = kBM * kBK, b_bytes = (uint32_t)BN * kBK;
     const uint16_t cmask = (uint16_t)((1u << CS) - 1u);
     const uint32_t W = (uint32_t)p.out_w;
     const uint32_t lgW = 31u - (uint32_t)__clz((int)W);   // W is a power of two
-    auto tile_n0 = [&](uint32_t u) -> int { return (int)(((u % n_groups) * CS + rank) * (uint32_t)BN); };
+    const bool resb = p.resb != 0;
+    // This CTA's tile sequence (identical in every role).  m-major: the cluster
+    // owns m-tiles cid, cid+nclus, ... and walks its n-groups innermost (the A tile
+    // is reused across them; required by resident B).  Otherwise the (m, n) units
+    // are dealt round-robin (more parallelism when there are few m-tiles).
+    const uint32_t my_m = cid < m_tiles ? (m_tiles - cid + nclus - 1) / nclus : 0u;
+    const uint32_t my_tiles = p.mt_major ? my_m * n_groups
+                                         : (cid < num_units ? (num_units - cid + nclus - 1) / nclus : 0u);
+    auto tile_at = [&](uint32_t it, uint32_t& m_tile, uint32_t& ng) {
+        if (p.mt_major) {
+            m_tile = cid + (it / n_groups) * nclus;
+            ng = it % n_groups;
+        } else {
+            const uint32_t u = cid + it * nclus;
+            m_tile = u / n_groups;
+            ng = u % n_groups;
+        }
+    };
+    auto n0_of = [&](uint32_t ng) -> int { return (int)((ng * CS + rank) * (uint32_t)BN); };
 
     // Producer, MMA and store roles run on the whole warp with warp-uniform control
     // flow (addresses and descriptors stay in uniform registers); one elected lane
@@ -275,27 +301,56 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (warp == 0) {
         // ============================ TMA producer ============================
         int s = 0;
-        uint32_t ph = 0, tu = 0;
+        uint32_t ph = 0;
         const int a_rows = kBM / (int)CS;
-        for (uint32_t u = cid; u < num_units; u += nclus, ++tu) {
-            const int n0 = tile_n0(u);
-            const int row0 = (int)((u / n_groups) * kBM);
-            for (int kb = 0; kb < num_kb; ++kb) {
-                mbar_wait(bar_empty + 8u * s, ph ^ 1u);
-                if (elect_one()) {
-                    if (trc && kb == 0 && tu < 512) trc[2 * tu] = gtimer();
-                    mbar_arrive_expect_tx(bar_full + 8u * s, a_bytes + b_bytes);
-                    tma_load_2d(&tmB, sB + (uint32_t)s * b_bytes, bar_full + 8u * s, kb * kBK, n0);
-                    if (CS == 1)
-                        tma_load_2d(&tmA, sA + (uint32_t)s * a_bytes, bar_full + 8u * s, kb * kBK, row0);
-                    else
-                        tma_load_2d_mc(&tmA, sA + (uint32_t)s * a_bytes + rank * (uint32_t)a_rows * kBK,
-                                       bar_full + 8u * s, kb * kBK, row0 + (int)rank * a_rows, cmask);
-                }
-                __syncwarp();
-                if (++s == stages) { s = 0; ph ^= 1u; }
+        auto load_a = [&](int kb, int row0) {
+            if (CS == 1)
+                tma_load_2d(&tmA, sA + (uint32_t)s * a_bytes, bar_full + 8u * s, kb * kBK, row0);
+            else
+                tma_load_2d_mc(&tmA, sA + (uint32_t)s * a_bytes + rank * (uint32_t)a_rows * kBK,
+                               bar_full + 8u * s, kb * kBK, row0 + (int)rank * a_rows, cmask);
+        };
+        if (resb) {
+            // resident B: every (n-group, k-block) weight tile of this CTA, loaded once
+            if (elect_one()) {
+                mbar_arrive_expect_tx(bar_bfull, n_groups * (uint32_t)num_kb * b_bytes);
+                for (uint32_t ng = 0; ng < n_groups; ++ng)
+                    for (int kb = 0; kb < num_kb; ++kb)
+                        tma_load_2d(&tmB, base + L.bres + (ng * (uint32_t)num_kb + (uint32_t)kb) * b_bytes, bar_bfull,
+                                    kb * kBK, n0_of(ng));
             }
-            if (trc && lane == 0 && tu < 512) trc[2 * tu + 1] = gtimer();
+            __syncwarp();
+            // the ring streams A only: one load per (m-tile, k-block)
+            for (uint32_t j = 0; j < my_m; ++j) {
+                const int row0 = (int)((cid + j * nclus) * kBM);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+                    if (elect_one()) {
+                        if (trc && kb == 0 && j < 512) trc[2 * j] = gtimer();
+                        mbar_arrive_expect_tx(bar_full + 8u * s, a_bytes);
+                        load_a(kb, row0);
+                    }
+                    __syncwarp();
+                    if (++s == stages) { s = 0; ph ^= 1u; }
+                }
+            }
+        } else {
+            for (uint32_t it = 0; it < my_tiles; ++it) {
+                uint32_t m_tile, ng;
+                tile_at(it, m_tile, ng);
+                const int n0 = n0_of(ng), row0 = (int)(m_tile * kBM);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+                    if (elect_one()) {
+                        if (trc && kb == 0 && it < 512) trc[2 * it] = gtimer();
+                        mbar_arrive_expect_tx(bar_full + 8u * s, a_bytes + b_bytes);
+                        tma_load_2d(&tmB, sB + (uint32_t)s * b_bytes, bar_full + 8u * s, kb * kBK, n0);
+                        load_a(kb, row0);
+                    }
+                    __syncwarp();
+                    if (++s == stages) { s = 0; ph ^= 1u; }
+                }
+            }
         }
         // Drain: every stage's last fill released by all consumers of the cluster,
         // so no multicast commit can still target this CTA after it exits.
@@ -307,44 +362,71 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // ============================ MMA issuer ==============================
         const uint32_t idesc = idesc_i8(kBM, (uint32_t)BN);
         int s = 0;
-        uint32_t ph = 0, it = 0;
-        for (uint32_t u = cid; u < num_units; u += nclus, ++it) {
+        uint32_t ph = 0;
+        if (resb) mbar_wait(bar_bfull, 0);
+        // one tile: MMAs over its k-blocks starting at ring slot (s0, ph0); with resident B
+        // the n-groups of an m-tile share the A slots (waited by the first, released by the last)
+        auto mma_tile = [&](uint32_t it, uint32_t ng, bool first, bool last, int& ss, uint32_t& pp) {
             const uint32_t buf = it & (G - 1u), aph = (it >> lgG) & 1u;
             mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);
             tc_fence_after();
             if (trc && lane == 0 && it < 256) trc[1024 + 4 * it] = gtimer();
             const uint32_t d = tmem_base + buf * (uint32_t)BN;
             for (int kb = 0; kb < num_kb; ++kb) {
-                mbar_wait(bar_full + 8u * s, ph);
+                if (first) mbar_wait(bar_full + 8u * ss, pp);
                 tc_fence_after();
                 if (trc && lane == 0 && it < 256 && kb == 0) trc[1024 + 4 * it + 1] = gtimer();
-                const uint64_t ad = umma_desc_k128(sA + (uint32_t)s * a_bytes);
-                const uint64_t bd = umma_desc_k128(sB + (uint32_t)s * b_bytes);
+                const uint64_t ad = umma_desc_k128(sA + (uint32_t)ss * a_bytes);
+                const uint64_t bd = umma_desc_k128(resb ? base + L.bres + (ng * (uint32_t)num_kb + (uint32_t)kb) * b_bytes
+                                                        : sB + (uint32_t)ss * b_bytes);
                 const int rem = p.K - kb * kBK;
                 const int nk = rem >= kBK ? 4 : rem / 32;
                 if (elect_one()) {
                     for (int k = 0; k < nk; ++k)
                         mma_i8(d, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
                     if (trc && it < 256 && kb == 0) trc[1024 + 4 * it + 2] = gtimer();
-                    if (CS == 1) mma_commit(bar_empty + 8u * s);
-                    else mma_commit_mc(bar_empty + 8u * s, cmask);
+                    if (last) {
+                        if (CS == 1) mma_commit(bar_empty + 8u * ss);
+                        else mma_commit_mc(bar_empty + 8u * ss, cmask);
+                    }
                 }
                 __syncwarp();
-                if (++s == stages) { s = 0; ph ^= 1u; }
+                if (++ss == stages) { ss = 0; pp ^= 1u; }
             }
             if (elect_one()) mma_commit(bar_tfull + 8u * buf);
             __syncwarp();
             if (trc && lane == 0 && it < 256) trc[1024 + 4 * it + 3] = gtimer();
+        };
+        if (resb) {
+            uint32_t it = 0;
+            for (uint32_t j = 0; j < my_m; ++j) {
+                int ss = s;
+                uint32_t pp = ph;
+                for (uint32_t ng = 0; ng < n_groups; ++ng, ++it) {
+                    ss = s;
+                    pp = ph;
+                    mma_tile(it, ng, ng == 0, ng + 1 == n_groups, ss, pp);
+                }
+                s = ss;
+                ph = pp;
+            }
+        } else {
+            for (uint32_t it = 0; it < my_tiles; ++it) {
+                uint32_t m_tile, ng;
+                tile_at(it, m_tile, ng);
+                mma_tile(it, ng, true, true, s, ph);
+            }
         }
     } else if (warp == 2) {
         // ============================ output store warp =========================
-        uint32_t it = 0;
-        for (uint32_t u = cid; u < num_units; u += nclus, ++it) {
+        for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t sb = it & (G - 1u), sph = (it >> lgG) & 1u;
             mbar_wait(bar_sfull + 8u * sb, sph);
             if (lane == 0) {
-                const int n0 = tile_n0(u);
-                const int32_t row0 = (int32_t)((u / n_groups) * kBM);
+                uint32_t m_tile, ng;
+                tile_at(it, m_tile, ng);
+                const int n0 = n0_of(ng);
+                const int32_t row0 = (int32_t)(m_tile * kBM);
                 const uint32_t src = base + L.out + sb * tile_bytes;
                 for (uint32_t sub = 0; sub < ((uint32_t)BN >> lgW); ++sub)
                     tma_store_2d(&tmO, src + (sub << (lgW + 7u)), n0 + (int)(sub << lgW), row0);
@@ -362,9 +444,10 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // as the previous user of that buffer finished pass 1 (xfree), then copy the
         // per-column constants once the buffer's previous tile is fully drained (tempty).
         const bool load_x = IS_LN && (p.resid == nullptr) && p.xstage;
-        uint32_t it = 0;
-        for (uint32_t u = cid; u < num_units; u += nclus, ++it) {
-            const int n0 = tile_n0(u);
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            uint32_t m_tile, ng;
+            tile_at(it, m_tile, ng);
+            const int n0 = n0_of(ng);
             const uint32_t buf = it & (G - 1u), aph = (it >> lgG) & 1u;
             if (load_x) {
                 mbar_wait(bar_xfree + 8u * buf, aph ^ 1u);
@@ -373,7 +456,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     mbar_arrive_expect_tx(bar_xfull + 8u * buf, tile_bytes);
                     for (uint32_t sub = 0; sub < ((uint32_t)BN >> lgW); ++sub)
                         tma_load_2d(&tmX, dst + (sub << (lgW + 7u)), bar_xfull + 8u * buf, n0 + (int)(sub << lgW),
-                                    (int32_t)((u / n_groups) * kBM));
+                                    (int32_t)(m_tile * kBM));
                 }
                 __syncwarp();
             }
@@ -419,10 +502,10 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const bool grp_leader = ((ew & (tile_warps - 1u)) == 0 && lane == 0);
         const float2 inv2 = make_float2(p.inv_q, p.inv_q);
 
-        uint32_t it = grp;
-        for (uint32_t u = cid + grp * nclus; u < num_units; u += G * nclus, it += G) {
-            const int n0 = tile_n0(u);
-            const uint32_t m_tile = u / n_groups;
+        for (uint32_t it = grp; it < my_tiles; it += G) {
+            uint32_t m_tile, ng;
+            tile_at(it, m_tile, ng);
+            const int n0 = n0_of(ng);
             const uint32_t buf = grp, aph = (it >> lgG) & 1u;
             const uint32_t sbuf = base + L.out + buf * tile_bytes;
             mbar_wait(bar_sfree + 8u * buf, aph ^ 1u);   // staging tile read by its last stores
@@ -519,6 +602,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const bool x_smem = x_res && p.xstage;
                 const uint32_t xtile = base + L.xres + buf * tile_bytes;
                 if (x_smem) mbar_wait(bar_xfull + 8u * buf, aph);   // residual x tile landed
+                if (trc && elected && it < 64) trc[2048 + 16 * it + 6] = gtimer();
                 const float2 sx2 = make_float2(p.s_x, p.s_x);
                 const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
                 const float2 xoff2 = make_float2(xoff, xoff);

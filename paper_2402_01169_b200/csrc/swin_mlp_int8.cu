@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <utility>
 #include <vector>
@@ -48,7 +49,7 @@ swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
 struct Plan {
     void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
     int epi = 0, threads = 0;
-    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1;
+    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0;
     uint32_t smem = 0;
     int max_clusters = 0;
 };
@@ -144,34 +145,46 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
 // full_row: the epilogue needs whole rows (LayerNorm) -> the cluster must
 // cover all N columns (CS * BN == N); otherwise column groups are independent.
 // The first candidate whose shared-memory plan fits wins.
-bool fit_smem(int epi, Plan& pl, int min_stages) {
+bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // output TMA box width: widest swizzle span dividing BN (full 128-B lines when possible)
     pl.out_w = pl.BN % 128 == 0 ? 128 : pl.BN % 64 == 0 ? 64 : pl.BN % 32 == 0 ? 32 : 16;
-    // ring depth vs. output staging: prefer 2 staged tiles while the operand ring
-    // keeps >= 3 stages, else 1 (op #6 always stages 2: one per ping-pong group)
-    const uint32_t stage = (uint32_t)(kBM * kBK + pl.BN * kBK);
-    // G ping-pong groups / accumulator buffers / staging tiles: 4 when 4*BN TMEM
-    // columns fit (smaller tiles -> more in flight), else 2
+    const int num_kb = (K + kBK - 1) / kBK;
+    // Resident B: the CTA's whole weight slice stays in smem and the ring streams
+    // A (activations) only -- 2x deeper prefetch per byte of smem, and the weights
+    // are read from L2 once per CTA instead of once per tile.  Tried first.
+    const uint32_t resb_bytes = (uint32_t)pl.n_groups * (uint32_t)num_kb * (uint32_t)pl.BN * kBK;
+    static const bool no_resb = std::getenv("SWIN_MLP_NO_RESB") != nullptr;   // debug / A-B switch
+    for (int rb : {1, 0}) {
+    if (rb && no_resb) continue;
+    // output staging: G ping-pong groups / accumulator buffers / staging tiles, 4 when
+    // 4*BN TMEM columns fit (more tiles in flight), else 2; op #6 also prefers its
+    // residual x tiles staged in smem
     for (int xs : {1, 0}) {
     if (epi != EP6_LN && xs == 0) continue;
     for (int G : {4, 2}) {
         if (G * pl.BN > 512) continue;
-        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs).total + 1024;
+        const uint32_t rbb = rb ? resb_bytes : 0u;
+        const uint32_t stage = (uint32_t)(kBM * kBK) + (rb ? 0u : (uint32_t)pl.BN * kBK);
+        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb).total + 1024;
         if (extra >= kSmemBudget) continue;
         int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
         if (stages > 8) stages = 8;
-        if (stages < min_stages) continue;
+        int need = min_stages;
+        if (rb) need = std::max(need, pl.n_groups > 1 ? num_kb + 2 : 3);   // an m-tile's k-blocks stay resident
+        if (stages < need) continue;
         pl.stages = stages;
         pl.G = G;
         pl.xstage = xs;
-        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs).total + 1024;
+        pl.resb = rb;
+        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb).total + 1024;
         if (pl.smem <= kSmemBudget) return true;
+    }
     }
     }
     return false;
 }
 
-bool make_plan(int epi, int N, bool full_row, Plan& pl, int ebytes = 4) {
+bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
     pl = Plan();
     pl.epi = epi;
     pl.ebytes = ebytes;
@@ -182,28 +195,29 @@ bool make_plan(int epi, int N, bool full_row, Plan& pl, int ebytes = 4) {
             const int bn = N / cs;
             if (bn > 256 || bn % 16) continue;
             pl.BN = bn; pl.CS = cs; pl.n_groups = 1;
-            if (fit_smem(epi, pl, 3)) return true;   // prefer a >= 3-deep operand ring
+            if (fit_smem(epi, pl, 3, K)) return true;   // prefer a >= 3-deep operand ring
         }
         for (int cs : {1, 2, 4, 8}) {
             if (N % cs) continue;
             const int bn = N / cs;
             if (bn > 256 || bn % 16) continue;
             pl.BN = bn; pl.CS = cs; pl.n_groups = 1;
-            if (fit_smem(epi, pl, 2)) return true;
+            if (fit_smem(epi, pl, 2, K)) return true;
         }
         return false;
     }
     for (int bn : {256, 128, 192, 96, 64, 32}) {
         if (N % bn) continue;
         pl.BN = bn; pl.CS = 1; pl.n_groups = N / bn;
-        if (fit_smem(epi, pl, 3) || fit_smem(epi, pl, 2)) return true;
+        if (fit_smem(epi, pl, 3, K) || fit_smem(epi, pl, 2, K)) return true;
     }
     return false;
 }
 
 swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                          const CUtensorMap& tx, const GemmArgs& a, cudaStream_t stream) {
-    const int64_t units = a.num_units;
+    // independent work items: m-tiles in m-major order, (m, n) units otherwise
+    const int64_t units = a.mt_major ? a.num_units / a.n_groups : a.num_units;
     int64_t clusters = units < pl.max_clusters ? units : pl.max_clusters;
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
@@ -395,8 +409,8 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     }
 
     // tile / cluster plans
-    if (!make_plan(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU, H, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
-    if (!make_plan(EP6_LN, C, true, h->p2, d.ln_fp64 ? 8 : 4))
+    if (!make_plan(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU, H, C, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
+    if (!make_plan(EP6_LN, C, H, true, h->p2, d.ln_fp64 ? 8 : 4))
         return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC2 tile plan for C=%d (needs C = CS*BN, BN%%16==0, BN<=256, CS in 1,2,4,8)", C));
 
     swin_mlp_status_t st;
@@ -469,14 +483,18 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     const int64_t m_tiles = (T + kBM - 1) / kBM;
 
     GemmArgs a1 = {};
-    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.G = h->p1.G; a1.out_w = h->p1.out_w;
+    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.G = h->p1.G; a1.resb = h->p1.resb;
+    a1.mt_major = h->p1.resb ? 1 : 0;   // resident B needs the m-major order; otherwise deal (m, n) units
+    a1.out_w = h->p1.out_w;
     a1.n_groups = h->p1.n_groups; a1.num_units = m_tiles * h->p1.n_groups; a1.ldo = H;
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
     a1.acc_tap = dbg ? acc1 : nullptr;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
 
     GemmArgs a2 = {};
-    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.xstage = h->p2.xstage; a2.x = x; a2.out_w = h->p2.out_w;
+    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.xstage = h->p2.xstage; a2.x = x;
+    a2.out_w = h->p2.out_w;
+    a2.resb = h->p2.resb; a2.mt_major = 1;   // op #6: one n-group per cluster
     a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
     a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
@@ -612,10 +630,11 @@ swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
 
 // Test/bench introspection: the launch plan chosen for this layer.
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
-    if (!h || !out10) return -1;
+    if (!h || !out10) return -1;  // out10 holds 12 entries
     out10[0] = h->p1.BN; out10[1] = h->p1.CS; out10[2] = h->p1.stages; out10[3] = h->p1.max_clusters;
     out10[4] = h->p2.BN; out10[5] = h->p2.CS; out10[6] = h->p2.stages; out10[7] = h->p2.max_clusters;
     out10[8] = h->p1.G; out10[9] = h->p2.G;
+    out10[10] = h->p1.resb; out10[11] = h->p2.resb;
     return 0;
 }
 
