@@ -178,6 +178,7 @@ def main():
     import synth
     import paper_2402_01169_b200 as P
     from paper_2402_01169_b200 import SwinMlpInt8Layer
+    from paper_2402_01169_b200.dist import broadcast_layer
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -187,19 +188,10 @@ def main():
 
     # ---- layers: rank 0 generates, weights broadcast once over NCCL --------------------------------
     spec = layers_spec(args.batch, synth.ACT_RELU)
-    names = ["w1", "s_w1", "w2", "s_w2", "b2", "gamma", "beta"]
     relu_layers, gelu_layers, xs_dev, xs_host, ys, T_list = [], [], [], [], [], []
     for li, (L, T, xseed) in enumerate(spec):
-        dev_arrays = {}
-        for n in names:
-            a = getattr(L, n)
-            t = torch.from_numpy(np.ascontiguousarray(a)).to(dev) if rank == 0 else \
-                torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
-            if ws > 1:
-                dist.broadcast(t, 0)
-            dev_arrays[n] = t
-        for n, t in dev_arrays.items():
-            setattr(L, n, t)          # create() copies from device pointers
+        if ws > 1:
+            broadcast_layer(L, dev)   # create() copies from the device tensors
         relu_layers.append(SwinMlpInt8Layer(L, device=local))
         L.act = synth.ACT_GELU
         gelu_layers.append(SwinMlpInt8Layer(L, device=local))
