@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--pairs", type=int, default=30, help="interleaved ReLU/GELU paired trials")
-    ap.add_argument("--cpu-stride", type=int, default=8, help="cpu_baseline samples every n-th token")
+    ap.add_argument("--cpu-stride", type=int, default=1, help="cpu_baseline samples every n-th token")
     ap.add_argument("--ref-stride", type=int, default=64, help="--impl reference samples every n-th token")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()

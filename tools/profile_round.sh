@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round profile capture on the GPU box (one GPU).  usage: bash tools/profile_round.sh <tag>
+# Every ncu pass runs only after the same command exited 0 without ncu.
+set -u
+tag=${1:-r1}
+o=gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > $o/build_$tag.log 2>&1 || exit 1
+python bench.py --steps 2 --warmup 3 --pairs 1 --no-cpu > $o/plain_bench_$tag.log 2>&1 || exit 2
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches_$tag.csv \
+    python bench.py --steps 2 --warmup 3 --pairs 1 --no-cpu > $o/ncu_launch_$tag.log 2>&1
+for s in 0 1 2 3; do
+  python tools/prof_layer.py $s 2 > $o/plain_${tag}_$s.log 2>&1 || continue
+  ncu --set full --clock-control none --import-source on -k regex:mlp_gemm_kernel -s 2 -c 2 \
+      -o $o/full_stage$s -f python tools/prof_layer.py $s 2 > $o/ncu_full_${tag}_$s.log 2>&1
+done
+for s in 0 1 2 3; do python tools/trace_layer.py $s > $o/trace_${tag}_$s.log 2>&1; done
+echo done
