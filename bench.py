@@ -264,12 +264,16 @@ def main():
     peaks = load_peaks()
     int8_peak_tops = 2.0 * peaks["bf16_burst"]      # nominal int8/bf16 dense ratio 4.5/2.25 = 2
     kernels = []
-    for (L, T, _), (f1, f2, n) in zip(spec, prof):
+    for (L, T, _), (f1, f2, n), l in zip(spec, prof, relu_layers):
         ops = 2.0 * T * L.C * L.H
-        for name, ms in (("fc1_relu_q", f1), ("fc2_ln_q", f2)):
+        if l.plan()["fused"]:
+            parts = (("fused_mlp", f1 + f2, 2.0 * ops),)
+        else:
+            parts = (("fc1_relu_q", f1, ops), ("fc2_ln_q", f2, ops))
+        for name, ms, kops in parts:
             avg_s = ms / max(n, 1) / 1e3
             kernels.append({"kernel": f"{name}[C={L.C},T={T}]", "avg_us": avg_s * 1e6,
-                            "tops": ops / avg_s / 1e12 if avg_s > 0 else None, "ops": ops})
+                            "tops": kops / avg_s / 1e12 if avg_s > 0 else None, "ops": kops})
     dom = max(kernels, key=lambda k: k["avg_us"])
     step_us = 1e3 * sum(per_step) / args.steps
     share = dom["avg_us"] / step_us
@@ -284,7 +288,8 @@ def main():
                 "unit": "TOPS", "frac": dom["tops"] / int8_peak_tops, "traffic": traffic,
                 "share_of_step": share,
                 "peak_source": f"{peaks['src']} bf16_tflops {peaks['bf16_burst']} x 2 (int8:bf16 nominal 4.5:2.25), burst",
-                "algorithmic": "2*T*C*H int8 MACs-as-ops per launch (SURVEY §8(d): 16*C^2 ops per token per layer)",
+                "algorithmic": "2*T*C*H ops per GEMM per launch (fused_mlp: both GEMMs, 4*T*C*H); "
+                               "SURVEY §8(d): 16*C^2 ops per token per layer",
                 "step_frac": (sum(k["ops"] for k in kernels) / (step_us / 1e6) / 1e12) / int8_peak_tops,
                 "kernels": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in kk.items() if k != "ops"}
                             for kk in kernels]}
@@ -342,7 +347,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "swin_mlp_int8_run_host"},
-                "gpu_launches": sum(n for (_, _, n) in prof) * 2,
+                "gpu_launches": sum(n * P.swin_mlp_int8_launches_per_run(l.handle) for (_, _, n), l in zip(prof, relu_layers)),
                 "relu_vs_gelu": relu_gelu,
                 "tensor_frac_of_step": roofline["step_frac"],
                 "clocks": sampler.result()}

@@ -98,7 +98,8 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
 
 /* Bytes of caller-provided device workspace `run` needs for T tokens
  * (the int8 hidden tensor Hq, [T][H], 128-byte aligned).  Returns 0 for a
- * NULL handle or T <= 0. */
+ * NULL handle, T <= 0, or a layer on the one-kernel plan (C <= 256: the hidden
+ * tile stays in shared memory; `run` then accepts workspace == NULL). */
 size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T);
 
 /* The hot path: Y = layer(X) for T tokens, stream-ordered, asynchronous.
@@ -160,10 +161,13 @@ swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, fl
  * loader (buffer acquired, constants published)).  trace = NULL disables. */
 swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_t cta);
 
-/* Introspection: the launch plan of this layer, out10[12] = {FC1 BN, FC1 cluster size,
+/* Introspection: the launch plan of this layer, out10[16] = {FC1 BN, FC1 cluster size,
  * FC1 stages, FC1 max co-resident clusters, FC2 BN, FC2 cluster size, FC2 stages,
  * FC2 max clusters, FC1 epilogue groups, FC2 epilogue groups, FC1 resident weights,
- * FC2 resident weights}.  Returns 0, or -1 on a NULL argument. */
+ * FC2 resident weights, one-kernel plan used (C <= 256, H % 128 == 0; 1/0), its weight
+ * ring depth (0 = weights resident in smem), its hidden-tile buffers, its FC1 TMEM
+ * buffers}.  Entries 0-11 describe the two-kernel plan, which runs when entry 12 is 0.
+ * Returns 0, or -1 on a NULL argument. */
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
 
 /* Release the handle's device memory.  No run may be in flight. NULL is OK. */

@@ -12,15 +12,17 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC_DIR = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(SRC_DIR, "swin_mlp_int8.cu")]
-DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("mlp_kernels.cuh", "sm100_ptx.cuh")] + \
+SOURCES = [os.path.join(SRC_DIR, f) for f in ("swin_mlp_int8.cu", "fused_mlp.cu")]
+# (source, extra flags, object) — fused_mlp.cu is compiled once per instantiation part
+UNITS = [(SOURCES[0], [], "swin_mlp_int8.o")] + \
+    [(SOURCES[1], [f"-DFUSED_PART={k}"], f"fused_mlp_{k}.o") for k in range(4)]
+DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("mlp_kernels.cuh", "sm100_ptx.cuh", "fused_mlp.cuh")] + \
     [os.path.join(ROOT, "include", "swin_mlp_int8.h")]
 LIB = os.path.join(HERE, "libswin_mlp_int8.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-fmad=false", "-Xcompiler", "-fPIC",
-         "-shared", "-cudart", "static", "-I" + os.path.join(ROOT, "include"),
+         "-fmad=false", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
          # a host-only call from device code compiles to UB (the whole kernel folded to EXIT once)
          "-Xcudafe", "--diag_error=20013", "-Xcudafe", "--diag_error=20014", "-Xcudafe", "--diag_error=20015"]
 
@@ -30,8 +32,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in DEPS):
             return LIB
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB] + SOURCES
-    subprocess.check_call(cmd)
+    # translation units compile in parallel (the kernel instantiations dominate), then link
+    objs, procs = [], []
+    for src, extra, oname in UNITS:
+        obj = os.path.join(SRC_DIR, oname)
+        cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", "-o", obj, src]
+        procs.append((subprocess.Popen(cmd), cmd))
+        objs.append(obj)
+    for p, cmd in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                           "-o", LIB] + objs)
+    for o in objs:
+        os.remove(o)
     return LIB
 
 

@@ -1,0 +1,722 @@
+// fused_mlp.cuh — the whole MLP sub-layer in ONE sm_100a kernel for C <= 256:
+// FC1 -> op #5 -> FC2 -> op #6 per 128-token tile, with the hidden activation
+// Hq never leaving the SM.
+//
+// The paper fuses each elementwise op into the GEMM that produces its input
+// and still round-trips every GEMM output through global
+// memory; on B200 the 4C-wide int8 hidden tile of a 128-token tile is at most
+// 128 KB, so it can live in shared memory and feed FC2 directly:
+//
+//   for each hidden chunk j of 128 columns (H = 128 * NJ):
+//       acc1_j  = X_tile . W1[j]^T                   (tcgen05, TMEM buffer j % NB1)
+//       Hq_j    = op #5(acc1_j)                      (epilogue warps -> smem, SW128 K-major:
+//                                                     exactly FC2's A-operand layout)
+//       acc2   += Hq_j . W2[:, j]^T                  (tcgen05, TMEM columns [0, C))
+//   Y_tile = op #6(acc2, X_tile)                     (LayerNorm rows on chip; Y written
+//                                                     in place over X_tile, then TMA-stored)
+//
+// Same arithmetic, in the same order, as the two-kernel path (mlp_kernels.cuh) and
+// the oracle; HBM traffic falls to the algorithmic 2C bytes per token (X in, Y out).
+//
+// CTA = 640 threads, one per SM, persistent over m-tiles cid, cid + grid, ...:
+//   warp 0       TMA producer: X tiles (2 slots) and, unless resident, the W1 / W2
+//                chunks through a `stages`-deep ring in the MMA's consumption order
+//   warp 1       MMA issuer: FC1 of chunk u + L is issued before FC2 of chunk u
+//                (L = NB1 - 1), so op #5 always has accumulators queued
+//   warp 2       TMEM allocator, then the Y store warp
+//   warp 3       loads the per-channel constants once
+//   warps 4-11   op #5: warp = (lane quadrant, 64-column half) of each acc1 chunk
+//   warps 12-19  op #6: warp = (lane quadrant, C/2-column half) of acc2
+#pragma once
+#include "mlp_kernels.cuh"
+
+namespace swinmlp {
+
+constexpr int kFEp5W0 = 4, kFEp6W0 = 12;
+constexpr int kFHc = 128;                    // hidden chunk = one 128-B K-block of FC2
+constexpr int kFMaxNB1 = 3, kFMaxNH = 4, kFMaxStages = 8;
+constexpr int kFMaxNch = 8;                  // op #6: 16-column chunks per warp (C/2 <= 128)
+constexpr uint32_t kKB = (uint32_t)kBM * kBK;   // one [128 rows][128 B] box
+// flags
+constexpr int kFGelu = 1, kFZh = 2, kFB1 = 4, kFS64 = 8, kFSmallK = 16, kFTaps = 32;
+constexpr int kFNumVariants = 64;
+
+struct FusedArgs {
+    int64_t M;          // tokens
+    int32_t C, H;
+    int32_t NJ;         // H / 128 hidden chunks
+    int32_t KBC;        // ceil(C / 128): K-blocks of the X tile and of a W1 chunk
+    int32_t NB1;        // acc1 TMEM buffers (128 columns each)
+    int32_t NH;         // Hq smem buffers
+    int32_t stages;     // weight ring depth; 0 = W1 and W2 resident in smem
+    int32_t a1_col;     // TMEM column of acc1 buffer 0 (acc2 buffers live below it)
+    int32_t NA2;        // acc2 TMEM buffers (2: op #6 of tile i overlaps FC2 of tile i + 1)
+    int32_t NX;         // X tile slots (2..4)
+    int32_t a2_stride;  // TMEM columns between acc2 buffers
+    const float* m1; const float* b1; const int32_t* zc1;   // [H]
+    const float* m2; const float* b2; const int32_t* zc2;   // [C]
+    const float* gamma; const float* beta;                  // [C]
+    float inv_h; int32_t z_h;
+    float inv_y; int32_t z_y;
+    float s_x; int32_t z_x; float eps;
+    const int8_t* x;                                        // [M][C] layer input (op #6 residual dQ(x))
+    const float* resid; float* resid_out;                   // [M][C] fp32 or nullptr
+    int32_t* acc1_tap; int8_t* hid_tap; int32_t* acc2_tap; float* ln_tap;   // debug taps
+    // pipeline trace (debug): CTA trace_cta stamps %globaltimer into trace[8192]:
+    // [q] FC1(q) issued, [512+u] FC2(u) issued, [1024+q] / [1536+q] FC1(q) before /
+    // after its waits, [2048+2u+{0,1}] op #5 chunk u start / end, [4096+4i+{0..3}] op #6
+    // tile i start / stats done / pass 1 done / end, [6144+i] Y tile i stored (reads
+    // done), [6656+u] / [7168+u] FC2(u) before / after its waits
+    unsigned long long* trace;
+    int32_t trace_cta;
+};
+
+struct FusedLayout {
+    uint32_t x, y, hq, w, w2, consts, red, bars, tmem_slot, total;
+};
+constexpr int kFMaxNX = 4;
+constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1;
+
+// ring item: one W1 K-block box [128 rows][128 B] or one W2 chunk [C rows][128 B]
+__host__ __device__ inline uint32_t fused_stage_bytes(int C) {
+    const uint32_t w2c = (uint32_t)C * kBK;
+    return kKB > w2c ? kKB : w2c;
+}
+
+__host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int stages, int ebytes, int NX) {
+    FusedLayout L;
+    const uint32_t kbc = (uint32_t)((C + kBK - 1) / kBK), nj = (uint32_t)(H / kFHc);
+    L.x = 0;                                             // [NX][KBC][128 rows][128 B] X tiles
+    L.y = L.x + (uint32_t)NX * kbc * kKB;                // [KBC][128 rows][128 B] Y staging
+    L.hq = L.y + kbc * kKB;                              // [NH][128 rows][128 B]
+    L.w = L.hq + (uint32_t)NH * kKB;                     // resident: W1 chunks then W2 chunks; else ring
+    if (stages == 0) {
+        L.w2 = L.w + nj * kbc * kKB;
+        L.consts = L.w2 + nj * (uint32_t)C * kBK;
+    } else {
+        L.w2 = 0;
+        L.consts = L.w + (uint32_t)stages * fused_stage_bytes(C);
+    }
+    L.red = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
+    L.red = (L.red + 15u) & ~15u;
+    L.bars = L.red + 2u * 2u * 2u * kBM * (uint32_t)ebytes;          // [pass][part][val][row]
+    L.tmem_slot = L.bars + 8u * kFNumBars;
+    L.total = L.tmem_slot + 16u;
+    return L;
+}
+
+template <int F>
+__global__ void __launch_bounds__(kThreads, 1)
+fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
+                 const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmY,
+                 const __grid_constant__ FusedArgs p) {
+    using namespace sm100;
+    constexpr bool GELU = (F & kFGelu) != 0, ZH = (F & kFZh) != 0, B1 = (F & kFB1) != 0;
+    constexpr bool TAPS = (F & kFTaps) != 0;   // debug taps compiled in (run_debug only)
+    constexpr bool STATS64 = (F & kFS64) != 0, SMALLK = (F & kFSmallK) != 0;
+    using acc_t = typename std::conditional<STATS64, double, float>::type;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* gbase = smem_raw + (base - raw);
+
+    const int C = p.C, H = p.H;
+    const uint32_t NJ = (uint32_t)p.NJ, KBC = (uint32_t)p.KBC, NB1 = (uint32_t)p.NB1, NH = (uint32_t)p.NH;
+    const uint32_t stages = (uint32_t)p.stages;
+    const bool resident = stages == 0;
+    const FusedLayout L = fused_layout(C, H, p.NH, p.stages, (int)sizeof(acc_t), p.NX);
+    const uint32_t NX = (uint32_t)p.NX;
+    const uint32_t sX = base + L.x, sY = base + L.y, sHq = base + L.hq, sW = base + L.w, sW2 = base + L.w2;
+    const uint32_t stage_bytes = fused_stage_bytes(C);
+    const uint32_t xslot = KBC * kKB;
+    float* cm1 = reinterpret_cast<float*>(gbase + L.consts);
+    float* cb1 = cm1 + H;
+    uint32_t* cmg1 = reinterpret_cast<uint32_t*>(cb1 + H);
+    float* cm2 = reinterpret_cast<float*>(cmg1 + H);
+    float* cb2 = cm2 + C;
+    int32_t* czc2 = reinterpret_cast<int32_t*>(cb2 + C);
+    float* cg = reinterpret_cast<float*>(czc2 + C);
+    float* cbt = cg + C;
+    acc_t* red = reinterpret_cast<acc_t*>(gbase + L.red);
+
+    const uint32_t bar0 = base + L.bars;
+    const uint32_t bar_xfull = bar0;                          // [NX]  X tile landed (1 + tx)
+    const uint32_t bar_xempty = bar_xfull + 8u * kFMaxNX;     // [NX]  X tile consumed (op #6 pass 1, 8 warps)
+    const uint32_t bar_wfull = bar_xempty + 8u * kFMaxNX;     // [S]   weight chunk landed (1 + tx)
+    const uint32_t bar_wempty = bar_wfull + 8u * kFMaxStages; // [S]   weight chunk consumed (commit)
+    const uint32_t bar_wres = bar_wempty + 8u * kFMaxStages;  //       resident weights landed
+    const uint32_t bar_a1full = bar_wres + 8u;                // [NB1] acc1 ready (commit)
+    const uint32_t bar_a1empty = bar_a1full + 8u * kFMaxNB1;  // [NB1] acc1 drained (8 warps)
+    const uint32_t bar_hqfull = bar_a1empty + 8u * kFMaxNB1;  // [NH]  Hq chunk written (8 warps)
+    const uint32_t bar_hqempty = bar_hqfull + 8u * kFMaxNH;   // [NH]  Hq chunk consumed by FC2 (commit)
+    const uint32_t bar_a2full = bar_hqempty + 8u * kFMaxNH;   // [NA2] acc2 complete (commit)
+    const uint32_t bar_a2empty = bar_a2full + 16u;            // [NA2] acc2 drained (8 warps)
+    const uint32_t bar_yfull = bar_a2empty + 16u;             //       Y tile staged (8 warps)
+    const uint32_t bar_yempty = bar_yfull + 8u;               //       Y staging read by its stores (1)
+    const uint32_t bar_cfull = bar_yempty + 16u;              //       constants loaded (32)
+    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long* trc = (p.trace && (int)blockIdx.x == p.trace_cta) ? p.trace : nullptr;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmX);
+        tma_prefetch_desc(&tmW1);
+        tma_prefetch_desc(&tmW2);
+        tma_prefetch_desc(&tmY);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int i = 0; i < kFMaxNX; ++i) {
+            mbar_init(bar_xfull + 8u * i, 1);
+            mbar_init(bar_xempty + 8u * i, 8);
+        }
+        mbar_init(bar_yfull, 8);
+        mbar_init(bar_yempty, 1);
+        for (int s = 0; s < kFMaxStages; ++s) {
+            mbar_init(bar_wfull + 8u * s, 1);
+            mbar_init(bar_wempty + 8u * s, 1);
+        }
+        mbar_init(bar_wres, 1);
+        for (int b = 0; b < kFMaxNB1; ++b) {
+            mbar_init(bar_a1full + 8u * b, 1);
+            mbar_init(bar_a1empty + 8u * b, 8);
+        }
+        for (int b = 0; b < kFMaxNH; ++b) {
+            mbar_init(bar_hqfull + 8u * b, 8);
+            mbar_init(bar_hqempty + 8u * b, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bar_a2full + 8u * b, 1);
+            mbar_init(bar_a2empty + 8u * b, 8);
+        }
+        mbar_init(bar_cfull, 32);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const uint32_t m_tiles = (uint32_t)((p.M + kBM - 1) / kBM);
+    const uint32_t cid = blockIdx.x, grid = gridDim.x;
+    const uint32_t n_my = cid < m_tiles ? (m_tiles - cid + grid - 1) / grid : 0u;
+    const uint32_t U = n_my * NJ;                 // hidden chunks this CTA processes
+    // FC1 lookahead (chunks): LA <= NB1 - 1 keeps every wait satisfiable by earlier
+    // work; LA <= NJ keeps the producer's X-slot wait behind the W2 loads it depends on
+    const uint32_t LA = min(NB1 - 1u, NJ);
+    auto row0_of = [&](uint32_t i) -> int32_t { return (int32_t)((cid + i * grid) * kBM); };
+
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        uint32_t s = 0, ph = 0;
+        auto load_w1 = [&](uint32_t j, uint32_t dst, uint32_t bar) {
+            for (uint32_t kb = 0; kb < KBC; ++kb)
+                tma_load_2d(&tmW1, dst + kb * kKB, bar, (int)(kb * kBK), (int)(j * kFHc));
+        };
+        if (resident) {
+            if (elect_one()) {
+                mbar_arrive_expect_tx(bar_wres, NJ * (KBC * kKB + (uint32_t)C * kBK));
+                for (uint32_t j = 0; j < NJ; ++j) {
+                    load_w1(j, sW + j * KBC * kKB, bar_wres);
+                    tma_load_2d(&tmW2, sW2 + j * (uint32_t)C * kBK, bar_wres, (int)(j * kFHc), 0);
+                }
+            }
+            __syncwarp();
+        }
+        // cursors advance incrementally (no runtime division in the role loops)
+        uint32_t i = 0, j = 0, j2 = 0;     // FC1 tile / chunk of q; FC2 chunk of q - LA
+        uint32_t xs = 0, xph = 0;          // X slot of tile i, its phase
+        for (uint32_t q = 0; q < U + LA; ++q) {
+            if (q < U) {                       // operands of FC1(q)
+                if (j == 0) {
+                    mbar_wait(bar_xempty + 8u * xs, xph ^ 1u);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(bar_xfull + 8u * xs, xslot);
+                        for (uint32_t kb = 0; kb < KBC; ++kb)
+                            tma_load_2d(&tmX, sX + xs * xslot + kb * kKB, bar_xfull + 8u * xs, (int)(kb * kBK),
+                                        row0_of(i));
+                    }
+                    __syncwarp();
+                }
+                if (!resident) {
+                    for (uint32_t kb = 0; kb < KBC; ++kb) {   // one ring item per K-block
+                        mbar_wait(bar_wempty + 8u * s, ph ^ 1u);
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(bar_wfull + 8u * s, kKB);
+                            tma_load_2d(&tmW1, sW + s * stage_bytes, bar_wfull + 8u * s, (int)(kb * kBK), (int)(j * kFHc));
+                        }
+                        __syncwarp();
+                        if (++s == stages) { s = 0; ph ^= 1u; }
+                    }
+                }
+                if (++j == NJ) {
+                    j = 0;
+                    ++i;
+                    if (++xs == NX) { xs = 0; xph ^= 1u; }
+                }
+            }
+            if (q >= LA) {                     // operands of FC2(q - LA)
+                if (!resident) {
+                    mbar_wait(bar_wempty + 8u * s, ph ^ 1u);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(bar_wfull + 8u * s, (uint32_t)C * kBK);
+                        tma_load_2d(&tmW2, sW + s * stage_bytes, bar_wfull + 8u * s, (int)(j2 * kFHc), 0);
+                    }
+                    __syncwarp();
+                    if (++s == stages) { s = 0; ph ^= 1u; }
+                }
+                if (++j2 == NJ) j2 = 0;
+            }
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer ==============================
+        // Lean on purpose: this warp shares its SM sub-partition with four epilogue
+        // warps, so every instruction per op costs ~5 issue slots.  Descriptors are
+        // base + offset (the 14-bit start-address field never carries: smem < 256 KB).
+        const uint32_t idesc1 = idesc_i8(kBM, kFHc), idesc2 = idesc_i8(kBM, (uint32_t)C);
+        const uint64_t dX = umma_desc_k128(sX), dW = umma_desc_k128(sW), dW2 = umma_desc_k128(sW2),
+                       dHq = umma_desc_k128(sHq);
+        const uint32_t xslot16 = xslot >> 4, stage16 = stage_bytes >> 4, w2c16 = ((uint32_t)C * kBK) >> 4;
+        const uint32_t kb16 = kKB >> 4;
+        const int nk_last = (C - (int)((KBC - 1u) * kBK)) / 32;   // MMAs (K = 32) in the last K-block
+        const uint32_t a1_tm = tmem_base + (uint32_t)p.a1_col;
+        uint32_t s = 0, ph = 0;
+        if (resident) mbar_wait(bar_wres, 0);
+        uint32_t i = 0, j = 0, b = 0, bph = 0;           // FC1 cursor: tile, chunk, acc1 buffer, its phase
+        uint32_t xs = 0, xph = 0;                        // FC1 cursor: X slot, its phase
+        uint32_t i2 = 0, j2 = 0, hb = 0, hph = 0;        // FC2 cursor: tile, chunk, Hq buffer, its phase
+        uint32_t ab = 0, aph = 0;                        // FC2 cursor: acc2 buffer, its phase
+        for (uint32_t q = 0; q < U + LA; ++q) {
+            if (q < U) {                       // FC1(q): acc1[b] = X_i . W1[j]^T
+                if (trc && lane == 0 && q < 512) trc[1024 + q] = gtimer();
+                if (j == 0) mbar_wait(bar_xfull + 8u * xs, xph);
+                mbar_wait(bar_a1empty + 8u * b, bph ^ 1u);
+                if (trc && lane == 0 && q < 512) trc[1536 + q] = gtimer();
+                const uint32_t d = a1_tm + b * (uint32_t)kFHc;
+                const uint64_t ad0 = dX + xs * xslot16;
+                for (uint32_t kb = 0; kb < KBC; ++kb) {
+                    if (!resident) mbar_wait(bar_wfull + 8u * s, ph);
+                    tc_fence_after();
+                    const uint64_t ad = ad0 + kb * kb16;
+                    const uint64_t bd = resident ? dW + (j * KBC + kb) * kb16 : dW + s * stage16;
+                    const int nk = kb + 1u == KBC ? nk_last : 4;
+                    if (elect_one()) {
+                        mma_i8(d, ad, bd, idesc1, kb);
+                        if (nk > 1) mma_i8(d, ad + 2u, bd + 2u, idesc1, 1u);
+                        if (nk > 2) mma_i8(d, ad + 4u, bd + 4u, idesc1, 1u);
+                        if (nk > 3) mma_i8(d, ad + 6u, bd + 6u, idesc1, 1u);
+                        if (!resident) mma_commit(bar_wempty + 8u * s);
+                    }
+                    __syncwarp();
+                    if (!resident && ++s == stages) { s = 0; ph ^= 1u; }
+                }
+                if (elect_one()) {
+                    mma_commit(bar_a1full + 8u * b);
+                    if (trc && q < 512) trc[q] = gtimer();
+                }
+                __syncwarp();
+                if (++j == NJ) {
+                    j = 0;
+                    ++i;
+                    if (++xs == NX) { xs = 0; xph ^= 1u; }
+                }
+                if (++b == NB1) { b = 0; bph ^= 1u; }
+            }
+            if (q >= LA) {                     // FC2(u = q - LA): acc2 += Hq_u . W2[:, j2]^T
+                if (trc && lane == 0 && q - LA < 512) trc[6656 + q - LA] = gtimer();
+                mbar_wait(bar_hqfull + 8u * hb, hph);
+                if (j2 == 0) mbar_wait(bar_a2empty + 8u * ab, aph ^ 1u);
+                if (!resident) mbar_wait(bar_wfull + 8u * s, ph);
+                if (trc && lane == 0 && q - LA < 512) trc[7168 + q - LA] = gtimer();
+                tc_fence_after();
+                const uint64_t ad = dHq + hb * kb16;
+                const uint64_t bd = resident ? dW2 + j2 * w2c16 : dW + s * stage16;
+                const uint32_t d2 = tmem_base + ab * (uint32_t)p.a2_stride;
+                if (elect_one()) {
+                    mma_i8(d2, ad, bd, idesc2, j2);
+                    mma_i8(d2, ad + 2u, bd + 2u, idesc2, 1u);
+                    mma_i8(d2, ad + 4u, bd + 4u, idesc2, 1u);
+                    mma_i8(d2, ad + 6u, bd + 6u, idesc2, 1u);
+                    if (!resident) mma_commit(bar_wempty + 8u * s);
+                    mma_commit(bar_hqempty + 8u * hb);
+                    if (j2 + 1u == NJ) mma_commit(bar_a2full + 8u * ab);
+                    if (trc && q - LA < 512) trc[512 + q - LA] = gtimer();
+                }
+                __syncwarp();
+                if (!resident && ++s == stages) { s = 0; ph ^= 1u; }
+                if (++j2 == NJ) {
+                    j2 = 0;
+                    ++i2;
+                    if (++ab == (uint32_t)p.NA2) { ab = 0; aph ^= 1u; }
+                }
+                if (++hb == NH) { hb = 0; hph ^= 1u; }
+            }
+        }
+    } else if (warp == 2) {
+        // ============================ Y store warp ============================
+        for (uint32_t i = 0; i < n_my; ++i) {
+            mbar_wait_backoff(bar_yfull, i & 1u);
+            if (lane == 0) {
+                for (uint32_t kb = 0; kb < KBC; ++kb)
+                    tma_store_2d(&tmY, sY + kb * kKB, (int)(kb * kBK), row0_of(i));
+                bulk_commit();
+                bulk_wait_read<0>();           // Y read out of the staging buffer
+                mbar_arrive(bar_yempty);
+                if (trc && i < 512) trc[6144 + i] = gtimer();
+            }
+            __syncwarp();
+        }
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
+    } else if (warp == 3) {
+        // ============================ constants ===============================
+        for (int n = (int)lane; n < H; n += 32) {
+            cm1[n] = __ldg(p.m1 + n);
+            cb1[n] = p.b1 ? __ldg(p.b1 + n) : 0.0f;
+            const int32_t zc = p.zc1 ? __ldg(p.zc1 + n) : 0;
+            cmg1[n] = SMALLK ? 0x4B400000u - (uint32_t)zc : (uint32_t)zc;   // magic - zc, or zc
+        }
+        for (int c = (int)lane; c < C; c += 32) {
+            cm2[c] = __ldg(p.m2 + c);
+            cb2[c] = p.b2 ? __ldg(p.b2 + c) : 0.0f;
+            czc2[c] = p.zc2 ? __ldg(p.zc2 + c) : 0;
+            cg[c] = __ldg(p.gamma + c);
+            cbt[c] = __ldg(p.beta + c);
+        }
+        mbar_arrive(bar_cfull);
+    } else if (warp < (uint32_t)kFEp6W0) {
+        // ============================ op #5 ===================================
+        // acc1 chunk (128 hidden columns) -> Hq chunk in smem, 128-B swizzled K-major
+        // rows (16-B granule g of row r at ((g ^ (r & 7)) << 4)): FC2's A operand.
+        const uint32_t ew = warp - (uint32_t)kFEp5W0;
+        const uint32_t quad = warp & 3u, half = ew >> 2;
+        const uint32_t rit = quad * 32u + lane;
+        const uint32_t row_off = rit * (uint32_t)kBK, rsw = rit & 7u;
+        const float2 inv2 = make_float2(p.inv_h, p.inv_h);
+        mbar_wait(bar_cfull, 0);
+        uint32_t i = 0, j = 0, b = 0, bph = 0, hb = 0, hph = 0;
+        for (uint32_t u = 0; u < U; ++u) {
+            mbar_wait_backoff(bar_a1full + 8u * b, bph);
+            mbar_wait_backoff(bar_hqempty + 8u * hb, hph ^ 1u);
+            tc_fence_after();
+            const bool stamp = trc && ew == 0 && lane == 0 && u < 1024;
+            if (stamp) trc[2048 + 2 * u] = gtimer();
+            const int64_t row = (int64_t)row0_of(i) + rit;
+            const bool valid = row < p.M;
+            const uint32_t tb = tmem_base + ((quad * 32u) << 16) + (uint32_t)p.a1_col + b * (uint32_t)kFHc + half * 64u;
+            const uint32_t hq = sHq + hb * kKB + row_off;
+            const int n_base = (int)(j * kFHc + half * 64u);
+            auto chunk = [&](uint32_t (&r)[16], int ch) {
+                const int n0 = n_base + ch * 16;
+                float v[16];
+#pragma unroll
+                for (int j4 = 0; j4 < 4; ++j4) {
+                    const float4 mv = *reinterpret_cast<const float4*>(cm1 + n0 + 4 * j4);
+                    const float4 bv = B1 ? *reinterpret_cast<const float4*>(cb1 + n0 + 4 * j4)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const uint4 gv = *reinterpret_cast<const uint4*>(cmg1 + n0 + 4 * j4);
+                    float2 a0, a1;
+                    if constexpr (SMALLK) {
+                        // bits (0x4B400000 - zc) + acc = float 1.5*2^23 + (acc - zc), exact
+                        const float2 mg = make_float2(12582912.0f, 12582912.0f);
+                        a0 = f2_sub(make_float2(__uint_as_float(r[4 * j4] + gv.x), __uint_as_float(r[4 * j4 + 1] + gv.y)), mg);
+                        a1 = f2_sub(make_float2(__uint_as_float(r[4 * j4 + 2] + gv.z), __uint_as_float(r[4 * j4 + 3] + gv.w)), mg);
+                    } else {
+                        a0 = make_float2(__int2float_rn((int32_t)(r[4 * j4] - gv.x)), __int2float_rn((int32_t)(r[4 * j4 + 1] - gv.y)));
+                        a1 = make_float2(__int2float_rn((int32_t)(r[4 * j4 + 2] - gv.z)), __int2float_rn((int32_t)(r[4 * j4 + 3] - gv.w)));
+                    }
+                    if (TAPS && p.acc1_tap && valid) {
+                        const uint32_t o = SMALLK ? 0x4B400000u : 0u;
+                        int4 t;
+                        if (SMALLK) t = make_int4((int)(r[4 * j4] + gv.x - o), (int)(r[4 * j4 + 1] + gv.y - o),
+                                                  (int)(r[4 * j4 + 2] + gv.z - o), (int)(r[4 * j4 + 3] + gv.w - o));
+                        else t = make_int4((int)(r[4 * j4] - gv.x), (int)(r[4 * j4 + 1] - gv.y),
+                                           (int)(r[4 * j4 + 2] - gv.z), (int)(r[4 * j4 + 3] - gv.w));
+                        st_v4(p.acc1_tap + row * (int64_t)H + n0 + 4 * j4, t);
+                    }
+                    // y = fl(fmaf(a, m1, b1))  (b1 = 0 without bias: bit-identical to fl(a*m1))
+                    float2 y0 = f2_fma(a0, make_float2(mv.x, mv.y), make_float2(bv.x, bv.y));
+                    float2 y1 = f2_fma(a1, make_float2(mv.z, mv.w), make_float2(bv.z, bv.w));
+                    if constexpr (GELU) {
+                        y0 = make_float2(gelu_erf_f32(y0.x), gelu_erf_f32(y0.y));
+                        y1 = make_float2(gelu_erf_f32(y1.x), gelu_erf_f32(y1.y));
+                    }
+                    const float2 t0 = f2_mul(y0, inv2), t1 = f2_mul(y1, inv2);
+                    v[4 * j4] = t0.x; v[4 * j4 + 1] = t0.y; v[4 * j4 + 2] = t1.x; v[4 * j4 + 3] = t1.y;
+                }
+                uint32_t w[4];
+                quant_pack16<!GELU, ZH>(v, p.z_h, w);
+                const uint32_t g = half * 4u + (uint32_t)ch;
+                st_shared_v4(hq + ((g ^ rsw) << 4), w[0], w[1], w[2], w[3]);
+                if (TAPS && p.hid_tap && valid)
+                    st_v4(p.hid_tap + row * (int64_t)H + n0, make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]));
+            };
+            uint32_t ra[16], rb[16];
+            tmem_ld16(tb, ra);
+            tmem_wait_ld_dep(ra);
+            tmem_ld16(tb + 16u, rb);
+            chunk(ra, 0);
+            tmem_wait_ld_dep(rb);
+            tmem_ld16(tb + 32u, ra);
+            chunk(rb, 1);
+            tmem_wait_ld_dep(ra);
+            tmem_ld16(tb + 48u, rb);
+            chunk(ra, 2);
+            tmem_wait_ld_dep(rb);
+            chunk(rb, 3);
+            tc_fence_before();
+            fence_proxy_async_smem();          // Hq visible to the tensor core (async proxy)
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(bar_a1empty + 8u * b);
+                mbar_arrive(bar_hqfull + 8u * hb);
+            }
+            if (stamp) trc[2048 + 2 * u + 1] = gtimer();
+            if (++j == NJ) { j = 0; ++i; }
+            if (++b == NB1) { b = 0; bph ^= 1u; }
+            if (++hb == NH) { hb = 0; hph ^= 1u; }
+        }
+    } else {
+        // ============================ op #6 ===================================
+        // dQ + bias + residual, LayerNorm over the C columns of a row (two warps per
+        // row, one per column half, combined through smem), Q; Y overwrites X_tile.
+        const uint32_t ew = warp - (uint32_t)kFEp6W0;
+        const uint32_t quad = warp & 3u, part = ew >> 2;
+        const uint32_t rit = quad * 32u + lane;
+        const uint32_t row_off = rit * (uint32_t)kBK, rsw = rit & 7u;
+        const int hc = C >> 1, nch = hc / 16, c_base = (int)part * hc;
+        const float2 inv2 = make_float2(p.inv_y, p.inv_y);
+        const float2 sx2 = make_float2(p.s_x, p.s_x);
+        const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
+        const float2 xoff2 = make_float2(xoff, xoff);
+        auto goff = [&](int c) -> uint32_t {       // this row's granule of column c (multiple of 16)
+            const uint32_t kb = (uint32_t)c >> 7, g = ((uint32_t)c >> 4) & 7u;
+            return kb * kKB + row_off + ((g ^ rsw) << 4);
+        };
+        auto row_sum2 = [&](acc_t v0, acc_t v1, uint32_t pass, acc_t& o1) -> acc_t {
+            const uint32_t slot = pass * 4u;                       // [pass][part][val]
+            red[(slot + part * 2u) * kBM + rit] = v0;
+            red[(slot + part * 2u + 1u) * kBM + rit] = v1;
+            named_bar_sync(1u, 256u);
+            o1 = (acc_t)red[(slot + 1u) * kBM + rit] + (acc_t)red[(slot + 3u) * kBM + rit];
+            return (acc_t)red[slot * kBM + rit] + (acc_t)red[(slot + 2u) * kBM + rit];
+        };
+        mbar_wait(bar_cfull, 0);
+        uint32_t ab = 0, aph = 0, xs = 0, xph = 0;
+        for (uint32_t i = 0; i < n_my; ++i) {
+            mbar_wait_backoff(bar_a2full + 8u * ab, aph);
+            mbar_wait(bar_xfull + 8u * xs, xph);     // (complete since FC1: visibility of X)
+            tc_fence_after();
+            const bool stamp = trc && ew == 0 && lane == 0 && i < 512;
+            if (stamp) trc[4096 + 4 * i] = gtimer();
+            const int64_t row = (int64_t)row0_of(i) + rit;
+            const bool valid = row < p.M;
+            const uint32_t tb = tmem_base + ((quad * 32u) << 16) + ab * (uint32_t)p.a2_stride + (uint32_t)c_base;
+            const uint32_t xt = sX + xs * xslot;
+
+            // pass 1: z = fl(fmaf(fl(A2), m2, b2) + r); z parked in TMEM; row sum.
+            // Two chunks' TMEM loads in flight per wait.
+            double s1d = 0.0;
+            float2 s1f = make_float2(0.f, 0.f);
+            uint32_t rn[16];
+            if (nch > 0) tmem_ld16(tb, rn);
+#pragma unroll
+            for (int ch = 0; ch < kFMaxNch; ++ch) {
+                if (ch < nch) {
+                const int c0 = c_base + ch * 16;
+                float2 rr[8];
+                if (p.resid) {
+#pragma unroll
+                    for (int j4 = 0; j4 < 4; ++j4) {
+                        const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(p.resid + row * C + c0) + j4)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                        rr[2 * j4] = make_float2(v.x, v.y);
+                        rr[2 * j4 + 1] = make_float2(v.z, v.w);
+                    }
+                } else {
+                    uint32_t xw[4];
+                    ld_shared_v4(xt + goff(c0), xw);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t ob = xw[q] ^ 0x80808080u;
+                        const float2 f01 = make_float2(__uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7650)),
+                                                       __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7651)));
+                        const float2 f23 = make_float2(__uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7652)),
+                                                       __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7653)));
+                        rr[2 * q] = f2_mul(f2_sub(f01, xoff2), sx2);
+                        rr[2 * q + 1] = f2_mul(f2_sub(f23, xoff2), sx2);
+                    }
+                }
+                tmem_wait_ld_dep(rn);
+                uint32_t r[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) r[k] = rn[k];
+                if (ch + 1 < nch) tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rn);   // next chunk in flight
+                float2 z[8];
+#pragma unroll
+                for (int j4 = 0; j4 < 4; ++j4) {
+                    const float4 mv = *reinterpret_cast<const float4*>(cm2 + c0 + 4 * j4);
+                    const float4 bv = *reinterpret_cast<const float4*>(cb2 + c0 + 4 * j4);
+                    if constexpr (ZH) {
+                        const int4 zv = *reinterpret_cast<const int4*>(czc2 + c0 + 4 * j4);
+                        r[4 * j4 + 0] -= (uint32_t)zv.x; r[4 * j4 + 1] -= (uint32_t)zv.y;
+                        r[4 * j4 + 2] -= (uint32_t)zv.z; r[4 * j4 + 3] -= (uint32_t)zv.w;
+                    }
+                    const float2 a0 = make_float2(__int2float_rn((int32_t)r[4 * j4]), __int2float_rn((int32_t)r[4 * j4 + 1]));
+                    const float2 a1 = make_float2(__int2float_rn((int32_t)r[4 * j4 + 2]), __int2float_rn((int32_t)r[4 * j4 + 3]));
+                    z[2 * j4] = f2_fma(a0, make_float2(mv.x, mv.y), make_float2(bv.x, bv.y));
+                    z[2 * j4 + 1] = f2_fma(a1, make_float2(mv.z, mv.w), make_float2(bv.z, bv.w));
+                }
+                if (TAPS && p.acc2_tap && valid) {
+#pragma unroll
+                    for (int j4 = 0; j4 < 4; ++j4)
+                        st_v4(p.acc2_tap + row * (int64_t)C + c0 + 4 * j4,
+                              make_int4((int)r[4 * j4], (int)r[4 * j4 + 1], (int)r[4 * j4 + 2], (int)r[4 * j4 + 3]));
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    z[j] = f2_add(z[j], rr[j]);
+                    if constexpr (STATS64) {
+                        s1d = __dadd_rn(s1d, (double)z[j].x);
+                        s1d = __dadd_rn(s1d, (double)z[j].y);
+                    } else {
+                        s1f = f2_add(s1f, z[j]);
+                    }
+                    r[2 * j] = __float_as_uint(z[j].x);
+                    r[2 * j + 1] = __float_as_uint(z[j].y);
+                }
+                if (p.resid_out && valid) {
+                    float* zrow = p.resid_out + row * (int64_t)C + c0;
+#pragma unroll
+                    for (int j4 = 0; j4 < 4; ++j4)
+                        *reinterpret_cast<float4*>(zrow + 4 * j4) =
+                            make_float4(z[2 * j4].x, z[2 * j4].y, z[2 * j4 + 1].x, z[2 * j4 + 1].y);
+                }
+                tmem_st16(tb + (uint32_t)(ch * 16), r);
+                }
+            }
+            tmem_wait_st();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_xempty + 8u * xs);   // X tile consumed: the next one may land
+            if (stamp) trc[4096 + 4 * i + 2] = gtimer();
+            acc_t s1, unused;
+            if constexpr (STATS64) s1 = s1d; else s1 = __fadd_rn(s1f.x, s1f.y);
+            const acc_t mu = row_sum2(s1, (acc_t)0, 0, unused) / (acc_t)C;
+
+            // pass 2: centred sum of squares (+ residual of the rounded mean, fp32)
+            double s2d = 0.0;
+            float2 s2f = make_float2(0.f, 0.f), e2f = make_float2(0.f, 0.f);
+            const float2 mu2 = make_float2((float)mu, (float)mu);
+            uint32_t rn2[16];
+            tmem_ld16(tb, rn2);
+            for (int ch = 0; ch < nch; ++ch) {
+                tmem_wait_ld_dep(rn2);
+                uint32_t r[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) r[k] = rn2[k];
+                if (ch + 1 < nch) tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rn2);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float2 zz = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                    if constexpr (STATS64) {
+                        const double d0 = __dsub_rn((double)zz.x, (double)mu), d1 = __dsub_rn((double)zz.y, (double)mu);
+                        s2d = __dadd_rn(s2d, __dmul_rn(d0, d0));
+                        s2d = __dadd_rn(s2d, __dmul_rn(d1, d1));
+                    } else {
+                        const float2 dz = f2_sub(zz, mu2);
+                        s2f = f2_fma(dz, dz, s2f);
+                        e2f = f2_add(e2f, dz);
+                    }
+                }
+            }
+            acc_t rstd;
+            float2 mu2c = mu2;
+            if constexpr (STATS64) {
+                double dummy;
+                const double SS = row_sum2(s2d, 0.0, 1, dummy);
+                rstd = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(SS, (double)C), (double)p.eps)));
+            } else {
+                float E;
+                const float SS = row_sum2(__fadd_rn(s2f.x, s2f.y), __fadd_rn(e2f.x, e2f.y), 1, E);
+                const float ec = __fdiv_rn(E, (float)C);
+                const float var = fmaxf(__fsub_rn(__fdiv_rn(SS, (float)C), __fmul_rn(ec, ec)), 0.0f);
+                rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
+                mu2c = make_float2(__fadd_rn((float)mu, ec), __fadd_rn((float)mu, ec));
+            }
+            const float2 rstd2 = make_float2((float)rstd, (float)rstd);
+            if (stamp) trc[4096 + 4 * i + 1] = gtimer();
+
+            // pass 3: yhat = fl(((z - mu) * rstd) * gamma + beta); Y = Q_y(yhat) into the staging
+            // buffer once the previous tile's stores have read it
+            mbar_wait_backoff(bar_yempty, (i & 1u) ^ 1u);
+            uint32_t rn3[16];
+            tmem_ld16(tb, rn3);
+            for (int ch = 0; ch < nch; ++ch) {
+                const int c0 = c_base + ch * 16;
+                tmem_wait_ld_dep(rn3);
+                uint32_t r[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) r[k] = rn3[k];
+                if (ch + 1 < nch) tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rn3);
+                float yh[16];
+#pragma unroll
+                for (int j4 = 0; j4 < 4; ++j4) {
+                    const float4 gv = *reinterpret_cast<const float4*>(cg + c0 + 4 * j4);
+                    const float4 bv = *reinterpret_cast<const float4*>(cbt + c0 + 4 * j4);
+                    if constexpr (STATS64) {
+                        const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
+                        const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const double xh = __dmul_rn(__dsub_rn((double)__uint_as_float(r[4 * j4 + jj]), mu), rstd);
+                            yh[4 * j4 + jj] = __double2float_rn(__dadd_rn(__dmul_rn(xh, (double)gg[jj]), (double)bb[jj]));
+                        }
+                    } else {
+                        const float2 z0 = make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]));
+                        const float2 z1 = make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3]));
+                        const float2 y0 = f2_fma(f2_mul(f2_sub(z0, mu2c), rstd2), make_float2(gv.x, gv.y), make_float2(bv.x, bv.y));
+                        const float2 y1 = f2_fma(f2_mul(f2_sub(z1, mu2c), rstd2), make_float2(gv.z, gv.w), make_float2(bv.z, bv.w));
+                        yh[4 * j4] = y0.x; yh[4 * j4 + 1] = y0.y; yh[4 * j4 + 2] = y1.x; yh[4 * j4 + 3] = y1.y;
+                    }
+                }
+                float v[16];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float2 t = f2_mul(make_float2(yh[2 * j], yh[2 * j + 1]), inv2);
+                    v[2 * j] = t.x;
+                    v[2 * j + 1] = t.y;
+                }
+                uint32_t w[4];
+                if (p.z_y) quant_pack16<false, true>(v, p.z_y, w);
+                else quant_pack16<false, false>(v, 0, w);
+                st_shared_v4(sY + goff(c0), w[0], w[1], w[2], w[3]);
+                if (TAPS && p.ln_tap && valid) {
+                    float* lrow = p.ln_tap + row * (int64_t)C + c0;
+#pragma unroll
+                    for (int j4 = 0; j4 < 4; ++j4)
+                        *reinterpret_cast<float4*>(lrow + 4 * j4) =
+                            make_float4(yh[4 * j4], yh[4 * j4 + 1], yh[4 * j4 + 2], yh[4 * j4 + 3]);
+                }
+            }
+            tc_fence_before();
+            fence_proxy_async_smem();          // Y visible to the TMA store
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(bar_a2empty + 8u * ab);
+                mbar_arrive(bar_yfull);
+            }
+            if (++ab == (uint32_t)p.NA2) { ab = 0; aph ^= 1u; }
+            if (++xs == NX) { xs = 0; xph ^= 1u; }
+            if (stamp) trc[4096 + 4 * i + 3] = gtimer();
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+}  // namespace swinmlp

@@ -71,6 +71,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         if (it > 64 && ((it & 1023) == 0) && clock64() - t0 > (1ll << 34)) __trap();
     }
 }
+// Same, backing off with nanosleep after a few failed probes: for warps whose spinning
+// would steal issue slots from the warps they share a sub-partition with (epilogue and
+// store warps waiting for work); costs at most ~the sleep time in wake-up latency.
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    long long t0 = 0;
+    for (uint32_t it = 0;; ++it) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        if (done) return;
+        if (it >= 2) __nanosleep(40);
+        if (it == 64) t0 = clock64();
+        if (it > 64 && ((it & 255) == 0) && clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
 // Same, with cluster-scope acquire (for data written by peer CTAs via st.async).
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
     uint32_t done;
@@ -216,6 +234,16 @@ namespace sm100 {
 // are only valid after it (no use can be hoisted above the wait).
 __device__ __forceinline__ void tmem_wait_ld_dep(uint32_t (&r)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15])
+                 :: "memory");
+}
+// Ties 16 registers to this point of the (volatile-ordered) instruction stream:
+// placed after a tcgen05.wait::ld that covers several loads, keeps the uses of the
+// other loads' registers below the wait.
+__device__ __forceinline__ void reg_fence16(uint32_t (&r)[16]) {
+    asm volatile(""
                  : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
                    "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
                    "+r"(r[15])

@@ -19,8 +19,25 @@
 
 #include "../../include/swin_mlp_int8.h"
 #include "mlp_kernels.cuh"
+#include "fused_mlp.cuh"
 
 using namespace swinmlp;
+
+namespace swinmlp {
+using FusedFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, FusedArgs);
+FusedFn fused_kernel_part0(int flags);   // fused_mlp.cu, -DFUSED_PART=0..3
+FusedFn fused_kernel_part1(int flags);
+FusedFn fused_kernel_part2(int flags);
+FusedFn fused_kernel_part3(int flags);
+inline FusedFn fused_kernel_for(int flags) {
+    switch ((flags >> 4) & 3) {
+        case 0: return fused_kernel_part0(flags);
+        case 1: return fused_kernel_part1(flags);
+        case 2: return fused_kernel_part2(flags);
+        default: return fused_kernel_part3(flags);
+    }
+}
+}  // namespace swinmlp
 
 namespace {
 
@@ -52,6 +69,14 @@ struct Plan {
     int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0;
     uint32_t smem = 0;
     int max_clusters = 0;
+};
+
+// One-kernel plan (fused_mlp.cuh): C <= 256, H % 128 == 0.
+struct FusedPlan {
+    bool on = false;
+    FusedFn fn = nullptr;
+    int NJ = 0, KBC = 0, NB1 = 0, NH = 0, stages = 0, a1_col = 0, NA2 = 1, a2_stride = 0, NX = 2;
+    uint32_t smem = 0;
 };
 
 bool normal_positive(float v) { return std::isfinite(v) && std::fpclassify(v) == FP_NORMAL && v > 0.0f; }
@@ -214,6 +239,49 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
     return false;
 }
 
+// The one-kernel plan: weights resident in smem when they fit (W1 and W2 each
+// 4C^2 bytes: C <= 128), else streamed through a ring; Hq buffers 2..4.
+bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
+    fp = FusedPlan();
+    const char* no = std::getenv("SWIN_MLP_NO_FUSED");   // A/B switch (read per create)
+    if (no && *no && *no != '0') return false;
+    if (C > 256 || H % kFHc) return false;
+    fp.KBC = (C + kBK - 1) / kBK;
+    fp.NJ = H / kFHc;
+    // TMEM (512 columns): acc2 buffers, then 128-column acc1 buffers.  C <= 128: two of
+    // each (op #6 of one tile overlaps FC2 of the next); else one acc2 (C or 256 columns).
+    if (C <= 128) { fp.NA2 = 2; fp.a2_stride = 128; fp.a1_col = 256; }
+    else { fp.NA2 = 1; fp.a2_stride = 0; fp.a1_col = 256; }
+    fp.NB1 = (512 - fp.a1_col) / kFHc;
+    // resident weights first (X slots 4..2, Hq buffers 3..2), else a weight ring
+    for (int nx : {4, 3, 2}) {
+        for (int nh : {3, 2}) {
+            const uint32_t need = fused_layout(C, H, nh, 0, ebytes, nx).total + 1024;
+            if (need <= kSmemBudget) {
+                fp.NX = nx; fp.NH = nh; fp.stages = 0; fp.smem = need; fp.on = true;
+                return true;
+            }
+        }
+    }
+    for (int nx : {3, 2}) {
+        for (int st = kFMaxStages; st >= 3; --st) {
+            const uint32_t need = fused_layout(C, H, 2, st, ebytes, nx).total + 1024;
+            if (need <= kSmemBudget) {
+                fp.NX = nx; fp.NH = 2; fp.stages = st; fp.smem = need; fp.on = true;
+                return true;
+            }
+        }
+    }
+    {
+        const uint32_t need = fused_layout(C, H, 2, 2, ebytes, 2).total + 1024;
+        if (need <= kSmemBudget) {
+            fp.NX = 2; fp.NH = 2; fp.stages = 2; fp.smem = need; fp.on = true;
+            return true;
+        }
+    }
+    return false;
+}
+
 swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to,
                          const CUtensorMap& tx, const GemmArgs& a, cudaStream_t stream) {
     // independent work items: m-tiles in m-major order, (m, n) units otherwise
@@ -247,6 +315,9 @@ struct swin_mlp_int8_s {
     swin_mlp_int8_desc_t d;   // scalars; pointers not retained
     int device = 0, num_sms = 0;
     Plan p1, p2;
+    FusedPlan fp;          // one-kernel plan (used when fp.on)
+    FusedFn fp_dbg = nullptr;   // its tap-writing variant (run_debug)
+    CUtensorMap tm_fw1, tm_fw2;
     // device copies (handle-owned)
     int8_t *w1 = nullptr, *w2 = nullptr;
     float *m1 = nullptr, *b1 = nullptr, *m2 = nullptr, *b2 = nullptr, *gamma = nullptr, *beta = nullptr;
@@ -439,6 +510,16 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
                                       (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0));
     H_TRY(prepare(h->p1, h->num_sms));
     H_TRY(prepare(h->p2, h->num_sms));
+    if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp)) {
+        const int ff = (d.act == SWIN_MLP_ACT_GELU_ERF ? kFGelu : 0) | (d.h_zero_point ? kFZh : 0) |
+                       (d.b1 ? kFB1 : 0) | (d.ln_fp64 ? kFS64 : 0) | (small_k1 ? kFSmallK : 0);
+        h->fp.fn = fused_kernel_for(ff);
+        h->fp_dbg = fused_kernel_for(ff | kFTaps);
+        H_TRY(encode_2d(&h->tm_fw1, h->w1, H, C, C, (uint32_t)kFHc));
+        H_TRY(encode_2d(&h->tm_fw2, h->w2, C, H, H, (uint32_t)C));
+        CUDA_TRY(cudaFuncSetAttribute(h->fp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+        CUDA_TRY(cudaFuncSetAttribute(h->fp_dbg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+    }
 #undef H_TRY
     *out = h;
     return SWIN_MLP_OK;
@@ -446,6 +527,7 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
 
 size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T) {
     if (!h || T <= 0) return 0;
+    if (h->fp.on) return 0;   // one kernel: the hidden tile never leaves the SM
     return (size_t)(((T * h->d.H) + 127) / 128 * 128);
 }
 
@@ -456,17 +538,55 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     if (T < 0) return fail(SWIN_MLP_EINVAL, "T=%lld < 0", (long long)T);
     if (T == 0) return SWIN_MLP_OK;
     if (T > (int64_t)1 << 31) return fail(SWIN_MLP_EUNSUPPORTED, "T=%lld too large", (long long)T);
-    if (!x || !y || !workspace) return fail(SWIN_MLP_EINVAL, "x, y and workspace are required");
+    const size_t ws_need = swin_mlp_int8_workspace_bytes(h, T);
+    if (!x || !y || (ws_need && !workspace)) return fail(SWIN_MLP_EINVAL, "x, y and workspace are required");
     if (!aligned16(x) || !aligned16(y) || (residual && !aligned16(residual)) ||
         (residual_out && !aligned16(residual_out)) || (reinterpret_cast<uintptr_t>(workspace) & 127u))
         return fail(SWIN_MLP_EINVAL, "x/y/residual/residual_out must be 16-byte aligned, workspace 128-byte aligned");
-    if (ws_bytes < swin_mlp_int8_workspace_bytes(h, T))
-        return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", ws_bytes, swin_mlp_int8_workspace_bytes(h, T));
+    if (ws_bytes < ws_need) return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", ws_bytes, ws_need);
     if ((const void*)x == (const void*)y) return fail(SWIN_MLP_EINVAL, "y may not alias x");
     const int C = h->d.C, H = h->d.H;
     DeviceGuard guard(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int8_t* hq = static_cast<int8_t*>(workspace);
+
+    if (h->fp.on) {
+        CUtensorMap fx, fy;
+        ST_TRY(encode_2d(&fx, x, T, C, C, kBM));
+        ST_TRY(encode_2d(&fy, y, T, C, C, kBM));
+        FusedArgs a = {};
+        a.M = T; a.C = C; a.H = H;
+        a.NJ = h->fp.NJ; a.KBC = h->fp.KBC; a.NB1 = h->fp.NB1; a.NH = h->fp.NH; a.stages = h->fp.stages;
+        a.a1_col = h->fp.a1_col; a.NA2 = h->fp.NA2; a.a2_stride = h->fp.a2_stride; a.NX = h->fp.NX;
+        a.m1 = h->m1; a.b1 = h->b1; a.zc1 = h->zc1;
+        a.m2 = h->m2; a.b2 = h->b2; a.zc2 = h->zc2;
+        a.gamma = h->gamma; a.beta = h->beta;
+        a.inv_h = h->inv_h; a.z_h = h->d.h_zero_point; a.inv_y = h->inv_y; a.z_y = h->d.y_zero_point;
+        a.s_x = h->d.x_scale; a.z_x = h->d.x_zero_point; a.eps = h->d.ln_eps;
+        a.x = x; a.resid = residual; a.resid_out = residual_out;
+        if (dbg) { a.acc1_tap = acc1; a.hid_tap = hidden; a.acc2_tap = acc2; a.ln_tap = ln_out; }
+        a.trace = h->trace; a.trace_cta = h->trace_cta;
+        const int64_t m_tiles = (T + kBM - 1) / kBM;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)std::min<int64_t>(m_tiles, h->num_sms));
+        cfg.blockDim = dim3((unsigned)kThreads);
+        cfg.dynamicSmemBytes = h->fp.smem;
+        cfg.stream = s;
+        cudaEvent_t* ev = nullptr;
+        if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
+        if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, dbg ? h->fp_dbg : h->fp.fn, fx, h->tm_fw1, h->tm_fw2, fy, a));
+        if (ev) {
+            CUDA_TRY(cudaEventRecord(ev[1], s));
+            CUDA_TRY(cudaEventRecord(ev[2], s));
+        }
+        static const bool sync_check = std::getenv("SWIN_MLP_SYNC_CHECK") != nullptr;
+        if (sync_check) {
+            CUDA_TRY(cudaStreamSynchronize(s));
+            CUDA_TRY(cudaGetLastError());
+        }
+        return SWIN_MLP_OK;
+    }
 
     CUtensorMap tm_x, tm_h, tm_ho, tm_y, tm_xr;
     ST_TRY(encode_2d(&tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
@@ -617,7 +737,7 @@ swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_
     return SWIN_MLP_OK;
 }
 
-int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h) { return h ? 2 : 0; }
+int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h) { return h ? (h->fp.on ? 1 : 2) : 0; }
 
 swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
     if (!h) return SWIN_MLP_OK;
@@ -630,11 +750,12 @@ swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
 
 // Test/bench introspection: the launch plan chosen for this layer.
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
-    if (!h || !out10) return -1;  // out10 holds 12 entries
+    if (!h || !out10) return -1;  // out10 holds 16 entries
     out10[0] = h->p1.BN; out10[1] = h->p1.CS; out10[2] = h->p1.stages; out10[3] = h->p1.max_clusters;
     out10[4] = h->p2.BN; out10[5] = h->p2.CS; out10[6] = h->p2.stages; out10[7] = h->p2.max_clusters;
     out10[8] = h->p1.G; out10[9] = h->p2.G;
     out10[10] = h->p1.resb; out10[11] = h->p2.resb;
+    out10[12] = h->fp.on ? 1 : 0; out10[13] = h->fp.stages; out10[14] = h->fp.NH; out10[15] = h->fp.NB1;
     return 0;
 }
 

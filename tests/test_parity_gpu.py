@@ -236,3 +236,35 @@ def test_parity_extreme_accumulators(dev, C):
     m1, ih, m2, iy = oracle.fold_constants(L.s_x, L.s_w1, L.s_h, L.s_w2, L.s_y)
     np.testing.assert_array_equal(taps["hidden"].cpu().numpy(), oracle.ep5(a1, m1, L.b1, ih, L.z_h))
     _tier_int8(taps["y"].cpu().numpy(), oracle.mlp(L, X), what="Y extreme")
+
+
+# ---- one-kernel plan (fused_mlp.cuh, C <= 256) vs the two-kernel plan ---------------------------
+
+@pytest.mark.parametrize("C,fused", [(96, 1), (128, 1), (192, 1), (256, 1), (384, 0), (768, 0)])
+def test_plan_selection(dev, C, fused, monkeypatch):
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(C, 7000 + C)
+    assert SwinMlpInt8Layer(L, device=0).plan()["fused"] == fused
+    monkeypatch.setenv("SWIN_MLP_NO_FUSED", "1")
+    assert SwinMlpInt8Layer(L, device=0).plan()["fused"] == 0
+
+
+@pytest.mark.parametrize("C,T", [(96, 1000), (192, 257), (256, 129)])
+def test_two_kernel_plan_small_c(dev, C, T, monkeypatch):
+    """The two-kernel plan stays correct for the channel counts the one-kernel plan now takes."""
+    monkeypatch.setenv("SWIN_MLP_NO_FUSED", "1")
+    _run_and_check(dev, _layer(C, 1000 + C), T)
+    _run_and_check(dev, _layer(C, 3000 + C, bias=True, zx=-5, zh=-128, zy=2), T)
+
+
+@pytest.mark.parametrize("C,T", [(96, 148 * 128 * 2 + 77), (192, 148 * 128 + 1000), (256, 148 * 128 + 129)])
+def test_fused_persistent_multi_tile(dev, C, T):
+    """Several m-tiles per CTA (X-slot reuse, TMEM / Hq buffer phases across tiles), resident and
+    streamed weights, ragged tail."""
+    _run_and_check(dev, _layer(C, 8000 + C), T, e2e=False)
+
+
+@pytest.mark.parametrize("C,T", [(96, 3000), (192, 1000)])
+def test_fused_gelu_and_ln_fp64(dev, C, T):
+    _run_and_check(dev, _layer(C, 9000 + C, act=1, bias=True, zh=-3), T)
+    _run_and_check(dev, _layer(C, 9100 + C), T, ln_fp64=True)
