@@ -157,8 +157,9 @@ void oracle_ep5(const int32_t* A1, int64_t nrows, int32_t H, const float* m1,
 /* O4-O6: fused op #6: dQ -> FC2 bias -> Add & LayerNorm,
  * then Q (reading R4).
  *   d = fmaf(fl(A2), m2[c], b2[c] or 0)
- *   r = R[t][c]  or  fl(fl(X[t][c] - z_x) * s_x)        (reading R3)
- *   z = fl(d + r)
+ *   z = fl(d + R[t][c])                          with an fp32 residual, else
+ *   z = fmaf(fl(X[t][c] - z_x), s_x, d)          the residual dQ(X) added with one
+ *                                                rounding (reading R3)
  *   mu  = (sum_c z) / C          double, ascending c
  *   var = (sum_c (z-mu)^2) / C   double, ascending c, biased (R9)
  *   rstd = 1 / sqrt(var + eps)   double
@@ -177,12 +178,10 @@ void oracle_ep6(const int32_t* A2, int64_t nrows, int32_t C, const float* m2,
     for (int64_t i = 0; i < nrows; ++i) {
         for (int32_t c = 0; c < C; ++c) {
             float d = fmaf((float)A2[i * C + c], m2[c], b2 ? b2[c] : 0.0f);
-            float r;
             if (R)
-                r = R[i * C + c];
+                z[c] = d + R[i * C + c];
             else
-                r = (float)((int32_t)X[i * C + c] - z_x) * s_x;
-            z[c] = d + r;
+                z[c] = fmaf((float)((int32_t)X[i * C + c] - z_x), s_x, d);
             if (z_out) z_out[i * C + c] = z[c];
         }
         double sum = 0.0;

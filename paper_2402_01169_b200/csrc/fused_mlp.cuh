@@ -12,13 +12,13 @@
 //       Hq_j    = op #5(acc1_j)                      (epilogue warps -> smem, SW128 K-major:
 //                                                     exactly FC2's A-operand layout)
 //       acc2   += Hq_j . W2[:, j]^T                  (tcgen05, TMEM columns [0, C))
-//   Y_tile = op #6(acc2, X_tile)                     (LayerNorm rows on chip; Y written
-//                                                     in place over X_tile, then TMA-stored)
+//   Y_tile = op #6(acc2, X_tile)                     (LayerNorm rows on chip; Y staged in
+//                                                     smem, then TMA-stored)
 //
 // Same arithmetic, in the same order, as the two-kernel path (mlp_kernels.cuh) and
 // the oracle; HBM traffic falls to the algorithmic 2C bytes per token (X in, Y out).
 //
-// CTA = 640 threads, one per SM, persistent over m-tiles cid, cid + grid, ...:
+// CTA = 512 threads, one per SM, persistent over m-tiles cid, cid + grid, ...:
 //   warp 0       TMA producer: X tiles (2 slots) and, unless resident, the W1 / W2
 //                chunks through a `stages`-deep ring in the MMA's consumption order
 //   warp 1       MMA issuer: FC1 of chunk u + L is issued before FC2 of chunk u
@@ -26,16 +26,17 @@
 //   warp 2       TMEM allocator, then the Y store warp
 //   warp 3       loads the per-channel constants once
 //   warps 4-11   op #5: warp = (lane quadrant, 64-column half) of each acc1 chunk
-//   warps 12-19  op #6: warp = (lane quadrant, C/2-column half) of acc2
+//   warps 12-15  op #6: warp = lane quadrant; one thread per token row, whole row
+// (512 threads: 128 registers per thread)
 #pragma once
 #include "mlp_kernels.cuh"
 
 namespace swinmlp {
 
 constexpr int kFEp5W0 = 4, kFEp6W0 = 12;
+constexpr int kFThreads = 32 * 16;          // 4 control + 8 op #5 + 4 op #6 warps (128 regs each)
 constexpr int kFHc = 128;                    // hidden chunk = one 128-B K-block of FC2
 constexpr int kFMaxNB1 = 3, kFMaxNH = 4, kFMaxStages = 8;
-constexpr int kFMaxNch = 8;                  // op #6: 16-column chunks per warp (C/2 <= 128)
 constexpr uint32_t kKB = (uint32_t)kBM * kBK;   // one [128 rows][128 B] box
 // flags
 constexpr int kFGelu = 1, kFZh = 2, kFB1 = 4, kFS64 = 8, kFSmallK = 16, kFTaps = 32;
@@ -72,7 +73,7 @@ struct FusedArgs {
 };
 
 struct FusedLayout {
-    uint32_t x, y, hq, w, w2, consts, red, bars, tmem_slot, total;
+    uint32_t x, y, hq, w, w2, consts, bars, tmem_slot, total;
 };
 constexpr int kFMaxNX = 4;
 constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1;
@@ -97,16 +98,16 @@ __host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int st
         L.w2 = 0;
         L.consts = L.w + (uint32_t)stages * fused_stage_bytes(C);
     }
-    L.red = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
-    L.red = (L.red + 15u) & ~15u;
-    L.bars = L.red + 2u * 2u * 2u * kBM * (uint32_t)ebytes;          // [pass][part][val][row]
+    L.bars = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
+    L.bars = (L.bars + 15u) & ~15u;
+    (void)ebytes;
     L.tmem_slot = L.bars + 8u * kFNumBars;
     L.total = L.tmem_slot + 16u;
     return L;
 }
 
 template <int F>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kFThreads, 1)
 fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                  const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmY,
                  const __grid_constant__ FusedArgs p) {
@@ -137,11 +138,10 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     int32_t* czc2 = reinterpret_cast<int32_t*>(cb2 + C);
     float* cg = reinterpret_cast<float*>(czc2 + C);
     float* cbt = cg + C;
-    acc_t* red = reinterpret_cast<acc_t*>(gbase + L.red);
 
     const uint32_t bar0 = base + L.bars;
     const uint32_t bar_xfull = bar0;                          // [NX]  X tile landed (1 + tx)
-    const uint32_t bar_xempty = bar_xfull + 8u * kFMaxNX;     // [NX]  X tile consumed (op #6 pass 1, 8 warps)
+    const uint32_t bar_xempty = bar_xfull + 8u * kFMaxNX;     // [NX]  X tile consumed (op #6 pass 1, 4 warps)
     const uint32_t bar_wfull = bar_xempty + 8u * kFMaxNX;     // [S]   weight chunk landed (1 + tx)
     const uint32_t bar_wempty = bar_wfull + 8u * kFMaxStages; // [S]   weight chunk consumed (commit)
     const uint32_t bar_wres = bar_wempty + 8u * kFMaxStages;  //       resident weights landed
@@ -150,8 +150,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t bar_hqfull = bar_a1empty + 8u * kFMaxNB1;  // [NH]  Hq chunk written (8 warps)
     const uint32_t bar_hqempty = bar_hqfull + 8u * kFMaxNH;   // [NH]  Hq chunk consumed by FC2 (commit)
     const uint32_t bar_a2full = bar_hqempty + 8u * kFMaxNH;   // [NA2] acc2 complete (commit)
-    const uint32_t bar_a2empty = bar_a2full + 16u;            // [NA2] acc2 drained (8 warps)
-    const uint32_t bar_yfull = bar_a2empty + 16u;             //       Y tile staged (8 warps)
+    const uint32_t bar_a2empty = bar_a2full + 16u;            // [NA2] acc2 drained (4 warps)
+    const uint32_t bar_yfull = bar_a2empty + 16u;             //       Y tile staged (4 warps)
     const uint32_t bar_yempty = bar_yfull + 8u;               //       Y staging read by its stores (1)
     const uint32_t bar_cfull = bar_yempty + 16u;              //       constants loaded (32)
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
@@ -167,9 +167,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < kFMaxNX; ++i) {
             mbar_init(bar_xfull + 8u * i, 1);
-            mbar_init(bar_xempty + 8u * i, 8);
+            mbar_init(bar_xempty + 8u * i, 4);
         }
-        mbar_init(bar_yfull, 8);
+        mbar_init(bar_yfull, 4);
         mbar_init(bar_yempty, 1);
         for (int s = 0; s < kFMaxStages; ++s) {
             mbar_init(bar_wfull + 8u * s, 1);
@@ -186,7 +186,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_a2full + 8u * b, 1);
-            mbar_init(bar_a2empty + 8u * b, 8);
+            mbar_init(bar_a2empty + 8u * b, 4);
         }
         mbar_init(bar_cfull, 32);
         fence_mbar_init();
@@ -478,13 +478,18 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         }
     } else {
         // ============================ op #6 ===================================
-        // dQ + bias + residual, LayerNorm over the C columns of a row (two warps per
-        // row, one per column half, combined through smem), Q; Y overwrites X_tile.
-        const uint32_t ew = warp - (uint32_t)kFEp6W0;
-        const uint32_t quad = warp & 3u, part = ew >> 2;
+        // One thread per token row, the whole row: dQ + bias + residual -> z (parked
+        // back in TMEM), row statistics in-thread (no cross-warp exchange), then
+        // LayerNorm + Q into the Y staging tile.
+        //   fp32: one pass of shifted sums, shift K = mean of the row's first 16 z
+        //         (any K gives the exact statistics; K near the mean keeps the
+        //         S2/C - (S1/C)^2 cancellation small): mu = K + S1/C,
+        //         var = S2/C - (S1/C)^2   (reading R15)
+        //   fp64: the oracle's two passes, ascending columns (O5)
+        const uint32_t quad = warp & 3u;
         const uint32_t rit = quad * 32u + lane;
         const uint32_t row_off = rit * (uint32_t)kBK, rsw = rit & 7u;
-        const int hc = C >> 1, nch = hc / 16, c_base = (int)part * hc;
+        const int nch = C >> 4;                    // even: C % 32 == 0
         const float2 inv2 = make_float2(p.inv_y, p.inv_y);
         const float2 sx2 = make_float2(p.s_x, p.s_x);
         const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
@@ -493,39 +498,42 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             const uint32_t kb = (uint32_t)c >> 7, g = ((uint32_t)c >> 4) & 7u;
             return kb * kKB + row_off + ((g ^ rsw) << 4);
         };
-        auto row_sum2 = [&](acc_t v0, acc_t v1, uint32_t pass, acc_t& o1) -> acc_t {
-            const uint32_t slot = pass * 4u;                       // [pass][part][val]
-            red[(slot + part * 2u) * kBM + rit] = v0;
-            red[(slot + part * 2u + 1u) * kBM + rit] = v1;
-            named_bar_sync(1u, 256u);
-            o1 = (acc_t)red[(slot + 1u) * kBM + rit] + (acc_t)red[(slot + 3u) * kBM + rit];
-            return (acc_t)red[slot * kBM + rit] + (acc_t)red[(slot + 2u) * kBM + rit];
-        };
         mbar_wait(bar_cfull, 0);
         uint32_t ab = 0, aph = 0, xs = 0, xph = 0;
         for (uint32_t i = 0; i < n_my; ++i) {
             mbar_wait_backoff(bar_a2full + 8u * ab, aph);
             mbar_wait(bar_xfull + 8u * xs, xph);     // (complete since FC1: visibility of X)
             tc_fence_after();
-            const bool stamp = trc && ew == 0 && lane == 0 && i < 512;
+            const bool stamp = trc && quad == 0 && lane == 0 && i < 512;
             if (stamp) trc[4096 + 4 * i] = gtimer();
             const int64_t row = (int64_t)row0_of(i) + rit;
             const bool valid = row < p.M;
-            const uint32_t tb = tmem_base + ((quad * 32u) << 16) + ab * (uint32_t)p.a2_stride + (uint32_t)c_base;
+            const uint32_t tb = tmem_base + ((quad * 32u) << 16) + ab * (uint32_t)p.a2_stride;
             const uint32_t xt = sX + xs * xslot;
 
-            // pass 1: z = fl(fmaf(fl(A2), m2, b2) + r); z parked in TMEM; row sum.
-            // Two chunks' TMEM loads in flight per wait.
+            // chunk loop for the passes over parked z: pairs of chunks behind one wait
+            auto for_chunks = [&](auto&& fn) {
+                for (int ch = 0; ch < nch; ch += 2) {
+                    uint32_t ra[16], rb[16];
+                    tmem_ld16(tb + (uint32_t)(ch * 16), ra);
+                    tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rb);
+                    tmem_wait_ld_dep(ra);
+                    reg_fence16(rb);
+                    fn(ra, ch);
+                    fn(rb, ch + 1);
+                }
+            };
+            // pass 1: z = fl(fl(fmaf(fl(A2), m2, b2)) + r), back into TMEM; statistics.
+            // Pairs of chunks behind one TMEM wait, branch-free bodies (residual source
+            // and taps resolved outside) so the two chunks' arithmetic interleaves.
+            float K = 0.f;
+            float2 s1f = make_float2(0.f, 0.f), s2f = make_float2(0.f, 0.f), Kv = make_float2(0.f, 0.f);
             double s1d = 0.0;
-            float2 s1f = make_float2(0.f, 0.f);
-            uint32_t rn[16];
-            if (nch > 0) tmem_ld16(tb, rn);
-#pragma unroll
-            for (int ch = 0; ch < kFMaxNch; ++ch) {
-                if (ch < nch) {
-                const int c0 = c_base + ch * 16;
+            // z of one 16-column chunk (r: raw accumulators, modified in place)
+            auto chunk_z = [&](auto resid_c, uint32_t (&r)[16], int c0, float2 (&z)[8]) {
+                constexpr bool RESID = decltype(resid_c)::value;
                 float2 rr[8];
-                if (p.resid) {
+                if constexpr (RESID) {
 #pragma unroll
                     for (int j4 = 0; j4 < 4; ++j4) {
                         const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(p.resid + row * C + c0) + j4)
@@ -534,8 +542,10 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                         rr[2 * j4 + 1] = make_float2(v.z, v.w);
                     }
                 } else {
-                    uint32_t xw[4];
-                    ld_shared_v4(xt + goff(c0), xw);
+                    // x - z_x as float, exactly, by offset binary: bits 0x4B0000uu =
+                    // 2^23 + u, u = x ^ 0x80 = x + 128
+                    const uint4 xv = *reinterpret_cast<const uint4*>(gbase + (xt - base) + goff(c0));
+                    const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint32_t ob = xw[q] ^ 0x80808080u;
@@ -543,16 +553,10 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                                                        __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7651)));
                         const float2 f23 = make_float2(__uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7652)),
                                                        __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7653)));
-                        rr[2 * q] = f2_mul(f2_sub(f01, xoff2), sx2);
-                        rr[2 * q + 1] = f2_mul(f2_sub(f23, xoff2), sx2);
+                        rr[2 * q] = f2_sub(f01, xoff2);          // x - z_x, exact
+                        rr[2 * q + 1] = f2_sub(f23, xoff2);
                     }
                 }
-                tmem_wait_ld_dep(rn);
-                uint32_t r[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) r[k] = rn[k];
-                if (ch + 1 < nch) tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rn);   // next chunk in flight
-                float2 z[8];
 #pragma unroll
                 for (int j4 = 0; j4 < 4; ++j4) {
                     const float4 mv = *reinterpret_cast<const float4*>(cm2 + c0 + 4 * j4);
@@ -564,140 +568,147 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     }
                     const float2 a0 = make_float2(__int2float_rn((int32_t)r[4 * j4]), __int2float_rn((int32_t)r[4 * j4 + 1]));
                     const float2 a1 = make_float2(__int2float_rn((int32_t)r[4 * j4 + 2]), __int2float_rn((int32_t)r[4 * j4 + 3]));
-                    z[2 * j4] = f2_fma(a0, make_float2(mv.x, mv.y), make_float2(bv.x, bv.y));
-                    z[2 * j4 + 1] = f2_fma(a1, make_float2(mv.z, mv.w), make_float2(bv.z, bv.w));
+                    const float2 d0 = f2_fma(a0, make_float2(mv.x, mv.y), make_float2(bv.x, bv.y));
+                    const float2 d1 = f2_fma(a1, make_float2(mv.z, mv.w), make_float2(bv.z, bv.w));
+                    if constexpr (RESID) {       // z = fl(d + R)
+                        z[2 * j4] = f2_add(d0, rr[2 * j4]);
+                        z[2 * j4 + 1] = f2_add(d1, rr[2 * j4 + 1]);
+                    } else {                     // z = fl((x - z_x) * s_x + d), one rounding (R3)
+                        z[2 * j4] = f2_fma(rr[2 * j4], sx2, d0);
+                        z[2 * j4 + 1] = f2_fma(rr[2 * j4 + 1], sx2, d1);
+                    }
                 }
+            };
+            auto stats = [&](const float2 (&z)[8]) {
+                if constexpr (STATS64) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        s1d = __dadd_rn(s1d, (double)z[j].x);
+                        s1d = __dadd_rn(s1d, (double)z[j].y);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float2 d = f2_sub(z[j], Kv);
+                        s1f = f2_add(s1f, d);
+                        s2f = f2_fma(d, d, s2f);
+                    }
+                }
+            };
+            auto park = [&](const float2 (&z)[8], const uint32_t (&r)[16], int c0) {   // z -> TMEM (+ taps)
                 if (TAPS && p.acc2_tap && valid) {
 #pragma unroll
                     for (int j4 = 0; j4 < 4; ++j4)
                         st_v4(p.acc2_tap + row * (int64_t)C + c0 + 4 * j4,
                               make_int4((int)r[4 * j4], (int)r[4 * j4 + 1], (int)r[4 * j4 + 2], (int)r[4 * j4 + 3]));
                 }
+                uint32_t zu[16];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    z[j] = f2_add(z[j], rr[j]);
-                    if constexpr (STATS64) {
-                        s1d = __dadd_rn(s1d, (double)z[j].x);
-                        s1d = __dadd_rn(s1d, (double)z[j].y);
-                    } else {
-                        s1f = f2_add(s1f, z[j]);
-                    }
-                    r[2 * j] = __float_as_uint(z[j].x);
-                    r[2 * j + 1] = __float_as_uint(z[j].y);
+                    zu[2 * j] = __float_as_uint(z[j].x);
+                    zu[2 * j + 1] = __float_as_uint(z[j].y);
                 }
-                if (p.resid_out && valid) {
-                    float* zrow = p.resid_out + row * (int64_t)C + c0;
+                tmem_st16(tb + (uint32_t)c0, zu);
+            };
+            auto pass1 = [&](auto resid_c) {
+                for (int ch = 0; ch < nch; ch += 2) {
+                    uint32_t ra[16], rb[16];
+                    tmem_ld16(tb + (uint32_t)(ch * 16), ra);
+                    tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rb);
+                    tmem_wait_ld_dep(ra);
+                    reg_fence16(rb);
+                    float2 za[8], zb[8];
+                    chunk_z(resid_c, ra, ch * 16, za);
+                    chunk_z(resid_c, rb, ch * 16 + 16, zb);
+                    if (!STATS64 && ch == 0) {   // shift: mean of the row's first 16 values
+                        float2 t = za[0];
 #pragma unroll
-                    for (int j4 = 0; j4 < 4; ++j4)
-                        *reinterpret_cast<float4*>(zrow + 4 * j4) =
-                            make_float4(z[2 * j4].x, z[2 * j4].y, z[2 * j4 + 1].x, z[2 * j4 + 1].y);
+                        for (int j = 1; j < 8; ++j) t = f2_add(t, za[j]);
+                        K = __fmul_rn(__fadd_rn(t.x, t.y), 0.0625f);
+                        Kv = make_float2(K, K);
+                    }
+                    stats(za);
+                    stats(zb);
+                    if (p.resid_out && valid) {
+                        float* zrow = p.resid_out + row * (int64_t)C + ch * 16;
+#pragma unroll
+                        for (int j4 = 0; j4 < 4; ++j4) {
+                            *reinterpret_cast<float4*>(zrow + 4 * j4) =
+                                make_float4(za[2 * j4].x, za[2 * j4].y, za[2 * j4 + 1].x, za[2 * j4 + 1].y);
+                            *reinterpret_cast<float4*>(zrow + 16 + 4 * j4) =
+                                make_float4(zb[2 * j4].x, zb[2 * j4].y, zb[2 * j4 + 1].x, zb[2 * j4 + 1].y);
+                        }
+                    }
+                    park(za, ra, ch * 16);
+                    park(zb, rb, ch * 16 + 16);
                 }
-                tmem_st16(tb + (uint32_t)(ch * 16), r);
-                }
-            }
+            };
+            if (p.resid) pass1(std::true_type{});
+            else pass1(std::false_type{});
             tmem_wait_st();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_xempty + 8u * xs);   // X tile consumed: the next one may land
+            if (lane == 0) mbar_arrive(bar_xempty + 8u * xs);   // X tile consumed
             if (stamp) trc[4096 + 4 * i + 2] = gtimer();
-            acc_t s1, unused;
-            if constexpr (STATS64) s1 = s1d; else s1 = __fadd_rn(s1f.x, s1f.y);
-            const acc_t mu = row_sum2(s1, (acc_t)0, 0, unused) / (acc_t)C;
 
-            // pass 2: centred sum of squares (+ residual of the rounded mean, fp32)
-            double s2d = 0.0;
-            float2 s2f = make_float2(0.f, 0.f), e2f = make_float2(0.f, 0.f);
-            const float2 mu2 = make_float2((float)mu, (float)mu);
-            uint32_t rn2[16];
-            tmem_ld16(tb, rn2);
-            for (int ch = 0; ch < nch; ++ch) {
-                tmem_wait_ld_dep(rn2);
-                uint32_t r[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) r[k] = rn2[k];
-                if (ch + 1 < nch) tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rn2);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float2 zz = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-                    if constexpr (STATS64) {
-                        const double d0 = __dsub_rn((double)zz.x, (double)mu), d1 = __dsub_rn((double)zz.y, (double)mu);
-                        s2d = __dadd_rn(s2d, __dmul_rn(d0, d0));
-                        s2d = __dadd_rn(s2d, __dmul_rn(d1, d1));
-                    } else {
-                        const float2 dz = f2_sub(zz, mu2);
-                        s2f = f2_fma(dz, dz, s2f);
-                        e2f = f2_add(e2f, dz);
-                    }
-                }
-            }
-            acc_t rstd;
-            float2 mu2c = mu2;
+            float mu_f = 0.f, rstd_f = 0.f;
+            double mu_d = 0.0, rstd_d = 0.0;
             if constexpr (STATS64) {
-                double dummy;
-                const double SS = row_sum2(s2d, 0.0, 1, dummy);
-                rstd = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(SS, (double)C), (double)p.eps)));
+                mu_d = s1d / (double)C;
+                double s2d = 0.0;
+                for_chunks([&](uint32_t (&r)[16], int) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const double d = __dsub_rn((double)__uint_as_float(r[j]), mu_d);
+                        s2d = __dadd_rn(s2d, __dmul_rn(d, d));
+                    }
+                });
+                rstd_d = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(s2d, (double)C), (double)p.eps)));
             } else {
-                float E;
-                const float SS = row_sum2(__fadd_rn(s2f.x, s2f.y), __fadd_rn(e2f.x, e2f.y), 1, E);
-                const float ec = __fdiv_rn(E, (float)C);
-                const float var = fmaxf(__fsub_rn(__fdiv_rn(SS, (float)C), __fmul_rn(ec, ec)), 0.0f);
-                rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
-                mu2c = make_float2(__fadd_rn((float)mu, ec), __fadd_rn((float)mu, ec));
+                const float m1 = __fdiv_rn(__fadd_rn(s1f.x, s1f.y), (float)C);
+                const float var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(s2f.x, s2f.y), (float)C), __fmul_rn(m1, m1)), 0.0f);
+                mu_f = __fadd_rn(K, m1);
+                rstd_f = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
             }
-            const float2 rstd2 = make_float2((float)rstd, (float)rstd);
+            const float2 mu2 = make_float2(mu_f, mu_f), rstd2 = make_float2(rstd_f, rstd_f);
             if (stamp) trc[4096 + 4 * i + 1] = gtimer();
 
-            // pass 3: yhat = fl(((z - mu) * rstd) * gamma + beta); Y = Q_y(yhat) into the staging
+            // pass 2: yhat = fl(((z - mu) * rstd) * gamma + beta); Y = Q_y(yhat) into the staging
             // buffer once the previous tile's stores have read it
             mbar_wait_backoff(bar_yempty, (i & 1u) ^ 1u);
-            uint32_t rn3[16];
-            tmem_ld16(tb, rn3);
-            for (int ch = 0; ch < nch; ++ch) {
-                const int c0 = c_base + ch * 16;
-                tmem_wait_ld_dep(rn3);
-                uint32_t r[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) r[k] = rn3[k];
-                if (ch + 1 < nch) tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rn3);
-                float yh[16];
+            for_chunks([&](uint32_t (&r)[16], int ch) {
+                const int c0 = ch * 16;
+                float v[16];
 #pragma unroll
                 for (int j4 = 0; j4 < 4; ++j4) {
                     const float4 gv = *reinterpret_cast<const float4*>(cg + c0 + 4 * j4);
                     const float4 bv = *reinterpret_cast<const float4*>(cbt + c0 + 4 * j4);
+                    float yh[4];
                     if constexpr (STATS64) {
                         const float gg[4] = {gv.x, gv.y, gv.z, gv.w};
                         const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
                         for (int jj = 0; jj < 4; ++jj) {
-                            const double xh = __dmul_rn(__dsub_rn((double)__uint_as_float(r[4 * j4 + jj]), mu), rstd);
-                            yh[4 * j4 + jj] = __double2float_rn(__dadd_rn(__dmul_rn(xh, (double)gg[jj]), (double)bb[jj]));
+                            const double xh = __dmul_rn(__dsub_rn((double)__uint_as_float(r[4 * j4 + jj]), mu_d), rstd_d);
+                            yh[jj] = __double2float_rn(__dadd_rn(__dmul_rn(xh, (double)gg[jj]), (double)bb[jj]));
                         }
                     } else {
                         const float2 z0 = make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]));
                         const float2 z1 = make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3]));
-                        const float2 y0 = f2_fma(f2_mul(f2_sub(z0, mu2c), rstd2), make_float2(gv.x, gv.y), make_float2(bv.x, bv.y));
-                        const float2 y1 = f2_fma(f2_mul(f2_sub(z1, mu2c), rstd2), make_float2(gv.z, gv.w), make_float2(bv.z, bv.w));
-                        yh[4 * j4] = y0.x; yh[4 * j4 + 1] = y0.y; yh[4 * j4 + 2] = y1.x; yh[4 * j4 + 3] = y1.y;
+                        const float2 y0 = f2_fma(f2_mul(f2_sub(z0, mu2), rstd2), make_float2(gv.x, gv.y), make_float2(bv.x, bv.y));
+                        const float2 y1 = f2_fma(f2_mul(f2_sub(z1, mu2), rstd2), make_float2(gv.z, gv.w), make_float2(bv.z, bv.w));
+                        yh[0] = y0.x; yh[1] = y0.y; yh[2] = y1.x; yh[3] = y1.y;
                     }
-                }
-                float v[16];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float2 t = f2_mul(make_float2(yh[2 * j], yh[2 * j + 1]), inv2);
-                    v[2 * j] = t.x;
-                    v[2 * j + 1] = t.y;
+                    if (TAPS && p.ln_tap && valid)
+                        *reinterpret_cast<float4*>(p.ln_tap + row * (int64_t)C + c0 + 4 * j4) =
+                            make_float4(yh[0], yh[1], yh[2], yh[3]);
+                    const float2 t0 = f2_mul(make_float2(yh[0], yh[1]), inv2), t1 = f2_mul(make_float2(yh[2], yh[3]), inv2);
+                    v[4 * j4] = t0.x; v[4 * j4 + 1] = t0.y; v[4 * j4 + 2] = t1.x; v[4 * j4 + 3] = t1.y;
                 }
                 uint32_t w[4];
                 if (p.z_y) quant_pack16<false, true>(v, p.z_y, w);
                 else quant_pack16<false, false>(v, 0, w);
                 st_shared_v4(sY + goff(c0), w[0], w[1], w[2], w[3]);
-                if (TAPS && p.ln_tap && valid) {
-                    float* lrow = p.ln_tap + row * (int64_t)C + c0;
-#pragma unroll
-                    for (int j4 = 0; j4 < 4; ++j4)
-                        *reinterpret_cast<float4*>(lrow + 4 * j4) =
-                            make_float4(yh[4 * j4], yh[4 * j4 + 1], yh[4 * j4 + 2], yh[4 * j4 + 3]);
-                }
-            }
+            });
             tc_fence_before();
             fence_proxy_async_smem();          // Y visible to the TMA store
             __syncwarp();
@@ -705,9 +716,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 mbar_arrive(bar_a2empty + 8u * ab);
                 mbar_arrive(bar_yfull);
             }
+            if (stamp) trc[4096 + 4 * i + 3] = gtimer();
             if (++ab == (uint32_t)p.NA2) { ab = 0; aph ^= 1u; }
             if (++xs == NX) { xs = 0; xph ^= 1u; }
-            if (stamp) trc[4096 + 4 * i + 3] = gtimer();
         }
     }
 

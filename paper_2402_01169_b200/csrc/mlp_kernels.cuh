@@ -621,7 +621,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             rr[2 * j4 + 1] = make_float2(v.z, v.w);
                         }
                     } else {
-                        // r = fl(fl(x - z_x) * s_x).  Exact int8 -> float without the
+                        // x - z_x as float (then z = fl((x - z_x) * s_x + d)).  Exact int8 -> float without the
                         // 1/8-rate I2F.S8: with u = x ^ 0x80 (offset binary) the bits
                         // 0x4B0000uu are the float 2^23 + u, and
                         // (2^23 + u) - (2^23 + 128 + z_x) = x - z_x exactly.
@@ -639,8 +639,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                                            __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7651)));
                             const float2 f23 = make_float2(__uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7652)),
                                                            __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7653)));
-                            rr[2 * q] = f2_mul(f2_sub(f01, xoff2), sx2);
-                            rr[2 * q + 1] = f2_mul(f2_sub(f23, xoff2), sx2);
+                            rr[2 * q] = f2_sub(f01, xoff2);      // x - z_x, exact
+                            rr[2 * q + 1] = f2_sub(f23, xoff2);
                         }
                     }
                     float2 z[8];
@@ -648,7 +648,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     tap_acc(r, n0 + cl);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        z[j] = f2_add(z[j], rr[j]);
+                        // z = fl(d + R), or fl((x - z_x) * s_x + d) with one rounding (R3)
+                        z[j] = x_res ? f2_fma(rr[j], sx2, z[j]) : f2_add(z[j], rr[j]);
                         if constexpr (STATS64) {
                             s1d = __dadd_rn(s1d, (double)z[j].x);
                             s1d = __dadd_rn(s1d, (double)z[j].y);

@@ -40,6 +40,13 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Per-warpgroup register budget (all 4 warps of the warpgroup execute it):
+// control warpgroups shrink, the heavy epilogue warpgroups grow.
+template <uint32_t N>
+__device__ __forceinline__ void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+template <uint32_t N>
+__device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+
 // ------------------------------------------------------------------ mbarrier
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -278,6 +285,11 @@ __device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
     uint64_t r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b))); return u2f(r);
+}
+// Product that ptxas cannot contract into a following add: fl(a * b) computed as
+// fma(a, b, -0) (exact same value; observed: ptxas fuses mul.rn.f32x2 + add.rn.f32x2).
+__device__ __forceinline__ float2 f2_mul_nc(float2 a, float2 b) {
+    uint64_t r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(0x8000000080000000ull)); return u2f(r);
 }
 __device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
     uint64_t r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c))); return u2f(r);

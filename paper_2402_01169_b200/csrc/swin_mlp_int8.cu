@@ -569,7 +569,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         const int64_t m_tiles = (T + kBM - 1) / kBM;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)std::min<int64_t>(m_tiles, h->num_sms));
-        cfg.blockDim = dim3((unsigned)kThreads);
+        cfg.blockDim = dim3((unsigned)kFThreads);
         cfg.dynamicSmemBytes = h->fp.smem;
         cfg.stream = s;
         cudaEvent_t* ev = nullptr;

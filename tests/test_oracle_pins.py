@@ -347,3 +347,32 @@ def test_recipe_non_degenerate():
         assert (h == 127).mean() < 0.01
         assert (np.abs(t["y"].astype(int)) >= 127).mean() < 0.01
         assert (np.abs(X.astype(int)).sum(1) > 0).all()
+
+
+def test_ep6_residual_added_with_one_rounding():
+    """Reading R3: with residual == NULL, z = fl((X - z_x) * s_x + d) rounded ONCE (an fma),
+    pinned against exact rational arithmetic (not against another float formula)."""
+    from fractions import Fraction
+
+    def f32(q):   # exact round-to-nearest-even of a rational to float32
+        c = np.float32(float(q))
+        cands = [np.nextafter(c, np.float32(-np.inf)), c, np.nextafter(c, np.float32(np.inf))]
+        return min(cands, key=lambda v: (abs(Fraction(float(v)) - q), int(np.float32(v).view(np.uint32)) & 1))
+
+    rng = np.random.default_rng(11)
+    C = 64
+    A2 = rng.integers(-20000, 20000, size=(4, C)).astype(np.int32)
+    m2 = (rng.random(C).astype(np.float32) * np.float32(1e-4)).astype(np.float32)
+    b2 = (rng.standard_normal(C) * 0.02).astype(np.float32)
+    X = rng.integers(-128, 128, size=(4, C)).astype(np.int8)
+    s_x, z_x = np.float32(0.2125984), 3
+    _, _, z = _ep6(A2, m2, b2, X, s_x=float(s_x), z_x=z_x)
+    differs = 0
+    for t in range(4):
+        for c in range(C):
+            d = f32(Fraction(float(np.float32(A2[t, c]))) * Fraction(float(m2[c])) +
+                    Fraction(float(b2[c])))                         # fmaf(fl(A2), m2, b2)
+            exact = Fraction(int(X[t, c]) - z_x) * Fraction(float(s_x)) + Fraction(float(d))
+            assert z[t, c] == f32(exact), (t, c)
+            differs += np.float32(np.float32(np.float32(int(X[t, c]) - z_x) * s_x) + d) != z[t, c]
+    assert differs > 0   # the case actually distinguishes one rounding from two
