@@ -18,7 +18,7 @@
 // Same arithmetic, in the same order, as the two-kernel path (mlp_kernels.cuh) and
 // the oracle; HBM traffic falls to the algorithmic 2C bytes per token (X in, Y out).
 //
-// CTA = 512 threads, one per SM, persistent over m-tiles cid, cid + grid, ...:
+// CTA = 640 threads, one per SM, persistent over m-tiles cid, cid + grid, ...:
 //   warp 0       TMA producer: X tiles (2 slots) and, unless resident, the W1 / W2
 //                chunks through a `stages`-deep ring in the MMA's consumption order
 //   warp 1       MMA issuer: FC1 of chunk u + L is issued before FC2 of chunk u
@@ -26,15 +26,15 @@
 //   warp 2       TMEM allocator, then the Y store warp
 //   warp 3       loads the per-channel constants once
 //   warps 4-11   op #5: warp = (lane quadrant, 64-column half) of each acc1 chunk
-//   warps 12-15  op #6: warp = lane quadrant; one thread per token row, whole row
-// (512 threads: 128 registers per thread)
+//   warps 12-19  op #6: warp = (lane quadrant, column half); a thread owns half a
+//                token row, the two halves combine their statistics pairwise
 #pragma once
 #include "mlp_kernels.cuh"
 
 namespace swinmlp {
 
 constexpr int kFEp5W0 = 4, kFEp6W0 = 12;
-constexpr int kFThreads = 32 * 16;          // 4 control + 8 op #5 + 4 op #6 warps (128 regs each)
+constexpr int kFThreads = 32 * 20;          // 4 control + 8 op #5 + 8 op #6 warps (96 regs each)
 constexpr int kFHc = 128;                    // hidden chunk = one 128-B K-block of FC2
 constexpr int kFMaxNB1 = 3, kFMaxNH = 4, kFMaxStages = 8;
 constexpr uint32_t kKB = (uint32_t)kBM * kBK;   // one [128 rows][128 B] box
@@ -73,7 +73,7 @@ struct FusedArgs {
 };
 
 struct FusedLayout {
-    uint32_t x, y, hq, w, w2, consts, bars, tmem_slot, total;
+    uint32_t x, y, hq, w, w2, consts, red, bars, tmem_slot, total;
 };
 constexpr int kFMaxNX = 4;
 constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1;
@@ -98,9 +98,9 @@ __host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int st
         L.w2 = 0;
         L.consts = L.w + (uint32_t)stages * fused_stage_bytes(C);
     }
-    L.bars = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
-    L.bars = (L.bars + 15u) & ~15u;
-    (void)ebytes;
+    L.red = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
+    L.red = (L.red + 15u) & ~15u;
+    L.bars = L.red + 2u * 2u * kBM * (uint32_t)ebytes;              // op #6 halves: [part][val][row]
     L.tmem_slot = L.bars + 8u * kFNumBars;
     L.total = L.tmem_slot + 16u;
     return L;
@@ -141,7 +141,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
 
     const uint32_t bar0 = base + L.bars;
     const uint32_t bar_xfull = bar0;                          // [NX]  X tile landed (1 + tx)
-    const uint32_t bar_xempty = bar_xfull + 8u * kFMaxNX;     // [NX]  X tile consumed (op #6 pass 1, 4 warps)
+    const uint32_t bar_xempty = bar_xfull + 8u * kFMaxNX;     // [NX]  X tile consumed (op #6 pass 1, 8 warps)
     const uint32_t bar_wfull = bar_xempty + 8u * kFMaxNX;     // [S]   weight chunk landed (1 + tx)
     const uint32_t bar_wempty = bar_wfull + 8u * kFMaxStages; // [S]   weight chunk consumed (commit)
     const uint32_t bar_wres = bar_wempty + 8u * kFMaxStages;  //       resident weights landed
@@ -150,8 +150,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t bar_hqfull = bar_a1empty + 8u * kFMaxNB1;  // [NH]  Hq chunk written (8 warps)
     const uint32_t bar_hqempty = bar_hqfull + 8u * kFMaxNH;   // [NH]  Hq chunk consumed by FC2 (commit)
     const uint32_t bar_a2full = bar_hqempty + 8u * kFMaxNH;   // [NA2] acc2 complete (commit)
-    const uint32_t bar_a2empty = bar_a2full + 16u;            // [NA2] acc2 drained (4 warps)
-    const uint32_t bar_yfull = bar_a2empty + 16u;             //       Y tile staged (4 warps)
+    const uint32_t bar_a2empty = bar_a2full + 16u;            // [NA2] acc2 drained (8 warps)
+    const uint32_t bar_yfull = bar_a2empty + 16u;             //       Y tile staged (8 warps)
     const uint32_t bar_yempty = bar_yfull + 8u;               //       Y staging read by its stores (1)
     const uint32_t bar_cfull = bar_yempty + 16u;              //       constants loaded (32)
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
@@ -167,9 +167,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < kFMaxNX; ++i) {
             mbar_init(bar_xfull + 8u * i, 1);
-            mbar_init(bar_xempty + 8u * i, 4);
+            mbar_init(bar_xempty + 8u * i, 8);
         }
-        mbar_init(bar_yfull, 4);
+        mbar_init(bar_yfull, 8);
         mbar_init(bar_yempty, 1);
         for (int s = 0; s < kFMaxStages; ++s) {
             mbar_init(bar_wfull + 8u * s, 1);
@@ -186,7 +186,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_a2full + 8u * b, 1);
-            mbar_init(bar_a2empty + 8u * b, 4);
+            mbar_init(bar_a2empty + 8u * b, 8);
         }
         mbar_init(bar_cfull, 32);
         fence_mbar_init();
@@ -486,10 +486,27 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         //         S2/C - (S1/C)^2 cancellation small): mu = K + S1/C,
         //         var = S2/C - (S1/C)^2   (reading R15)
         //   fp64: the oracle's two passes, ascending columns (O5)
-        const uint32_t quad = warp & 3u;
+        const uint32_t quad = warp & 3u, part = (warp - (uint32_t)kFEp6W0) >> 2;
         const uint32_t rit = quad * 32u + lane;
         const uint32_t row_off = rit * (uint32_t)kBK, rsw = rit & 7u;
-        const int nch = C >> 4;                    // even: C % 32 == 0
+        const int hc = C >> 1;                     // columns of this half: [cb, cb + hc)
+        const int cb = (int)part * hc;
+        const int nch = hc >> 4;                   // chunks of 16 (C % 32 == 0)
+        // pairwise combine of the two halves' statistics through smem; both halves
+        // combine in the same (part 0, part 1) order, so they agree bit for bit
+        using acc_t2 = typename std::conditional<STATS64, double, float>::type;
+        acc_t2* red = reinterpret_cast<acc_t2*>(gbase + L.red);
+        auto exchange = [&](acc_t2 v0, acc_t2 v1, acc_t2 (&o)[2][2]) {
+            red[(part * 2u) * kBM + rit] = v0;
+            red[(part * 2u + 1u) * kBM + rit] = v1;
+            named_bar_sync(1u + quad, 64u);       // the two warps of this lane quadrant
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                o[q][0] = red[((uint32_t)q * 2u) * kBM + rit];
+                o[q][1] = red[((uint32_t)q * 2u + 1u) * kBM + rit];
+            }
+            named_bar_sync(1u + quad, 64u);       // reads done before the next tile's writes
+        };
         const float2 inv2 = make_float2(p.inv_y, p.inv_y);
         const float2 sx2 = make_float2(p.s_x, p.s_x);
         const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
@@ -508,12 +525,14 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             if (stamp) trc[4096 + 4 * i] = gtimer();
             const int64_t row = (int64_t)row0_of(i) + rit;
             const bool valid = row < p.M;
-            const uint32_t tb = tmem_base + ((quad * 32u) << 16) + ab * (uint32_t)p.a2_stride;
+            const uint32_t tb = tmem_base + ((quad * 32u) << 16) + ab * (uint32_t)p.a2_stride + (uint32_t)cb;
             const uint32_t xt = sX + xs * xslot;
 
             // chunk loop for the passes over parked z: pairs of chunks behind one wait
+            // (chunk index ch is local to this half; column = cb + 16 ch)
             auto for_chunks = [&](auto&& fn) {
-                for (int ch = 0; ch < nch; ch += 2) {
+                int ch = 0;
+                for (; ch + 1 < nch; ch += 2) {
                     uint32_t ra[16], rb[16];
                     tmem_ld16(tb + (uint32_t)(ch * 16), ra);
                     tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rb);
@@ -521,6 +540,12 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     reg_fence16(rb);
                     fn(ra, ch);
                     fn(rb, ch + 1);
+                }
+                if (ch < nch) {
+                    uint32_t ra[16];
+                    tmem_ld16(tb + (uint32_t)(ch * 16), ra);
+                    tmem_wait_ld_dep(ra);
+                    fn(ra, ch);
                 }
             };
             // pass 1: z = fl(fl(fmaf(fl(A2), m2, b2)) + r), back into TMEM; statistics.
@@ -599,7 +624,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 if (TAPS && p.acc2_tap && valid) {
 #pragma unroll
                     for (int j4 = 0; j4 < 4; ++j4)
-                        st_v4(p.acc2_tap + row * (int64_t)C + c0 + 4 * j4,
+                        st_v4(p.acc2_tap + row * (int64_t)C + cb + c0 + 4 * j4,
                               make_int4((int)r[4 * j4], (int)r[4 * j4 + 1], (int)r[4 * j4 + 2], (int)r[4 * j4 + 3]));
                 }
                 uint32_t zu[16];
@@ -610,37 +635,51 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 }
                 tmem_st16(tb + (uint32_t)c0, zu);
             };
+            auto set_shift = [&](const float2 (&z)[8]) {   // K = mean of this half's first 16 values
+                float2 t = z[0];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) t = f2_add(t, z[j]);
+                K = __fmul_rn(__fadd_rn(t.x, t.y), 0.0625f);
+                Kv = make_float2(K, K);
+            };
+            auto store_z = [&](const float2 (&z)[8], int c0) {
+                if (p.resid_out && valid) {
+                    float* zrow = p.resid_out + row * (int64_t)C + c0;
+#pragma unroll
+                    for (int j4 = 0; j4 < 4; ++j4)
+                        *reinterpret_cast<float4*>(zrow + 4 * j4) =
+                            make_float4(z[2 * j4].x, z[2 * j4].y, z[2 * j4 + 1].x, z[2 * j4 + 1].y);
+                }
+            };
             auto pass1 = [&](auto resid_c) {
-                for (int ch = 0; ch < nch; ch += 2) {
+                int ch = 0;
+                for (; ch + 1 < nch; ch += 2) {
                     uint32_t ra[16], rb[16];
                     tmem_ld16(tb + (uint32_t)(ch * 16), ra);
                     tmem_ld16(tb + (uint32_t)((ch + 1) * 16), rb);
                     tmem_wait_ld_dep(ra);
                     reg_fence16(rb);
                     float2 za[8], zb[8];
-                    chunk_z(resid_c, ra, ch * 16, za);
-                    chunk_z(resid_c, rb, ch * 16 + 16, zb);
-                    if (!STATS64 && ch == 0) {   // shift: mean of the row's first 16 values
-                        float2 t = za[0];
-#pragma unroll
-                        for (int j = 1; j < 8; ++j) t = f2_add(t, za[j]);
-                        K = __fmul_rn(__fadd_rn(t.x, t.y), 0.0625f);
-                        Kv = make_float2(K, K);
-                    }
+                    chunk_z(resid_c, ra, cb + ch * 16, za);
+                    chunk_z(resid_c, rb, cb + ch * 16 + 16, zb);
+                    if (!STATS64 && ch == 0) set_shift(za);
                     stats(za);
                     stats(zb);
-                    if (p.resid_out && valid) {
-                        float* zrow = p.resid_out + row * (int64_t)C + ch * 16;
-#pragma unroll
-                        for (int j4 = 0; j4 < 4; ++j4) {
-                            *reinterpret_cast<float4*>(zrow + 4 * j4) =
-                                make_float4(za[2 * j4].x, za[2 * j4].y, za[2 * j4 + 1].x, za[2 * j4 + 1].y);
-                            *reinterpret_cast<float4*>(zrow + 16 + 4 * j4) =
-                                make_float4(zb[2 * j4].x, zb[2 * j4].y, zb[2 * j4 + 1].x, zb[2 * j4 + 1].y);
-                        }
-                    }
+                    store_z(za, cb + ch * 16);
+                    store_z(zb, cb + ch * 16 + 16);
                     park(za, ra, ch * 16);
                     park(zb, rb, ch * 16 + 16);
+                }
+                if (ch < nch) {
+                    uint32_t ra[16];
+                    tmem_ld16(tb + (uint32_t)(ch * 16), ra);
+                    tmem_wait_ld_dep(ra);
+                    float2 za[8];
+                    chunk_z(resid_c, ra, cb + ch * 16, za);
+                    if (!STATS64 && ch == 0) set_shift(za);
+                    stats(za);
+                    store_z(za, cb + ch * 16);
+                    park(za, ra, ch * 16);
                 }
             };
             if (p.resid) pass1(std::true_type{});
@@ -653,7 +692,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             float mu_f = 0.f, rstd_f = 0.f;
             double mu_d = 0.0, rstd_d = 0.0;
             if constexpr (STATS64) {
-                mu_d = s1d / (double)C;
+                acc_t2 o[2][2];
+                exchange(s1d, 0.0, o);
+                mu_d = __dadd_rn(o[0][0], o[1][0]) / (double)C;
                 double s2d = 0.0;
                 for_chunks([&](uint32_t (&r)[16], int) {
 #pragma unroll
@@ -662,11 +703,21 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                         s2d = __dadd_rn(s2d, __dmul_rn(d, d));
                     }
                 });
-                rstd_d = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(s2d, (double)C), (double)p.eps)));
+                exchange(s2d, 0.0, o);
+                const double SS = __dadd_rn(o[0][0], o[1][0]);
+                rstd_d = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(SS, (double)C), (double)p.eps)));
             } else {
-                const float m1 = __fdiv_rn(__fadd_rn(s1f.x, s1f.y), (float)C);
-                const float var = fmaxf(__fsub_rn(__fdiv_rn(__fadd_rn(s2f.x, s2f.y), (float)C), __fmul_rn(m1, m1)), 0.0f);
-                mu_f = __fadd_rn(K, m1);
+                // each half: mean m_h = K + S1/n, M2_h = S2 - S1^2/n (n = C/2); combined
+                // (Chan): mean = (m_0 + m_1)/2, M2 = M2_0 + M2_1 + (m_1 - m_0)^2 n/2
+                const float nh = (float)hc;
+                const float S1 = __fadd_rn(s1f.x, s1f.y), S2 = __fadd_rn(s2f.x, s2f.y);
+                const float q1 = __fdiv_rn(S1, nh);
+                acc_t2 o[2][2];
+                exchange(__fadd_rn(K, q1), __fsub_rn(S2, __fmul_rn(S1, q1)), o);
+                const float dm = __fsub_rn(o[1][0], o[0][0]);
+                mu_f = __fmul_rn(__fadd_rn(o[0][0], o[1][0]), 0.5f);
+                const float M2 = __fadd_rn(__fadd_rn(o[0][1], o[1][1]), __fmul_rn(__fmul_rn(dm, dm), __fmul_rn(nh, 0.5f)));
+                const float var = fmaxf(__fdiv_rn(M2, (float)C), 0.0f);
                 rstd_f = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
             }
             const float2 mu2 = make_float2(mu_f, mu_f), rstd2 = make_float2(rstd_f, rstd_f);
@@ -676,7 +727,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             // buffer once the previous tile's stores have read it
             mbar_wait_backoff(bar_yempty, (i & 1u) ^ 1u);
             for_chunks([&](uint32_t (&r)[16], int ch) {
-                const int c0 = ch * 16;
+                const int c0 = cb + ch * 16;
                 float v[16];
 #pragma unroll
                 for (int j4 = 0; j4 < 4; ++j4) {
