@@ -72,7 +72,8 @@ struct GemmArgs {
     int32_t CS;            // CTAs per cluster (share one m-tile, A multicast)
     int32_t stages;        // smem ring depth
     int32_t G;             // ping-pong groups = accumulator buffers = staging tiles (2 or 4)
-    int32_t xstage;        // op #6: residual x tiles staged in smem by TMA (else read from x)
+    int32_t xstage;        // op #6: residual x tile buffers in smem, loaded by TMA (G: one per
+                           // group, 1: one shared by the groups, 0: pass 1 reads x from global)
     int32_t resb;          // B (weights) resident in smem for the whole kernel (requires mt_major)
     int32_t mt_major;      // tile order: the cluster's m-tiles with the n-groups innermost
     int32_t out_w;         // output TMA box width in bytes (128/64/32/16; swizzle of the same width)
@@ -125,7 +126,7 @@ __host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int s
     L.bres = L.b + (resb_bytes ? 0u : (uint32_t)stages * (uint32_t)BN * kBK);
     L.out = L.bres + resb_bytes;                                   // [G] output staging tiles
     L.xres = L.out + (uint32_t)G * tile;                           // op #6: [G] residual x tiles
-    L.consts = L.xres + (epi == EP6_LN && xstage ? (uint32_t)G * tile : 0u); // [G][kNConst][BN] fp32
+    L.consts = L.xres + (epi == EP6_LN ? (uint32_t)xstage * tile : 0u);       // [G][kNConst][BN] fp32
     L.bars = L.consts + (uint32_t)G * kNConst * (uint32_t)BN * 4u;
     L.tmem_slot = L.bars + 8u * kNumBars(stages);
     const uint32_t eb = (uint32_t)ebytes;
@@ -294,6 +295,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     };
     auto n0_of = [&](uint32_t ng) -> int { return (int)((ng * CS + rank) * (uint32_t)BN); };
+    // op #6 x tile buffer of tile `it` and its phase (xstage buffers: 1 or G, powers of two)
+    const uint32_t xsb = p.xstage > 0 ? (uint32_t)p.xstage : 1u;
+    const uint32_t lgX = xsb == 4u ? 2u : xsb == 2u ? 1u : 0u;
+    auto xbuf_of = [&](uint32_t it) -> uint32_t { return it & (xsb - 1u); };
+    auto xph_of = [&](uint32_t it) -> uint32_t { return (it >> lgX) & 1u; };
 
     // Producer, MMA and store roles run on the whole warp with warp-uniform control
     // flow (addresses and descriptors stay in uniform registers); one elected lane
@@ -450,12 +456,13 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const int n0 = n0_of(ng);
             const uint32_t buf = it & (G - 1u), aph = (it >> lgG) & 1u;
             if (load_x) {
-                mbar_wait(bar_xfree + 8u * buf, aph ^ 1u);
+                const uint32_t xb = xbuf_of(it), xph = xph_of(it);
+                mbar_wait(bar_xfree + 8u * xb, xph ^ 1u);
                 if (lane == 0) {
-                    const uint32_t dst = base + L.xres + buf * tile_bytes;
-                    mbar_arrive_expect_tx(bar_xfull + 8u * buf, tile_bytes);
+                    const uint32_t dst = base + L.xres + xb * tile_bytes;
+                    mbar_arrive_expect_tx(bar_xfull + 8u * xb, tile_bytes);
                     for (uint32_t sub = 0; sub < ((uint32_t)BN >> lgW); ++sub)
-                        tma_load_2d(&tmX, dst + (sub << (lgW + 7u)), bar_xfull + 8u * buf, n0 + (int)(sub << lgW),
+                        tma_load_2d(&tmX, dst + (sub << (lgW + 7u)), bar_xfull + 8u * xb, n0 + (int)(sub << lgW),
                                     (int32_t)(m_tile * kBM));
                 }
                 __syncwarp();
@@ -600,8 +607,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int C = p.ldo;
                 const bool x_res = (p.resid == nullptr);
                 const bool x_smem = x_res && p.xstage;
-                const uint32_t xtile = base + L.xres + buf * tile_bytes;
-                if (x_smem) mbar_wait(bar_xfull + 8u * buf, aph);   // residual x tile landed
+                const uint32_t xtile = base + L.xres + xbuf_of(it) * tile_bytes;
+                if (x_smem) mbar_wait(bar_xfull + 8u * xbuf_of(it), xph_of(it));   // residual x tile landed
                 if (trc && elected && it < 64) trc[2048 + 16 * it + 6] = gtimer();
                 const float2 sx2 = make_float2(p.s_x, p.s_x);
                 const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
@@ -671,7 +678,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 tmem_wait_st();
                 if (x_smem) {   // the x tile has been consumed: let the loader prefetch the next one
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(bar_xfree + 8u * buf);
+                    if (lane == 0) mbar_arrive(bar_xfree + 8u * xbuf_of(it));
                 }
                 if (trc && elected && it < 64) trc[2048 + 16 * it + 3] = gtimer();
 

@@ -184,10 +184,11 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // output staging: G ping-pong groups / accumulator buffers / staging tiles, 4 when
     // 4*BN TMEM columns fit (more tiles in flight), else 2; op #6 also prefers its
     // residual x tiles staged in smem
-    for (int xs : {1, 0}) {
-    if (epi != EP6_LN && xs == 0) continue;
+    for (int xs : {4, 2, 1, 0}) {   // op #6 x tile buffers: one per group, one shared, none
+    if (epi != EP6_LN && xs != 0) continue;
     for (int G : {4, 2}) {
         if (G * pl.BN > 512) continue;
+        if (xs > 1 && xs != G) continue;
         const uint32_t rbb = rb ? resb_bytes : 0u;
         const uint32_t stage = (uint32_t)(kBM * kBK) + (rb ? 0u : (uint32_t)pl.BN * kBK);
         const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb).total + 1024;
