@@ -613,9 +613,12 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const float2 sx2 = make_float2(p.s_x, p.s_x);
                 const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
                 const float2 xoff2 = make_float2(xoff, xoff);
-                // pass 1: z = fl(fl(fmaf(fl(A2), m2, b2)) + r); park z in TMEM; row sum
+                // pass 1: z = fl(fl(fmaf(fl(A2), m2, b2)) + r); park z in TMEM; row statistics:
+                // fp64 the plain sum (two-pass, O5 order); fp32 shifted sums (S1, S2) about
+                // K = mean of this warp's first 16 columns (R15)
                 double s1d = 0.0;
-                float2 s1f = make_float2(0.f, 0.f);
+                float2 s1f = make_float2(0.f, 0.f), s2f = make_float2(0.f, 0.f), Kv = make_float2(0.f, 0.f);
+                float K = 0.f;
                 for_chunks([&](uint32_t (&r)[16], int ch) {
                     const int cl = ch * kChunk;
                     float2 rr[8];
@@ -660,11 +663,24 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         if constexpr (STATS64) {
                             s1d = __dadd_rn(s1d, (double)z[j].x);
                             s1d = __dadd_rn(s1d, (double)z[j].y);
-                        } else {
-                            s1f = f2_add(s1f, z[j]);
                         }
                         r[2 * j] = __float_as_uint(z[j].x);
                         r[2 * j + 1] = __float_as_uint(z[j].y);
+                    }
+                    if constexpr (!STATS64) {
+                        if (ch == ch_lo) {
+                            float2 t = z[0];
+#pragma unroll
+                            for (int j = 1; j < 8; ++j) t = f2_add(t, z[j]);
+                            K = __fmul_rn(__fadd_rn(t.x, t.y), 0.0625f);
+                            Kv = make_float2(K, K);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float2 d = f2_sub(z[j], Kv);
+                            s1f = f2_add(s1f, d);
+                            s2f = f2_fma(d, d, s2f);
+                        }
                     }
                     if (p.resid_out && valid) {
                         float* zrow = p.resid_out + row * (int64_t)C + n0 + cl;
@@ -716,45 +732,80 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     o1 = S1;
                     return S0;
                 };
-                acc_t s1, unused;
-                if constexpr (STATS64) s1 = s1d; else s1 = __fadd_rn(s1f.x, s1f.y);
-                const acc_t mu = row_sum2(s1, (acc_t)0, 0, unused) / (acc_t)C;
-                if (trc && elected && it < 64) trc[2048 + 16 * it + 4] = gtimer();
-
-                // pass 2: centred sum of squares
-                double s2d = 0.0;
-                float2 s2f = make_float2(0.f, 0.f), e2f = make_float2(0.f, 0.f);
-                const float2 mu2 = make_float2((float)mu, (float)mu);
-                for_chunks([&](uint32_t (&r)[16], int) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float2 zz = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-                        if constexpr (STATS64) {
-                            const double d0 = __dsub_rn((double)zz.x, (double)mu), d1 = __dsub_rn((double)zz.y, (double)mu);
-                            s2d = __dadd_rn(s2d, __dmul_rn(d0, d0));
-                            s2d = __dadd_rn(s2d, __dmul_rn(d1, d1));
-                        } else {
-                            const float2 dz = f2_sub(zz, mu2);
-                            s2f = f2_fma(dz, dz, s2f);
-                            e2f = f2_add(e2f, dz);   // residual of the rounded mean
-                        }
-                    }
-                });
+                double mu_d64 = 0.0;
                 acc_t rstd;
-                float2 mu2c = mu2;
+                float2 mu2c;
                 if constexpr (STATS64) {
+                    acc_t unused;
+                    const acc_t mu = row_sum2(s1d, (acc_t)0, 0, unused) / (acc_t)C;
+                    if (trc && elected && it < 64) trc[2048 + 16 * it + 4] = gtimer();
+                    // pass 2: centred sum of squares
+                    double s2d = 0.0;
+                    for_chunks([&](uint32_t (&r)[16], int) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const double d0 = __dsub_rn((double)__uint_as_float(r[j]), (double)mu);
+                            s2d = __dadd_rn(s2d, __dmul_rn(d0, d0));
+                        }
+                    });
                     double dummy;
                     const double SS = row_sum2(s2d, 0.0, 1, dummy);
                     rstd = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(SS, (double)C), (double)p.eps)));
+                    mu2c = make_float2((float)mu, (float)mu);
+                    mu_d64 = (double)mu;
                 } else {
-                    // corrected two-pass (Bjorck): var = S2/C - (E/C)^2, mean += E/C, where E is
-                    // the sum of the residuals z - mu of the rounded mean; robust when |mean| >> std
-                    float E;
-                    const float SS = row_sum2(__fadd_rn(s2f.x, s2f.y), __fadd_rn(e2f.x, e2f.y), 1, E);
-                    const float ec = __fdiv_rn(E, (float)C);
-                    const float var = fmaxf(__fsub_rn(__fdiv_rn(SS, (float)C), __fmul_rn(ec, ec)), 0.0f);
-                    rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
-                    mu2c = make_float2(__fadd_rn((float)mu, ec), __fadd_rn((float)mu, ec));
+                    // one round of statistics exchange: per warp (mean, M2) of its columns,
+                    // combined pairwise (Chan) over the column parts (smem), then over the CS
+                    // CTAs of the cluster (DSMEM), in the same order everywhere
+                    const float S1 = __fadd_rn(s1f.x, s1f.y), S2 = __fadd_rn(s2f.x, s2f.y);
+                    const float nw = (float)((ch_hi - ch_lo) * kChunk);
+                    const float q1 = nw > 0.f ? __fdiv_rn(S1, nw) : 0.f;
+                    float m = __fadd_rn(K, q1), M2 = __fsub_rn(S2, __fmul_rn(S1, q1)), n = nw;
+                    if (P > 1) {
+                        const uint32_t slot = (buf * 2u * 2u) * 2u;     // [G][pass 0][part][val]
+                        red[(slot + part * 2u) * kBM + rit] = m;
+                        red[(slot + part * 2u + 1u) * kBM + rit] = M2;
+                        named_bar_sync(1u + buf, 32u * tile_warps);
+                        const float m0 = red[slot * kBM + rit], qa = red[(slot + 1u) * kBM + rit];
+                        const float m1 = red[(slot + 2u) * kBM + rit], qb = red[(slot + 3u) * kBM + rit];
+                        const float n0 = (float)(min(per, nch) * kChunk);
+                        const float n1 = (float)(BN - min(per, nch) * kChunk);
+                        const float nt = __fadd_rn(n0, n1);
+                        const float dm = __fsub_rn(m1, m0);
+                        m = __fadd_rn(m0, __fmul_rn(dm, __fdiv_rn(n1, nt)));
+                        M2 = __fadd_rn(__fadd_rn(qa, qb), __fmul_rn(__fmul_rn(dm, dm), __fdiv_rn(__fmul_rn(n0, n1), nt)));
+                        n = nt;
+                    }
+                    if (CS > 1) {
+                        const uint32_t sid = buf * 2u;
+                        const uint32_t xb = bar_xst + 8u * sid;
+                        if (part == 0) {
+                            if (grp_leader) mbar_arrive_expect_tx(xb, CS * kBM * 2u * (uint32_t)sizeof(acc_t));
+                            const uint32_t d0 = smem_u32(xbuf + (((size_t)sid * CS + rank) * 2u) * kBM + rit);
+                            for (uint32_t r = 0; r < CS; ++r) {
+                                st_async_val(mapa(d0, r), (acc_t)m, mapa(xb, r));
+                                st_async_val(mapa(d0 + kBM * (uint32_t)sizeof(acc_t), r), (acc_t)M2, mapa(xb, r));
+                            }
+                        }
+                        mbar_wait_cluster(xb, aph);
+                        float msum = 0.f, qsum = 0.f;
+                        for (uint32_t r = 0; r < CS; ++r) {
+                            msum = __fadd_rn(msum, (float)xbuf[(((size_t)sid * CS + r) * 2u) * kBM + rit]);
+                            qsum = __fadd_rn(qsum, (float)xbuf[(((size_t)sid * CS + r) * 2u + 1u) * kBM + rit]);
+                        }
+                        const float mean = __fdiv_rn(msum, (float)CS);
+                        float dsq = 0.f;
+                        for (uint32_t r = 0; r < CS; ++r) {
+                            const float dr = __fsub_rn((float)xbuf[(((size_t)sid * CS + r) * 2u) * kBM + rit], mean);
+                            dsq = __fmaf_rn(dr, dr, dsq);
+                        }
+                        m = mean;
+                        M2 = __fmaf_rn(dsq, n, qsum);
+                    }
+                    if (trc && elected && it < 64) trc[2048 + 16 * it + 4] = gtimer();
+                    const float var = fmaxf(__fdiv_rn(M2, (float)C), 0.0f);
+                    rstd = (acc_t)__fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
+                    mu2c = make_float2(m, m);
                 }
                 const float2 rstd2 = make_float2((float)rstd, (float)rstd);
                 if (trc && elected && it < 64) trc[2048 + 16 * it + 5] = gtimer();
@@ -774,7 +825,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                const double xh = __dmul_rn(__dsub_rn((double)__uint_as_float(r[4 * j4 + j]), mu), rstd);
+                                const double xh = __dmul_rn(__dsub_rn((double)__uint_as_float(r[4 * j4 + j]), mu_d64), rstd);
                                 yh[4 * j4 + j] = __double2float_rn(__dadd_rn(__dmul_rn(xh, (double)gg[j]), (double)bb[j]));
                             }
                         } else {
