@@ -196,6 +196,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_launch_dependents();   // PDL: see mlp_kernels.cuh
 
     const uint32_t m_tiles = (uint32_t)((p.M + kBM - 1) / kBM);
     const uint32_t cid = blockIdx.x, grid = gridDim.x;
@@ -223,6 +224,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             }
             __syncwarp();
         }
+        pdl_wait();   // X: produced by the previous kernel
         // cursors advance incrementally (no runtime division in the role loops)
         uint32_t i = 0, j = 0, j2 = 0;     // FC1 tile / chunk of q; FC2 chunk of q - LA
         uint32_t xs = 0, xph = 0;          // X slot of tile i, its phase
@@ -354,6 +356,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         }
     } else if (warp == 2) {
         // ============================ Y store warp ============================
+        pdl_wait();   // Y may overwrite what the previous kernel still reads
         for (uint32_t i = 0; i < n_my; ++i) {
             mbar_wait_backoff(bar_yfull, i & 1u);
             if (lane == 0) {
@@ -393,6 +396,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         const uint32_t rit = quad * 32u + lane;
         const uint32_t row_off = rit * (uint32_t)kBK, rsw = rit & 7u;
         const float2 inv2 = make_float2(p.inv_h, p.inv_h);
+        pdl_wait();   // (taps)
         mbar_wait(bar_cfull, 0);
         uint32_t i = 0, j = 0, b = 0, bph = 0, hb = 0, hph = 0;
         for (uint32_t u = 0; u < U; ++u) {
@@ -515,6 +519,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             const uint32_t kb = (uint32_t)c >> 7, g = ((uint32_t)c >> 4) & 7u;
             return kb * kKB + row_off + ((g ^ rsw) << 4);
         };
+        pdl_wait();   // (global residual, residual_out, taps)
         mbar_wait(bar_cfull, 0);
         uint32_t ab = 0, aph = 0, xs = 0, xph = 0;
         for (uint32_t i = 0; i < n_my; ++i) {

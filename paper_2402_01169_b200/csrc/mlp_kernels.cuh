@@ -267,6 +267,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: the next kernel may start its prologue as soon as SMs free up; every access
+    // to activation memory (written / read by the neighbouring kernels) waits below
+    pdl_launch_dependents();
 
     const uint32_t cid = blockIdx.x / CS, nclus = gridDim.x / CS;
     const uint32_t num_units = (uint32_t)p.num_units, n_groups = (uint32_t)p.n_groups;
@@ -326,6 +329,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                     kb * kBK, n0_of(ng));
             }
             __syncwarp();
+            pdl_wait();   // activations: produced by the previous kernel
             // the ring streams A only: one load per (m-tile, k-block)
             for (uint32_t j = 0; j < my_m; ++j) {
                 const int row0 = (int)((cid + j * nclus) * kBM);
@@ -341,6 +345,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
             }
         } else {
+            pdl_wait();   // activations: produced by the previous kernel
             for (uint32_t it = 0; it < my_tiles; ++it) {
                 uint32_t m_tile, ng;
                 tile_at(it, m_tile, ng);
@@ -425,6 +430,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp == 2) {
         // ============================ output store warp =========================
+        pdl_wait();   // outputs may overwrite what the previous kernel still reads
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t sb = it & (G - 1u), sph = (it >> lgG) & 1u;
             mbar_wait(bar_sfull + 8u * sb, sph);
@@ -450,6 +456,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // as the previous user of that buffer finished pass 1 (xfree), then copy the
         // per-column constants once the buffer's previous tile is fully drained (tempty).
         const bool load_x = IS_LN && (p.resid == nullptr) && p.xstage;
+        if (load_x) pdl_wait();
         for (uint32_t it = 0; it < my_tiles; ++it) {
             uint32_t m_tile, ng;
             tile_at(it, m_tile, ng);
@@ -508,6 +515,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const bool elected = (ew == 0 && lane == 0);
         const bool grp_leader = ((ew & (tile_warps - 1u)) == 0 && lane == 0);
         const float2 inv2 = make_float2(p.inv_q, p.inv_q);
+        pdl_wait();   // (global residual / taps)
 
         for (uint32_t it = grp; it < my_tiles; it += G) {
             uint32_t m_tile, ng;

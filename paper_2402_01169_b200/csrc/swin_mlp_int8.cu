@@ -79,6 +79,15 @@ struct FusedPlan {
     uint32_t smem = 0;
 };
 
+// Programmatic dependent launch between consecutive kernels (SWIN_MLP_NO_PDL=1 disables).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SWIN_MLP_NO_PDL");
+        return !(e && *e && *e != '0');
+    }();
+    return on;
+}
+
 bool normal_positive(float v) { return std::isfinite(v) && std::fpclassify(v) == FP_NORMAL && v > 0.0f; }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -294,13 +303,15 @@ swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMa
     cfg.blockDim = dim3((unsigned)pl.threads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)pl.CS;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see the kernels)
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, pl.fn, ta, tb, to, tx, a));
     static const bool sync_check = std::getenv("SWIN_MLP_SYNC_CHECK") != nullptr;
     if (sync_check) {   // debug: surface asynchronous kernel faults at the launch that caused them
@@ -573,6 +584,11 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         cfg.blockDim = dim3((unsigned)kFThreads);
         cfg.dynamicSmemBytes = h->fp.smem;
         cfg.stream = s;
+        cudaLaunchAttribute fat[1];
+        fat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        fat[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = fat;
+        cfg.numAttrs = 1;
         cudaEvent_t* ev = nullptr;
         if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
         if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
