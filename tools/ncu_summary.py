@@ -4,7 +4,7 @@
 
 Reads gpurun_out/launches_<tag>.csv (the gpu__time_duration launch list of
 `bench.py --steps 2 --warmup 1 --pairs 1 --no-cpu`) and gpurun_out/full_stage{0..3}.ncu-rep
-(`ncu --set full` of tools/prof_layer.py <stage>: FC1 then FC2 of the 2nd run),
+(`ncu --set full` of tools/prof_layer.py <stage>: the 2nd run's kernels),
 writes profiles/<tag>_launches.csv, profiles/<tag>_ncu_summary.md and
 profiles/ncu_traffic.json (DRAM bytes per launch, keyed like bench.py's kernels).
 """
@@ -21,6 +21,21 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+
+
+def fused_stage(L):
+    """The one-kernel plan covers C <= 256 with H % 128 == 0 (swin_mlp_int8.cu make_fused)."""
+    return L.C <= 256 and L.H % 128 == 0
+
+
+def step_kernel_names():
+    names = []
+    for L, T, _ in synth.swin_t_batch64_layers():
+        if fused_stage(L):
+            names.append(f"fused_mlp[C={L.C},T={T}]")
+        else:
+            names += [f"fc1_relu_q[C={L.C},T={T}]", f"fc2_ln_q[C={L.C},T={T}]"]
+    return names
 out = os.path.join(ROOT, "profiles")
 os.makedirs(out, exist_ok=True)
 lines = []
@@ -32,7 +47,7 @@ if os.path.exists(src):
     txt = open(src).read()
     body = txt[txt.index('"ID"'):] if '"ID"' in txt else txt
     rows = list(csv.DictReader(io.StringIO(body)))
-    per = {}
+    per, ours_seq = {}, []
     for r in rows:
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
@@ -40,8 +55,11 @@ if os.path.exists(src):
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
         us = v / 1000.0 if unit == "ns" else v if unit == "us" else v * 1000.0 if unit == "ms" else v
-        key = "mlp_gemm_kernel" if "mlp_gemm_kernel" in name else name[:60]
+        key = "fused_mlp_kernel" if "fused_mlp_kernel" in name else \
+            "mlp_gemm_kernel" if "mlp_gemm_kernel" in name else name[:60]
         per.setdefault(key, []).append(us)
+        if key in ("fused_mlp_kernel", "mlp_gemm_kernel"):
+            ours_seq.append(us)
     lines.append(f"## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, {tag})\n")
     lines.append("Cold-cache, serialised per-launch times: compare shares, not absolutes.\n")
     lines.append("| kernel | launches | total us | mean us |")
@@ -49,20 +67,17 @@ if os.path.exists(src):
     tot = sum(sum(v) for v in per.values())
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.2f} |")
-    ours = per.get("mlp_gemm_kernel", [])
-    if ours:
-        # the bench's timed steps: 8 launches per step; the last 16 mlp launches before e2e are 2 steps
-        lines.append(f"\nOur kernels: {len(ours)} launches, {sum(ours):.1f} us of {tot:.1f} us listed "
-                     f"({sum(ours)/tot:.1%}; the rest is the L2-flush fill, copies and torch setup).\n")
-        step = ours[8:16] if len(ours) >= 16 else ours[:8]
-        names = []
-        for L, T, _ in synth.swin_t_batch64_layers():
-            names += [f"fc1_relu_q[C={L.C},T={T}]", f"fc2_ln_q[C={L.C},T={T}]"]
-        lines.append("Per-launch share of one timed step (launches 9-16):\n")
+    names = step_kernel_names()
+    n = len(names)
+    if len(ours_seq) >= 2 * n:
+        lines.append(f"\nOur kernels: {len(ours_seq)} launches, {sum(ours_seq):.1f} us of {tot:.1f} us listed "
+                     f"({sum(ours_seq)/tot:.1%}; the rest is the L2-flush fill, copies and torch setup).\n")
+        step = ours_seq[n:2 * n]      # the second step (warm)
+        lines.append(f"Per-launch share of one step (launches {n + 1}-{2 * n}):\n")
         lines.append("| launch | us | share |")
         lines.append("|---|---|---|")
-        for n, us in zip(names, step):
-            lines.append(f"| {n} | {us:.2f} | {us/sum(step):.1%} |")
+        for nm, us in zip(names, step):
+            lines.append(f"| {nm} | {us:.2f} | {us/sum(step):.1%} |")
 
 # ---- full captures
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -100,7 +115,8 @@ for st in range(4):
                 f = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(un, 1)
                 return v * f
             return v
-        name = f"{'fc1_relu_q' if j == 0 else 'fc2_ln_q'}[C={L.C},T={T}]"
+        name = f"fused_mlp[C={L.C},T={T}]" if fused_stage(L) else \
+            f"{'fc1_relu_q' if j == 0 else 'fc2_ln_q'}[C={L.C},T={T}]"
         rd, wr = val("dram__bytes_read.sum", "MB"), val("dram__bytes_write.sum", "MB")
         traffic[name] = (rd + wr) * 1e6
         lines.append(f"| {name} | {val('gpu__time_duration.sum', 'us'):.1f} | {rd:.1f} | {wr:.1f} | "

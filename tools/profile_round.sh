@@ -10,8 +10,12 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
     python bench.py --steps 2 --warmup 3 --pairs 1 --no-cpu > $o/ncu_launch_$tag.log 2>&1
 for s in 0 1 2 3; do
   python tools/prof_layer.py $s 2 > $o/plain_${tag}_$s.log 2>&1 || continue
-  ncu --set full --clock-control none --import-source on -k regex:mlp_gemm_kernel -s 2 -c 2 \
-      -o $o/full_stage$s -f python tools/prof_layer.py $s 2 > $o/ncu_full_${tag}_$s.log 2>&1
+  # stages 0/1 run the one-kernel plan (1 launch per run), stages 2/3 two kernels
+  if [ $s -lt 2 ]; then skip=1; cnt=1; else skip=2; cnt=2; fi
+  ncu --set full --clock-control none --import-source on -k regex:"mlp_gemm_kernel|fused_mlp_kernel" \
+      -s $skip -c $cnt -o $o/full_stage$s -f python tools/prof_layer.py $s 2 > $o/ncu_full_${tag}_$s.log 2>&1
 done
-for s in 0 1 2 3; do python tools/trace_layer.py $s > $o/trace_${tag}_$s.log 2>&1; done
+for s in 2 3; do python tools/trace_layer.py $s > $o/trace_${tag}_$s.log 2>&1; done
+python tools/trace_fused.py 96 200704 > $o/trace_${tag}_0.log 2>&1
+python tools/trace_fused.py 192 50176 > $o/trace_${tag}_1.log 2>&1
 echo done
