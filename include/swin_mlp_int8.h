@@ -128,8 +128,12 @@ swin_mlp_status_t swin_mlp_int8_run_debug(swin_mlp_int8_t h, const int8_t* x, co
 /* End-to-end convenience: x, residual (or NULL) and y are HOST buffers
  * (pinned for full bandwidth); device staging is taken from `workspace`,
  * which must hold swin_mlp_int8_host_workspace_bytes(h, T, residual != NULL).
- * Copies H2D, runs, copies D2H, all on `stream`; returns after enqueueing
- * (synchronize the stream before reading y). */
+ * Pipelined over up to 8 token chunks: the copy-in of a chunk and the copy-out
+ * of the previous one (on two handle-owned streams) overlap the kernels of the
+ * current one (on `stream`).  Ordered after earlier work on `stream`; returns
+ * after enqueueing, and `stream` completes only when y_host is written
+ * (synchronize it before reading y).  Not re-entrant per handle: one run_host
+ * at a time for a given handle. */
 size_t swin_mlp_int8_host_workspace_bytes(swin_mlp_int8_t h, int64_t T, int32_t with_residual);
 swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host, const float* residual_host,
                                          int8_t* y_host, int64_t T, void* workspace, size_t workspace_bytes,

@@ -260,6 +260,9 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
     fp.NJ = H / kFHc;
     // TMEM (512 columns): acc2 buffers, then 128-column acc1 buffers.  C <= 128: two of
     // each (op #6 of one tile overlaps FC2 of the next); else one acc2 (C or 256 columns).
+    //   C <= 128:  2 acc2 (128-column stride) + 2 acc1
+    //   C <= 256:  1 acc2 + 2 acc1 (measured: 2 acc2 + 1 acc1 at C = 192 is slower, the
+    //              single acc1 serialises FC1 and op #5)
     if (C <= 128) { fp.NA2 = 2; fp.a2_stride = 128; fp.a1_col = 256; }
     else { fp.NA2 = 1; fp.a2_stride = 0; fp.a1_col = 256; }
     fp.NB1 = (512 - fp.a1_col) / kFHc;
@@ -273,6 +276,10 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
             }
         }
     }
+    // streamed weights (measured at C = 192: a 2-CTA cluster sharing the weight items by
+    // multicast, W2 chunks split in two ring items, or a deeper ring instead of a third X
+    // slot did not help; the weight stream runs at ~half the ~78 B/ns per-SM TMA rate
+    // tools/probes/tma_ring.cu measures)
     for (int nx : {3, 2}) {
         for (int st = kFMaxStages; st >= 3; --st) {
             const uint32_t need = fused_layout(C, H, 2, st, ebytes, nx).total + 1024;
@@ -346,9 +353,15 @@ struct swin_mlp_int8_s {
     std::vector<cudaEvent_t> prof_ev;
     unsigned long long* trace = nullptr;
     int trace_cta = 0;
+    // run_host pipeline: copy-in and copy-out streams + per-chunk events (created lazily)
+    cudaStream_t io_in = nullptr, io_out = nullptr;
+    std::vector<cudaEvent_t> io_ev;
     ~swin_mlp_int8_s() {
         for (void* p : allocs) cudaFree(p);
         for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
+        for (cudaEvent_t e : io_ev) cudaEventDestroy(e);
+        if (io_in) cudaStreamDestroy(io_in);
+        if (io_out) cudaStreamDestroy(io_out);
     }
 };
 
@@ -685,16 +698,50 @@ swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host
     if (workspace_bytes < need) return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", workspace_bytes, need);
     DeviceGuard guard(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const size_t tc = (size_t)T * h->d.C;
+    const int C = h->d.C;
+    const size_t tc = (size_t)T * C;
     uint8_t* w = static_cast<uint8_t*>(workspace);
     const size_t ws = swin_mlp_int8_workspace_bytes(h, T);
     int8_t* xd = reinterpret_cast<int8_t*>(w + ws);
     int8_t* yd = reinterpret_cast<int8_t*>(w + ws + align128(tc));
     float* rd = residual_host ? reinterpret_cast<float*>(w + ws + 2 * align128(tc)) : nullptr;
-    CUDA_TRY(cudaMemcpyAsync(xd, x_host, tc, cudaMemcpyHostToDevice, s));
-    if (rd) CUDA_TRY(cudaMemcpyAsync(rd, residual_host, tc * 4, cudaMemcpyHostToDevice, s));
-    ST_TRY(swin_mlp_int8_run(h, xd, rd, yd, nullptr, T, w, ws, stream));
-    CUDA_TRY(cudaMemcpyAsync(y_host, yd, tc, cudaMemcpyDeviceToHost, s));
+
+    // Pipeline over token chunks (rows are independent): copy-in of chunk k+1 and
+    // copy-out of chunk k-1 overlap the kernels of chunk k (PCIe is full duplex).
+    // Kernels run on the caller's stream; the copies on two handle-owned streams,
+    // ordered by events; the caller's stream finally waits for the last copy-out.
+    constexpr int kMaxChunks = 8;
+    int64_t rows = (T + kMaxChunks - 1) / kMaxChunks;
+    rows = std::max<int64_t>((rows + kBM - 1) / kBM * kBM, 4096);
+    const int nch = (int)((T + rows - 1) / rows);
+    if (!h->io_in) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->io_in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->io_out, cudaStreamNonBlocking));
+        for (int i = 0; i < 2 * kMaxChunks + 2; ++i) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            h->io_ev.push_back(e);
+        }
+    }
+    cudaEvent_t ev_start = h->io_ev[2 * kMaxChunks], ev_done = h->io_ev[2 * kMaxChunks + 1];
+    CUDA_TRY(cudaEventRecord(ev_start, s));
+    CUDA_TRY(cudaStreamWaitEvent(h->io_in, ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(h->io_out, ev_start, 0));
+    for (int k = 0; k < nch; ++k) {
+        const int64_t r0 = (int64_t)k * rows, n = std::min<int64_t>(rows, T - r0);
+        const size_t off = (size_t)r0 * C, bytes = (size_t)n * C;
+        cudaEvent_t ev_in = h->io_ev[2 * k], ev_out = h->io_ev[2 * k + 1];
+        CUDA_TRY(cudaMemcpyAsync(xd + off, x_host + off, bytes, cudaMemcpyHostToDevice, h->io_in));
+        if (rd) CUDA_TRY(cudaMemcpyAsync(rd + off, residual_host + off, bytes * 4, cudaMemcpyHostToDevice, h->io_in));
+        CUDA_TRY(cudaEventRecord(ev_in, h->io_in));
+        CUDA_TRY(cudaStreamWaitEvent(s, ev_in, 0));
+        ST_TRY(swin_mlp_int8_run(h, xd + off, rd ? rd + off : nullptr, yd + off, nullptr, n, w, ws, stream));
+        CUDA_TRY(cudaEventRecord(ev_out, s));
+        CUDA_TRY(cudaStreamWaitEvent(h->io_out, ev_out, 0));
+        CUDA_TRY(cudaMemcpyAsync(y_host + off, yd + off, bytes, cudaMemcpyDeviceToHost, h->io_out));
+    }
+    CUDA_TRY(cudaEventRecord(ev_done, h->io_out));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
     return SWIN_MLP_OK;
 }
 
