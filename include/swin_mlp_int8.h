@@ -139,6 +139,21 @@ swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host
                                          int8_t* y_host, int64_t T, void* workspace, size_t workspace_bytes,
                                          void* stream);
 
+/* End-to-end batch over several independent layers (e.g. the four stage MLPs of a
+ * network step, or several batches through one layer): host inputs x_hosts[l]
+ * ([Ts[l]][C_l] int8, pinned) -> host outputs y_hosts[l]; residual = dQ(x) (NULL
+ * residual) for every layer.  One copy-in / kernels / copy-out pipeline over the
+ * token chunks of all layers, so the transfers of one layer overlap the kernels and
+ * transfers of its neighbours.  All handles must live on one device; their copy
+ * streams and events are taken from hs[0] (one batch at a time per hs[0]).
+ * `workspace` (device) must hold swin_mlp_int8_host_batch_workspace_bytes(n, hs, Ts).
+ * Ordered after earlier work on `stream`; `stream` completes when every y_hosts[l]
+ * is written. */
+size_t swin_mlp_int8_host_batch_workspace_bytes(int32_t n, const swin_mlp_int8_t* hs, const int64_t* Ts);
+swin_mlp_status_t swin_mlp_int8_run_host_batch(int32_t n, const swin_mlp_int8_t* hs, const int8_t* const* x_hosts,
+                                               int8_t* const* y_hosts, const int64_t* Ts, void* workspace,
+                                               size_t workspace_bytes, void* stream);
+
 /* Debug getter: the folded fp32 constants exactly as the kernels use them
  * (host arrays m1[H], m2[C]; scalars inv_h, inv_y), and the int32
  * zero-point corrections wsum1[H], wsum2[C].  Any pointer may be NULL. */

@@ -31,6 +31,7 @@ EXPORTS = [
     "swin_mlp_int8_get_constants", "swin_mlp_int8_launches_per_run", "swin_mlp_int8_plan",
     "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end", "swin_mlp_int8_set_trace",
     "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
+    "swin_mlp_int8_host_batch_workspace_bytes", "swin_mlp_int8_run_host_batch",
 ]
 
 
@@ -91,6 +92,10 @@ def lib():
     L.swin_mlp_int8_set_trace.restype = i32
     L.swin_mlp_int8_destroy.argtypes = [P]
     L.swin_mlp_int8_destroy.restype = i32
+    L.swin_mlp_int8_host_batch_workspace_bytes.argtypes = [i32, P, P]
+    L.swin_mlp_int8_host_batch_workspace_bytes.restype = sz
+    L.swin_mlp_int8_run_host_batch.argtypes = [i32, P, P, P, P, P, sz, P]
+    L.swin_mlp_int8_run_host_batch.restype = i32
     L.swin_mlp_int8_last_error.argtypes = []
     L.swin_mlp_int8_last_error.restype = ctypes.c_char_p
     _lib = L
@@ -133,6 +138,28 @@ def swin_mlp_int8_host_workspace_bytes(h, T, with_residual) -> int:
 
 def swin_mlp_int8_run_host(h, x_host, residual_host, y_host, T, workspace, workspace_bytes, stream):
     _check(lib().swin_mlp_int8_run_host(h, x_host, residual_host, y_host, T, workspace, workspace_bytes, stream))
+
+
+def _arrays(handles, xs, ys, Ts):
+    n = len(handles)
+    hv = (ctypes.c_void_p * n)(*[h for h in handles])
+    xv = (ctypes.c_void_p * n)(*[0 if x is None else (x if isinstance(x, int) else x.data_ptr()) for x in xs]) \
+        if xs is not None else None
+    yv = (ctypes.c_void_p * n)(*[0 if y is None else (y if isinstance(y, int) else y.data_ptr()) for y in ys]) \
+        if ys is not None else None
+    tv = (ctypes.c_int64 * n)(*[int(t) for t in Ts])
+    return n, hv, xv, yv, tv
+
+
+def swin_mlp_int8_host_batch_workspace_bytes(handles, Ts) -> int:
+    n, hv, _, _, tv = _arrays(handles, None, None, Ts)
+    return int(lib().swin_mlp_int8_host_batch_workspace_bytes(n, hv, tv))
+
+
+def swin_mlp_int8_run_host_batch(handles, x_hosts, y_hosts, Ts, workspace, workspace_bytes, stream):
+    """x_hosts / y_hosts: pinned CPU tensors (or raw host pointers as ints)."""
+    n, hv, xv, yv, tv = _arrays(handles, x_hosts, y_hosts, Ts)
+    _check(lib().swin_mlp_int8_run_host_batch(n, hv, xv, yv, tv, workspace, workspace_bytes, stream))
 
 
 def swin_mlp_int8_destroy(h):

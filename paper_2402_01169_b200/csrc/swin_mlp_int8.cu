@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <string>
 #include <utility>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "../../include/swin_mlp_int8.h"
@@ -353,6 +355,18 @@ struct swin_mlp_int8_s {
     std::vector<cudaEvent_t> prof_ev;
     unsigned long long* trace = nullptr;
     int trace_cta = 0;
+    // activation tensor maps of recent runs (encoding costs microseconds of host time per
+    // map; a serving loop reuses the same buffers): key -> map, small linear cache
+    struct MapKey {
+        const void* ptr; int64_t rows, cols, ld; uint32_t box_rows, box_cols; int swz;
+        bool operator==(const MapKey& o) const {
+            return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows &&
+                   box_cols == o.box_cols && swz == o.swz;
+        }
+    };
+    std::vector<std::pair<MapKey, CUtensorMap>> map_cache;
+    size_t map_next = 0;
+    std::mutex map_mu;
     // run_host pipeline: copy-in and copy-out streams + per-chunk events (created lazily)
     cudaStream_t io_in = nullptr, io_out = nullptr;
     std::vector<cudaEvent_t> io_ev;
@@ -366,6 +380,25 @@ struct swin_mlp_int8_s {
 };
 
 namespace {
+
+// encode_2d through the handle's cache of activation maps
+swin_mlp_status_t encode_cached(swin_mlp_int8_s* h, CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
+                                int64_t ld, uint32_t box_rows, uint32_t box_cols = kBK,
+                                CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+    const swin_mlp_int8_s::MapKey key{ptr, rows, cols, ld, box_rows, box_cols, (int)swz};
+    {
+        std::lock_guard<std::mutex> lk(h->map_mu);
+        for (auto& e : h->map_cache)
+            if (e.first == key) { *map = e.second; return SWIN_MLP_OK; }
+    }
+    const swin_mlp_status_t st = encode_2d(map, ptr, rows, cols, ld, box_rows, box_cols, swz);
+    if (st != SWIN_MLP_OK) return st;
+    std::lock_guard<std::mutex> lk(h->map_mu);
+    constexpr size_t kCap = 64;
+    if (h->map_cache.size() < kCap) h->map_cache.emplace_back(key, *map);
+    else { h->map_cache[h->map_next] = {key, *map}; h->map_next = (h->map_next + 1) % kCap; }
+    return SWIN_MLP_OK;
+}
 
 struct DeviceGuard {
     int prev = -1;
@@ -577,8 +610,8 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
 
     if (h->fp.on) {
         CUtensorMap fx, fy;
-        ST_TRY(encode_2d(&fx, x, T, C, C, kBM));
-        ST_TRY(encode_2d(&fy, y, T, C, C, kBM));
+        ST_TRY(encode_cached(h, &fx, x, T, C, C, kBM));
+        ST_TRY(encode_cached(h, &fy, y, T, C, C, kBM));
         FusedArgs a = {};
         a.M = T; a.C = C; a.H = H;
         a.NJ = h->fp.NJ; a.KBC = h->fp.KBC; a.NB1 = h->fp.NB1; a.NH = h->fp.NH; a.stages = h->fp.stages;
@@ -619,17 +652,17 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     }
 
     CUtensorMap tm_x, tm_h, tm_ho, tm_y, tm_xr;
-    ST_TRY(encode_2d(&tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
-    ST_TRY(encode_2d(&tm_h, hq, T, H, H, (uint32_t)(kBM / h->p2.CS)));
+    ST_TRY(encode_cached(h, &tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
+    ST_TRY(encode_cached(h, &tm_h, hq, T, H, H, (uint32_t)(kBM / h->p2.CS)));
     // epilogue output maps: [128 rows][W B] boxes with the W-byte swizzle the staging uses
     auto swz = [](int w) {
         return w == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : w == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
              : w == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
     };
-    ST_TRY(encode_2d(&tm_ho, hq, T, H, H, kBM, (uint32_t)h->p1.out_w, swz(h->p1.out_w)));
-    ST_TRY(encode_2d(&tm_y, y, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
+    ST_TRY(encode_cached(h, &tm_ho, hq, T, H, H, kBM, (uint32_t)h->p1.out_w, swz(h->p1.out_w)));
+    ST_TRY(encode_cached(h, &tm_y, y, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
     // op #6 residual source x, staged by TMA with the output tile's box and swizzle
-    ST_TRY(encode_2d(&tm_xr, x, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
+    ST_TRY(encode_cached(h, &tm_xr, x, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
     const int64_t m_tiles = (T + kBM - 1) / kBM;
 
     GemmArgs a1 = {};
@@ -741,6 +774,85 @@ swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host
         CUDA_TRY(cudaMemcpyAsync(y_host + off, yd + off, bytes, cudaMemcpyDeviceToHost, h->io_out));
     }
     CUDA_TRY(cudaEventRecord(ev_done, h->io_out));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
+    return SWIN_MLP_OK;
+}
+
+size_t swin_mlp_int8_host_batch_workspace_bytes(int32_t n, const swin_mlp_int8_t* hs, const int64_t* Ts) {
+    if (n <= 0 || !hs || !Ts) return 0;
+    size_t ws = 0, stage = 0;
+    for (int32_t l = 0; l < n; ++l) {
+        if (!hs[l] || Ts[l] < 0) return 0;
+        ws = std::max(ws, swin_mlp_int8_workspace_bytes(hs[l], Ts[l]));
+        stage += 2 * align128((size_t)Ts[l] * hs[l]->d.C);
+    }
+    return align128(ws) + stage;
+}
+
+swin_mlp_status_t swin_mlp_int8_run_host_batch(int32_t n, const swin_mlp_int8_t* hs, const int8_t* const* x_hosts,
+                                               int8_t* const* y_hosts, const int64_t* Ts, void* workspace,
+                                               size_t workspace_bytes, void* stream) {
+    if (n <= 0 || !hs || !x_hosts || !y_hosts || !Ts || !workspace)
+        return fail(SWIN_MLP_EINVAL, "n > 0 and non-NULL arrays and workspace are required");
+    for (int32_t l = 0; l < n; ++l) {
+        if (!hs[l]) return fail(SWIN_MLP_EINVAL, "handle %d is NULL", l);
+        if (Ts[l] < 0) return fail(SWIN_MLP_EINVAL, "T[%d] < 0", l);
+        if (Ts[l] > 0 && (!x_hosts[l] || !y_hosts[l])) return fail(SWIN_MLP_EINVAL, "x/y of layer %d NULL", l);
+        if (hs[l]->device != hs[0]->device) return fail(SWIN_MLP_EINVAL, "all handles must live on one device");
+    }
+    const size_t need = swin_mlp_int8_host_batch_workspace_bytes(n, hs, Ts);
+    if (workspace_bytes < need) return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", workspace_bytes, need);
+    swin_mlp_int8_t h0 = hs[0];
+    DeviceGuard guard(h0->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint8_t* w = static_cast<uint8_t*>(workspace);
+    size_t ws = 0;
+    for (int32_t l = 0; l < n; ++l) ws = std::max(ws, swin_mlp_int8_workspace_bytes(hs[l], Ts[l]));
+    ws = align128(ws);
+
+    // one pipeline over the chunks of all layers (see run_host): copy-in on one stream,
+    // kernels on `stream`, copy-out on another, chunk by chunk in layer order
+    constexpr int64_t kRows = 16384;
+    std::vector<std::tuple<int32_t, int64_t, int64_t>> chunks;   // (layer, first row, rows)
+    for (int32_t l = 0; l < n; ++l)
+        for (int64_t r0 = 0; r0 < Ts[l]; r0 += kRows) chunks.emplace_back(l, r0, std::min<int64_t>(kRows, Ts[l] - r0));
+    if (!h0->io_in) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h0->io_in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&h0->io_out, cudaStreamNonBlocking));
+    }
+    while (h0->io_ev.size() < 2 * chunks.size() + 2) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h0->io_ev.push_back(e);
+    }
+    const size_t nev = h0->io_ev.size();
+    cudaEvent_t ev_start = h0->io_ev[nev - 2], ev_done = h0->io_ev[nev - 1];
+    CUDA_TRY(cudaEventRecord(ev_start, s));
+    CUDA_TRY(cudaStreamWaitEvent(h0->io_in, ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(h0->io_out, ev_start, 0));
+    std::vector<size_t> stage_off(n);
+    size_t off = ws;
+    for (int32_t l = 0; l < n; ++l) {
+        stage_off[l] = off;
+        off += 2 * align128((size_t)Ts[l] * hs[l]->d.C);
+    }
+    for (size_t k = 0; k < chunks.size(); ++k) {
+        const int32_t l = std::get<0>(chunks[k]);
+        const int64_t r0 = std::get<1>(chunks[k]), rows = std::get<2>(chunks[k]);
+        const int C = hs[l]->d.C;
+        const size_t tc = (size_t)Ts[l] * C, o = (size_t)r0 * C, bytes = (size_t)rows * C;
+        int8_t* xd = reinterpret_cast<int8_t*>(w + stage_off[l]);
+        int8_t* yd = reinterpret_cast<int8_t*>(w + stage_off[l] + align128(tc));
+        cudaEvent_t ev_in = h0->io_ev[2 * k], ev_out = h0->io_ev[2 * k + 1];
+        CUDA_TRY(cudaMemcpyAsync(xd + o, x_hosts[l] + o, bytes, cudaMemcpyHostToDevice, h0->io_in));
+        CUDA_TRY(cudaEventRecord(ev_in, h0->io_in));
+        CUDA_TRY(cudaStreamWaitEvent(s, ev_in, 0));
+        ST_TRY(swin_mlp_int8_run(hs[l], xd + o, nullptr, yd + o, nullptr, rows, w, ws, stream));
+        CUDA_TRY(cudaEventRecord(ev_out, s));
+        CUDA_TRY(cudaStreamWaitEvent(h0->io_out, ev_out, 0));
+        CUDA_TRY(cudaMemcpyAsync(y_hosts[l] + o, yd + o, bytes, cudaMemcpyDeviceToHost, h0->io_out));
+    }
+    CUDA_TRY(cudaEventRecord(ev_done, h0->io_out));
     CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
     return SWIN_MLP_OK;
 }

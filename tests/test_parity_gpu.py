@@ -182,6 +182,39 @@ def test_run_host_matches_device(dev):
     assert torch.equal(yh, yd)
 
 
+def test_run_host_pipelined_and_batch(dev):
+    """run_host over several token chunks (T > one chunk) and run_host_batch over layers of
+    different widths (one pipeline over all their chunks) give the device-path outputs."""
+    import paper_2402_01169_b200 as P
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    specs = [(_layer(96, 8100), 40000), (_layer(384, 8101), 5000), (_layer(768, 8102), 333)]
+    layers, xs, ys, refs = [], [], [], []
+    for L, T in specs:
+        layer = SwinMlpInt8Layer(L, device=0)
+        xh = torch.from_numpy(synth.make_activations(L, T, 4)).pin_memory()
+        refs.append(layer(xh.to(dev)).cpu())
+        layers.append(layer)
+        xs.append(xh)
+        ys.append(torch.zeros((T, L.C), dtype=torch.int8).pin_memory())
+    torch.cuda.synchronize()
+    # pipelined single-layer calls
+    for layer, xh, yh, ref in zip(layers, xs, ys, refs):
+        layer.run_host(xh, yh)
+        torch.cuda.synchronize()
+        assert torch.equal(yh, ref)
+        yh.zero_()
+    # one batch over all layers
+    Ts = [x.shape[0] for x in xs]
+    hs = [l.handle for l in layers]
+    n = P.swin_mlp_int8_host_batch_workspace_bytes(hs, Ts)
+    ws = torch.empty(n, dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    P.swin_mlp_int8_run_host_batch(hs, xs, ys, Ts, ws.data_ptr(), n, s)
+    torch.cuda.synchronize()
+    for yh, ref in zip(ys, refs):
+        assert torch.equal(yh, ref)
+
+
 def test_full_size_config2_sampled(dev):
     """BASELINE configs[1] (Swin-T, four stage MLPs, batch 64) at full size, in the
     bench's launch configuration: sampled rows (first/last tile, tile boundaries,
