@@ -178,7 +178,9 @@ swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, fl
  * trace[role*1024 + 2*i + {0,1}] for its i-th tile, roles 0 TMA producer
  * (first stage acquired, last k-block issued), 1 MMA (accumulator acquired,
  * tile committed), 2 epilogue (accumulator ready, tile stored), 3 constant
- * loader (buffer acquired, constants published)).  trace = NULL disables. */
+ * loader (buffer acquired, constants published)).  The trace buffer must then hold 9216
+ * uint64: every CTA also stamps its entry / exit at [8192 + 2*cta + {0,1}] (FC1 or
+ * the one-kernel plan) and [8704 + 2*cta + {0,1}] (FC2).  trace = NULL disables. */
 swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_t cta);
 
 /* Introspection: the launch plan of this layer, out10[16] = {FC1 BN, FC1 cluster size,

@@ -236,7 +236,7 @@ class SwinMlpInt8Layer:
                 "fc1_groups": out[8], "fc2_groups": out[9], "fc1_resb": out[10], "fc2_resb": out[11]}
 
     def set_trace(self, buf=None, cta=0):
-        """buf: int64 device tensor of >= 8192 elements (see swin_mlp_int8_set_trace), or None."""
+        """buf: int64 device tensor of >= 9216 elements (see swin_mlp_int8_set_trace), or None."""
         _check(lib().swin_mlp_int8_set_trace(self.handle, _ptr(buf), int(cta)))
 
     def profile_begin(self, max_runs):

@@ -70,6 +70,7 @@ struct FusedArgs {
     // done), [6656+u] / [7168+u] FC2(u) before / after its waits
     unsigned long long* trace;
     int32_t trace_cta;
+    unsigned long long* cta_stamps;   // debug: per CTA %globaltimer at entry / exit ([2 * blockIdx.x + {0,1}])
 };
 
 struct FusedLayout {
@@ -120,6 +121,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
+    if (p.cta_stamps && threadIdx.x == 0) p.cta_stamps[2 * blockIdx.x] = gtimer();
 
     const int C = p.C, H = p.H;
     const uint32_t NJ = (uint32_t)p.NJ, KBC = (uint32_t)p.KBC, NB1 = (uint32_t)p.NB1, NH = (uint32_t)p.NH;
@@ -784,6 +786,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
     }
+    if (p.cta_stamps && threadIdx.x == 0) p.cta_stamps[2 * blockIdx.x + 1] = gtimer();
 }
 
 }  // namespace swinmlp

@@ -101,6 +101,7 @@ struct GemmArgs {
     // stamps (see swin_mlp_int8_set_trace in the header for the layout)
     unsigned long long* trace;
     int32_t trace_cta;
+    unsigned long long* cta_stamps;   // debug: per CTA %globaltimer at entry / exit ([2 * blockIdx.x + {0,1}])
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -204,6 +205,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
+    if (p.cta_stamps && threadIdx.x == 0) p.cta_stamps[2 * blockIdx.x] = gtimer();
 
     const int BN = p.BN;
     const uint32_t CS = (uint32_t)p.CS;
@@ -881,6 +883,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         tc_fence_after();
         tmem_dealloc(tmem_base, tmem_cols);
     }
+    if (p.cta_stamps && threadIdx.x == 0) p.cta_stamps[2 * blockIdx.x + 1] = gtimer();
 }
 
 }  // namespace swinmlp

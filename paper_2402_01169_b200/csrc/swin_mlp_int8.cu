@@ -624,6 +624,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         a.x = x; a.resid = residual; a.resid_out = residual_out;
         if (dbg) { a.acc1_tap = acc1; a.hid_tap = hidden; a.acc2_tap = acc2; a.ln_tap = ln_out; }
         a.trace = h->trace; a.trace_cta = h->trace_cta;
+        a.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
         const int64_t m_tiles = (T + kBM - 1) / kBM;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)std::min<int64_t>(m_tiles, h->num_sms));
@@ -673,6 +674,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
     a1.acc_tap = dbg ? acc1 : nullptr;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
+    a1.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
 
     GemmArgs a2 = {};
     a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.xstage = h->p2.xstage; a2.x = x;
@@ -685,6 +687,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
     a2.acc_tap = dbg ? acc2 : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
     a2.trace = h->trace ? h->trace + 4096 : nullptr; a2.trace_cta = h->trace_cta;
+    a2.cta_stamps = h->trace ? h->trace + 8192 + 512 : nullptr;
 
     cudaEvent_t* ev = nullptr;
     if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];

@@ -19,7 +19,7 @@ x = torch.from_numpy(synth.make_activations(L, T, 12)).cuda()
 y = torch.empty((T, C), dtype=torch.int8, device="cuda")
 for _ in range(3):
     layer(x, y=y)
-buf = torch.zeros(8192, dtype=torch.int64, device="cuda")
+buf = torch.zeros(9216, dtype=torch.int64, device="cuda")
 layer.set_trace(buf, cta)
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
@@ -48,3 +48,9 @@ for i in range(min(ntile, 12)):
               f"  FC2 [{f(fc2a[u]):7d},{f(fc2b[u]):7d},{f(fc2[u]):7d}]")
 last = max(f(v) for v in nz)
 print("last stamp", last)
+cs = t[8192:8192 + 296].reshape(148, 2)
+ok = cs[:, 0] > 0
+base = cs[ok, 0].min()
+st, en = cs[ok, 0] - base, cs[ok, 1] - base
+print(f"CTAs {ok.sum()}: entry min {st.min()} max {st.max()} | exit min {en.min()} median {int(np.median(en))} "
+      f"max {en.max()} | duration median {int(np.median(en - st))} max {(en - st).max()}")

@@ -17,7 +17,7 @@ x = torch.from_numpy(synth.make_activations(L, T, xs)).cuda()
 y = torch.empty((T, L.C), dtype=torch.int8, device="cuda")
 for _ in range(3):
     layer(x, y=y)
-buf = torch.zeros(8192, dtype=torch.int64, device="cuda")
+buf = torch.zeros(9216, dtype=torch.int64, device="cuda")
 layer.set_trace(buf, cta)
 layer(x, y=y)
 torch.cuda.synchronize()
@@ -44,3 +44,14 @@ for k, name in ((0, "FC1"), (1, "FC2")):
         ep = " ".join(f"{f(epi[i, j]) if i < 64 else -1:9d}" for j in range(len(EPI)))
         print(f"{i:3d} {f(prod[i,0]):7d},{f(prod[i,1]):7d} {f(mma4[i,0]):7d},{f(mma4[i,1]):7d},{f(mma4[i,2]):7d},{f(mma4[i,3]):7d} "
               f"{f(cst[i,0]):7d},{f(cst[i,1]):7d}  {ep}")
+# per-CTA entry / exit (ns, relative to the earliest FC1 entry)
+for name, off in (("FC1", 8192), ("FC2", 8704)):
+    cs = t[off:off + 2 * 148].reshape(148, 2)
+    ok = cs[:, 0] > 0
+    if not ok.any():
+        continue
+    t0c = t[8192:8192 + 296].reshape(148, 2)[:, 0]
+    base = t0c[t0c > 0].min()
+    st, en = cs[ok, 0] - base, cs[ok, 1] - base
+    print(f"{name} CTAs {ok.sum()}: entry min {st.min()} max {st.max()} | exit min {en.min()} "
+          f"median {int(np.median(en))} max {en.max()} | duration median {int(np.median(en - st))} max {(en - st).max()}")
