@@ -398,6 +398,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         const uint32_t rit = quad * 32u + lane;
         const uint32_t row_off = rit * (uint32_t)kBK, rsw = rit & 7u;
         const float2 inv2 = make_float2(p.inv_h, p.inv_h);
+        const bool zx_zero = SMALLK && p.z_x == 0;
         pdl_wait();   // (taps)
         mbar_wait(bar_cfull, 0);
         uint32_t i = 0, j = 0, b = 0, bph = 0, hb = 0, hph = 0;
@@ -420,7 +421,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     const float4 mv = *reinterpret_cast<const float4*>(cm1 + n0 + 4 * j4);
                     const float4 bv = B1 ? *reinterpret_cast<const float4*>(cb1 + n0 + 4 * j4)
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-                    const uint4 gv = *reinterpret_cast<const uint4*>(cmg1 + n0 + 4 * j4);
+                    // (z_x == 0: the magic constant is the same for every column, no load)
+                    const uint4 gv = zx_zero ? make_uint4(0x4B400000u, 0x4B400000u, 0x4B400000u, 0x4B400000u)
+                                             : *reinterpret_cast<const uint4*>(cmg1 + n0 + 4 * j4);
                     float2 a0, a1;
                     if constexpr (SMALLK) {
                         // bits (0x4B400000 - zc) + acc = float 1.5*2^23 + (acc - zc), exact

@@ -84,9 +84,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         if (it > 64 && ((it & 1023) == 0) && clock64() - t0 > (1ll << 34)) __trap();
     }
 }
-// Same, backing off with nanosleep after a few failed probes: for warps whose spinning
-// would steal issue slots from the warps they share a sub-partition with (epilogue and
-// store warps waiting for work); costs at most ~the sleep time in wake-up latency.
+// Same, backing off with nanosleep (32 ns doubling to 256 ns) after a failed probe: for
+// warps whose spinning would steal issue slots from the warps they share a sub-partition
+// with (epilogue and store warps waiting for work); costs at most ~the sleep time in
+// wake-up latency.
 __device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
     uint32_t done;
     long long t0 = 0;
@@ -97,9 +98,9 @@ __device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity)
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done) : "r"(bar), "r"(parity) : "memory");
         if (done) return;
-        if (it >= 2) __nanosleep(40);
+        if (it >= 1) __nanosleep(it < 4 ? 32u : it < 8 ? 64u : it < 16 ? 128u : 256u);   // exponential backoff
         if (it == 64) t0 = clock64();
-        if (it > 64 && ((it & 255) == 0) && clock64() - t0 > (1ll << 34)) __trap();
+        if (it > 64 && ((it & 63) == 0) && clock64() - t0 > (1ll << 34)) __trap();
     }
 }
 // Same, with cluster-scope acquire (for data written by peer CTAs via st.async).
