@@ -21,10 +21,9 @@
 // CTA = 640 threads, one per SM, persistent over m-tiles cid, cid + grid, ...:
 //   warp 0       TMA producer: X tiles (2 slots) and, unless resident, the W1 / W2
 //                chunks through a `stages`-deep ring in the MMA's consumption order
-//   warp 1       MMA issuer: FC1 of chunk u + L is issued before FC2 of chunk u
-//                (L = NB1 - 1), so op #5 always has accumulators queued
+//   warp 1       FC1 MMA issuer
+//   warp 3       loads the per-channel constants once, then issues the FC2 MMAs
 //   warp 2       TMEM allocator, then the Y store warp
-//   warp 3       loads the per-channel constants once
 //   warps 4-11   op #5: warp = (lane quadrant, 64-column half) of each acc1 chunk
 //   warps 12-19  op #6: warp = (lane quadrant, column half); a thread owns half a
 //                token row, the two halves combine their statistics pairwise
@@ -49,10 +48,13 @@ struct FusedArgs {
     int32_t KBC;        // ceil(C / 128): K-blocks of the X tile and of a W1 chunk
     int32_t NB1;        // acc1 TMEM buffers (128 columns each)
     int32_t NH;         // Hq smem buffers
-    int32_t stages;     // weight ring depth; 0 = W1 and W2 resident in smem
+    int32_t stages;     // W1 ring depth (16 KB K-block items); 0 = W1 and W2 resident in smem
+    int32_t stages2;    // W2 ring depth ([C rows][128 B] chunk items), streamed mode
     int32_t a1_col;     // TMEM column of acc1 buffer 0 (acc2 buffers live below it)
     int32_t NA2;        // acc2 TMEM buffers (2: op #6 of tile i overlaps FC2 of tile i + 1)
     int32_t NX;         // X tile slots (2..4)
+    int32_t y_inplace;  // 1: Y is staged over its tile's X slot (no separate Y buffer; the
+                        //    slot is released by the Y store) -- frees smem for the weight ring
     int32_t a2_stride;  // TMEM columns between acc2 buffers
     const float* m1; const float* b1; const int32_t* zc1;   // [H]
     const float* m2; const float* b2; const int32_t* zc2;   // [C]
@@ -77,27 +79,23 @@ struct FusedLayout {
     uint32_t x, y, hq, w, w2, consts, red, bars, tmem_slot, total;
 };
 constexpr int kFMaxNX = 4;
-constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1;
+constexpr int kFMaxStages2 = 4;
+constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 2 * kFMaxStages2 + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1;
 
-// ring item: one W1 K-block box [128 rows][128 B] or one W2 chunk [C rows][128 B]
-__host__ __device__ inline uint32_t fused_stage_bytes(int C) {
-    const uint32_t w2c = (uint32_t)C * kBK;
-    return kKB > w2c ? kKB : w2c;
-}
-
-__host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int stages, int ebytes, int NX) {
+__host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int stages, int ebytes, int NX,
+                                                    int y_inplace = 0, int stages2 = 0) {
     FusedLayout L;
     const uint32_t kbc = (uint32_t)((C + kBK - 1) / kBK), nj = (uint32_t)(H / kFHc);
     L.x = 0;                                             // [NX][KBC][128 rows][128 B] X tiles
     L.y = L.x + (uint32_t)NX * kbc * kKB;                // [KBC][128 rows][128 B] Y staging
-    L.hq = L.y + kbc * kKB;                              // [NH][128 rows][128 B]
+    L.hq = L.y + (y_inplace ? 0u : kbc * kKB);           // [NH][128 rows][128 B]
     L.w = L.hq + (uint32_t)NH * kKB;                     // resident: W1 chunks then W2 chunks; else ring
     if (stages == 0) {
         L.w2 = L.w + nj * kbc * kKB;
         L.consts = L.w2 + nj * (uint32_t)C * kBK;
-    } else {
-        L.w2 = 0;
-        L.consts = L.w + (uint32_t)stages * fused_stage_bytes(C);
+    } else {   // two rings: W1 K-blocks, W2 chunks (each consumed in its own order)
+        L.w2 = L.w + (uint32_t)stages * kKB;
+        L.consts = L.w2 + (uint32_t)stages2 * (uint32_t)C * kBK;
     }
     L.red = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
     L.red = (L.red + 15u) & ~15u;
@@ -127,10 +125,11 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t NJ = (uint32_t)p.NJ, KBC = (uint32_t)p.KBC, NB1 = (uint32_t)p.NB1, NH = (uint32_t)p.NH;
     const uint32_t stages = (uint32_t)p.stages;
     const bool resident = stages == 0;
-    const FusedLayout L = fused_layout(C, H, p.NH, p.stages, (int)sizeof(acc_t), p.NX);
+    const FusedLayout L = fused_layout(C, H, p.NH, p.stages, (int)sizeof(acc_t), p.NX, p.y_inplace, p.stages2);
+    const uint32_t stages2 = (uint32_t)p.stages2;
+    const bool yin = p.y_inplace != 0;
     const uint32_t NX = (uint32_t)p.NX;
     const uint32_t sX = base + L.x, sY = base + L.y, sHq = base + L.hq, sW = base + L.w, sW2 = base + L.w2;
-    const uint32_t stage_bytes = fused_stage_bytes(C);
     const uint32_t xslot = KBC * kKB;
     float* cm1 = reinterpret_cast<float*>(gbase + L.consts);
     float* cb1 = cm1 + H;
@@ -146,7 +145,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t bar_xempty = bar_xfull + 8u * kFMaxNX;     // [NX]  X tile consumed (op #6 pass 1, 8 warps)
     const uint32_t bar_wfull = bar_xempty + 8u * kFMaxNX;     // [S]   weight chunk landed (1 + tx)
     const uint32_t bar_wempty = bar_wfull + 8u * kFMaxStages; // [S]   weight chunk consumed (commit)
-    const uint32_t bar_wres = bar_wempty + 8u * kFMaxStages;  //       resident weights landed
+    const uint32_t bar_w2full = bar_wempty + 8u * kFMaxStages;   // [S2] W2 chunk landed (1 + tx)
+    const uint32_t bar_w2empty = bar_w2full + 8u * kFMaxStages2; // [S2] W2 chunk consumed (commit)
+    const uint32_t bar_wres = bar_w2empty + 8u * kFMaxStages2;   //       resident weights landed
     const uint32_t bar_a1full = bar_wres + 8u;                // [NB1] acc1 ready (commit)
     const uint32_t bar_a1empty = bar_a1full + 8u * kFMaxNB1;  // [NB1] acc1 drained (8 warps)
     const uint32_t bar_hqfull = bar_a1empty + 8u * kFMaxNB1;  // [NH]  Hq chunk written (8 warps)
@@ -169,13 +170,17 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < kFMaxNX; ++i) {
             mbar_init(bar_xfull + 8u * i, 1);
-            mbar_init(bar_xempty + 8u * i, 8);
+            mbar_init(bar_xempty + 8u * i, p.y_inplace ? 1u : 8u);   // Y store, or op #6 pass 1
         }
         mbar_init(bar_yfull, 8);
         mbar_init(bar_yempty, 1);
         for (int s = 0; s < kFMaxStages; ++s) {
             mbar_init(bar_wfull + 8u * s, 1);
             mbar_init(bar_wempty + 8u * s, 1);
+            if (s < kFMaxStages2) {
+                mbar_init(bar_w2full + 8u * s, 1);
+                mbar_init(bar_w2empty + 8u * s, 1);
+            }
         }
         mbar_init(bar_wres, 1);
         for (int b = 0; b < kFMaxNB1; ++b) {
@@ -211,7 +216,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
 
     if (warp == 0) {
         // ============================ TMA producer ============================
-        uint32_t s = 0, ph = 0;
+        uint32_t s = 0, ph = 0, s2 = 0, ph2 = 0;
         auto load_w1 = [&](uint32_t j, uint32_t dst, uint32_t bar) {
             for (uint32_t kb = 0; kb < KBC; ++kb)
                 tma_load_2d(&tmW1, dst + kb * kKB, bar, (int)(kb * kBK), (int)(j * kFHc));
@@ -247,7 +252,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                         mbar_wait(bar_wempty + 8u * s, ph ^ 1u);
                         if (elect_one()) {
                             mbar_arrive_expect_tx(bar_wfull + 8u * s, kKB);
-                            tma_load_2d(&tmW1, sW + s * stage_bytes, bar_wfull + 8u * s, (int)(kb * kBK), (int)(j * kFHc));
+                            tma_load_2d(&tmW1, sW + s * kKB, bar_wfull + 8u * s, (int)(kb * kBK), (int)(j * kFHc));
                         }
                         __syncwarp();
                         if (++s == stages) { s = 0; ph ^= 1u; }
@@ -261,115 +266,88 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             }
             if (q >= LA) {                     // operands of FC2(q - LA)
                 if (!resident) {
-                    mbar_wait(bar_wempty + 8u * s, ph ^ 1u);
+                    mbar_wait(bar_w2empty + 8u * s2, ph2 ^ 1u);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(bar_wfull + 8u * s, (uint32_t)C * kBK);
-                        tma_load_2d(&tmW2, sW + s * stage_bytes, bar_wfull + 8u * s, (int)(j2 * kFHc), 0);
+                        mbar_arrive_expect_tx(bar_w2full + 8u * s2, (uint32_t)C * kBK);
+                        tma_load_2d(&tmW2, sW2 + s2 * (uint32_t)C * kBK, bar_w2full + 8u * s2, (int)(j2 * kFHc), 0);
                     }
                     __syncwarp();
-                    if (++s == stages) { s = 0; ph ^= 1u; }
+                    if (++s2 == stages2) { s2 = 0; ph2 ^= 1u; }
                 }
                 if (++j2 == NJ) j2 = 0;
             }
         }
     } else if (warp == 1) {
-        // ============================ MMA issuer ==============================
-        // Lean on purpose: this warp shares its SM sub-partition with four epilogue
-        // warps, so every instruction per op costs ~5 issue slots.  Descriptors are
-        // base + offset (the 14-bit start-address field never carries: smem < 256 KB).
-        const uint32_t idesc1 = idesc_i8(kBM, kFHc), idesc2 = idesc_i8(kBM, (uint32_t)C);
-        const uint64_t dX = umma_desc_k128(sX), dW = umma_desc_k128(sW), dW2 = umma_desc_k128(sW2),
-                       dHq = umma_desc_k128(sHq);
-        const uint32_t xslot16 = xslot >> 4, stage16 = stage_bytes >> 4, w2c16 = ((uint32_t)C * kBK) >> 4;
+        // ============================ FC1 issuer ==============================
+        // FC1 and FC2 are issued by two warps (this one and warp 3 after the constants):
+        // a tcgen05.mma issue can stall while earlier MMAs execute, and in one in-order
+        // warp FC1 of the next chunk would queue behind FC2's wait for op #5.  Each
+        // warp's tcgen05.commit tracks its own MMAs.  Descriptors are base + offset (the
+        // 14-bit start-address field never carries: smem < 256 KB).
+        const uint32_t idesc1 = idesc_i8(kBM, kFHc);
+        const uint64_t dX = umma_desc_k128(sX), dW = umma_desc_k128(sW);
+        const uint32_t xslot16 = xslot >> 4, stage16 = kKB >> 4;
         const uint32_t kb16 = kKB >> 4;
         const int nk_last = (C - (int)((KBC - 1u) * kBK)) / 32;   // MMAs (K = 32) in the last K-block
         const uint32_t a1_tm = tmem_base + (uint32_t)p.a1_col;
         uint32_t s = 0, ph = 0;
         if (resident) mbar_wait(bar_wres, 0);
-        uint32_t i = 0, j = 0, b = 0, bph = 0;           // FC1 cursor: tile, chunk, acc1 buffer, its phase
-        uint32_t xs = 0, xph = 0;                        // FC1 cursor: X slot, its phase
-        uint32_t i2 = 0, j2 = 0, hb = 0, hph = 0;        // FC2 cursor: tile, chunk, Hq buffer, its phase
-        uint32_t ab = 0, aph = 0;                        // FC2 cursor: acc2 buffer, its phase
-        for (uint32_t q = 0; q < U + LA; ++q) {
-            if (q < U) {                       // FC1(q): acc1[b] = X_i . W1[j]^T
-                if (trc && lane == 0 && q < 512) trc[1024 + q] = gtimer();
-                if (j == 0) mbar_wait(bar_xfull + 8u * xs, xph);
-                mbar_wait(bar_a1empty + 8u * b, bph ^ 1u);
-                if (trc && lane == 0 && q < 512) trc[1536 + q] = gtimer();
-                const uint32_t d = a1_tm + b * (uint32_t)kFHc;
-                const uint64_t ad0 = dX + xs * xslot16;
-                for (uint32_t kb = 0; kb < KBC; ++kb) {
-                    if (!resident) mbar_wait(bar_wfull + 8u * s, ph);
-                    tc_fence_after();
-                    const uint64_t ad = ad0 + kb * kb16;
-                    const uint64_t bd = resident ? dW + (j * KBC + kb) * kb16 : dW + s * stage16;
-                    const int nk = kb + 1u == KBC ? nk_last : 4;
-                    if (elect_one()) {
-                        mma_i8(d, ad, bd, idesc1, kb);
-                        if (nk > 1) mma_i8(d, ad + 2u, bd + 2u, idesc1, 1u);
-                        if (nk > 2) mma_i8(d, ad + 4u, bd + 4u, idesc1, 1u);
-                        if (nk > 3) mma_i8(d, ad + 6u, bd + 6u, idesc1, 1u);
-                        if (!resident) mma_commit(bar_wempty + 8u * s);
-                    }
-                    __syncwarp();
-                    if (!resident && ++s == stages) { s = 0; ph ^= 1u; }
-                }
-                if (elect_one()) {
-                    mma_commit(bar_a1full + 8u * b);
-                    if (trc && q < 512) trc[q] = gtimer();
-                }
-                __syncwarp();
-                if (++j == NJ) {
-                    j = 0;
-                    ++i;
-                    if (++xs == NX) { xs = 0; xph ^= 1u; }
-                }
-                if (++b == NB1) { b = 0; bph ^= 1u; }
-            }
-            if (q >= LA) {                     // FC2(u = q - LA): acc2 += Hq_u . W2[:, j2]^T
-                if (trc && lane == 0 && q - LA < 512) trc[6656 + q - LA] = gtimer();
-                mbar_wait(bar_hqfull + 8u * hb, hph);
-                if (j2 == 0) mbar_wait(bar_a2empty + 8u * ab, aph ^ 1u);
+        uint32_t i = 0, j = 0, b = 0, bph = 0;           // tile, chunk, acc1 buffer, its phase
+        uint32_t xs = 0, xph = 0;                        // X slot, its phase
+        for (uint32_t q = 0; q < U; ++q) {               // FC1(q): acc1[b] = X_i . W1[j]^T
+            if (trc && lane == 0 && q < 512) trc[1024 + q] = gtimer();
+            if (j == 0) mbar_wait(bar_xfull + 8u * xs, xph);
+            mbar_wait(bar_a1empty + 8u * b, bph ^ 1u);
+            if (trc && lane == 0 && q < 512) trc[1536 + q] = gtimer();
+            const uint32_t d = a1_tm + b * (uint32_t)kFHc;
+            const uint64_t ad0 = dX + xs * xslot16;
+            for (uint32_t kb = 0; kb < KBC; ++kb) {
                 if (!resident) mbar_wait(bar_wfull + 8u * s, ph);
-                if (trc && lane == 0 && q - LA < 512) trc[7168 + q - LA] = gtimer();
+                if (trc && lane == 0 && q < 512 && kb + 1 == KBC) trc[7680 + q] = gtimer();   // weights in
                 tc_fence_after();
-                const uint64_t ad = dHq + hb * kb16;
-                const uint64_t bd = resident ? dW2 + j2 * w2c16 : dW + s * stage16;
-                const uint32_t d2 = tmem_base + ab * (uint32_t)p.a2_stride;
+                const uint64_t ad = ad0 + kb * kb16;
+                const uint64_t bd = resident ? dW + (j * KBC + kb) * kb16 : dW + s * stage16;
+                const int nk = kb + 1u == KBC ? nk_last : 4;
                 if (elect_one()) {
-                    mma_i8(d2, ad, bd, idesc2, j2);
-                    mma_i8(d2, ad + 2u, bd + 2u, idesc2, 1u);
-                    mma_i8(d2, ad + 4u, bd + 4u, idesc2, 1u);
-                    mma_i8(d2, ad + 6u, bd + 6u, idesc2, 1u);
+                    mma_i8(d, ad, bd, idesc1, kb);
+                    if (nk > 1) mma_i8(d, ad + 2u, bd + 2u, idesc1, 1u);
+                    if (nk > 2) mma_i8(d, ad + 4u, bd + 4u, idesc1, 1u);
+                    if (nk > 3) mma_i8(d, ad + 6u, bd + 6u, idesc1, 1u);
                     if (!resident) mma_commit(bar_wempty + 8u * s);
-                    mma_commit(bar_hqempty + 8u * hb);
-                    if (j2 + 1u == NJ) mma_commit(bar_a2full + 8u * ab);
-                    if (trc && q - LA < 512) trc[512 + q - LA] = gtimer();
                 }
                 __syncwarp();
                 if (!resident && ++s == stages) { s = 0; ph ^= 1u; }
-                if (++j2 == NJ) {
-                    j2 = 0;
-                    ++i2;
-                    if (++ab == (uint32_t)p.NA2) { ab = 0; aph ^= 1u; }
-                }
-                if (++hb == NH) { hb = 0; hph ^= 1u; }
             }
+            if (elect_one()) {
+                mma_commit(bar_a1full + 8u * b);
+                if (trc && q < 512) trc[q] = gtimer();
+            }
+            __syncwarp();
+            if (++j == NJ) {
+                j = 0;
+                ++i;
+                if (++xs == NX) { xs = 0; xph ^= 1u; }
+            }
+            if (++b == NB1) { b = 0; bph ^= 1u; }
         }
     } else if (warp == 2) {
         // ============================ Y store warp ============================
         pdl_wait();   // Y may overwrite what the previous kernel still reads
+        uint32_t xs = 0;
         for (uint32_t i = 0; i < n_my; ++i) {
             mbar_wait_backoff(bar_yfull, i & 1u);
             if (lane == 0) {
+                const uint32_t src = yin ? sX + xs * xslot : sY;
                 for (uint32_t kb = 0; kb < KBC; ++kb)
-                    tma_store_2d(&tmY, sY + kb * kKB, (int)(kb * kBK), row0_of(i));
+                    tma_store_2d(&tmY, src + kb * kKB, (int)(kb * kBK), row0_of(i));
                 bulk_commit();
                 bulk_wait_read<0>();           // Y read out of the staging buffer
-                mbar_arrive(bar_yempty);
+                if (yin) mbar_arrive(bar_xempty + 8u * xs);   // the X slot (Y staged over it) is free
+                else mbar_arrive(bar_yempty);
                 if (trc && i < 512) trc[6144 + i] = gtimer();
             }
             __syncwarp();
+            if (++xs == NX) xs = 0;
         }
         if (lane == 0) bulk_wait_all();
         __syncwarp();
@@ -389,6 +367,42 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             cbt[c] = __ldg(p.beta + c);
         }
         mbar_arrive(bar_cfull);
+
+        // ============================ FC2 issuer ==============================
+        const uint32_t idesc2 = idesc_i8(kBM, (uint32_t)C);
+        const uint64_t dW2 = umma_desc_k128(sW2), dHq = umma_desc_k128(sHq);
+        const uint32_t w2c16 = ((uint32_t)C * kBK) >> 4, kb16 = kKB >> 4;
+        uint32_t s2 = 0, ph2 = 0;
+        if (resident) mbar_wait(bar_wres, 0);
+        uint32_t j2 = 0, hb = 0, hph = 0, ab = 0, aph = 0;   // chunk, Hq buffer, acc2 buffer (+ phases)
+        for (uint32_t u = 0; u < U; ++u) {                    // FC2(u): acc2 += Hq_u . W2[:, j2]^T
+            if (trc && lane == 0 && u < 512) trc[6656 + u] = gtimer();
+            mbar_wait(bar_hqfull + 8u * hb, hph);
+            if (j2 == 0) mbar_wait(bar_a2empty + 8u * ab, aph ^ 1u);
+            if (!resident) mbar_wait(bar_w2full + 8u * s2, ph2);
+            if (trc && lane == 0 && u < 512) trc[7168 + u] = gtimer();
+            tc_fence_after();
+            const uint64_t ad = dHq + hb * kb16;
+            const uint64_t bd = dW2 + (resident ? j2 : s2) * w2c16;
+            const uint32_t d2 = tmem_base + ab * (uint32_t)p.a2_stride;
+            if (elect_one()) {
+                mma_i8(d2, ad, bd, idesc2, j2);
+                mma_i8(d2, ad + 2u, bd + 2u, idesc2, 1u);
+                mma_i8(d2, ad + 4u, bd + 4u, idesc2, 1u);
+                mma_i8(d2, ad + 6u, bd + 6u, idesc2, 1u);
+                if (!resident) mma_commit(bar_w2empty + 8u * s2);
+                mma_commit(bar_hqempty + 8u * hb);
+                if (j2 + 1u == NJ) mma_commit(bar_a2full + 8u * ab);
+                if (trc && u < 512) trc[512 + u] = gtimer();
+            }
+            __syncwarp();
+            if (!resident && ++s2 == stages2) { s2 = 0; ph2 ^= 1u; }
+            if (++j2 == NJ) {
+                j2 = 0;
+                if (++ab == (uint32_t)p.NA2) { ab = 0; aph ^= 1u; }
+            }
+            if (++hb == NH) { hb = 0; hph ^= 1u; }
+        }
     } else if (warp < (uint32_t)kFEp6W0) {
         // ============================ op #5 ===================================
         // acc1 chunk (128 hidden columns) -> Hq chunk in smem, 128-B swizzled K-major
@@ -696,7 +710,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             else pass1(std::false_type{});
             tmem_wait_st();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_xempty + 8u * xs);   // X tile consumed
+            if (lane == 0 && !yin) mbar_arrive(bar_xempty + 8u * xs);   // X tile consumed
             if (stamp) trc[4096 + 4 * i + 2] = gtimer();
 
             float mu_f = 0.f, rstd_f = 0.f;
@@ -735,7 +749,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
 
             // pass 2: yhat = fl(((z - mu) * rstd) * gamma + beta); Y = Q_y(yhat) into the staging
             // buffer once the previous tile's stores have read it
-            mbar_wait_backoff(bar_yempty, (i & 1u) ^ 1u);
+            if (!yin) mbar_wait_backoff(bar_yempty, (i & 1u) ^ 1u);
+            const uint32_t sYt = yin ? xt : sY;   // Y staging: own X slot, or the Y buffer
             for_chunks([&](uint32_t (&r)[16], int ch) {
                 const int c0 = cb + ch * 16;
                 float v[16];
@@ -768,7 +783,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 uint32_t w[4];
                 if (p.z_y) quant_pack16<false, true>(v, p.z_y, w);
                 else quant_pack16<false, false>(v, 0, w);
-                st_shared_v4(sY + goff(c0), w[0], w[1], w[2], w[3]);
+                st_shared_v4(sYt + goff(c0), w[0], w[1], w[2], w[3]);
             });
             tc_fence_before();
             fence_proxy_async_smem();          // Y visible to the TMA store

@@ -77,7 +77,8 @@ struct Plan {
 struct FusedPlan {
     bool on = false;
     FusedFn fn = nullptr;
-    int NJ = 0, KBC = 0, NB1 = 0, NH = 0, stages = 0, a1_col = 0, NA2 = 1, a2_stride = 0, NX = 2;
+    int NJ = 0, KBC = 0, NB1 = 0, NH = 0, stages = 0, a1_col = 0, NA2 = 1, a2_stride = 0, NX = 2, y_inplace = 0,
+        stages2 = 0;
     uint32_t smem = 0;
 };
 
@@ -278,24 +279,20 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
             }
         }
     }
-    // streamed weights (measured at C = 192: a 2-CTA cluster sharing the weight items by
-    // multicast, W2 chunks split in two ring items, or a deeper ring instead of a third X
-    // slot did not help; the weight stream runs at ~half the ~78 B/ns per-SM TMA rate
-    // tools/probes/tma_ring.cu measures)
-    for (int nx : {3, 2}) {
-        for (int st = kFMaxStages; st >= 3; --st) {
-            const uint32_t need = fused_layout(C, H, 2, st, ebytes, nx).total + 1024;
+    // streamed weights: two rings (W1 K-blocks, W2 chunks) so the W1 items of the next
+    // chunks load while FC2 still holds W2 items; Y staged over its X slot (frees a Y
+    // buffer); the W1 ring as deep as fits (measured at C = 192: a 2-CTA cluster
+    // multicasting the weight items, or W2 split in two items, did not help)
+    const char* yie = std::getenv("SWIN_MLP_FUSED_YIN");
+    const int yin = (yie && *yie == '0') ? 0 : 1;
+    for (int st2 : {2, 1}) {
+        for (int st = kFMaxStages; st >= 2 * fp.KBC; --st) {
+            const uint32_t need = fused_layout(C, H, 2, st, ebytes, 2, yin, st2).total + 1024;
             if (need <= kSmemBudget) {
-                fp.NX = nx; fp.NH = 2; fp.stages = st; fp.smem = need; fp.on = true;
+                fp.NX = 2; fp.NH = 2; fp.stages = st; fp.stages2 = st2; fp.smem = need; fp.on = true;
+                fp.y_inplace = yin;
                 return true;
             }
-        }
-    }
-    {
-        const uint32_t need = fused_layout(C, H, 2, 2, ebytes, 2).total + 1024;
-        if (need <= kSmemBudget) {
-            fp.NX = 2; fp.NH = 2; fp.stages = 2; fp.smem = need; fp.on = true;
-            return true;
         }
     }
     return false;
@@ -616,6 +613,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         a.M = T; a.C = C; a.H = H;
         a.NJ = h->fp.NJ; a.KBC = h->fp.KBC; a.NB1 = h->fp.NB1; a.NH = h->fp.NH; a.stages = h->fp.stages;
         a.a1_col = h->fp.a1_col; a.NA2 = h->fp.NA2; a.a2_stride = h->fp.a2_stride; a.NX = h->fp.NX;
+        a.y_inplace = h->fp.y_inplace; a.stages2 = h->fp.stages2;
         a.m1 = h->m1; a.b1 = h->b1; a.zc1 = h->zc1;
         a.m2 = h->m2; a.b2 = h->b2; a.zc2 = h->zc2;
         a.gamma = h->gamma; a.beta = h->beta;

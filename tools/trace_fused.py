@@ -35,6 +35,7 @@ f = lambda v: int(v - t0) if v > 0 else -1
 NJ = 4 * C // 128
 fc1, fc2 = t[0:512], t[512:1024]
 fc1a, fc1b, fc2a, fc2b = t[1024:1536], t[1536:2048], t[6656:7168], t[7168:7680]
+fc1w = t[7680:8192]
 e5 = t[2048:4096].reshape(1024, 2)
 e6 = t[4096:6144].reshape(512, 4)
 st = t[6144:8192]
@@ -44,7 +45,7 @@ for i in range(min(ntile, 12)):
     print(f"tile {i}: ep6 start {f(e6[i,0])} pass1 {f(e6[i,2])} stats {f(e6[i,1])} end {f(e6[i,3])} stored {f(st[i])}")
     for j in range(NJ):
         u = i * NJ + j
-        print(f"   chunk {u:3d}: FC1 [{f(fc1a[u]):7d},{f(fc1b[u]):7d},{f(fc1[u]):7d}]  ep5 [{f(e5[u,0]):7d},{f(e5[u,1]):7d}]"
+        print(f"   chunk {u:3d}: FC1 [{f(fc1a[u]):7d},{f(fc1b[u]):7d},w {f(fc1w[u]):7d},{f(fc1[u]):7d}]  ep5 [{f(e5[u,0]):7d},{f(e5[u,1]):7d}]"
               f"  FC2 [{f(fc2a[u]):7d},{f(fc2b[u]):7d},{f(fc2[u]):7d}]")
 last = max(f(v) for v in nz)
 print("last stamp", last)
