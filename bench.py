@@ -275,14 +275,15 @@ def main():
     kernels = []
     for (L, T, _), (f1, f2, n), l in zip(spec, prof, relu_layers):
         ops = 2.0 * T * L.C * L.H
+        e5, e6 = T * L.H * 3.5, T * L.C * 15.0     # algorithmic epilogue lane-instructions
         if l.plan()["fused"]:
-            parts = (("fused_mlp", f1 + f2, 2.0 * ops),)
+            parts = (("fused_mlp", f1 + f2, 2.0 * ops, e5 + e6),)
         else:
-            parts = (("fc1_relu_q", f1, ops), ("fc2_ln_q", f2, ops))
-        for name, ms, kops in parts:
+            parts = (("fc1_relu_q", f1, ops, e5), ("fc2_ln_q", f2, ops, e6))
+        for name, ms, kops, alu in parts:
             avg_s = ms / max(n, 1) / 1e3
             kernels.append({"kernel": f"{name}[C={L.C},T={T}]", "avg_us": avg_s * 1e6,
-                            "tops": kops / avg_s / 1e12 if avg_s > 0 else None, "ops": kops})
+                            "tops": kops / avg_s / 1e12 if avg_s > 0 else None, "ops": kops, "alu": alu})
     dom = max(kernels, key=lambda k: k["avg_us"])
     step_us = 1e3 * sum(per_step_prof) / args.steps    # the profiled pass's own step time
     share = dom["avg_us"] / step_us
@@ -293,16 +294,33 @@ def main():
             traffic = json.load(open(tpath)).get(dom["kernel"])
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": dom["kernel"], "achieved": dom["tops"], "peak": int8_peak_tops,
-                "unit": "TOPS", "frac": dom["tops"] / int8_peak_tops, "traffic": traffic,
+    # The binding roof of the dominant kernel: tensor (algorithmic int8 ops) or ALU (the
+    # epilogues' algorithmic fp32 lane-instructions: e5 = 3.5 per hidden value
+    # for ReLU op #5, e6 = 15 per output value for op #6, against 148 SMs x 128 lanes x the
+    # max SM clock) -- whichever the kernel is closer to
+    sm_hz = 1e6 * (peaks.get("sm_max_mhz") or 1965.0)
+    alu_peak = 148 * 128 * sm_hz / 1e12          # T lane-instr/s
+    tensor_view = {"bound": "tensor", "achieved": dom["tops"], "peak": int8_peak_tops, "unit": "TOPS",
+                   "frac": dom["tops"] / int8_peak_tops,
+                   "algorithmic": "2*T*C*H ops per GEMM per launch (fused_mlp: both GEMMs, 4*T*C*H); "
+                                  "SURVEY §8(d): 16*C^2 ops per token per layer",
+                   "peak_source": f"{peaks['src']} bf16_tflops {peaks['bf16_burst']} x 2 (int8:bf16 nominal 4.5:2.25), burst"}
+    alu_ach = dom["alu"] / (dom["avg_us"] / 1e6) / 1e12
+    alu_view = {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "T lane-instr/s",
+                "frac": alu_ach / alu_peak,
+                "algorithmic": "T*(H*3.5 + C*15) lane-instructions per layer (SURVEY §8(d) e5, e6); op #5 only "
+                               "for fc1_relu_q, op #6 only for fc2_ln_q",
+                "peak_source": "148 SMs x 128 fp32 lanes x max SM clock (B200_PROFILING / MEASURED_PEAKS)"}
+    bind, other = (alu_view, tensor_view) if alu_view["frac"] > tensor_view["frac"] else (tensor_view, alu_view)
+    roofline = {"bound": bind["bound"], "kernel": dom["kernel"], "achieved": bind["achieved"], "peak": bind["peak"],
+                "unit": bind["unit"], "frac": bind["frac"], "traffic": traffic,
                 "share_of_step": share,
-                "peak_source": f"{peaks['src']} bf16_tflops {peaks['bf16_burst']} x 2 (int8:bf16 nominal 4.5:2.25), burst",
-                "algorithmic": "2*T*C*H ops per GEMM per launch (fused_mlp: both GEMMs, 4*T*C*H); "
-                               "SURVEY §8(d): 16*C^2 ops per token per layer",
+                "peak_source": bind["peak_source"], "algorithmic": bind["algorithmic"],
+                "other_roof": other,
                 "step_frac": (sum(k["ops"] for k in kernels) / (t_ms / args.steps / 1e3) / 1e12) / int8_peak_tops,
                 "profiled_step_us": step_us,
-                "kernels": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in kk.items() if k != "ops"}
-                            for kk in kernels]}
+                "kernels": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in kk.items()
+                             if k not in ("ops", "alu")} for kk in kernels]}
 
     # ---- end to end through the C ABI with host buffers (H2D + run + D2H per step) ----------------
     # the user call for a step of the four independent stage MLPs: swin_mlp_int8_run_host_batch
