@@ -412,7 +412,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         const uint32_t rit = quad * 32u + lane;
         const uint32_t row_off = rit * (uint32_t)kBK, rsw = rit & 7u;
         const float2 inv2 = make_float2(p.inv_h, p.inv_h);
-        const bool zx_zero = SMALLK && p.z_x == 0;
+        const bool zx0 = p.z_x == 0;
         pdl_wait();   // (taps)
         mbar_wait(bar_cfull, 0);
         uint32_t i = 0, j = 0, b = 0, bph = 0, hb = 0, hph = 0;
@@ -427,7 +427,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             const uint32_t tb = tmem_base + ((quad * 32u) << 16) + (uint32_t)p.a1_col + b * (uint32_t)kFHc + half * 64u;
             const uint32_t hq = sHq + hb * kKB + row_off;
             const int n_base = (int)(j * kFHc + half * 64u);
-            auto chunk = [&](uint32_t (&r)[16], int ch) {
+            auto chunk_t = [&](auto zx0_c, uint32_t (&r)[16], int ch) {
+                constexpr bool ZX0 = decltype(zx0_c)::value;   // z_x == 0: plain I2FP, no correction
                 const int n0 = n_base + ch * 16;
                 float v[16];
 #pragma unroll
@@ -435,11 +436,15 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     const float4 mv = *reinterpret_cast<const float4*>(cm1 + n0 + 4 * j4);
                     const float4 bv = B1 ? *reinterpret_cast<const float4*>(cb1 + n0 + 4 * j4)
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-                    // (z_x == 0: the magic constant is the same for every column, no load)
-                    const uint4 gv = zx_zero ? make_uint4(0x4B400000u, 0x4B400000u, 0x4B400000u, 0x4B400000u)
-                                             : *reinterpret_cast<const uint4*>(cmg1 + n0 + 4 * j4);
+                    const uint4 gv = ZX0 ? make_uint4(0x4B400000u, 0x4B400000u, 0x4B400000u, 0x4B400000u)
+                                         : *reinterpret_cast<const uint4*>(cmg1 + n0 + 4 * j4);
                     float2 a0, a1;
-                    if constexpr (SMALLK) {
+                    if constexpr (ZX0) {
+                        // one I2FP per value (a conversion-pipe op, ~25 % busy here) instead of
+                        // the magic add + subtract (1.5 issue slots): the epilogue is issue-bound
+                        a0 = make_float2(__int2float_rn((int32_t)r[4 * j4]), __int2float_rn((int32_t)r[4 * j4 + 1]));
+                        a1 = make_float2(__int2float_rn((int32_t)r[4 * j4 + 2]), __int2float_rn((int32_t)r[4 * j4 + 3]));
+                    } else if constexpr (SMALLK) {
                         // bits (0x4B400000 - zc) + acc = float 1.5*2^23 + (acc - zc), exact
                         const float2 mg = make_float2(12582912.0f, 12582912.0f);
                         a0 = f2_sub(make_float2(__uint_as_float(r[4 * j4] + gv.x), __uint_as_float(r[4 * j4 + 1] + gv.y)), mg);
@@ -451,7 +456,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     if (TAPS && p.acc1_tap && valid) {
                         const uint32_t o = SMALLK ? 0x4B400000u : 0u;
                         int4 t;
-                        if (SMALLK) t = make_int4((int)(r[4 * j4] + gv.x - o), (int)(r[4 * j4 + 1] + gv.y - o),
+                        if (ZX0) t = make_int4((int)r[4 * j4], (int)r[4 * j4 + 1], (int)r[4 * j4 + 2], (int)r[4 * j4 + 3]);
+                        else if (SMALLK) t = make_int4((int)(r[4 * j4] + gv.x - o), (int)(r[4 * j4 + 1] + gv.y - o),
                                                   (int)(r[4 * j4 + 2] + gv.z - o), (int)(r[4 * j4 + 3] + gv.w - o));
                         else t = make_int4((int)(r[4 * j4] - gv.x), (int)(r[4 * j4 + 1] - gv.y),
                                            (int)(r[4 * j4 + 2] - gv.z), (int)(r[4 * j4 + 3] - gv.w));
@@ -473,6 +479,10 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 st_shared_v4(hq + ((g ^ rsw) << 4), w[0], w[1], w[2], w[3]);
                 if (TAPS && p.hid_tap && valid)
                     st_v4(p.hid_tap + row * (int64_t)H + n0, make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]));
+            };
+            auto chunk = [&](uint32_t (&r)[16], int ch) {
+                if (zx0) chunk_t(std::true_type{}, r, ch);
+                else chunk_t(std::false_type{}, r, ch);
             };
             uint32_t ra[16], rb[16];
             tmem_ld16(tb, ra);
