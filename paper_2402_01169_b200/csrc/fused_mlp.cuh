@@ -525,6 +525,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         const int hc = C >> 1;                     // columns of this half: [cb, cb + hc)
         const int cb = (int)part * hc;
         const int nch = hc >> 4;                   // chunks of 16 (C % 32 == 0)
+        const float inv_nh = 1.0f / (float)hc, inv_c = 1.0f / (float)C;
         // pairwise combine of the two halves' statistics through smem; both halves
         // combine in the same (part 0, part 1) order, so they agree bit for bit
         using acc_t2 = typename std::conditional<STATS64, double, float>::type;
@@ -745,14 +746,14 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 // (Chan): mean = (m_0 + m_1)/2, M2 = M2_0 + M2_1 + (m_1 - m_0)^2 n/2
                 const float nh = (float)hc;
                 const float S1 = __fadd_rn(s1f.x, s1f.y), S2 = __fadd_rn(s2f.x, s2f.y);
-                const float q1 = __fdiv_rn(S1, nh);
+                const float q1 = __fmul_rn(S1, inv_nh);   // (fp32 LN tier: reciprocal multiplies, rsqrt)
                 acc_t2 o[2][2];
                 exchange(__fadd_rn(K, q1), __fsub_rn(S2, __fmul_rn(S1, q1)), o);
                 const float dm = __fsub_rn(o[1][0], o[0][0]);
                 mu_f = __fmul_rn(__fadd_rn(o[0][0], o[1][0]), 0.5f);
                 const float M2 = __fadd_rn(__fadd_rn(o[0][1], o[1][1]), __fmul_rn(__fmul_rn(dm, dm), __fmul_rn(nh, 0.5f)));
-                const float var = fmaxf(__fdiv_rn(M2, (float)C), 0.0f);
-                rstd_f = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
+                const float var = fmaxf(__fmul_rn(M2, inv_c), 0.0f);
+                rstd_f = rsqrtf(__fadd_rn(var, p.eps));
             }
             const float2 mu2 = make_float2(mu_f, mu_f), rstd2 = make_float2(rstd_f, rstd_f);
             if (stamp) trc[4096 + 4 * i + 1] = gtimer();
