@@ -66,42 +66,32 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-// Bounded wait: a lost arrival traps (kernel error) after ~2^34 cycles
-// instead of hanging the GPU.
-// (try_wait without a suspend-time hint: with the hint ptxas emits
+// Up to 256 polls of the phase in a tight PTX loop (2 instructions per poll while
+// waiting: try_wait + branch); true once the phase with `parity` has completed.
+__device__ __forceinline__ bool mbar_poll256(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t.reg .u32 c;\n\t"
+        "mov.u32 c, 0;\n"
+        "LAB_POLL:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "@P bra.uni LAB_DONE;\n\t"
+        "add.u32 c, c, 1;\n\t"
+        "setp.lt.u32 P, c, 256;\n\t"
+        "@P bra.uni LAB_POLL;\n"
+        "LAB_DONE:\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    return done != 0;
+}
+// Bounded wait: a lost arrival traps (kernel error) after seconds instead of hanging
+// the GPU.  (try_wait without a suspend-time hint: with the hint ptxas emits
 // NANOSLEEP.SYNCS after a failed probe, which delayed wake-ups by 100s of ns.)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    long long t0 = 0;
-    for (uint32_t it = 0;; ++it) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-        if (done) return;
-        if (it == 64) t0 = clock64();
-        if (it > 64 && ((it & 1023) == 0) && clock64() - t0 > (1ll << 34)) __trap();
-    }
-}
-// Same, backing off with nanosleep (32 ns doubling to 256 ns) after a failed probe: for
-// warps whose spinning would steal issue slots from the warps they share a sub-partition
-// with (epilogue and store warps waiting for work); costs at most ~the sleep time in
-// wake-up latency.
-__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    long long t0 = 0;
-    for (uint32_t it = 0;; ++it) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-        if (done) return;
-        if (it >= 1) __nanosleep(it < 4 ? 32u : it < 8 ? 64u : it < 16 ? 128u : 256u);   // exponential backoff
-        if (it == 64) t0 = clock64();
-        if (it > 64 && ((it & 63) == 0) && clock64() - t0 > (1ll << 34)) __trap();
-    }
+    // (a 32-bit round counter, no 64-bit clock kept live: 2^26 rounds of 256 polls is far
+    // beyond any legitimate wait)
+    for (uint32_t round = 0; !mbar_poll256(bar, parity);)
+        if (++round > (1u << 26)) __trap();
 }
 // Same, with cluster-scope acquire (for data written by peer CTAs via st.async).
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
@@ -116,6 +106,25 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
         if (done) return;
         if (it == 64) t0 = clock64();
         if (it > 64 && ((it & 1023) == 0) && clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
+// Same, backing off with nanosleep (32 ns doubling to 256 ns) after a failed probe: for
+// warps whose spinning would steal issue slots from the warps they share a sub-partition
+// with (epilogue and store warps waiting for work); costs at most ~the sleep time in
+// wake-up latency.
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
+    uint32_t ns = 32;
+    for (uint32_t it = 0;; ++it) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        if (done) return;
+        __nanosleep(ns);
+        ns = ns < 256u ? ns * 2u : 256u;   // exponential backoff
+        if (it > (1u << 26)) __trap();     // (~17 s of 256 ns sleeps)
     }
 }
 
