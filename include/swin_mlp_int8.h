@@ -183,12 +183,13 @@ swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, fl
  * the one-kernel plan) and [8704 + 2*cta + {0,1}] (FC2).  trace = NULL disables. */
 swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_t cta);
 
-/* Introspection: the launch plan of this layer, out10[16] = {FC1 BN, FC1 cluster size,
+/* Introspection: the launch plan of this layer, out10[20] = {FC1 BN, FC1 cluster size,
  * FC1 stages, FC1 max co-resident clusters, FC2 BN, FC2 cluster size, FC2 stages,
  * FC2 max clusters, FC1 epilogue groups, FC2 epilogue groups, FC1 resident weights,
  * FC2 resident weights, one-kernel plan used (C <= 256, H % 128 == 0; 1/0), its weight
  * ring depth (0 = weights resident in smem), its hidden-tile buffers, its FC1 TMEM
- * buffers}.  Entries 0-11 describe the two-kernel plan, which runs when entry 12 is 0.
+ * buffers, FC1 CTA pair (cta_group::2 MMA, M = 256; 1/0), 0, 0, 0}.  Entries 0-11 and 16
+ * describe the two-kernel plan, which runs when entry 12 is 0.
  * Returns 0, or -1 on a NULL argument. */
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
 

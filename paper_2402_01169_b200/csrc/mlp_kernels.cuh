@@ -61,7 +61,7 @@ constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 constexpr int kChunk = 16;           // columns per tcgen05.ld (32x32b.x16)
 constexpr int kGMax = 4;             // max ping-pong groups / accumulator buffers
 constexpr int kNConst = 5;           // m, b, zc, gamma, beta
-constexpr int kHasB = 1, kHasZc = 2, kZqNz = 4, kS64 = 8, kSmallK = 16;
+constexpr int kHasB = 1, kHasZc = 2, kZqNz = 4, kS64 = 8, kSmallK = 16, kPair = 32;
 
 __host__ __device__ constexpr int kernel_threads(int) { return kThreads; }
 
@@ -102,6 +102,8 @@ struct GemmArgs {
     unsigned long long* trace;
     int32_t trace_cta;
     unsigned long long* cta_stamps;   // debug: per CTA %globaltimer at entry / exit ([2 * blockIdx.x + {0,1}])
+    int32_t dbg;                      // debug experiments (0 in production)
+    int32_t eg;                       // op #5 epilogue groups (1: all 16 warps drain every tile; or G)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -113,26 +115,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct SmemLayout {
     uint32_t a, b, bres, out, xres, consts, bars, tmem_slot, red, xbuf, total;
 };
-__host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages + 7u * kGMax + 2u * kGMax + 1u; }
+__host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages + 7u * kGMax + 2u * kGMax + 1u + kGMax; }
 
 // ebytes: size of one exchanged row statistic (4: fp32 LN, 8: fp64 LN);
 // xstage: op #6 stages the residual x tiles in smem (else pass 1 reads x from global)
 // resb_bytes: resident-B region (0 when B streams through the ring with A)
+// bn_b: B rows per ring stage (BN; BN / 2 for a CTA pair, each CTA holds half of B)
+// eg: epilogue groups (G ping-pong groups, or 1: all 16 warps per tile), 4/eg column parts
 __host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int stages, int G, int ebytes = 4,
-                                                  int xstage = 1, uint32_t resb_bytes = 0) {
+                                                  int xstage = 1, uint32_t resb_bytes = 0, int bn_b = 0,
+                                                  int eg = 0) {
     SmemLayout L;
     const uint32_t tile = (uint32_t)BN * kBM;
     L.a = 0;
     L.b = L.a + (uint32_t)stages * kBM * kBK;
-    L.bres = L.b + (resb_bytes ? 0u : (uint32_t)stages * (uint32_t)BN * kBK);
+    L.bres = L.b + (resb_bytes ? 0u : (uint32_t)stages * (uint32_t)(bn_b ? bn_b : BN) * kBK);
     L.out = L.bres + resb_bytes;                                   // [G] output staging tiles
     L.xres = L.out + (uint32_t)G * tile;                           // op #6: [G] residual x tiles
     L.consts = L.xres + (epi == EP6_LN ? (uint32_t)xstage * tile : 0u);       // [G][kNConst][BN] fp32
     L.bars = L.consts + (uint32_t)G * kNConst * (uint32_t)BN * 4u;
     L.tmem_slot = L.bars + 8u * kNumBars(stages);
     const uint32_t eb = (uint32_t)ebytes;
+    const uint32_t parts = 4u / (uint32_t)(eg ? eg : G);
     L.red = (L.tmem_slot + 8 + 15) & ~15u;      // op #6: [G][pass][part][val][row] (parts > 1 only)
-    L.xbuf = L.red + (epi == EP6_LN && G == 2 ? (uint32_t)G * 2u * 2u * 2u * kBM * eb : 0u);
+    L.xbuf = L.red + (epi == EP6_LN && parts > 1 ? (uint32_t)G * 2u * parts * 2u * kBM * eb : 0u);
     L.total = L.xbuf + (epi == EP6_LN && CS > 1 ? (uint32_t)G * 2u * (uint32_t)CS * 2u * kBM * eb : 0u);
     return L;
 }
@@ -201,6 +207,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     constexpr bool HAS_B = (F & kHasB) != 0, HAS_ZC = (F & kHasZc) != 0, ZQNZ = (F & kZqNz) != 0;
     constexpr bool STATS64 = (F & kS64) != 0, SMALLK = (F & kSmallK) != 0;
     constexpr bool IS_LN = (EPI == EP6_LN);
+    // CTA pair (cta_group::2, M = 256 per MMA): the two CTAs of a cluster take m-tiles
+    // 2u and 2u+1 of the same n-group; each loads its A rows and half of the B rows,
+    // the leader issues the MMAs (op #5 only: no cross-CTA row statistics)
+    constexpr bool PAIR = (F & kPair) != 0;
+    static_assert(!(PAIR && IS_LN), "pair mode is an FC1 (op #5) plan");
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -212,10 +223,16 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int stages = p.stages;
     const uint32_t G = (uint32_t)p.G;
     const uint32_t lgG = G == 4 ? 2u : 1u;
-    const uint32_t tile_warps = kEpiWarps / G;
+    // epilogue groups: op #6 G ping-pong groups (one per accumulator buffer); op #5 may
+    // use one group of all 16 warps per tile (shorter per-tile drain, so the MMA of tile
+    // t + G waits less for the drain of tile t)
+    const uint32_t EG = (uint32_t)p.eg;
+    const uint32_t lgEG = EG == 4u ? 2u : EG == 2u ? 1u : 0u;
+    const uint32_t tile_warps = kEpiWarps / EG;
     using acc_t = typename std::conditional<STATS64, double, float>::type;   // LN statistics type
     const uint32_t resb_bytes = p.resb ? (uint32_t)p.n_groups * (uint32_t)((p.K + kBK - 1) / kBK) * (uint32_t)BN * kBK : 0u;
-    const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage, resb_bytes);
+    const int bn_b = PAIR ? BN / 2 : BN;                 // B rows per ring stage in this CTA
+    const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage, resb_bytes, bn_b, p.eg);
     const uint32_t tile_bytes = (uint32_t)BN * kBM;
     const uint32_t sA = base + L.a, sB = base + L.b;
     const uint32_t bar_full = base + L.bars;              // [stages] operands landed (count 1 + tx)
@@ -229,6 +246,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t bar_xfree = bar_xfull + 8u * kGMax;    // [G] op #6 x tile consumed (tile warps)
     const uint32_t bar_xst = bar_xfree + 8u * kGMax;      // [G][pass] op #6 DSMEM row stats (1 + tx)
     const uint32_t bar_bfull = bar_xst + 16u * kGMax;     // resident B landed (count 1 + tx)
+    const uint32_t bar_ptempty = bar_bfull + 8u;          // [G] pair: accumulator drained in both CTAs
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
     float* consts = reinterpret_cast<float*>(gbase + L.consts);
     acc_t* red = reinterpret_cast<acc_t*>(gbase + L.red);
@@ -262,9 +280,13 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_init(bar_xst + 16u * i + 8u, 1);
         }
         mbar_init(bar_bfull, 1);
+        for (uint32_t i = 0; i < (uint32_t)kGMax; ++i) mbar_init(bar_ptempty + 8u * i, 2u * tile_warps);
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), tmem_cols);
+    if (warp == 2) {
+        if constexpr (PAIR) tmem_alloc_pair(smem_u32(const_cast<uint32_t*>(tmem_slot)), tmem_cols);
+        else tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), tmem_cols);
+    }
     tc_fence_before();
     cluster_sync_all();
     tc_fence_after();
@@ -273,11 +295,12 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // to activation memory (written / read by the neighbouring kernels) waits below
     pdl_launch_dependents();
 
-    const uint32_t cid = blockIdx.x / CS, nclus = gridDim.x / CS;
+    const uint32_t CL = PAIR ? 2u : CS;                   // CTAs per cluster
+    const uint32_t cid = blockIdx.x / CL, nclus = gridDim.x / CL;
     const uint32_t num_units = (uint32_t)p.num_units, n_groups = (uint32_t)p.n_groups;
     const uint32_t m_tiles = num_units / n_groups;
     const int num_kb = (p.K + kBK - 1) / kBK;
-    const uint32_t a_bytes = kBM * kBK, b_bytes = (uint32_t)BN * kBK;
+    const uint32_t a_bytes = kBM * kBK, b_bytes = (uint32_t)bn_b * kBK;
     const uint16_t cmask = (uint16_t)((1u << CS) - 1u);
     const uint32_t W = (uint32_t)p.out_w;
     const uint32_t lgW = 31u - (uint32_t)__clz((int)W);   // W is a power of two
@@ -295,11 +318,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ng = it % n_groups;
         } else {
             const uint32_t u = cid + it * nclus;
-            m_tile = u / n_groups;
+            m_tile = PAIR ? 2u * (u / n_groups) + rank : u / n_groups;   // pair: units are m-tile pairs
             ng = u % n_groups;
         }
     };
-    auto n0_of = [&](uint32_t ng) -> int { return (int)((ng * CS + rank) * (uint32_t)BN); };
+    auto n0_of = [&](uint32_t ng) -> int { return (int)((PAIR ? ng : ng * CS + rank) * (uint32_t)BN); };
     // op #6 x tile buffer of tile `it` and its phase (xstage buffers: 1 or G, powers of two)
     const uint32_t xsb = p.xstage > 0 ? (uint32_t)p.xstage : 1u;
     const uint32_t lgX = xsb == 4u ? 2u : xsb == 2u ? 1u : 0u;
@@ -354,10 +377,24 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int n0 = n0_of(ng), row0 = (int)(m_tile * kBM);
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+                    if constexpr (PAIR) {
+                        // both CTAs load their halves; the bytes complete on the leader's barrier
+                        if (elect_one()) {
+                            if (trc && kb == 0 && it < 512) trc[2 * it] = gtimer();
+                            if (rank == 0) mbar_arrive_expect_tx(bar_full + 8u * s, 2u * (a_bytes + b_bytes));
+                            const uint32_t fb = mapa(bar_full + 8u * s, 0);
+                            tma_load_2d_pair(&tmB, sB + (uint32_t)s * b_bytes, fb, kb * kBK, n0 + (int)rank * bn_b);
+                            tma_load_2d_pair(&tmA, sA + (uint32_t)s * a_bytes, fb, kb * kBK, row0);
+                        }
+                        __syncwarp();
+                        if (++s == stages) { s = 0; ph ^= 1u; }
+                        continue;
+                    }
                     if (elect_one()) {
                         if (trc && kb == 0 && it < 512) trc[2 * it] = gtimer();
-                        mbar_arrive_expect_tx(bar_full + 8u * s, a_bytes + b_bytes);
-                        tma_load_2d(&tmB, sB + (uint32_t)s * b_bytes, bar_full + 8u * s, kb * kBK, n0);
+                        if (trc && it < 4 && kb < 16) trc[2048 + 16 * (40 + it) + kb] = gtimer();
+                        mbar_arrive_expect_tx(bar_full + 8u * s, (p.dbg & 1) ? a_bytes : a_bytes + b_bytes);
+                        if (!(p.dbg & 1)) tma_load_2d(&tmB, sB + (uint32_t)s * b_bytes, bar_full + 8u * s, kb * kBK, n0);
                         load_a(kb, row0);
                     }
                     __syncwarp();
@@ -373,7 +410,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp == 1) {
         // ============================ MMA issuer ==============================
-        const uint32_t idesc = idesc_i8(kBM, (uint32_t)BN);
+        const uint32_t idesc = idesc_i8(PAIR ? 2u * kBM : kBM, (uint32_t)BN);
         int s = 0;
         uint32_t ph = 0;
         if (resb) mbar_wait(bar_bfull, 0);
@@ -381,13 +418,14 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // the n-groups of an m-tile share the A slots (waited by the first, released by the last)
         auto mma_tile = [&](uint32_t it, uint32_t ng, bool first, bool last, int& ss, uint32_t& pp) {
             const uint32_t buf = it & (G - 1u), aph = (it >> lgG) & 1u;
-            mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);
+            mbar_wait((PAIR ? bar_ptempty : bar_tempty) + 8u * buf, aph ^ 1u);
             tc_fence_after();
             if (trc && lane == 0 && it < 256) trc[1024 + 4 * it] = gtimer();
             const uint32_t d = tmem_base + buf * (uint32_t)BN;
             for (int kb = 0; kb < num_kb; ++kb) {
                 if (first) mbar_wait(bar_full + 8u * ss, pp);
                 tc_fence_after();
+                if (trc && lane == 0 && it < 4 && kb < 16) trc[2048 + 16 * (44 + it) + kb] = gtimer();
                 if (trc && lane == 0 && it < 256 && kb == 0) trc[1024 + 4 * it + 1] = gtimer();
                 const uint64_t ad = umma_desc_k128(sA + (uint32_t)ss * a_bytes);
                 const uint64_t bd = umma_desc_k128(resb ? base + L.bres + (ng * (uint32_t)num_kb + (uint32_t)kb) * b_bytes
@@ -395,18 +433,27 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int rem = p.K - kb * kBK;
                 const int nk = rem >= kBK ? 4 : rem / 32;
                 if (elect_one()) {
-                    for (int k = 0; k < nk; ++k)
-                        mma_i8(d, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
-                    if (trc && it < 256 && kb == 0) trc[1024 + 4 * it + 2] = gtimer();
-                    if (last) {
-                        if (CS == 1) mma_commit(bar_empty + 8u * ss);
-                        else mma_commit_mc(bar_empty + 8u * ss, cmask);
+                    if constexpr (PAIR) {
+                        for (int k = 0; k < nk; ++k)
+                            mma_i8_pair(d, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                        mma_commit_pair_mc(bar_empty + 8u * ss, 3);   // both CTAs' slots free
+                    } else {
+                        for (int k = 0; k < nk; ++k)
+                            mma_i8(d, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                        if (last) {
+                            if (CS == 1) mma_commit(bar_empty + 8u * ss);
+                            else mma_commit_mc(bar_empty + 8u * ss, cmask);
+                        }
                     }
+                    if (trc && it < 256 && kb == 0) trc[1024 + 4 * it + 2] = gtimer();
                 }
                 __syncwarp();
                 if (++ss == stages) { ss = 0; pp ^= 1u; }
             }
-            if (elect_one()) mma_commit(bar_tfull + 8u * buf);
+            if (elect_one()) {
+                if constexpr (PAIR) mma_commit_pair_mc(bar_tfull + 8u * buf, 3);   // both CTAs' accumulators
+                else mma_commit(bar_tfull + 8u * buf);
+            }
             __syncwarp();
             if (trc && lane == 0 && it < 256) trc[1024 + 4 * it + 3] = gtimer();
         };
@@ -423,7 +470,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 s = ss;
                 ph = pp;
             }
-        } else {
+        } else if (!PAIR || rank == 0) {   // pair: the leader issues for both CTAs
             for (uint32_t it = 0; it < my_tiles; ++it) {
                 uint32_t m_tile, ng;
                 tile_at(it, m_tile, ng);
@@ -436,21 +483,25 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t sb = it & (G - 1u), sph = (it >> lgG) & 1u;
             mbar_wait(bar_sfull + 8u * sb, sph);
+            if (trc && lane == 0 && it < 64) trc[2048 + 16 * it + 8] = gtimer();
             if (lane == 0) {
                 uint32_t m_tile, ng;
                 tile_at(it, m_tile, ng);
                 const int n0 = n0_of(ng);
                 const int32_t row0 = (int32_t)(m_tile * kBM);
                 const uint32_t src = base + L.out + sb * tile_bytes;
+                if (!(p.dbg & 2))
                 for (uint32_t sub = 0; sub < ((uint32_t)BN >> lgW); ++sub)
                     tma_store_2d(&tmO, src + (sub << (lgW + 7u)), n0 + (int)(sub << lgW), row0);
                 bulk_commit();
                 bulk_wait_read<0>();              // the stores have read the staging tile
+                if (trc && it < 64) trc[2048 + 16 * it + 9] = gtimer();
                 mbar_arrive(bar_sfree + 8u * sb);
             }
             __syncwarp();
         }
         if (lane == 0) bulk_wait_all();           // output writes complete before the CTA retires
+        if (trc && lane == 0) trc[2048 + 16 * 63 + 10] = gtimer();
         __syncwarp();
     } else if (warp == 3) {
         // ============================ loader ====================================
@@ -496,8 +547,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // ============================ epilogue ================================
         const uint32_t ew = warp - kEpiWarp0;
         const uint32_t quad = warp & 3u;            // TMEM lane quadrant this warp may access
-        const uint32_t grp = ew >> (4u - lgG);      // ping-pong group: 16/G warps each
-        const uint32_t P = 4u >> lgG;               // column parts per group (G=4: 1, G=2: 2)
+        const uint32_t grp = ew >> (4u - lgEG);     // ping-pong group: 16/EG warps each
+        const uint32_t P = 4u >> lgEG;              // column parts per group (4/EG)
         const uint32_t part = (ew >> 2) & (P - 1u);
         const uint32_t rit = quad * 32u + lane;     // row in tile
         const int nch = BN / kChunk;
@@ -519,17 +570,17 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const float2 inv2 = make_float2(p.inv_q, p.inv_q);
         pdl_wait();   // (global residual / taps)
 
-        for (uint32_t it = grp; it < my_tiles; it += G) {
+        for (uint32_t it = grp; it < my_tiles; it += EG) {
             uint32_t m_tile, ng;
             tile_at(it, m_tile, ng);
             const int n0 = n0_of(ng);
-            const uint32_t buf = grp, aph = (it >> lgG) & 1u;
+            const uint32_t buf = it & (G - 1u), aph = (it >> lgG) & 1u;
             const uint32_t sbuf = base + L.out + buf * tile_bytes;
             mbar_wait(bar_sfree + 8u * buf, aph ^ 1u);   // staging tile read by its last stores
             mbar_wait(bar_cfull + 8u * buf, aph);
             mbar_wait(bar_tfull + 8u * buf, aph);
             tc_fence_after();
-            if (trc && elected && it < 64) trc[2048 + 16 * it + 2] = gtimer();
+            if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 2] = gtimer();
             const int64_t row = (int64_t)m_tile * kBM + rit;
             const bool valid = row < p.M;
             const uint32_t tb = tmem_base + ((quad * 32u) << 16) + buf * (uint32_t)BN;
@@ -619,7 +670,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const bool x_smem = x_res && p.xstage;
                 const uint32_t xtile = base + L.xres + xbuf_of(it) * tile_bytes;
                 if (x_smem) mbar_wait(bar_xfull + 8u * xbuf_of(it), xph_of(it));   // residual x tile landed
-                if (trc && elected && it < 64) trc[2048 + 16 * it + 6] = gtimer();
+                if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 6] = gtimer();
                 const float2 sx2 = make_float2(p.s_x, p.s_x);
                 const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
                 const float2 xoff2 = make_float2(xoff, xoff);
@@ -706,7 +757,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bar_xfree + 8u * xbuf_of(it));
                 }
-                if (trc && elected && it < 64) trc[2048 + 16 * it + 3] = gtimer();
+                if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 3] = gtimer();
 
                 // row statistics: column parts via smem (named barrier of the group's
                 // threads), the CS CTAs of the cluster via DSMEM; always summed in the
@@ -715,12 +766,16 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 auto row_sum2 = [&](acc_t v0, acc_t v1, uint32_t pass, acc_t& o1) -> acc_t {
                     acc_t t0 = v0, t1 = v1;
                     if (P > 1) {
-                        const uint32_t slot = ((buf * 2u + pass) * 2u) * 2u;   // [G][pass][part][val]
+                        const uint32_t slot = ((buf * 2u + pass) * P) * 2u;   // [G][pass][part][val]
                         red[(slot + part * 2u) * kBM + rit] = v0;
                         red[(slot + part * 2u + 1u) * kBM + rit] = v1;
                         named_bar_sync(1u + buf, 32u * tile_warps);
-                        t0 = (acc_t)red[slot * kBM + rit] + (acc_t)red[(slot + 2u) * kBM + rit];
-                        t1 = (acc_t)red[(slot + 1u) * kBM + rit] + (acc_t)red[(slot + 3u) * kBM + rit];
+                        t0 = (acc_t)red[slot * kBM + rit];
+                        t1 = (acc_t)red[(slot + 1u) * kBM + rit];
+                        for (uint32_t q = 1; q < P; ++q) {   // parts in order
+                            t0 = t0 + (acc_t)red[(slot + 2u * q) * kBM + rit];
+                            t1 = t1 + (acc_t)red[(slot + 2u * q + 1u) * kBM + rit];
+                        }
                     }
                     if (CS == 1) { o1 = t1; return t0; }
                     const uint32_t sid = buf * 2u + pass;
@@ -748,7 +803,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if constexpr (STATS64) {
                     acc_t unused;
                     const acc_t mu = row_sum2(s1d, (acc_t)0, 0, unused) / (acc_t)C;
-                    if (trc && elected && it < 64) trc[2048 + 16 * it + 4] = gtimer();
+                    if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 4] = gtimer();
                     // pass 2: centred sum of squares
                     double s2d = 0.0;
                     for_chunks([&](uint32_t (&r)[16], int) {
@@ -772,19 +827,27 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     const float q1 = nw > 0.f ? __fdiv_rn(S1, nw) : 0.f;
                     float m = __fadd_rn(K, q1), M2 = __fsub_rn(S2, __fmul_rn(S1, q1)), n = nw;
                     if (P > 1) {
-                        const uint32_t slot = (buf * 2u * 2u) * 2u;     // [G][pass 0][part][val]
+                        const uint32_t slot = (buf * 2u * P) * 2u;      // [G][pass 0][part][val]
                         red[(slot + part * 2u) * kBM + rit] = m;
                         red[(slot + part * 2u + 1u) * kBM + rit] = M2;
                         named_bar_sync(1u + buf, 32u * tile_warps);
-                        const float m0 = red[slot * kBM + rit], qa = red[(slot + 1u) * kBM + rit];
-                        const float m1 = red[(slot + 2u) * kBM + rit], qb = red[(slot + 3u) * kBM + rit];
-                        const float n0 = (float)(min(per, nch) * kChunk);
-                        const float n1 = (float)(BN - min(per, nch) * kChunk);
-                        const float nt = __fadd_rn(n0, n1);
-                        const float dm = __fsub_rn(m1, m0);
-                        m = __fadd_rn(m0, __fmul_rn(dm, __fdiv_rn(n1, nt)));
-                        M2 = __fadd_rn(__fadd_rn(qa, qb), __fmul_rn(__fmul_rn(dm, dm), __fdiv_rn(__fmul_rn(n0, n1), nt)));
-                        n = nt;
+                        // pairwise (Chan) combine of the parts, in part order
+                        float ma = red[slot * kBM + rit], qa = red[(slot + 1u) * kBM + rit];
+                        float na = (float)(min(per, nch) * kChunk);
+                        for (uint32_t q = 1; q < P; ++q) {
+                            const int lo = min((int)q * per, nch), hi = min(lo + per, nch);
+                            if (hi <= lo) continue;
+                            const float nb = (float)((hi - lo) * kChunk);
+                            const float mb = red[(slot + 2u * q) * kBM + rit], qb = red[(slot + 2u * q + 1u) * kBM + rit];
+                            const float nt = __fadd_rn(na, nb);
+                            const float dm = __fsub_rn(mb, ma);
+                            ma = __fadd_rn(ma, __fmul_rn(dm, __fdiv_rn(nb, nt)));
+                            qa = __fadd_rn(__fadd_rn(qa, qb), __fmul_rn(__fmul_rn(dm, dm), __fdiv_rn(__fmul_rn(na, nb), nt)));
+                            na = nt;
+                        }
+                        m = ma;
+                        M2 = qa;
+                        n = na;
                     }
                     if (CS > 1) {
                         const uint32_t sid = buf * 2u;
@@ -812,13 +875,13 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         m = mean;
                         M2 = __fmaf_rn(dsq, n, qsum);
                     }
-                    if (trc && elected && it < 64) trc[2048 + 16 * it + 4] = gtimer();
+                    if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 4] = gtimer();
                     const float var = fmaxf(__fdiv_rn(M2, (float)C), 0.0f);
                     rstd = (acc_t)__fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, p.eps)));
                     mu2c = make_float2(m, m);
                 }
                 const float2 rstd2 = make_float2((float)rstd, (float)rstd);
-                if (trc && elected && it < 64) trc[2048 + 16 * it + 5] = gtimer();
+                if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 5] = gtimer();
 
                 // pass 3: yhat = fl(((z-mu)*rstd)*gamma + beta); Y = Q_y(yhat)
                 const float* cg = cm + 3 * BN;
@@ -870,18 +933,25 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(bar_tempty + 8u * buf);   // TMEM free: the next MMA may start
+                if constexpr (PAIR) {                 // (pair: the leader's MMA waits on both CTAs)
+                    if (rank == 0) mbar_arrive(bar_ptempty + 8u * buf);
+                    else mbar_arrive_cluster(mapa(bar_ptempty + 8u * buf, 0));
+                }
                 mbar_arrive(bar_sfull + 8u * buf);    // this warp's part of the tile is staged
             }
-            if (trc && elected && it < 64) trc[2048 + 16 * it + 7] = gtimer();
+            if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 7] = gtimer();
         }
     }
 
     // teardown: no CTA leaves while a peer may still address its shared memory
+    if (trc && lane == 0) trc[2048 + 16 * 60 + warp] = gtimer();   // (debug: role done)
     tc_fence_before();
     cluster_sync_all();
+    if (trc && threadIdx.x == 0) trc[2048 + 16 * 62] = gtimer();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, tmem_cols);
+        if constexpr (PAIR) tmem_dealloc_pair(tmem_base, tmem_cols);
+        else tmem_dealloc(tmem_base, tmem_cols);
     }
     if (p.cta_stamps && threadIdx.x == 0) p.cta_stamps[2 * blockIdx.x + 1] = gtimer();
 }

@@ -69,6 +69,8 @@ struct Plan {
     void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
     int epi = 0, threads = 0;
     int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0;
+    int eg = 2;     // epilogue groups: G ping-pong groups, or 1 (all 16 warps drain every tile)
+    int pair = 0;   // CTA pair (cta_group::2): clusters of 2 CTAs on m-tiles 2u, 2u+1 (CS == 1)
     uint32_t smem = 0;
     int max_clusters = 0;
 };
@@ -130,9 +132,11 @@ constexpr uint32_t kSmemBudget = 227 * 1024;
 
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
 
-// table index bit 3 means kSmallK for op #5 and kS64 for op #6
+// table index bit 3 means kSmallK for op #5 and kS64 for op #6; bit 4 (op #5) the CTA pair
 template <int EPI, int I>
-constexpr int flags_of() { return (I & 7) | ((I & 8) ? (EPI == EP6_LN ? kS64 : kSmallK) : 0); }
+constexpr int flags_of() {
+    return (I & 7) | ((I & 8) ? (EPI == EP6_LN ? kS64 : kSmallK) : 0) | ((I & 16) ? kPair : 0);
+}
 template <int EPI, int... Is>
 KernelFn pick(int f, std::integer_sequence<int, Is...>, bool) {
     static const KernelFn table[] = {mlp_gemm_kernel<EPI, flags_of<EPI, Is>()>...};
@@ -145,10 +149,10 @@ KernelFn kernel_for(int epi, int flags) {
     switch (epi) {
         // op #5: bias, zero points, small-K conversion (no fp64 LN); op #6: bias, zero
         // points, fp64 LN (its K = H is never small)
-        case EP5_RELU: return pick<EP5_RELU>((flags & 7) | ((flags & kSmallK) ? 8 : 0),
-                                             std::make_integer_sequence<int, 16>{}, true);
-        case EP5_GELU: return pick<EP5_GELU>((flags & 7) | ((flags & kSmallK) ? 8 : 0),
-                                             std::make_integer_sequence<int, 16>{}, true);
+        case EP5_RELU: return pick<EP5_RELU>((flags & 7) | ((flags & kSmallK) ? 8 : 0) | ((flags & kPair) ? 16 : 0),
+                                             std::make_integer_sequence<int, 32>{}, true);
+        case EP5_GELU: return pick<EP5_GELU>((flags & 7) | ((flags & kSmallK) ? 8 : 0) | ((flags & kPair) ? 16 : 0),
+                                             std::make_integer_sequence<int, 32>{}, true);
         default: return pick<EP6_LN>(flags & 15, std::make_integer_sequence<int, 16>{}, false);
     }
 }
@@ -158,12 +162,13 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
     // always grant the full budget so one layer's plan never shrinks another's.
     CUDA_TRY(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)pl.CS);
+    const int cl = pl.pair ? 2 : pl.CS;
+    cfg.gridDim = dim3((unsigned)cl);
     cfg.blockDim = dim3((unsigned)pl.threads);
     cfg.dynamicSmemBytes = pl.smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)pl.CS;
+    at[0].val.clusterDim.x = (unsigned)cl;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -172,7 +177,7 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
     cudaError_t e = cudaOccupancyMaxActiveClusters(&n, pl.fn, &cfg);
     if (e != cudaSuccess || n <= 0) {
         cudaGetLastError();
-        n = num_sms / pl.CS;
+        n = num_sms / cl;
     }
     pl.max_clusters = n;
     return SWIN_MLP_OK;
@@ -182,6 +187,20 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
 // full_row: the epilogue needs whole rows (LayerNorm) -> the cluster must
 // cover all N columns (CS * BN == N); otherwise column groups are independent.
 // The first candidate whose shared-memory plan fits wins.
+// Epilogue groups for G accumulator buffers: G ping-pong groups (default), or one
+// group of all 16 warps per tile.  Measured on the Swin-T stages: no gain for op #5
+// (its drain is issue-bound, the same SM-wide rate either way) and op #6 slower by
+// ~1 us (the 4-part statistics combine).  SWIN_MLP_EP5_GROUPS / SWIN_MLP_EP6_GROUPS
+// = 1, 2 or 4 (dividing G) select another split; a plan that does not fit falls back
+// to G.
+int epilogue_groups(int epi, int G) {
+    static const char* e5 = std::getenv("SWIN_MLP_EP5_GROUPS");
+    static const char* e6 = std::getenv("SWIN_MLP_EP6_GROUPS");
+    const char* e = epi == EP6_LN ? e6 : e5;
+    const int want = e ? atoi(e) : G;
+    return (want == 1 || want == 2 || want == 4) && G % want == 0 ? want : G;
+}
+
 bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // output TMA box width: widest swizzle span dividing BN (full 128-B lines when possible)
     pl.out_w = pl.BN % 128 == 0 ? 128 : pl.BN % 64 == 0 ? 64 : pl.BN % 32 == 0 ? 32 : 16;
@@ -193,6 +212,7 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     static const bool no_resb = std::getenv("SWIN_MLP_NO_RESB") != nullptr;   // debug / A-B switch
     for (int rb : {1, 0}) {
     if (rb && no_resb) continue;
+    if (rb && pl.pair) continue;   // pair: B streams (half per CTA)
     // output staging: G ping-pong groups / accumulator buffers / staging tiles, 4 when
     // 4*BN TMEM columns fit (more tiles in flight), else 2; op #6 also prefers its
     // residual x tiles staged in smem
@@ -202,8 +222,11 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         if (G * pl.BN > 512) continue;
         if (xs > 1 && xs != G) continue;
         const uint32_t rbb = rb ? resb_bytes : 0u;
-        const uint32_t stage = (uint32_t)(kBM * kBK) + (rb ? 0u : (uint32_t)pl.BN * kBK);
-        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb).total + 1024;
+        const int bn_b = pl.pair ? pl.BN / 2 : pl.BN;   // B rows per stage in one CTA
+        for (int eg : {epilogue_groups(epi, G), G}) {
+        pl.eg = eg;
+        const uint32_t stage = (uint32_t)(kBM * kBK) + (rb ? 0u : (uint32_t)bn_b * kBK);
+        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb, bn_b, pl.eg).total + 1024;
         if (extra >= kSmemBudget) continue;
         int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
         if (stages > 8) stages = 8;
@@ -214,8 +237,9 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         pl.G = G;
         pl.xstage = xs;
         pl.resb = rb;
-        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb).total + 1024;
+        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb, bn_b, pl.eg).total + 1024;
         if (pl.smem <= kSmemBudget) return true;
+        }
     }
     }
     }
@@ -243,6 +267,18 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
             if (fit_smem(epi, pl, 2, K)) return true;
         }
         return false;
+    }
+    // op #5 with K >= 512: a CTA pair (cta_group::2, 256 x 256 tiles: each CTA streams
+    // its A rows and half of B, 2/3 of the single-CTA operand bytes per MAC in a 4-deep
+    // ring).  Measured on the Swin-T stages: FC1 at C = 768 2 us faster, at C = 384
+    // 0.5 us slower (there the single-CTA ring already holds a whole tile's K).
+    // SWIN_MLP_PAIR=1 / 0 forces it on / off.
+    static const char* pair_env = std::getenv("SWIN_MLP_PAIR");
+    const bool want_pair = pair_env ? (*pair_env == '1') : K >= 512;
+    if (epi != EP6_LN && want_pair && N % 256 == 0) {
+        pl.BN = 256; pl.CS = 1; pl.n_groups = N / 256; pl.pair = 1;
+        if (fit_smem(epi, pl, 3, K)) return true;
+        pl.pair = 0;
     }
     for (int bn : {256, 128, 192, 96, 64, 32}) {
         if (N % bn) continue;
@@ -305,13 +341,14 @@ swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMa
     int64_t clusters = units < pl.max_clusters ? units : pl.max_clusters;
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(clusters * pl.CS));
+    const int cl = pl.pair ? 2 : pl.CS;   // CTAs per cluster
+    cfg.gridDim = dim3((unsigned)(clusters * cl));
     cfg.blockDim = dim3((unsigned)pl.threads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)pl.CS;
+    at[0].val.clusterDim.x = (unsigned)cl;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see the kernels)
@@ -554,13 +591,13 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     if (d.b2) H_TRY(upload(h, b2, &h->b2));
     if (d.x_zero_point) H_TRY(upload(h, zc1, &h->zc1));
     if (d.h_zero_point) H_TRY(upload(h, zc2, &h->zc2));
-    H_TRY(encode_2d(&h->tm_w1, h->w1, H, C, C, (uint32_t)h->p1.BN));
+    H_TRY(encode_2d(&h->tm_w1, h->w1, H, C, C, (uint32_t)(h->p1.pair ? h->p1.BN / 2 : h->p1.BN)));
     H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H, (uint32_t)h->p2.BN));
     // |A1| <= (128 + |z_x|) * 127 * C: below 2^22 the exact magic-number int->float applies
     const bool small_k1 = (int64_t)(128 + std::abs(d.x_zero_point)) * 127 * C < (int64_t(1) << 22);
     h->p1.fn = kernel_for(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU,
                           (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (d.h_zero_point ? kZqNz : 0) |
-                          (small_k1 ? kSmallK : 0));
+                          (small_k1 ? kSmallK : 0) | (h->p1.pair ? kPair : 0));
     h->p2.fn = kernel_for(EP6_LN, (d.b2 ? kHasB : 0) | (d.h_zero_point ? kHasZc : 0) |
                                       (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0));
     H_TRY(prepare(h->p1, h->num_sms));
@@ -668,14 +705,16 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.G = h->p1.G; a1.resb = h->p1.resb;
     a1.mt_major = h->p1.resb ? 1 : 0;   // resident B needs the m-major order; otherwise deal (m, n) units
     a1.out_w = h->p1.out_w;
-    a1.n_groups = h->p1.n_groups; a1.num_units = m_tiles * h->p1.n_groups; a1.ldo = H;
+    a1.n_groups = h->p1.n_groups; a1.num_units = (h->p1.pair ? (m_tiles + 1) / 2 : m_tiles) * h->p1.n_groups;
+    a1.eg = h->p1.eg; a1.ldo = H;
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
     a1.acc_tap = dbg ? acc1 : nullptr;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
     a1.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
+    { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }
 
     GemmArgs a2 = {};
-    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.xstage = h->p2.xstage; a2.x = x;
+    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.eg = h->p2.eg; a2.xstage = h->p2.xstage; a2.x = x;
     a2.out_w = h->p2.out_w;
     a2.resb = h->p2.resb; a2.mt_major = 1;   // op #6: one n-group per cluster
     a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
@@ -927,12 +966,13 @@ swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
 
 // Test/bench introspection: the launch plan chosen for this layer.
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
-    if (!h || !out10) return -1;  // out10 holds 16 entries
+    if (!h || !out10) return -1;  // out10 holds 20 entries
     out10[0] = h->p1.BN; out10[1] = h->p1.CS; out10[2] = h->p1.stages; out10[3] = h->p1.max_clusters;
     out10[4] = h->p2.BN; out10[5] = h->p2.CS; out10[6] = h->p2.stages; out10[7] = h->p2.max_clusters;
     out10[8] = h->p1.G; out10[9] = h->p2.G;
     out10[10] = h->p1.resb; out10[11] = h->p2.resb;
     out10[12] = h->fp.on ? 1 : 0; out10[13] = h->fp.stages; out10[14] = h->fp.NH; out10[15] = h->fp.NB1;
+    out10[16] = h->p1.pair; out10[17] = out10[18] = out10[19] = 0;
     return 0;
 }
 

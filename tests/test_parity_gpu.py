@@ -301,3 +301,14 @@ def test_fused_persistent_multi_tile(dev, C, T):
 def test_fused_gelu_and_ln_fp64(dev, C, T):
     _run_and_check(dev, _layer(C, 9000 + C, act=1, bias=True, zh=-3), T)
     _run_and_check(dev, _layer(C, 9100 + C), T, ln_fp64=True)
+
+
+@pytest.mark.parametrize("C,T", [(768, 3 * 128 - 51), (512, 20 * 128 + 77)])
+def test_fc1_cta_pair(dev, C, T):
+    """FC1 on a CTA pair (cta_group::2, M = 256): odd m-tile counts (the last pair's second
+    tile entirely out of range), several pair tiles per cluster, ReLU and GELU, zero points."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(C, 9500 + C)
+    assert SwinMlpInt8Layer(L, device=0).plan()["fc1_pair"] == 1
+    _run_and_check(dev, L, T, e2e=False)
+    _run_and_check(dev, _layer(C, 9600 + C, act=1, bias=True, zx=-5, zh=-3, zy=2), T, e2e=False)

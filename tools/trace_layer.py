@@ -24,7 +24,7 @@ torch.cuda.synchronize()
 layer.set_trace(None)
 t = buf.cpu().numpy().astype(np.int64)
 print("C", L.C, "T", T, layer.plan())
-EPI = ["top", "bufok", "tfull", "pass1", "mean", "var", "-", "end", "cfull"]
+EPI = ["top", "bufok", "tfull", "pass1", "mean", "var", "-", "end", "sfull", "sread"]
 for k, name in ((0, "FC1"), (1, "FC2")):
     base = t[k * 4096:(k + 1) * 4096]
     nz = base[base > 0]
@@ -38,12 +38,19 @@ for k, name in ((0, "FC1"), (1, "FC2")):
     cst = base[3072:4096].reshape(512, 2)
     print(f"== {name}: ns from first stamp")
     print("tile  prod[s,e]       mma[s,full,issued,e]            const[s,e]      epi: " + " ".join(f"{e:>9s}" for e in EPI))
-    n = int((mma[:, 0] > 0).sum())
+    n = max(int((mma[:, 0] > 0).sum()), int((epi[:40, 2] > 0).sum()))
     f = lambda v: (v - t0) if v else -1
     for i in range(min(n, 40)):
         ep = " ".join(f"{f(epi[i, j]) if i < 64 else -1:9d}" for j in range(len(EPI)))
         print(f"{i:3d} {f(prod[i,0]):7d},{f(prod[i,1]):7d} {f(mma4[i,0]):7d},{f(mma4[i,1]):7d},{f(mma4[i,2]):7d},{f(mma4[i,3]):7d} "
               f"{f(cst[i,0]):7d},{f(cst[i,1]):7d}  {ep}")
+    for i in range(4):
+        print("tile", i, "TMA issue", [int(v - t0) if v else -1 for v in epi[40 + i, :6]],
+              "MMA full", [int(v - t0) if v else -1 for v in epi[44 + i, :6]])
+    rd = [int(v - t0) if v else -1 for v in base[2048 + 16 * 60:2048 + 16 * 62]]
+    print("role done per warp", rd[:24], "synced", int(epi[62, 0] - t0) if epi[62, 0] else -1)
+    if epi[63, 10]:
+        print("store warp done (bulk_wait_all)", epi[63, 10] - t0)
 # per-CTA entry / exit (ns, relative to the earliest FC1 entry)
 for name, off in (("FC1", 8192), ("FC2", 8704)):
     cs = t[off:off + 2 * 148].reshape(148, 2)
