@@ -207,6 +207,10 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     constexpr bool HAS_B = (F & kHasB) != 0, HAS_ZC = (F & kHasZc) != 0, ZQNZ = (F & kZqNz) != 0;
     constexpr bool STATS64 = (F & kS64) != 0, SMALLK = (F & kSmallK) != 0;
     constexpr bool IS_LN = (EPI == EP6_LN);
+#ifndef SWIN_LN_PREFETCH
+#define SWIN_LN_PREFETCH 0
+#endif
+    constexpr bool LN_PREFETCH = SWIN_LN_PREFETCH != 0;   // op #6 chunk loop keeps the next tcgen05.ld in flight
     // CTA pair (cta_group::2, M = 256 per MMA): the two CTAs of a cluster take m-tiles
     // 2u and 2u+1 of the same n-group; each loads its A rows and half of the B rows,
     // the leader issues the MMAs (op #5 only: no cross-CTA row statistics)
@@ -620,7 +624,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             };
             // chunk loop; op #5 keeps the next tcgen05.ld in flight while processing
             auto for_chunks = [&](auto&& fn) {
-                if constexpr (IS_LN) {
+                if constexpr (IS_LN && !LN_PREFETCH) {
                     for (int ch = ch_lo; ch < ch_hi; ++ch) {
                         uint32_t ra[16];
                         tmem_ld16(tb + (uint32_t)(ch * kChunk), ra);
@@ -750,7 +754,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             *reinterpret_cast<float4*>(zrow + 4 * j4) =
                                 make_float4(z[2 * j4].x, z[2 * j4].y, z[2 * j4 + 1].x, z[2 * j4 + 1].y);
                     }
-                    tmem_st16(tb + (uint32_t)cl, r);
+                    if (!(p.dbg & 4)) tmem_st16(tb + (uint32_t)cl, r);
                 });
                 tmem_wait_st();
                 if (x_smem) {   // the x tile has been consumed: let the loader prefetch the next one

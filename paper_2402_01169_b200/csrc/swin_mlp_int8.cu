@@ -714,7 +714,8 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }
 
     GemmArgs a2 = {};
-    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.eg = h->p2.eg; a2.xstage = h->p2.xstage; a2.x = x;
+    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.eg = h->p2.eg;
+    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; } a2.xstage = h->p2.xstage; a2.x = x;
     a2.out_w = h->p2.out_w;
     a2.resb = h->p2.resb; a2.mt_major = 1;   // op #6: one n-group per cluster
     a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
