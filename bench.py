@@ -189,12 +189,15 @@ def main():
     # ---- layers: rank 0 generates, weights broadcast once over NCCL --------------------------------
     spec = layers_spec(args.batch, synth.ACT_RELU)
     relu_layers, gelu_layers, xs_dev, xs_host, ys, T_list = [], [], [], [], [], []
+    ft_gelu_layers, ft_relu_layers = [], []   # FasterTransformer layout: op #5 unfused (NEXT-1)
     for li, (L, T, xseed) in enumerate(spec):
         if ws > 1:
             broadcast_layer(L, dev)   # create() copies from the device tensors
         relu_layers.append(SwinMlpInt8Layer(L, device=local))
+        ft_relu_layers.append(SwinMlpInt8Layer(L, device=local, op5_unfused=True))
         L.act = synth.ACT_GELU
         gelu_layers.append(SwinMlpInt8Layer(L, device=local))
+        ft_gelu_layers.append(SwinMlpInt8Layer(L, device=local, op5_unfused=True))
         L.act = synth.ACT_RELU
         X = synth.make_activations(L, T, xseed + 7919 * rank)
         xh = torch.from_numpy(X).pin_memory()
@@ -202,7 +205,7 @@ def main():
         xs_dev.append(xh.to(dev))
         ys.append(torch.empty((T, L.C), dtype=torch.int8, device=dev))
         T_list.append(T)
-    ws_bytes = max(P.swin_mlp_int8_workspace_bytes(l.handle, T) for l, T in zip(relu_layers, T_list))
+    ws_bytes = max(P.swin_mlp_int8_workspace_bytes(l.handle, T) for l, T in zip(ft_gelu_layers, T_list))
     host_ws = max(P.swin_mlp_int8_host_workspace_bytes(l.handle, T, 0) for l, T in zip(relu_layers, T_list))
     workspace = torch.empty(max(ws_bytes, host_ws), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -351,22 +354,34 @@ def main():
     h2d = sum(int(x.numel()) for x in xs_host)
     d2h = sum(int(y.numel()) for y in ys_host)
 
-    # ---- ReLU vs GELU epilogue: interleaved paired trials (SPEC.md:525 style) ---------------------
-    for _ in range(3):
-        step(gelu_layers)
-    relu_us, gelu_us, wins = [], [], 0
+    # ---- ReLU vs GELU: interleaved trials of four arms, order rotated per trial --------------------
+    #   relu     the GELU-less layer, ReLU folded into FC1's drain (the product)
+    #   gelu     the same kernels with the exact-erf GELU epilogue (control)
+    #   gelu_ft  the paper's baseline layout: FC1 -> A1 int32 in HBM -> separate dQ/GELU/Q kernel
+    #            -> FC2 (FasterTransformer)
+    #   relu_ft  the same unfused layout with ReLU (separates the fusion gain from the activation)
+    arms = {"relu": relu_layers, "gelu": gelu_layers, "gelu_ft": ft_gelu_layers, "relu_ft": ft_relu_layers}
+    for layers in arms.values():
+        for _ in range(3):
+            step(layers)
+    samples = {k: [] for k in arms}
+    wins = 0
+    names = list(arms)
     for i in range(args.pairs):
-        order = (relu_layers, gelu_layers) if i % 2 == 0 else (gelu_layers, relu_layers)
         res = {}
-        for layers in order:
-            res[id(layers)] = 1e3 * timed(lambda: step(layers), 1)[0]
-        r, g = res[id(relu_layers)], res[id(gelu_layers)]
-        relu_us.append(r)
-        gelu_us.append(g)
-        wins += r < g
-    relu_gelu = {"relu_us_median": statistics.median(relu_us), "gelu_us_median": statistics.median(gelu_us),
-                 "gelu_over_relu": statistics.median(gelu_us) / statistics.median(relu_us),
-                 "pairs": args.pairs, "relu_wins": wins,
+        for k in names[i % 4:] + names[:i % 4]:
+            res[k] = 1e3 * timed(lambda: step(arms[k]), 1)[0]
+        for k in names:
+            samples[k].append(res[k])
+        wins += res["relu"] < min(res["gelu"], res["gelu_ft"])
+    med = {k: statistics.median(v) for k, v in samples.items()}
+    relu_gelu = {"relu_us_median": med["relu"], "gelu_us_median": med["gelu"],
+                 "gelu_over_relu": med["gelu"] / med["relu"],
+                 "gelu_ft_us_median": med["gelu_ft"], "relu_ft_us_median": med["relu_ft"],
+                 "latency_gain_vs_ft_gelu": 1.0 - med["relu"] / med["gelu_ft"],
+                 "latency_gain_vs_fused_gelu": 1.0 - med["relu"] / med["gelu"],
+                 "paper_context": "RTX 4090, whole Swin model: >= 11% latency gain from GELU->ReLU (PAPER.md:13)",
+                 "pairs": args.pairs, "relu_wins": wins, "b1": "None in every arm (paper mode)",
                  "unit": "us per step (4 layers)"}
 
     # ---- CPU baseline: the oracle as it stands on this host (rank 0, N=1 only) ----------------------

@@ -88,6 +88,15 @@ typedef struct {
                                  *   1: fp64 in the oracle's operation order (Y, yhat bit-exact
                                  *      up to the order of the row sums)
                                  *   0: fp32 (faster; Y within 1 LSB on <= 0.01 % of elements) */
+    int32_t op5_unfused;        /* 0: op #5 fused into FC1's TMEM drain (this design).
+                                 * 1: the paper's FasterTransformer baseline layout (SURVEY.md
+                                 *    §8(f) NEXT-1): FC1 writes the int32
+                                 *    accumulators A1 [T][H] to global memory, a separate
+                                 *    elementwise kernel runs op #5 (dQ -> b1 -> act -> Q) into Hq,
+                                 *    then FC2 + op #6.  Same arithmetic, same results; it exists
+                                 *    to measure on B200 what fusing / deleting op #5 saves.  Uses
+                                 *    the three-kernel plan for every C (the workspace grows by
+                                 *    4*T*H bytes for A1). */
 } swin_mlp_int8_desc_t;
 
 /* Create a layer handle: validates the description, folds the fp32
@@ -98,9 +107,10 @@ typedef struct {
 swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_mlp_int8_t* out);
 
 /* Bytes of caller-provided device workspace `run` needs for T tokens
- * (the int8 hidden tensor Hq, [T][H], 128-byte aligned).  Returns 0 for a
- * NULL handle, T <= 0, or a layer on the one-kernel plan (C <= 256: the hidden
- * tile stays in shared memory; `run` then accepts workspace == NULL). */
+ * (the int8 hidden tensor Hq, [T][H], 128-byte aligned; with desc.op5_unfused
+ * also the int32 A1 [T][H] behind it).  Returns 0 for a NULL handle, T <= 0, or
+ * a layer on the one-kernel plan (C <= 256: the hidden tile stays in shared
+ * memory; `run` then accepts workspace == NULL). */
 size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T);
 
 /* The hot path: Y = layer(X) for T tokens, stream-ordered, asynchronous.
@@ -168,7 +178,8 @@ int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h);
  * and after FC2 on its stream (at most max_runs runs are recorded; later
  * runs are not).  profile_end synchronizes those events, returns the summed
  * FC1+ep5 and FC2+ep6 kernel durations in ms and the number of recorded runs,
- * and stops recording.  Any output pointer may be NULL. */
+ * and stops recording (desc.op5_unfused: the first interval holds FC1 and the
+ * separate op #5 kernel).  Any output pointer may be NULL. */
 swin_mlp_status_t swin_mlp_int8_profile_begin(swin_mlp_int8_t h, int32_t max_runs);
 swin_mlp_status_t swin_mlp_int8_profile_end(swin_mlp_int8_t h, float* fc1_ms, float* fc2_ms, int32_t* runs);
 

@@ -45,6 +45,7 @@ class swin_mlp_int8_desc_t(ctypes.Structure):
         ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
         ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32),
         ("device", ctypes.c_int32), ("ln_fp64", ctypes.c_int32),
+        ("op5_unfused", ctypes.c_int32),
     ]
 
 
@@ -184,7 +185,7 @@ class SwinMlpInt8Layer:
     swin_mlp_int8_desc_t (e.g. synth.Layer); numpy arrays are passed as host
     pointers and copied by swin_mlp_int8_create."""
 
-    def __init__(self, layer, device: int = 0, ln_fp64: bool = False):
+    def __init__(self, layer, device: int = 0, ln_fp64: bool = False, op5_unfused: bool = False):
         import numpy as np
         import torch
         self._keep = []
@@ -210,6 +211,7 @@ class SwinMlpInt8Layer:
         d.y_scale, d.y_zero_point = float(layer.s_y), int(layer.z_y)
         d.device = int(device)
         d.ln_fp64 = int(bool(ln_fp64))
+        d.op5_unfused = int(bool(op5_unfused))   # FT-style baseline: A1 through HBM, separate op #5
         self.C, self.H, self.device = d.C, d.H, device
         self.handle = swin_mlp_int8_create(d)
         self._keep = []

@@ -10,6 +10,10 @@
 //   EP5_GELU  FC1 + fused op #5 with exact-erf GELU (the control the paper removes)
 //   EP6_LN    FC2 + fused op #6: dQ, FC2 bias, residual add, LayerNorm, Q
 //             (trailing Q per DESIGN.md reading R4)
+//   EP_ACC    FC1 alone, the int32 accumulators A1 (zero-point term included) written
+//             to global memory: the FasterTransformer layout the paper starts from,
+//             where op #5 is a separate kernel (SURVEY.md
+//             §8(f) NEXT-1).  Used only by the desc.op5_unfused comparison plan.
 //
 // CTA = 640 threads, 1 per SM, persistent over 128-row tiles (a tile = 128 token
 // rows x BN columns of one GEMM):
@@ -51,7 +55,7 @@
 
 namespace swinmlp {
 
-enum Epi : int { EP5_RELU = 0, EP5_GELU = 1, EP6_LN = 2 };
+enum Epi : int { EP5_RELU = 0, EP5_GELU = 1, EP6_LN = 2, EP_ACC = 3 };
 
 constexpr int kBM = 128;             // rows per tile (UMMA M, TMEM lanes)
 constexpr int kBK = 128;             // K bytes per pipeline stage (one 128-B swizzle row)
@@ -104,6 +108,7 @@ struct GemmArgs {
     unsigned long long* cta_stamps;   // debug: per CTA %globaltimer at entry / exit ([2 * blockIdx.x + {0,1}])
     int32_t dbg;                      // debug experiments (0 in production)
     int32_t eg;                       // op #5 epilogue groups (1: all 16 warps drain every tile; or G)
+    int32_t* acc_out;                 // EP_ACC: [M][ldo] int32 A1 (the unfused plan's GEMM output)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -131,7 +136,7 @@ __host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int s
     L.b = L.a + (uint32_t)stages * kBM * kBK;
     L.bres = L.b + (resb_bytes ? 0u : (uint32_t)stages * (uint32_t)(bn_b ? bn_b : BN) * kBK);
     L.out = L.bres + resb_bytes;                                   // [G] output staging tiles
-    L.xres = L.out + (uint32_t)G * tile;                           // op #6: [G] residual x tiles
+    L.xres = L.out + (epi == EP_ACC ? 0u : (uint32_t)G * tile);   // (EP_ACC stores from registers)                           // op #6: [G] residual x tiles
     L.consts = L.xres + (epi == EP6_LN ? (uint32_t)xstage * tile : 0u);       // [G][kNConst][BN] fp32
     L.bars = L.consts + (uint32_t)G * kNConst * (uint32_t)BN * 4u;
     L.tmem_slot = L.bars + 8u * kNumBars(stages);
@@ -494,7 +499,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int n0 = n0_of(ng);
                 const int32_t row0 = (int32_t)(m_tile * kBM);
                 const uint32_t src = base + L.out + sb * tile_bytes;
-                if (!(p.dbg & 2))
+                if (EPI != EP_ACC && !(p.dbg & 2))
                 for (uint32_t sub = 0; sub < ((uint32_t)BN >> lgW); ++sub)
                     tma_store_2d(&tmO, src + (sub << (lgW + 7u)), n0 + (int)(sub << lgW), row0);
                 bulk_commit();
@@ -648,7 +653,28 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
             };
 
-            if constexpr (!IS_LN) {
+            if constexpr (EPI == EP_ACC) {
+                // A1 = raw dot - z_x * wsum1[n], straight to global (64 contiguous bytes of
+                // this thread's row per chunk): the round trip the unfused plan measures
+                for_chunks([&](uint32_t (&r)[16], int ch) {
+                    const int cl = ch * kChunk;
+                    if constexpr (HAS_ZC) {
+#pragma unroll
+                        for (int j4 = 0; j4 < 4; ++j4) {
+                            const int4 zv = *reinterpret_cast<const int4*>(cm + 2 * BN + cl + 4 * j4);
+                            r[4 * j4 + 0] -= (uint32_t)zv.x; r[4 * j4 + 1] -= (uint32_t)zv.y;
+                            r[4 * j4 + 2] -= (uint32_t)zv.z; r[4 * j4 + 3] -= (uint32_t)zv.w;
+                        }
+                    }
+                    if (valid) {
+                        int32_t* orow = p.acc_out + row * (int64_t)p.ldo + n0 + cl;
+#pragma unroll
+                        for (int j4 = 0; j4 < 4; ++j4)
+                            st_v4(orow + 4 * j4, make_int4((int)r[4 * j4], (int)r[4 * j4 + 1], (int)r[4 * j4 + 2],
+                                                           (int)r[4 * j4 + 3]));
+                    }
+                });
+            } else if constexpr (!IS_LN) {
                 for_chunks([&](uint32_t (&r)[16], int ch) {
                     const int cl = ch * kChunk;
                     float2 y[8];

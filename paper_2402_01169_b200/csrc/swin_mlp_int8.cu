@@ -22,6 +22,7 @@
 #include "../../include/swin_mlp_int8.h"
 #include "mlp_kernels.cuh"
 #include "fused_mlp.cuh"
+#include "op5_unfused.cuh"
 
 using namespace swinmlp;
 
@@ -153,8 +154,24 @@ KernelFn kernel_for(int epi, int flags) {
                                              std::make_integer_sequence<int, 32>{}, true);
         case EP5_GELU: return pick<EP5_GELU>((flags & 7) | ((flags & kSmallK) ? 8 : 0) | ((flags & kPair) ? 16 : 0),
                                              std::make_integer_sequence<int, 32>{}, true);
+        case EP_ACC: {   // the unfused plan's FC1: only the zero-point correction and the pair matter
+            static const KernelFn t[4] = {mlp_gemm_kernel<EP_ACC, 0>, mlp_gemm_kernel<EP_ACC, kHasZc>,
+                                          mlp_gemm_kernel<EP_ACC, kPair>, mlp_gemm_kernel<EP_ACC, kHasZc | kPair>};
+            return t[((flags & kHasZc) ? 1 : 0) | ((flags & kPair) ? 2 : 0)];
+        }
         default: return pick<EP6_LN>(flags & 15, std::make_integer_sequence<int, 16>{}, false);
     }
+}
+
+using Op5Fn = void (*)(Op5Args);
+// The separate op #5 kernel of the unfused plan, specialised like the fused epilogue.
+Op5Fn op5_kernel_for(bool gelu, bool has_b, bool zh) {
+    static const Op5Fn t[8] = {
+        op5_unfused_kernel<false, false, false>, op5_unfused_kernel<false, false, true>,
+        op5_unfused_kernel<false, true, false>,  op5_unfused_kernel<false, true, true>,
+        op5_unfused_kernel<true, false, false>,  op5_unfused_kernel<true, false, true>,
+        op5_unfused_kernel<true, true, false>,   op5_unfused_kernel<true, true, true>};
+    return t[(gelu ? 4 : 0) | (has_b ? 2 : 0) | (zh ? 1 : 0)];
 }
 
 swin_mlp_status_t prepare(Plan& pl, int num_sms) {
@@ -372,6 +389,9 @@ struct swin_mlp_int8_s {
     Plan p1, p2;
     FusedPlan fp;          // one-kernel plan (used when fp.on)
     FusedFn fp_dbg = nullptr;   // its tap-writing variant (run_debug)
+    bool unfused = false;       // desc.op5_unfused: FC1 (EP_ACC) -> op5_fn -> FC2 + op #6
+    Op5Fn op5_fn = nullptr;
+    int op5_grid = 0;
     CUtensorMap tm_fw1, tm_fw2;
     // device copies (handle-owned)
     int8_t *w1 = nullptr, *w2 = nullptr;
@@ -486,6 +506,7 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     if (d.C > 1536 || d.H > 6144) return fail(SWIN_MLP_EUNSUPPORTED, "C=%d H=%d exceed 1536/6144", d.C, d.H);
     if (d.act != SWIN_MLP_ACT_RELU && d.act != SWIN_MLP_ACT_GELU_ERF)
         return fail(SWIN_MLP_EINVAL, "unknown activation %d", (int)d.act);
+    if (d.op5_unfused != 0 && d.op5_unfused != 1) return fail(SWIN_MLP_EINVAL, "op5_unfused=%d must be 0 or 1", d.op5_unfused);
     if (!normal_positive(d.x_scale) || !normal_positive(d.h_scale) || !normal_positive(d.y_scale))
         return fail(SWIN_MLP_EINVAL, "activation scales must be finite, normal and > 0");
     if (!(d.ln_eps > 0.0f) || !std::isfinite(d.ln_eps)) return fail(SWIN_MLP_EINVAL, "ln_eps must be > 0");
@@ -572,7 +593,9 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     }
 
     // tile / cluster plans
-    if (!make_plan(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU, H, C, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
+    h->unfused = d.op5_unfused != 0;
+    const int epi1 = h->unfused ? EP_ACC : d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU;
+    if (!make_plan(epi1, H, C, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
     if (!make_plan(EP6_LN, C, H, true, h->p2, d.ln_fp64 ? 8 : 4))
         return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC2 tile plan for C=%d (needs C = CS*BN, BN%%16==0, BN<=256, CS in 1,2,4,8)", C));
 
@@ -595,14 +618,19 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H, (uint32_t)h->p2.BN));
     // |A1| <= (128 + |z_x|) * 127 * C: below 2^22 the exact magic-number int->float applies
     const bool small_k1 = (int64_t)(128 + std::abs(d.x_zero_point)) * 127 * C < (int64_t(1) << 22);
-    h->p1.fn = kernel_for(d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU,
+    h->p1.fn = kernel_for(epi1,
                           (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (d.h_zero_point ? kZqNz : 0) |
                           (small_k1 ? kSmallK : 0) | (h->p1.pair ? kPair : 0));
     h->p2.fn = kernel_for(EP6_LN, (d.b2 ? kHasB : 0) | (d.h_zero_point ? kHasZc : 0) |
                                       (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0));
     H_TRY(prepare(h->p1, h->num_sms));
     H_TRY(prepare(h->p2, h->num_sms));
-    if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp)) {
+    if (h->unfused) {
+        h->op5_fn = op5_kernel_for(d.act == SWIN_MLP_ACT_GELU_ERF, d.b1 != nullptr, d.h_zero_point != 0);
+        int per_sm = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->op5_fn, kOp5Threads, 0));
+        h->op5_grid = std::max(1, per_sm) * h->num_sms;   // persistent grid-stride: whole waves
+    } else if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp)) {
         const int ff = (d.act == SWIN_MLP_ACT_GELU_ERF ? kFGelu : 0) | (d.h_zero_point ? kFZh : 0) |
                        (d.b1 ? kFB1 : 0) | (d.ln_fp64 ? kFS64 : 0) | (small_k1 ? kFSmallK : 0);
         h->fp.fn = fused_kernel_for(ff);
@@ -620,7 +648,8 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
 size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T) {
     if (!h || T <= 0) return 0;
     if (h->fp.on) return 0;   // one kernel: the hidden tile never leaves the SM
-    return (size_t)(((T * h->d.H) + 127) / 128 * 128);
+    const size_t hq = (size_t)(((T * h->d.H) + 127) / 128 * 128);
+    return h->unfused ? hq + (size_t)T * h->d.H * 4 : hq;   // unfused plan: + A1 int32 [T][H]
 }
 
 static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const float* residual, int8_t* y,
@@ -709,6 +738,8 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a1.eg = h->p1.eg; a1.ldo = H;
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
     a1.acc_tap = dbg ? acc1 : nullptr;
+    int32_t* a1ws = h->unfused ? reinterpret_cast<int32_t*>(hq + ((T * H + 127) / 128 * 128)) : nullptr;
+    a1.acc_out = a1ws;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
     a1.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
     { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }
@@ -731,6 +762,23 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
     ST_TRY(launch(h->p1, tm_x, h->tm_w1, tm_ho, tm_ho, a1, s));
+    if (h->unfused) {   // the separate op #5 kernel (PDL-chained like the GEMMs)
+        if (dbg && acc1) CUDA_TRY(cudaMemcpyAsync(acc1, a1ws, (size_t)T * H * 4, cudaMemcpyDeviceToDevice, s));
+        Op5Args o = {};
+        o.a1 = a1ws; o.hq = hq; o.m1 = h->m1; o.b1 = h->b1; o.inv_h = h->inv_h; o.z_h = h->d.h_zero_point;
+        o.H = H; o.quads = T * (int64_t)H / 4;
+        cudaLaunchConfig_t cfg = {};
+        const int64_t need = (o.quads + kOp5Threads * kOp5Unroll - 1) / (kOp5Threads * kOp5Unroll);
+        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, h->op5_grid)));
+        cfg.blockDim = dim3((unsigned)kOp5Threads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, h->op5_fn, o));
+    }
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
     if (dbg && hidden) CUDA_TRY(cudaMemcpyAsync(hidden, hq, (size_t)T * H, cudaMemcpyDeviceToDevice, s));
     ST_TRY(launch(h->p2, tm_h, h->tm_w2, tm_y, tm_xr, a2, s));
@@ -954,7 +1002,7 @@ swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_
     return SWIN_MLP_OK;
 }
 
-int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h) { return h ? (h->fp.on ? 1 : 2) : 0; }
+int32_t swin_mlp_int8_launches_per_run(swin_mlp_int8_t h) { return h ? (h->fp.on ? 1 : h->unfused ? 3 : 2) : 0; }
 
 swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
     if (!h) return SWIN_MLP_OK;

@@ -52,7 +52,12 @@ def test_sm100a_code_only():
     assert len(funcs) >= 16
     for f in funcs:
         name = f.split()[0]
-        assert "UTCIMMA" in f and "LDTM" in f and "UTMASTG" in f, name
+        if "op5_unfused_kernel" in name:   # the unfused plan's elementwise op #5 (NEXT-1)
+            assert "LDG" in f and "STG" in f and "F2I" in f, name
+        elif "mlp_gemm_kernelILi3E" in name:   # EP_ACC: FC1 storing int32 A1 from registers
+            assert "UTCIMMA" in f and "LDTM" in f and "STG" in f, name
+        else:
+            assert "UTCIMMA" in f and "LDTM" in f and "UTMASTG" in f, name
 
 
 def _desc(P, **kw):

@@ -48,11 +48,11 @@ def _tier_yhat(got, ref, what="yhat"):
     assert (err <= tol).all(), f"{what}: max rel err {(err / tol).max() * 1e-5:.3e}"
 
 
-def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True, ln_fp64=False):
+def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True, ln_fp64=False, op5_unfused=False):
     from paper_2402_01169_b200 import SwinMlpInt8Layer
     X = synth.make_activations(L, T, x_seed)
     R = synth.make_residual(T, L.C, x_seed + 1) if resid else None
-    layer = SwinMlpInt8Layer(L, device=0, ln_fp64=ln_fp64)
+    layer = SwinMlpInt8Layer(L, device=0, ln_fp64=ln_fp64, op5_unfused=op5_unfused)
     xd = torch.from_numpy(X).to(dev)
     rd = torch.from_numpy(R).to(dev) if resid else None
     zo = torch.empty((T, L.C), dtype=torch.float32, device=dev)
@@ -123,6 +123,34 @@ def test_parity_fp32_residual(dev, C, T):
 def test_parity_tile_edges(dev, T):
     """Ragged token tails around the 128-row tile."""
     _run_and_check(dev, _layer(192, 5000), T)
+
+
+@pytest.mark.parametrize("C,T,act,bias,zx,zh", [
+    (96, 1000, 0, False, 0, 0), (192, 257, 1, True, 0, 0), (384, 200, 0, True, -7, 0),
+    (768, 131, 1, False, 0, -128), (256, 129, 0, False, 5, -7), (1536, 129, 0, False, 0, 0)])
+def test_parity_op5_unfused(dev, C, T, act, bias, zx, zh):
+    """SURVEY.md §8(f) NEXT-1, the FasterTransformer layout: FC1
+    writes A1 to HBM and op #5 runs as a separate kernel.  Same arithmetic: A1, Hq (ReLU), A2, z
+    bit-exact; GELU Hq and Y within the tiers."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(C, 6000 + C, act=act, bias=bias, zx=zx, zh=zh)
+    _run_and_check(dev, L, T, op5_unfused=True)
+    assert SwinMlpInt8Layer(L, device=0, op5_unfused=True).plan()["fused"] == 0
+
+
+def test_op5_unfused_matches_fused_plan(dev):
+    """Same Y from the unfused (3-kernel) and the production plan on the same inputs (fp64 LN:
+    the one-kernel and two-kernel plans order their fp32 row statistics differently)."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer, lib
+    for C, T, act in ((96, 3000, 0), (384, 1000, 0), (192, 700, 1)):
+        L = _layer(C, 6100 + C, act=act)
+        x = torch.from_numpy(synth.make_activations(L, T, 9)).to(dev)
+        a = SwinMlpInt8Layer(L, device=0, ln_fp64=True)
+        b = SwinMlpInt8Layer(L, device=0, ln_fp64=True, op5_unfused=True)
+        ya, yb = a(x), b(x)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+        assert lib().swin_mlp_int8_launches_per_run(b.handle) == 3
 
 
 def test_t_zero_is_noop(dev):
