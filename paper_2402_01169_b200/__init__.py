@@ -232,11 +232,12 @@ class SwinMlpInt8Layer:
         lib().swin_mlp_int8_plan(self.handle, out)
         if out[12]:
             return {"fused": 1, "stages": out[13], "hq_buffers": out[14], "acc1_buffers": out[15],
+                    "x_slots": out[17], "w2_stages": out[18],
                     "weights": "resident" if out[13] == 0 else "streamed"}
         return {"fused": 0, "fc1_bn": out[0], "fc1_cs": out[1], "fc1_stages": out[2], "fc1_max_clusters": out[3],
                 "fc2_bn": out[4], "fc2_cs": out[5], "fc2_stages": out[6], "fc2_max_clusters": out[7],
                 "fc1_groups": out[8], "fc2_groups": out[9], "fc1_resb": out[10], "fc2_resb": out[11],
-                "fc1_pair": out[16]}
+                "fc1_pair": out[16], "op5_unfused": out[19]}
 
     def set_trace(self, buf=None, cta=0):
         """buf: int64 device tensor of >= 9216 elements (see swin_mlp_int8_set_trace), or None."""

@@ -6,7 +6,7 @@
 #include "fused_mlp.cuh"
 
 #ifndef FUSED_PART
-#error "compile with -DFUSED_PART=<0..3>"
+#error "compile with -DFUSED_PART=<0..5>"
 #endif
 
 namespace swinmlp {

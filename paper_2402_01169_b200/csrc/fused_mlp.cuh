@@ -1,4 +1,4 @@
-// fused_mlp.cuh — the whole MLP sub-layer in ONE sm_100a kernel for C <= 256:
+// fused_mlp.cuh — the whole MLP sub-layer in ONE sm_100a kernel for C <= 384:
 // FC1 -> op #5 -> FC2 -> op #6 per 128-token tile, with the hidden activation
 // Hq never leaving the SM.
 //
@@ -27,19 +27,23 @@
 //   warps 4-11   op #5: warp = (lane quadrant, 64-column half) of each acc1 chunk
 //   warps 12-19  op #6: warp = (lane quadrant, column half); a thread owns half a
 //                token row, the two halves combine their statistics pairwise
+//   warp 20      streamed weights: the W2 ring (its own warp, so the W1 items of the
+//                next chunks never queue behind a W2 slot still held by FC2)
 #pragma once
 #include "mlp_kernels.cuh"
 
 namespace swinmlp {
 
 constexpr int kFEp5W0 = 4, kFEp6W0 = 12;
-constexpr int kFThreads = 32 * 20;          // 4 control + 8 op #5 + 8 op #6 warps (96 regs each)
+constexpr int kFW2Warp = 20;                 // streamed W2 producer
+constexpr int kFThreads = 32 * 21;          // 4 control + 8 op #5 + 8 op #6 + 1 W2 producer (96 regs each)
 constexpr int kFHc = 128;                    // hidden chunk = one 128-B K-block of FC2
 constexpr int kFMaxNB1 = 3, kFMaxNH = 4, kFMaxStages = 8;
 constexpr uint32_t kKB = (uint32_t)kBM * kBK;   // one [128 rows][128 B] box
 // flags
 constexpr int kFGelu = 1, kFZh = 2, kFB1 = 4, kFS64 = 8, kFSmallK = 16, kFTaps = 32;
-constexpr int kFNumVariants = 64;
+constexpr int kFReg = 64;   // op #6 register path (C <= 32 * kFRegCh; not with kFS64 / kFTaps)
+constexpr int kFNumVariants = 96;   // flags 0..95 (kFReg only without kFTaps)
 
 struct FusedArgs {
     int64_t M;          // tokens
@@ -49,7 +53,8 @@ struct FusedArgs {
     int32_t NB1;        // acc1 TMEM buffers (128 columns each)
     int32_t NH;         // Hq smem buffers
     int32_t stages;     // W1 ring depth (16 KB K-block items); 0 = W1 and W2 resident in smem
-    int32_t stages2;    // W2 ring depth ([C rows][128 B] chunk items), streamed mode
+    int32_t stages2;    // W2 ring depth, streamed mode: items of [C rows][128 B] (one per chunk),
+                        // or of [C/2 rows][128 B] when C > 256 (two per chunk, one per FC2 MMA half)
     int32_t a1_col;     // TMEM column of acc1 buffer 0 (acc2 buffers live below it)
     int32_t NA2;        // acc2 TMEM buffers (2: op #6 of tile i overlaps FC2 of tile i + 1)
     int32_t NX;         // X tile slots (2..4)
@@ -79,6 +84,10 @@ struct FusedLayout {
     uint32_t x, y, hq, w, w2, consts, red, bars, tmem_slot, total;
 };
 constexpr int kFMaxNX = 4;
+// op #6 holds a thread's whole half row in registers when it has at most this many
+// 16-column chunks (C <= 128): acc2 is released right after its TMEM loads and z is
+// never parked back in TMEM (no tcgen05.st / second tcgen05.ld per value)
+constexpr int kFRegCh = 3;
 constexpr int kFMaxStages2 = 4;
 constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 2 * kFMaxStages2 + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1;
 
@@ -95,7 +104,7 @@ __host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int st
         L.consts = L.w2 + nj * (uint32_t)C * kBK;
     } else {   // two rings: W1 K-blocks, W2 chunks (each consumed in its own order)
         L.w2 = L.w + (uint32_t)stages * kKB;
-        L.consts = L.w2 + (uint32_t)stages2 * (uint32_t)C * kBK;
+        L.consts = L.w2 + (uint32_t)stages2 * (uint32_t)(C > 256 ? C / 2 : C) * kBK;
     }
     L.red = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
     L.red = (L.red + 15u) & ~15u;
@@ -114,6 +123,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     constexpr bool GELU = (F & kFGelu) != 0, ZH = (F & kFZh) != 0, B1 = (F & kFB1) != 0;
     constexpr bool TAPS = (F & kFTaps) != 0;   // debug taps compiled in (run_debug only)
     constexpr bool STATS64 = (F & kFS64) != 0, SMALLK = (F & kFSmallK) != 0;
+    constexpr bool REG = (F & kFReg) != 0 && !STATS64 && !TAPS;   // op #6 half rows in registers
     using acc_t = typename std::conditional<STATS64, double, float>::type;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -209,14 +219,24 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t cid = blockIdx.x, grid = gridDim.x;
     const uint32_t n_my = cid < m_tiles ? (m_tiles - cid + grid - 1) / grid : 0u;
     const uint32_t U = n_my * NJ;                 // hidden chunks this CTA processes
-    // FC1 lookahead (chunks): LA <= NB1 - 1 keeps every wait satisfiable by earlier
-    // work; LA <= NJ keeps the producer's X-slot wait behind the W2 loads it depends on
-    const uint32_t LA = min(NB1 - 1u, NJ);
     auto row0_of = [&](uint32_t i) -> int32_t { return (int32_t)((cid + i * grid) * kBM); };
+    // Hidden-chunk order rotated per CTA: position jj of a tile is chunk (jj + rot) mod NJ.
+    // FC2 sums exact int32 partial products, so the order changes no result; it spreads
+    // the CTAs' streamed weight reads over different chunks (different L2 lines) instead
+    // of every SM requesting the same chunk at the same time.
+    const uint32_t rot = cid % NJ;
+    auto chunk_of = [&](uint32_t jj) -> uint32_t { const uint32_t c = jj + rot; return c >= NJ ? c - NJ : c; };
 
     if (warp == 0) {
         // ============================ TMA producer ============================
-        uint32_t s = 0, ph = 0, s2 = 0, ph2 = 0;
+        uint32_t s = 0, ph = 0;
+        // a W2 chunk [C rows][128 B]: one box, or two of C/2 rows when C > 256 (TMA boxes
+        // span at most 256 rows; FC2 then runs as two N = C/2 MMAs)
+        const uint32_t w2rows = C > 256 ? (uint32_t)C / 2u : (uint32_t)C;
+        auto load_w2 = [&](uint32_t dst, uint32_t bar, uint32_t j) {
+            tma_load_2d(&tmW2, dst, bar, (int)(j * kFHc), 0);
+            if (C > 256) tma_load_2d(&tmW2, dst + w2rows * kBK, bar, (int)(j * kFHc), (int)w2rows);
+        };
         auto load_w1 = [&](uint32_t j, uint32_t dst, uint32_t bar) {
             for (uint32_t kb = 0; kb < KBC; ++kb)
                 tma_load_2d(&tmW1, dst + kb * kKB, bar, (int)(kb * kBK), (int)(j * kFHc));
@@ -226,17 +246,17 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 mbar_arrive_expect_tx(bar_wres, NJ * (KBC * kKB + (uint32_t)C * kBK));
                 for (uint32_t j = 0; j < NJ; ++j) {
                     load_w1(j, sW + j * KBC * kKB, bar_wres);
-                    tma_load_2d(&tmW2, sW2 + j * (uint32_t)C * kBK, bar_wres, (int)(j * kFHc), 0);
+                    load_w2(sW2 + j * (uint32_t)C * kBK, bar_wres, j);
                 }
             }
             __syncwarp();
         }
         pdl_wait();   // X: produced by the previous kernel
         // cursors advance incrementally (no runtime division in the role loops)
-        uint32_t i = 0, j = 0, j2 = 0;     // FC1 tile / chunk of q; FC2 chunk of q - LA
+        uint32_t i = 0, j = 0;             // FC1 tile / chunk of q
         uint32_t xs = 0, xph = 0;          // X slot of tile i, its phase
-        for (uint32_t q = 0; q < U + LA; ++q) {
-            if (q < U) {                       // operands of FC1(q)
+        for (uint32_t q = 0; q < U; ++q) {
+            {                                  // operands of FC1(q) (W2: warp kFW2Warp)
                 if (j == 0) {
                     mbar_wait(bar_xempty + 8u * xs, xph ^ 1u);
                     if (elect_one()) {
@@ -252,7 +272,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                         mbar_wait(bar_wempty + 8u * s, ph ^ 1u);
                         if (elect_one()) {
                             mbar_arrive_expect_tx(bar_wfull + 8u * s, kKB);
-                            tma_load_2d(&tmW1, sW + s * kKB, bar_wfull + 8u * s, (int)(kb * kBK), (int)(j * kFHc));
+                            tma_load_2d(&tmW1, sW + s * kKB, bar_wfull + 8u * s, (int)(kb * kBK),
+                                        (int)(chunk_of(j) * kFHc));
                         }
                         __syncwarp();
                         if (++s == stages) { s = 0; ph ^= 1u; }
@@ -264,12 +285,20 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     if (++xs == NX) { xs = 0; xph ^= 1u; }
                 }
             }
-            if (q >= LA) {                     // operands of FC2(q - LA)
-                if (!resident) {
+        }
+    } else if (warp == (uint32_t)kFW2Warp) {
+        // ====================== W2 producer (streamed weights) ======================
+        if (!resident) {
+            const uint32_t w2rows = C > 256 ? (uint32_t)C / 2u : (uint32_t)C;
+            const uint32_t w2items = C > 256 ? 2u : 1u;
+            uint32_t s2 = 0, ph2 = 0, j2 = 0;
+            for (uint32_t u = 0; u < U; ++u) {   // operands of FC2(u), in FC2's order
+                for (uint32_t h = 0; h < w2items; ++h) {   // one ring item per FC2 MMA half
                     mbar_wait(bar_w2empty + 8u * s2, ph2 ^ 1u);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(bar_w2full + 8u * s2, (uint32_t)C * kBK);
-                        tma_load_2d(&tmW2, sW2 + s2 * (uint32_t)C * kBK, bar_w2full + 8u * s2, (int)(j2 * kFHc), 0);
+                        mbar_arrive_expect_tx(bar_w2full + 8u * s2, w2rows * kBK);
+                        tma_load_2d(&tmW2, sW2 + s2 * w2rows * kBK, bar_w2full + 8u * s2, (int)(chunk_of(j2) * kFHc),
+                                    (int)(h * w2rows));
                     }
                     __syncwarp();
                     if (++s2 == stages2) { s2 = 0; ph2 ^= 1u; }
@@ -306,7 +335,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 if (trc && lane == 0 && q < 512 && kb + 1 == KBC) trc[7680 + q] = gtimer();   // weights in
                 tc_fence_after();
                 const uint64_t ad = ad0 + kb * kb16;
-                const uint64_t bd = resident ? dW + (j * KBC + kb) * kb16 : dW + s * stage16;
+                const uint64_t bd = resident ? dW + (chunk_of(j) * KBC + kb) * kb16 : dW + s * stage16;
                 const int nk = kb + 1u == KBC ? nk_last : 4;
                 if (elect_one()) {
                     mma_i8(d, ad, bd, idesc1, kb);
@@ -369,7 +398,10 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         mbar_arrive(bar_cfull);
 
         // ============================ FC2 issuer ==============================
-        const uint32_t idesc2 = idesc_i8(kBM, (uint32_t)C);
+        const uint32_t n2 = C > 256 ? (uint32_t)C / 2u : (uint32_t)C;   // N per FC2 MMA (<= 256)
+        const uint32_t idesc2 = idesc_i8(kBM, n2);
+        const uint32_t n2off16 = (n2 * kBK) >> 4;                        // bytes/16 of N2 B rows
+        const uint32_t w2n = C > 256 ? 2u : 1u;
         const uint64_t dW2 = umma_desc_k128(sW2), dHq = umma_desc_k128(sHq);
         const uint32_t w2c16 = ((uint32_t)C * kBK) >> 4, kb16 = kKB >> 4;
         uint32_t s2 = 0, ph2 = 0;
@@ -379,24 +411,32 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             if (trc && lane == 0 && u < 512) trc[6656 + u] = gtimer();
             mbar_wait(bar_hqfull + 8u * hb, hph);
             if (j2 == 0) mbar_wait(bar_a2empty + 8u * ab, aph ^ 1u);
-            if (!resident) mbar_wait(bar_w2full + 8u * s2, ph2);
             if (trc && lane == 0 && u < 512) trc[7168 + u] = gtimer();
-            tc_fence_after();
             const uint64_t ad = dHq + hb * kb16;
-            const uint64_t bd = dW2 + (resident ? j2 : s2) * w2c16;
             const uint32_t d2 = tmem_base + ab * (uint32_t)p.a2_stride;
+            // C > 256: two MMA halves of N = C/2 (W2 rows [h C/2, (h+1) C/2) -> TMEM columns
+            // h C/2 ..), each on its own streamed ring item
+            for (uint32_t h = 0; h < w2n; ++h) {
+                if (!resident) mbar_wait(bar_w2full + 8u * s2, ph2);
+                tc_fence_after();
+                const uint64_t bd = resident ? dW2 + chunk_of(j2) * w2c16 + h * n2off16 : dW2 + s2 * n2off16;
+                const uint32_t dh = d2 + h * n2;
+                if (elect_one()) {
+                    mma_i8(dh, ad, bd, idesc2, j2);
+                    mma_i8(dh, ad + 2u, bd + 2u, idesc2, 1u);
+                    mma_i8(dh, ad + 4u, bd + 4u, idesc2, 1u);
+                    mma_i8(dh, ad + 6u, bd + 6u, idesc2, 1u);
+                    if (!resident) mma_commit(bar_w2empty + 8u * s2);
+                }
+                __syncwarp();
+                if (!resident && ++s2 == stages2) { s2 = 0; ph2 ^= 1u; }
+            }
             if (elect_one()) {
-                mma_i8(d2, ad, bd, idesc2, j2);
-                mma_i8(d2, ad + 2u, bd + 2u, idesc2, 1u);
-                mma_i8(d2, ad + 4u, bd + 4u, idesc2, 1u);
-                mma_i8(d2, ad + 6u, bd + 6u, idesc2, 1u);
-                if (!resident) mma_commit(bar_w2empty + 8u * s2);
                 mma_commit(bar_hqempty + 8u * hb);
                 if (j2 + 1u == NJ) mma_commit(bar_a2full + 8u * ab);
                 if (trc && u < 512) trc[512 + u] = gtimer();
             }
             __syncwarp();
-            if (!resident && ++s2 == stages2) { s2 = 0; ph2 ^= 1u; }
             if (++j2 == NJ) {
                 j2 = 0;
                 if (++ab == (uint32_t)p.NA2) { ab = 0; aph ^= 1u; }
@@ -426,7 +466,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             const bool valid = row < p.M;
             const uint32_t tb = tmem_base + ((quad * 32u) << 16) + (uint32_t)p.a1_col + b * (uint32_t)kFHc + half * 64u;
             const uint32_t hq = sHq + hb * kKB + row_off;
-            const int n_base = (int)(j * kFHc + half * 64u);
+            const int n_base = (int)(chunk_of(j) * kFHc + half * 64u);
             auto chunk_t = [&](auto zx0_c, uint32_t (&r)[16], int ch) {
                 constexpr bool ZX0 = decltype(zx0_c)::value;   // z_x == 0: plain I2FP, no correction
                 const int n0 = n_base + ch * 16;
@@ -549,6 +589,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             const uint32_t kb = (uint32_t)c >> 7, g = ((uint32_t)c >> 4) & 7u;
             return kb * kKB + row_off + ((g ^ rsw) << 4);
         };
+        constexpr bool regpath = REG;   // (host: only when nch <= kFRegCh)
         pdl_wait();   // (global residual, residual_out, taps)
         mbar_wait(bar_cfull, 0);
         uint32_t ab = 0, aph = 0, xs = 0, xph = 0;
@@ -717,9 +758,43 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     park(za, ra, ch * 16);
                 }
             };
-            if (p.resid) pass1(std::true_type{});
-            else pass1(std::false_type{});
-            tmem_wait_st();
+            // register path: all of this half row's A2 chunks in one batch of TMEM loads,
+            // acc2 released at once (FC2 of the next tile may start), z kept in registers
+            uint32_t r[REG ? kFRegCh : 1][16];   // A2, then z (fp32 bits) in place
+            auto pass1_reg = [&](auto resid_c) {
+#pragma unroll
+                for (int ch = 0; ch < (REG ? kFRegCh : 1); ++ch)
+                    if (ch < nch) tmem_ld16(tb + (uint32_t)(ch * 16), r[ch]);
+                tmem_wait_ld_dep(r[0]);
+#pragma unroll
+                for (int ch = 1; ch < (REG ? kFRegCh : 1); ++ch) reg_fence16(r[ch]);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_a2empty + 8u * ab);   // acc2 drained
+#pragma unroll
+                for (int ch = 0; ch < (REG ? kFRegCh : 1); ++ch) {
+                    if (ch < nch) {
+                        float2 z[8];
+                        chunk_z(resid_c, r[ch], cb + ch * 16, z);
+                        if (ch == 0) set_shift(z);
+                        stats(z);
+                        store_z(z, cb + ch * 16);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            r[ch][2 * j] = __float_as_uint(z[j].x);
+                            r[ch][2 * j + 1] = __float_as_uint(z[j].y);
+                        }
+                    }
+                }
+            };
+            if constexpr (regpath) {
+                if (p.resid) pass1_reg(std::true_type{});
+                else pass1_reg(std::false_type{});
+            } else {
+                if (p.resid) pass1(std::true_type{});
+                else pass1(std::false_type{});
+                tmem_wait_st();
+            }
             __syncwarp();
             if (lane == 0 && !yin) mbar_arrive(bar_xempty + 8u * xs);   // X tile consumed
             if (stamp) trc[4096 + 4 * i + 2] = gtimer();
@@ -762,7 +837,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             // buffer once the previous tile's stores have read it
             if (!yin) mbar_wait_backoff(bar_yempty, (i & 1u) ^ 1u);
             const uint32_t sYt = yin ? xt : sY;   // Y staging: own X slot, or the Y buffer
-            for_chunks([&](uint32_t (&r)[16], int ch) {
+            auto ln_chunk = [&](const uint32_t (&r)[16], int ch) {
                 const int c0 = cb + ch * 16;
                 float v[16];
 #pragma unroll
@@ -795,12 +870,19 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 if (p.z_y) quant_pack16<false, true>(v, p.z_y, w);
                 else quant_pack16<false, false>(v, 0, w);
                 st_shared_v4(sYt + goff(c0), w[0], w[1], w[2], w[3]);
-            });
+            };
+            if constexpr (regpath) {
+#pragma unroll
+                for (int ch = 0; ch < (REG ? kFRegCh : 1); ++ch)
+                    if (ch < nch) ln_chunk(r[ch], ch);
+            } else {
+                for_chunks([&](uint32_t (&r)[16], int ch) { ln_chunk(r, ch); });
+            }
             tc_fence_before();
             fence_proxy_async_smem();          // Y visible to the TMA store
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(bar_a2empty + 8u * ab);
+                if (!regpath) mbar_arrive(bar_a2empty + 8u * ab);
                 mbar_arrive(bar_yfull);
             }
             if (stamp) trc[4096 + 4 * i + 3] = gtimer();

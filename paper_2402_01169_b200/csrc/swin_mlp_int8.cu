@@ -28,16 +28,20 @@ using namespace swinmlp;
 
 namespace swinmlp {
 using FusedFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, FusedArgs);
-FusedFn fused_kernel_part0(int flags);   // fused_mlp.cu, -DFUSED_PART=0..3
+FusedFn fused_kernel_part0(int flags);   // fused_mlp.cu, -DFUSED_PART=0..5 (flags >> 4)
 FusedFn fused_kernel_part1(int flags);
 FusedFn fused_kernel_part2(int flags);
 FusedFn fused_kernel_part3(int flags);
+FusedFn fused_kernel_part4(int flags);
+FusedFn fused_kernel_part5(int flags);
 inline FusedFn fused_kernel_for(int flags) {
-    switch ((flags >> 4) & 3) {
+    switch (flags >> 4) {
         case 0: return fused_kernel_part0(flags);
         case 1: return fused_kernel_part1(flags);
         case 2: return fused_kernel_part2(flags);
-        default: return fused_kernel_part3(flags);
+        case 3: return fused_kernel_part3(flags);
+        case 4: return fused_kernel_part4(flags);
+        default: return fused_kernel_part5(flags);
     }
 }
 }  // namespace swinmlp
@@ -311,7 +315,7 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
     fp = FusedPlan();
     const char* no = std::getenv("SWIN_MLP_NO_FUSED");   // A/B switch (read per create)
     if (no && *no && *no != '0') return false;
-    if (C > 256 || H % kFHc) return false;
+    if (C > 384 || H % kFHc) return false;
     fp.KBC = (C + kBK - 1) / kBK;
     fp.NJ = H / kFHc;
     // TMEM (512 columns): acc2 buffers, then 128-column acc1 buffers.  C <= 128: two of
@@ -319,8 +323,12 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
     //   C <= 128:  2 acc2 (128-column stride) + 2 acc1
     //   C <= 256:  1 acc2 + 2 acc1 (measured: 2 acc2 + 1 acc1 at C = 192 is slower, the
     //              single acc1 serialises FC1 and op #5)
+    //   C <= 384:  1 acc2 + 1 acc1 (FC1 of chunk j+1 waits for op #5 to drain chunk j; at
+    //              C = 384 the alternative is the two-kernel plan, whose GEMM tiles are
+    //              bound by operand ingest and an exposed LayerNorm drain)
     if (C <= 128) { fp.NA2 = 2; fp.a2_stride = 128; fp.a1_col = 256; }
-    else { fp.NA2 = 1; fp.a2_stride = 0; fp.a1_col = 256; }
+    else if (C <= 256) { fp.NA2 = 1; fp.a2_stride = 0; fp.a1_col = 256; }
+    else { fp.NA2 = 1; fp.a2_stride = 0; fp.a1_col = 384; }
     fp.NB1 = (512 - fp.a1_col) / kFHc;
     // resident weights first (X slots 4..2, Hq buffers 3..2), else a weight ring
     for (int nx : {4, 3, 2}) {
@@ -338,15 +346,18 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
     // multicasting the weight items, or W2 split in two items, did not help)
     const char* yie = std::getenv("SWIN_MLP_FUSED_YIN");
     const int yin = (yie && *yie == '0') ? 0 : 1;
-    for (int st2 : {2, 1}) {
-        for (int st = kFMaxStages; st >= 2 * fp.KBC; --st) {
-            const uint32_t need = fused_layout(C, H, 2, st, ebytes, 2, yin, st2).total + 1024;
+    // C > 256: one X slot (a CTA gets about one tile) so the weight rings get the smem
+    for (int nx : {C > 256 ? 1 : 2, C > 256 ? 2 : 1}) {
+    for (int st2 : {2, 1}) {   // (C > 256: half-chunk W2 items, 2 = one chunk)
+        for (int st = kFMaxStages; st >= (fp.NB1 > 1 ? 2 * fp.KBC : 2); --st) {
+            const uint32_t need = fused_layout(C, H, 2, st, ebytes, nx, yin, st2).total + 1024;
             if (need <= kSmemBudget) {
-                fp.NX = 2; fp.NH = 2; fp.stages = st; fp.stages2 = st2; fp.smem = need; fp.on = true;
+                fp.NX = nx; fp.NH = 2; fp.stages = st; fp.stages2 = st2; fp.smem = need; fp.on = true;
                 fp.y_inplace = yin;
                 return true;
             }
         }
+    }
     }
     return false;
 }
@@ -633,10 +644,14 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     } else if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp)) {
         const int ff = (d.act == SWIN_MLP_ACT_GELU_ERF ? kFGelu : 0) | (d.h_zero_point ? kFZh : 0) |
                        (d.b1 ? kFB1 : 0) | (d.ln_fp64 ? kFS64 : 0) | (small_k1 ? kFSmallK : 0);
-        h->fp.fn = fused_kernel_for(ff);
+        // op #6 register path when a thread's half row is at most kFRegCh chunks of 16
+        // (SWIN_MLP_FUSED_REG=0 disables: A/B switch)
+        static const char* re = std::getenv("SWIN_MLP_FUSED_REG");
+        const bool reg = !(re && *re == '0') && !d.ln_fp64 && C / 2 <= 16 * kFRegCh;
+        h->fp.fn = fused_kernel_for(ff | (reg ? kFReg : 0));
         h->fp_dbg = fused_kernel_for(ff | kFTaps);
         H_TRY(encode_2d(&h->tm_fw1, h->w1, H, C, C, (uint32_t)kFHc));
-        H_TRY(encode_2d(&h->tm_fw2, h->w2, C, H, H, (uint32_t)C));
+        H_TRY(encode_2d(&h->tm_fw2, h->w2, C, H, H, (uint32_t)(C > 256 ? C / 2 : C)));
         CUDA_TRY(cudaFuncSetAttribute(h->fp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
         CUDA_TRY(cudaFuncSetAttribute(h->fp_dbg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
     }
@@ -1021,7 +1036,7 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
     out10[8] = h->p1.G; out10[9] = h->p2.G;
     out10[10] = h->p1.resb; out10[11] = h->p2.resb;
     out10[12] = h->fp.on ? 1 : 0; out10[13] = h->fp.stages; out10[14] = h->fp.NH; out10[15] = h->fp.NB1;
-    out10[16] = h->p1.pair; out10[17] = out10[18] = out10[19] = 0;
+    out10[16] = h->p1.pair; out10[17] = h->fp.NX; out10[18] = h->fp.stages2; out10[19] = h->unfused ? 1 : 0;
     return 0;
 }
 

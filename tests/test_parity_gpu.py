@@ -301,7 +301,7 @@ def test_parity_extreme_accumulators(dev, C):
 
 # ---- one-kernel plan (fused_mlp.cuh, C <= 256) vs the two-kernel plan ---------------------------
 
-@pytest.mark.parametrize("C,fused", [(96, 1), (128, 1), (192, 1), (256, 1), (384, 0), (768, 0)])
+@pytest.mark.parametrize("C,fused", [(96, 1), (128, 1), (192, 1), (256, 1), (384, 1), (512, 0), (768, 0)])
 def test_plan_selection(dev, C, fused, monkeypatch):
     from paper_2402_01169_b200 import SwinMlpInt8Layer
     L = _layer(C, 7000 + C)
@@ -310,7 +310,7 @@ def test_plan_selection(dev, C, fused, monkeypatch):
     assert SwinMlpInt8Layer(L, device=0).plan()["fused"] == 0
 
 
-@pytest.mark.parametrize("C,T", [(96, 1000), (192, 257), (256, 129)])
+@pytest.mark.parametrize("C,T", [(96, 1000), (192, 257), (256, 129), (384, 200)])
 def test_two_kernel_plan_small_c(dev, C, T, monkeypatch):
     """The two-kernel plan stays correct for the channel counts the one-kernel plan now takes."""
     monkeypatch.setenv("SWIN_MLP_NO_FUSED", "1")
@@ -318,14 +318,15 @@ def test_two_kernel_plan_small_c(dev, C, T, monkeypatch):
     _run_and_check(dev, _layer(C, 3000 + C, bias=True, zx=-5, zh=-128, zy=2), T)
 
 
-@pytest.mark.parametrize("C,T", [(96, 148 * 128 * 2 + 77), (192, 148 * 128 + 1000), (256, 148 * 128 + 129)])
+@pytest.mark.parametrize("C,T", [(96, 148 * 128 * 2 + 77), (192, 148 * 128 + 1000), (256, 148 * 128 + 129),
+                                 (384, 148 * 128 + 300), (320, 700)])
 def test_fused_persistent_multi_tile(dev, C, T):
     """Several m-tiles per CTA (X-slot reuse, TMEM / Hq buffer phases across tiles), resident and
     streamed weights, ragged tail."""
     _run_and_check(dev, _layer(C, 8000 + C), T, e2e=False)
 
 
-@pytest.mark.parametrize("C,T", [(96, 3000), (192, 1000)])
+@pytest.mark.parametrize("C,T", [(96, 3000), (192, 1000), (384, 300)])
 def test_fused_gelu_and_ln_fp64(dev, C, T):
     _run_and_check(dev, _layer(C, 9000 + C, act=1, bias=True, zh=-3), T)
     _run_and_check(dev, _layer(C, 9100 + C), T, ln_fp64=True)
