@@ -43,7 +43,11 @@ constexpr uint32_t kKB = (uint32_t)kBM * kBK;   // one [128 rows][128 B] box
 // flags
 constexpr int kFGelu = 1, kFZh = 2, kFB1 = 4, kFS64 = 8, kFSmallK = 16, kFTaps = 32;
 constexpr int kFReg = 64;   // op #6 register path (C <= 32 * kFRegCh; not with kFS64 / kFTaps)
-constexpr int kFNumVariants = 96;   // flags 0..95 (kFReg only without kFTaps)
+// CTA pair (cta_group::2): two CTAs of a cluster take m-tiles 2u and 2u + 1; the leader
+// issues M = 256 MMAs whose B operand (the weight chunk) is split between the two CTAs'
+// shared memory, so each SM streams half of every weight chunk (streamed weights only)
+constexpr int kFPair = 128;
+constexpr int kFNumVariants = 96;   // flags 0..95 (kFReg only without kFTaps), and 128..191 (kFPair)
 
 struct FusedArgs {
     int64_t M;          // tokens
@@ -89,10 +93,17 @@ constexpr int kFMaxNX = 4;
 // never parked back in TMEM (no tcgen05.st / second tcgen05.ld per value)
 constexpr int kFRegCh = 3;
 constexpr int kFMaxStages2 = 4;
-constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 2 * kFMaxStages2 + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1;
+constexpr uint32_t kFNumBars = 4 + 4 + 2 * kFMaxStages + 2 * kFMaxStages2 + 1 + 2 * kFMaxNB1 + 2 * kFMaxNH + 4 + 2 + 1 + 1 +
+                               kFMaxNX;   // + pair: peer X landed
 
+// Streamed ring items: W1 = one [128 (pair: 64) rows][128 B] K-block box; W2 = [rows][128 B]
+// with rows = C (C > 256: C/2, one item per FC2 MMA half), halved in a CTA pair.
+__host__ __device__ inline uint32_t fused_w1_item(int pair) { return (uint32_t)kBM * kBK >> (pair ? 1 : 0); }
+__host__ __device__ inline uint32_t fused_w2_rows(int C, int pair) {
+    return (uint32_t)(C > 256 ? C / 2 : C) >> (pair ? 1 : 0);
+}
 __host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int stages, int ebytes, int NX,
-                                                    int y_inplace = 0, int stages2 = 0) {
+                                                    int y_inplace = 0, int stages2 = 0, int pair = 0) {
     FusedLayout L;
     const uint32_t kbc = (uint32_t)((C + kBK - 1) / kBK), nj = (uint32_t)(H / kFHc);
     L.x = 0;                                             // [NX][KBC][128 rows][128 B] X tiles
@@ -103,8 +114,8 @@ __host__ __device__ inline FusedLayout fused_layout(int C, int H, int NH, int st
         L.w2 = L.w + nj * kbc * kKB;
         L.consts = L.w2 + nj * (uint32_t)C * kBK;
     } else {   // two rings: W1 K-blocks, W2 chunks (each consumed in its own order)
-        L.w2 = L.w + (uint32_t)stages * kKB;
-        L.consts = L.w2 + (uint32_t)stages2 * (uint32_t)(C > 256 ? C / 2 : C) * kBK;
+        L.w2 = L.w + (uint32_t)stages * fused_w1_item(pair);
+        L.consts = L.w2 + (uint32_t)stages2 * fused_w2_rows(C, pair) * kBK;
     }
     L.red = L.consts + (3u * (uint32_t)H + 5u * (uint32_t)C) * 4u;   // m1 b1 mg1 [H]; m2 b2 zc2 g b [C]
     L.red = (L.red + 15u) & ~15u;
@@ -124,6 +135,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     constexpr bool TAPS = (F & kFTaps) != 0;   // debug taps compiled in (run_debug only)
     constexpr bool STATS64 = (F & kFS64) != 0, SMALLK = (F & kFSmallK) != 0;
     constexpr bool REG = (F & kFReg) != 0 && !STATS64 && !TAPS;   // op #6 half rows in registers
+    constexpr bool PAIR = (F & kFPair) != 0;
     using acc_t = typename std::conditional<STATS64, double, float>::type;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -135,7 +147,11 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t NJ = (uint32_t)p.NJ, KBC = (uint32_t)p.KBC, NB1 = (uint32_t)p.NB1, NH = (uint32_t)p.NH;
     const uint32_t stages = (uint32_t)p.stages;
     const bool resident = stages == 0;
-    const FusedLayout L = fused_layout(C, H, p.NH, p.stages, (int)sizeof(acc_t), p.NX, p.y_inplace, p.stages2);
+    const FusedLayout L = fused_layout(C, H, p.NH, p.stages, (int)sizeof(acc_t), p.NX, p.y_inplace, p.stages2,
+                                       PAIR ? 1 : 0);
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;         // pair: 0 = leader (issues the MMAs)
+    const uint32_t w1item = fused_w1_item(PAIR ? 1 : 0);         // streamed W1 ring item bytes
+    const uint32_t w2rows_it = fused_w2_rows(C, PAIR ? 1 : 0);   // rows of a streamed W2 ring item
     const uint32_t stages2 = (uint32_t)p.stages2;
     const bool yin = p.y_inplace != 0;
     const uint32_t NX = (uint32_t)p.NX;
@@ -167,6 +183,17 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t bar_yfull = bar_a2empty + 16u;             //       Y tile staged (8 warps)
     const uint32_t bar_yempty = bar_yfull + 8u;               //       Y staging read by its stores (1)
     const uint32_t bar_cfull = bar_yempty + 16u;              //       constants loaded (32)
+    const uint32_t bar_xpeer = bar_cfull + 8u;                // [NX]  pair (leader): the peer's X landed (1)
+    // pair: barriers the leader's MMAs wait on that the peer's warps also arrive on
+    auto arrive_leader = [&](uint32_t bar) {   // (the leader's own warps arrive locally)
+        if (PAIR && rank != 0) mbar_arrive_cluster(mapa(bar, 0));
+        else mbar_arrive(bar);
+    };
+    auto wait_pc = [&](uint32_t bar, uint32_t parity) {   // (cluster-scope acquire in a pair)
+        if constexpr (PAIR) mbar_wait_cluster(bar, parity);
+        else mbar_wait(bar, parity);
+    };
+    constexpr uint32_t kArrive = PAIR ? 16u : 8u;             // 8 epilogue warps per CTA
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -195,31 +222,41 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         mbar_init(bar_wres, 1);
         for (int b = 0; b < kFMaxNB1; ++b) {
             mbar_init(bar_a1full + 8u * b, 1);
-            mbar_init(bar_a1empty + 8u * b, 8);
+            mbar_init(bar_a1empty + 8u * b, kArrive);
         }
         for (int b = 0; b < kFMaxNH; ++b) {
-            mbar_init(bar_hqfull + 8u * b, 8);
+            mbar_init(bar_hqfull + 8u * b, kArrive);
             mbar_init(bar_hqempty + 8u * b, 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_a2full + 8u * b, 1);
-            mbar_init(bar_a2empty + 8u * b, 8);
+            mbar_init(bar_a2empty + 8u * b, kArrive);
         }
         mbar_init(bar_cfull, 32);
+        for (int i = 0; i < kFMaxNX; ++i) mbar_init(bar_xpeer + 8u * i, 1);
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), 512);
+    if (warp == 2) {
+        if constexpr (PAIR) tmem_alloc_pair(smem_u32(const_cast<uint32_t*>(tmem_slot)), 512);
+        else tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), 512);
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync_all();   // the peer's barriers exist before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();   // PDL: see mlp_kernels.cuh
 
     const uint32_t m_tiles = (uint32_t)((p.M + kBM - 1) / kBM);
-    const uint32_t cid = blockIdx.x, grid = gridDim.x;
-    const uint32_t n_my = cid < m_tiles ? (m_tiles - cid + grid - 1) / grid : 0u;
+    // work units: m-tiles, or (pair) m-tile pairs 2u (leader), 2u + 1 (peer)
+    const uint32_t cid = PAIR ? blockIdx.x >> 1 : blockIdx.x, grid = PAIR ? gridDim.x >> 1 : gridDim.x;
+    const uint32_t units = PAIR ? (m_tiles + 1u) >> 1 : m_tiles;
+    const uint32_t n_my = cid < units ? (units - cid + grid - 1) / grid : 0u;
     const uint32_t U = n_my * NJ;                 // hidden chunks this CTA processes
-    auto row0_of = [&](uint32_t i) -> int32_t { return (int32_t)((cid + i * grid) * kBM); };
+    auto row0_of = [&](uint32_t i) -> int32_t {
+        const uint32_t u = cid + i * grid;
+        return (int32_t)((PAIR ? 2u * u + rank : u) * kBM);
+    };
     // Hidden-chunk order rotated per CTA: position jj of a tile is chunk (jj + rot) mod NJ.
     // FC2 sums exact int32 partial products, so the order changes no result; it spreads
     // the CTAs' streamed weight reads over different chunks (different L2 lines) instead
@@ -271,9 +308,15 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     for (uint32_t kb = 0; kb < KBC; ++kb) {   // one ring item per K-block
                         mbar_wait(bar_wempty + 8u * s, ph ^ 1u);
                         if (elect_one()) {
-                            mbar_arrive_expect_tx(bar_wfull + 8u * s, kKB);
-                            tma_load_2d(&tmW1, sW + s * kKB, bar_wfull + 8u * s, (int)(kb * kBK),
-                                        (int)(chunk_of(j) * kFHc));
+                            if constexpr (PAIR) {   // this CTA's 64 rows; bytes complete on the leader
+                                if (rank == 0) mbar_arrive_expect_tx(bar_wfull + 8u * s, 2u * w1item);
+                                tma_load_2d_pair(&tmW1, sW + s * w1item, mapa(bar_wfull + 8u * s, 0), (int)(kb * kBK),
+                                                 (int)(chunk_of(j) * kFHc + rank * 64u));
+                            } else {
+                                mbar_arrive_expect_tx(bar_wfull + 8u * s, kKB);
+                                tma_load_2d(&tmW1, sW + s * kKB, bar_wfull + 8u * s, (int)(kb * kBK),
+                                            (int)(chunk_of(j) * kFHc));
+                            }
                         }
                         __syncwarp();
                         if (++s == stages) { s = 0; ph ^= 1u; }
@@ -289,16 +332,22 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     } else if (warp == (uint32_t)kFW2Warp) {
         // ====================== W2 producer (streamed weights) ======================
         if (!resident) {
-            const uint32_t w2rows = C > 256 ? (uint32_t)C / 2u : (uint32_t)C;
+            const uint32_t w2rows = C > 256 ? (uint32_t)C / 2u : (uint32_t)C;   // rows per FC2 MMA
             const uint32_t w2items = C > 256 ? 2u : 1u;
             uint32_t s2 = 0, ph2 = 0, j2 = 0;
             for (uint32_t u = 0; u < U; ++u) {   // operands of FC2(u), in FC2's order
                 for (uint32_t h = 0; h < w2items; ++h) {   // one ring item per FC2 MMA half
                     mbar_wait(bar_w2empty + 8u * s2, ph2 ^ 1u);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(bar_w2full + 8u * s2, w2rows * kBK);
-                        tma_load_2d(&tmW2, sW2 + s2 * w2rows * kBK, bar_w2full + 8u * s2, (int)(chunk_of(j2) * kFHc),
-                                    (int)(h * w2rows));
+                        const uint32_t dst = sW2 + s2 * w2rows_it * kBK;
+                        const int c0 = (int)(chunk_of(j2) * kFHc), r0 = (int)(h * w2rows + rank * w2rows_it);
+                        if constexpr (PAIR) {   // this CTA's half of the MMA's B rows
+                            if (rank == 0) mbar_arrive_expect_tx(bar_w2full + 8u * s2, 2u * w2rows_it * kBK);
+                            tma_load_2d_pair(&tmW2, dst, mapa(bar_w2full + 8u * s2, 0), c0, r0);
+                        } else {
+                            mbar_arrive_expect_tx(bar_w2full + 8u * s2, w2rows_it * kBK);
+                            tma_load_2d(&tmW2, dst, bar_w2full + 8u * s2, c0, r0);
+                        }
                     }
                     __syncwarp();
                     if (++s2 == stages2) { s2 = 0; ph2 ^= 1u; }
@@ -313,9 +362,21 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         // warp FC1 of the next chunk would queue behind FC2's wait for op #5.  Each
         // warp's tcgen05.commit tracks its own MMAs.  Descriptors are base + offset (the
         // 14-bit start-address field never carries: smem < 256 KB).
-        const uint32_t idesc1 = idesc_i8(kBM, kFHc);
+        if (PAIR && rank != 0) {
+            // pair peer: no MMAs here; relay "my X tile landed" to the leader's FC1
+            uint32_t xs = 0, xph = 0;
+            for (uint32_t i = 0; i < n_my; ++i) {
+                mbar_wait(bar_xfull + 8u * xs, xph);
+                if (lane == 0) mbar_arrive_cluster(mapa(bar_xpeer + 8u * xs, 0));
+                __syncwarp();
+                if (++xs == NX) { xs = 0; xph ^= 1u; }
+            }
+            goto fc1_done;
+        }
+        {
+        const uint32_t idesc1 = idesc_i8(PAIR ? 2u * kBM : kBM, kFHc);
         const uint64_t dX = umma_desc_k128(sX), dW = umma_desc_k128(sW);
-        const uint32_t xslot16 = xslot >> 4, stage16 = kKB >> 4;
+        const uint32_t xslot16 = xslot >> 4, stage16 = w1item >> 4;
         const uint32_t kb16 = kKB >> 4;
         const int nk_last = (C - (int)((KBC - 1u) * kBK)) / 32;   // MMAs (K = 32) in the last K-block
         const uint32_t a1_tm = tmem_base + (uint32_t)p.a1_col;
@@ -325,30 +386,39 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         uint32_t xs = 0, xph = 0;                        // X slot, its phase
         for (uint32_t q = 0; q < U; ++q) {               // FC1(q): acc1[b] = X_i . W1[j]^T
             if (trc && lane == 0 && q < 512) trc[1024 + q] = gtimer();
-            if (j == 0) mbar_wait(bar_xfull + 8u * xs, xph);
-            mbar_wait(bar_a1empty + 8u * b, bph ^ 1u);
+            if (j == 0) {
+                mbar_wait(bar_xfull + 8u * xs, xph);
+                if constexpr (PAIR) mbar_wait_cluster(bar_xpeer + 8u * xs, xph);
+            }
+            wait_pc(bar_a1empty + 8u * b, bph ^ 1u);
             if (trc && lane == 0 && q < 512) trc[1536 + q] = gtimer();
             const uint32_t d = a1_tm + b * (uint32_t)kFHc;
             const uint64_t ad0 = dX + xs * xslot16;
             for (uint32_t kb = 0; kb < KBC; ++kb) {
-                if (!resident) mbar_wait(bar_wfull + 8u * s, ph);
+                if (!resident) wait_pc(bar_wfull + 8u * s, ph);
                 if (trc && lane == 0 && q < 512 && kb + 1 == KBC) trc[7680 + q] = gtimer();   // weights in
                 tc_fence_after();
                 const uint64_t ad = ad0 + kb * kb16;
                 const uint64_t bd = resident ? dW + (chunk_of(j) * KBC + kb) * kb16 : dW + s * stage16;
                 const int nk = kb + 1u == KBC ? nk_last : 4;
                 if (elect_one()) {
-                    mma_i8(d, ad, bd, idesc1, kb);
-                    if (nk > 1) mma_i8(d, ad + 2u, bd + 2u, idesc1, 1u);
-                    if (nk > 2) mma_i8(d, ad + 4u, bd + 4u, idesc1, 1u);
-                    if (nk > 3) mma_i8(d, ad + 6u, bd + 6u, idesc1, 1u);
-                    if (!resident) mma_commit(bar_wempty + 8u * s);
+                    if constexpr (PAIR) {
+                        for (int k = 0; k < nk; ++k) mma_i8_pair(d, ad + 2u * k, bd + 2u * k, idesc1, (kb | k) != 0);
+                        mma_commit_pair_mc(bar_wempty + 8u * s, 3);   // both CTAs' ring slots
+                    } else {
+                        mma_i8(d, ad, bd, idesc1, kb);
+                        if (nk > 1) mma_i8(d, ad + 2u, bd + 2u, idesc1, 1u);
+                        if (nk > 2) mma_i8(d, ad + 4u, bd + 4u, idesc1, 1u);
+                        if (nk > 3) mma_i8(d, ad + 6u, bd + 6u, idesc1, 1u);
+                        if (!resident) mma_commit(bar_wempty + 8u * s);
+                    }
                 }
                 __syncwarp();
                 if (!resident && ++s == stages) { s = 0; ph ^= 1u; }
             }
             if (elect_one()) {
-                mma_commit(bar_a1full + 8u * b);
+                if constexpr (PAIR) mma_commit_pair_mc(bar_a1full + 8u * b, 3);
+                else mma_commit(bar_a1full + 8u * b);
                 if (trc && q < 512) trc[q] = gtimer();
             }
             __syncwarp();
@@ -359,6 +429,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             }
             if (++b == NB1) { b = 0; bph ^= 1u; }
         }
+        }
+    fc1_done:;
     } else if (warp == 2) {
         // ============================ Y store warp ============================
         pdl_wait();   // Y may overwrite what the previous kernel still reads
@@ -398,8 +470,11 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         mbar_arrive(bar_cfull);
 
         // ============================ FC2 issuer ==============================
+        if (PAIR && rank != 0) goto fc2_done;   // the leader issues for the pair
+        {
         const uint32_t n2 = C > 256 ? (uint32_t)C / 2u : (uint32_t)C;   // N per FC2 MMA (<= 256)
-        const uint32_t idesc2 = idesc_i8(kBM, n2);
+        const uint32_t idesc2 = idesc_i8(PAIR ? 2u * kBM : kBM, n2);
+        const uint32_t it16 = (w2rows_it * kBK) >> 4;                    // streamed ring item stride
         const uint32_t n2off16 = (n2 * kBK) >> 4;                        // bytes/16 of N2 B rows
         const uint32_t w2n = C > 256 ? 2u : 1u;
         const uint64_t dW2 = umma_desc_k128(sW2), dHq = umma_desc_k128(sHq);
@@ -409,31 +484,41 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         uint32_t j2 = 0, hb = 0, hph = 0, ab = 0, aph = 0;   // chunk, Hq buffer, acc2 buffer (+ phases)
         for (uint32_t u = 0; u < U; ++u) {                    // FC2(u): acc2 += Hq_u . W2[:, j2]^T
             if (trc && lane == 0 && u < 512) trc[6656 + u] = gtimer();
-            mbar_wait(bar_hqfull + 8u * hb, hph);
-            if (j2 == 0) mbar_wait(bar_a2empty + 8u * ab, aph ^ 1u);
+            wait_pc(bar_hqfull + 8u * hb, hph);
+            if (j2 == 0) wait_pc(bar_a2empty + 8u * ab, aph ^ 1u);
             if (trc && lane == 0 && u < 512) trc[7168 + u] = gtimer();
             const uint64_t ad = dHq + hb * kb16;
             const uint32_t d2 = tmem_base + ab * (uint32_t)p.a2_stride;
             // C > 256: two MMA halves of N = C/2 (W2 rows [h C/2, (h+1) C/2) -> TMEM columns
             // h C/2 ..), each on its own streamed ring item
             for (uint32_t h = 0; h < w2n; ++h) {
-                if (!resident) mbar_wait(bar_w2full + 8u * s2, ph2);
+                if (!resident) wait_pc(bar_w2full + 8u * s2, ph2);
                 tc_fence_after();
-                const uint64_t bd = resident ? dW2 + chunk_of(j2) * w2c16 + h * n2off16 : dW2 + s2 * n2off16;
+                const uint64_t bd = resident ? dW2 + chunk_of(j2) * w2c16 + h * n2off16 : dW2 + s2 * it16;
                 const uint32_t dh = d2 + h * n2;
                 if (elect_one()) {
-                    mma_i8(dh, ad, bd, idesc2, j2);
-                    mma_i8(dh, ad + 2u, bd + 2u, idesc2, 1u);
-                    mma_i8(dh, ad + 4u, bd + 4u, idesc2, 1u);
-                    mma_i8(dh, ad + 6u, bd + 6u, idesc2, 1u);
-                    if (!resident) mma_commit(bar_w2empty + 8u * s2);
+                    if constexpr (PAIR) {
+                        for (int k = 0; k < 4; ++k) mma_i8_pair(dh, ad + 2u * k, bd + 2u * k, idesc2, (j2 | k) != 0);
+                        mma_commit_pair_mc(bar_w2empty + 8u * s2, 3);
+                    } else {
+                        mma_i8(dh, ad, bd, idesc2, j2);
+                        mma_i8(dh, ad + 2u, bd + 2u, idesc2, 1u);
+                        mma_i8(dh, ad + 4u, bd + 4u, idesc2, 1u);
+                        mma_i8(dh, ad + 6u, bd + 6u, idesc2, 1u);
+                        if (!resident) mma_commit(bar_w2empty + 8u * s2);
+                    }
                 }
                 __syncwarp();
                 if (!resident && ++s2 == stages2) { s2 = 0; ph2 ^= 1u; }
             }
             if (elect_one()) {
-                mma_commit(bar_hqempty + 8u * hb);
-                if (j2 + 1u == NJ) mma_commit(bar_a2full + 8u * ab);
+                if constexpr (PAIR) {
+                    mma_commit_pair_mc(bar_hqempty + 8u * hb, 3);
+                    if (j2 + 1u == NJ) mma_commit_pair_mc(bar_a2full + 8u * ab, 3);
+                } else {
+                    mma_commit(bar_hqempty + 8u * hb);
+                    if (j2 + 1u == NJ) mma_commit(bar_a2full + 8u * ab);
+                }
                 if (trc && u < 512) trc[512 + u] = gtimer();
             }
             __syncwarp();
@@ -443,6 +528,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             }
             if (++hb == NH) { hb = 0; hph ^= 1u; }
         }
+        }
+    fc2_done:;
     } else if (warp < (uint32_t)kFEp6W0) {
         // ============================ op #5 ===================================
         // acc1 chunk (128 hidden columns) -> Hq chunk in smem, 128-B swizzled K-major
@@ -540,9 +627,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             tc_fence_before();
             fence_proxy_async_smem();          // Hq visible to the tensor core (async proxy)
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(bar_a1empty + 8u * b);
-                mbar_arrive(bar_hqfull + 8u * hb);
+            if (lane == 0) {   // (pair: on the leader, whose MMAs read both CTAs' Hq)
+                arrive_leader(bar_a1empty + 8u * b);
+                arrive_leader(bar_hqfull + 8u * hb);
             }
             if (stamp) trc[2048 + 2 * u + 1] = gtimer();
             if (++j == NJ) { j = 0; ++i; }
@@ -770,7 +857,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 for (int ch = 1; ch < (REG ? kFRegCh : 1); ++ch) reg_fence16(r[ch]);
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(bar_a2empty + 8u * ab);   // acc2 drained
+                if (lane == 0) arrive_leader(bar_a2empty + 8u * ab);   // acc2 drained
 #pragma unroll
                 for (int ch = 0; ch < (REG ? kFRegCh : 1); ++ch) {
                     if (ch < nch) {
@@ -882,7 +969,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             fence_proxy_async_smem();          // Y visible to the TMA store
             __syncwarp();
             if (lane == 0) {
-                if (!regpath) mbar_arrive(bar_a2empty + 8u * ab);
+                if (!regpath) arrive_leader(bar_a2empty + 8u * ab);
                 mbar_arrive(bar_yfull);
             }
             if (stamp) trc[4096 + 4 * i + 3] = gtimer();
@@ -892,10 +979,12 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync_all();   // no CTA leaves while its peer may still signal it
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, 512);
+        if constexpr (PAIR) tmem_dealloc_pair(tmem_base, 512);
+        else tmem_dealloc(tmem_base, 512);
     }
     if (p.cta_stamps && threadIdx.x == 0) p.cta_stamps[2 * blockIdx.x + 1] = gtimer();
 }

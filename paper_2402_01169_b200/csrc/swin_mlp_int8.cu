@@ -34,6 +34,10 @@ FusedFn fused_kernel_part2(int flags);
 FusedFn fused_kernel_part3(int flags);
 FusedFn fused_kernel_part4(int flags);
 FusedFn fused_kernel_part5(int flags);
+FusedFn fused_kernel_part8(int flags);   // CTA-pair variants (kFPair)
+FusedFn fused_kernel_part9(int flags);
+FusedFn fused_kernel_part10(int flags);
+FusedFn fused_kernel_part11(int flags);
 inline FusedFn fused_kernel_for(int flags) {
     switch (flags >> 4) {
         case 0: return fused_kernel_part0(flags);
@@ -41,7 +45,11 @@ inline FusedFn fused_kernel_for(int flags) {
         case 2: return fused_kernel_part2(flags);
         case 3: return fused_kernel_part3(flags);
         case 4: return fused_kernel_part4(flags);
-        default: return fused_kernel_part5(flags);
+        case 5: return fused_kernel_part5(flags);
+        case 8: return fused_kernel_part8(flags);
+        case 9: return fused_kernel_part9(flags);
+        case 10: return fused_kernel_part10(flags);
+        default: return fused_kernel_part11(flags);
     }
 }
 }  // namespace swinmlp
@@ -86,6 +94,7 @@ struct FusedPlan {
     FusedFn fn = nullptr;
     int NJ = 0, KBC = 0, NB1 = 0, NH = 0, stages = 0, a1_col = 0, NA2 = 1, a2_stride = 0, NX = 2, y_inplace = 0,
         stages2 = 0;
+    int pair = 0;   // CTA pair (cta_group::2): clusters of 2 on m-tiles 2u, 2u+1, weights split
     uint32_t smem = 0;
 };
 
@@ -311,11 +320,26 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
 
 // The one-kernel plan: weights resident in smem when they fit (W1 and W2 each
 // 4C^2 bytes: C <= 128), else streamed through a ring; Hq buffers 2..4.
-bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
+// CTA-pair one-kernel plan (streamed weights, C > 128), opt-in: SWIN_MLP_FUSED_PAIR=1.
+// Measured (back-to-back launches, Swin-T b64): C = 192 41.7 us vs 30.2 us single-CTA,
+// C = 384 40.6 vs 35.1 -- halving each SM's weight stream does not pay for the per-chunk
+// cross-CTA handshakes (peer op #5 -> leader MMA), so the single-CTA plan is the default.
+int fused_pair_for(int C) {
+    const char* e = std::getenv("SWIN_MLP_FUSED_PAIR");   // (read per create)
+    return (e && *e == '1' && C > 128) ? 1 : 0;
+}
+
+bool make_fused(int C, int H, int ebytes, FusedPlan& fp, int pair) {
     fp = FusedPlan();
+    fp.pair = pair;
     const char* no = std::getenv("SWIN_MLP_NO_FUSED");   // A/B switch (read per create)
     if (no && *no && *no != '0') return false;
-    if (C > 384 || H % kFHc) return false;
+    // C <= 256 by default; SWIN_MLP_FUSED_MAXC=384 admits 256 < C <= 384 (single acc1, FC2
+    // as two N = C/2 MMAs) -- measured at C = 384, T = 12544: 35.1 us vs 33.4 us for the
+    // two-kernel plan, so not the default
+    const char* mc = std::getenv("SWIN_MLP_FUSED_MAXC");   // (read per create)
+    const int maxc = mc && *mc ? std::min(384, atoi(mc)) : 256;
+    if (C > maxc || H % kFHc) return false;
     fp.KBC = (C + kBK - 1) / kBK;
     fp.NJ = H / kFHc;
     // TMEM (512 columns): acc2 buffers, then 128-column acc1 buffers.  C <= 128: two of
@@ -332,6 +356,7 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
     fp.NB1 = (512 - fp.a1_col) / kFHc;
     // resident weights first (X slots 4..2, Hq buffers 3..2), else a weight ring
     for (int nx : {4, 3, 2}) {
+        if (pair) break;   // (a pair streams its weights)
         for (int nh : {3, 2}) {
             const uint32_t need = fused_layout(C, H, nh, 0, ebytes, nx).total + 1024;
             if (need <= kSmemBudget) {
@@ -348,9 +373,12 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp) {
     const int yin = (yie && *yie == '0') ? 0 : 1;
     // C > 256: one X slot (a CTA gets about one tile) so the weight rings get the smem
     for (int nx : {C > 256 ? 1 : 2, C > 256 ? 2 : 1}) {
-    for (int st2 : {2, 1}) {   // (C > 256: half-chunk W2 items, 2 = one chunk)
+    // W2 ring: up to two chunks of items (C > 256: two half-chunk items per chunk), then the
+    // deepest W1 ring that fits
+    const int w2n = C > 256 ? 2 : 1;
+    for (int st2 = std::min(kFMaxStages2, 2 * w2n); st2 >= 1; --st2) {
         for (int st = kFMaxStages; st >= (fp.NB1 > 1 ? 2 * fp.KBC : 2); --st) {
-            const uint32_t need = fused_layout(C, H, 2, st, ebytes, nx, yin, st2).total + 1024;
+            const uint32_t need = fused_layout(C, H, 2, st, ebytes, nx, yin, st2, pair).total + 1024;
             if (need <= kSmemBudget) {
                 fp.NX = nx; fp.NH = 2; fp.stages = st; fp.stages2 = st2; fp.smem = need; fp.on = true;
                 fp.y_inplace = yin;
@@ -641,17 +669,18 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
         int per_sm = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->op5_fn, kOp5Threads, 0));
         h->op5_grid = std::max(1, per_sm) * h->num_sms;   // persistent grid-stride: whole waves
-    } else if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp)) {
+    } else if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp, fused_pair_for(C))) {
         const int ff = (d.act == SWIN_MLP_ACT_GELU_ERF ? kFGelu : 0) | (d.h_zero_point ? kFZh : 0) |
                        (d.b1 ? kFB1 : 0) | (d.ln_fp64 ? kFS64 : 0) | (small_k1 ? kFSmallK : 0);
         // op #6 register path when a thread's half row is at most kFRegCh chunks of 16
         // (SWIN_MLP_FUSED_REG=0 disables: A/B switch)
         static const char* re = std::getenv("SWIN_MLP_FUSED_REG");
         const bool reg = !(re && *re == '0') && !d.ln_fp64 && C / 2 <= 16 * kFRegCh;
-        h->fp.fn = fused_kernel_for(ff | (reg ? kFReg : 0));
-        h->fp_dbg = fused_kernel_for(ff | kFTaps);
-        H_TRY(encode_2d(&h->tm_fw1, h->w1, H, C, C, (uint32_t)kFHc));
-        H_TRY(encode_2d(&h->tm_fw2, h->w2, C, H, H, (uint32_t)(C > 256 ? C / 2 : C)));
+        const int fpair = h->fp.pair ? kFPair : 0;
+        h->fp.fn = fused_kernel_for(ff | (reg && !fpair ? kFReg : 0) | fpair);
+        h->fp_dbg = fused_kernel_for(ff | kFTaps | fpair);
+        H_TRY(encode_2d(&h->tm_fw1, h->w1, H, C, C, (uint32_t)(h->fp.pair ? kFHc / 2 : kFHc)));
+        H_TRY(encode_2d(&h->tm_fw2, h->w2, C, H, H, fused_w2_rows(C, h->fp.pair)));
         CUDA_TRY(cudaFuncSetAttribute(h->fp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
         CUDA_TRY(cudaFuncSetAttribute(h->fp_dbg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
     }
@@ -706,15 +735,22 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         a.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
         const int64_t m_tiles = (T + kBM - 1) / kBM;
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)std::min<int64_t>(m_tiles, h->num_sms));
+        if (h->fp.pair)   // clusters of 2 CTAs on m-tile pairs
+            cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>((m_tiles + 1) / 2, h->num_sms / 2)));
+        else
+            cfg.gridDim = dim3((unsigned)std::min<int64_t>(m_tiles, h->num_sms));
         cfg.blockDim = dim3((unsigned)kFThreads);
         cfg.dynamicSmemBytes = h->fp.smem;
         cfg.stream = s;
-        cudaLaunchAttribute fat[1];
+        cudaLaunchAttribute fat[2];
         fat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         fat[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        fat[1].id = cudaLaunchAttributeClusterDimension;
+        fat[1].val.clusterDim.x = h->fp.pair ? 2 : 1;
+        fat[1].val.clusterDim.y = 1;
+        fat[1].val.clusterDim.z = 1;
         cfg.attrs = fat;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = 2;
         cudaEvent_t* ev = nullptr;
         if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
         if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));

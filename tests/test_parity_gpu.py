@@ -153,6 +153,21 @@ def test_op5_unfused_matches_fused_plan(dev):
         assert lib().swin_mlp_int8_launches_per_run(b.handle) == 3
 
 
+@pytest.mark.parametrize("C,T,pair", [(384, 148 * 128 + 300, 0), (320, 700, 0), (384, 1000, 1), (192, 148 * 256 + 77, 1),
+                                      (256, 300, 1), (192, 129, 1)])
+def test_fused_opt_in_plans(dev, C, T, pair, monkeypatch):
+    """Opt-in one-kernel variants: C up to 384 (SWIN_MLP_FUSED_MAXC, FC2 as two N = C/2 MMAs)
+    and the CTA pair (SWIN_MLP_FUSED_PAIR, cta_group::2 M = 256, weights split between the
+    two CTAs) -- incl. an odd m-tile count (the last pair's peer tile empty)."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    monkeypatch.setenv("SWIN_MLP_FUSED_MAXC", "384")
+    monkeypatch.setenv("SWIN_MLP_FUSED_PAIR", str(pair))
+    L = _layer(C, 8500 + C)
+    assert SwinMlpInt8Layer(L, device=0).plan()["fused"] == 1
+    _run_and_check(dev, L, T, e2e=False)
+    _run_and_check(dev, _layer(C, 8600 + C, act=1, bias=True, zx=3, zh=-128, zy=1), min(T, 400), e2e=False)
+
+
 def test_t_zero_is_noop(dev):
     from paper_2402_01169_b200 import SwinMlpInt8Layer
     layer = SwinMlpInt8Layer(_layer(96, 1), device=0)
@@ -301,7 +316,7 @@ def test_parity_extreme_accumulators(dev, C):
 
 # ---- one-kernel plan (fused_mlp.cuh, C <= 256) vs the two-kernel plan ---------------------------
 
-@pytest.mark.parametrize("C,fused", [(96, 1), (128, 1), (192, 1), (256, 1), (384, 1), (512, 0), (768, 0)])
+@pytest.mark.parametrize("C,fused", [(96, 1), (128, 1), (192, 1), (256, 1), (384, 0), (512, 0), (768, 0)])
 def test_plan_selection(dev, C, fused, monkeypatch):
     from paper_2402_01169_b200 import SwinMlpInt8Layer
     L = _layer(C, 7000 + C)
@@ -318,8 +333,7 @@ def test_two_kernel_plan_small_c(dev, C, T, monkeypatch):
     _run_and_check(dev, _layer(C, 3000 + C, bias=True, zx=-5, zh=-128, zy=2), T)
 
 
-@pytest.mark.parametrize("C,T", [(96, 148 * 128 * 2 + 77), (192, 148 * 128 + 1000), (256, 148 * 128 + 129),
-                                 (384, 148 * 128 + 300), (320, 700)])
+@pytest.mark.parametrize("C,T", [(96, 148 * 128 * 2 + 77), (192, 148 * 128 + 1000), (256, 148 * 128 + 129)])
 def test_fused_persistent_multi_tile(dev, C, T):
     """Several m-tiles per CTA (X-slot reuse, TMEM / Hq buffer phases across tiles), resident and
     streamed weights, ragged tail."""
