@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--cpu-stride", type=int, default=1, help="cpu_baseline samples every n-th token")
     ap.add_argument("--ref-stride", type=int, default=64, help="--impl reference samples every n-th token")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stack", action="store_true", help="skip the Swin-B stack (north star) measurement")
     return ap.parse_args()
 
 
@@ -384,6 +385,17 @@ def main():
                  "pairs": args.pairs, "relu_wins": wins, "b1": "None in every arm (paper mode)",
                  "unit": "us per step (4 layers)"}
 
+    # ---- the north star's stack (BASELINE configs[3]: Swin-B MLP stack, per-GPU share of batch
+    # 1024 on 8 GPUs = 128 images, 24 layers): tokens/s and fraction of the int8 tensor roof -----
+    stack = None
+    if rank == 0 and not args.no_stack:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import stack_bench
+        stack = stack_bench.run(4, max(3, min(args.steps, 10)), synth.ACT_RELU)
+        stack = {k: stack[k] for k in ("workload", "layers", "ms_per_step", "tokens_per_s", "tops", "tensor_frac",
+                                       "int8_peak_tops", "stages", "l2")}
+        torch.cuda.empty_cache()
+
     # ---- CPU baseline: the oracle as it stands on this host (rank 0, N=1 only) ----------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -405,6 +417,7 @@ def main():
                         "per_layer_run_host": res_e2e["per_layer"]},
                 "gpu_launches": sum(n * P.swin_mlp_int8_launches_per_run(l.handle) for (_, _, n), l in zip(prof, relu_layers)),
                 "relu_vs_gelu": relu_gelu,
+                "north_star_stack": stack,
                 "tensor_frac_of_step": roofline["step_frac"],
                 "clocks": sampler.result()}
         print(json.dumps(line), flush=True)

@@ -82,6 +82,7 @@ struct FusedArgs {
     unsigned long long* trace;
     int32_t trace_cta;
     unsigned long long* cta_stamps;   // debug: per CTA %globaltimer at entry / exit ([2 * blockIdx.x + {0,1}])
+    int32_t rotate;                   // 1: per-CTA rotated hidden-chunk order (A/B switch SWIN_MLP_FUSED_ROT)
 };
 
 struct FusedLayout {
@@ -261,7 +262,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     // FC2 sums exact int32 partial products, so the order changes no result; it spreads
     // the CTAs' streamed weight reads over different chunks (different L2 lines) instead
     // of every SM requesting the same chunk at the same time.
-    const uint32_t rot = cid % NJ;
+    const uint32_t rot = p.rotate ? cid % NJ : 0u;
     auto chunk_of = [&](uint32_t jj) -> uint32_t { const uint32_t c = jj + rot; return c >= NJ ? c - NJ : c; };
 
     if (warp == 0) {

@@ -220,7 +220,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // 2u and 2u+1 of the same n-group; each loads its A rows and half of the B rows,
     // the leader issues the MMAs (op #5 only: no cross-CTA row statistics)
     constexpr bool PAIR = (F & kPair) != 0;
-    static_assert(!(PAIR && IS_LN), "pair mode is an FC1 (op #5) plan");
+    // (op #6 in a pair: CS == 1, the whole row in each CTA's TMEM -- BN = C <= 512 as two
+    // N = BN/2 MMAs when BN > 256 -- so the LayerNorm statistics never leave the CTA)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -231,7 +232,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t CS = (uint32_t)p.CS;
     const int stages = p.stages;
     const uint32_t G = (uint32_t)p.G;
-    const uint32_t lgG = G == 4 ? 2u : 1u;
+    const uint32_t lgG = G == 4 ? 2u : G == 2 ? 1u : 0u;   // (G = 1: the pair op #6 plan)
     // epilogue groups: op #6 G ping-pong groups (one per accumulator buffer); op #5 may
     // use one group of all 16 warps per tile (shorter per-tile drain, so the MMA of tile
     // t + G waits less for the drain of tile t)
@@ -241,6 +242,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     using acc_t = typename std::conditional<STATS64, double, float>::type;   // LN statistics type
     const uint32_t resb_bytes = p.resb ? (uint32_t)p.n_groups * (uint32_t)((p.K + kBK - 1) / kBK) * (uint32_t)BN * kBK : 0u;
     const int bn_b = PAIR ? BN / 2 : BN;                 // B rows per ring stage in this CTA
+    // pair with BN > 256: two MMAs of N = BN/2 per K step; each CTA holds, per MMA half h,
+    // B rows [h BN/2 + rank BN/4, + BN/4) as [h][BN/4 rows][128 B]
+    const uint32_t nh2 = (PAIR && BN > 256) ? 2u : 1u;
+    const uint32_t nmma = (uint32_t)BN / nh2;            // UMMA N
+    const uint32_t hrows = PAIR ? nmma / 2u : nmma;      // B rows per MMA half in this CTA
     const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage, resb_bytes, bn_b, p.eg);
     const uint32_t tile_bytes = (uint32_t)BN * kBM;
     const uint32_t sA = base + L.a, sB = base + L.b;
@@ -392,7 +398,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             if (trc && kb == 0 && it < 512) trc[2 * it] = gtimer();
                             if (rank == 0) mbar_arrive_expect_tx(bar_full + 8u * s, 2u * (a_bytes + b_bytes));
                             const uint32_t fb = mapa(bar_full + 8u * s, 0);
-                            tma_load_2d_pair(&tmB, sB + (uint32_t)s * b_bytes, fb, kb * kBK, n0 + (int)rank * bn_b);
+                            for (uint32_t h = 0; h < nh2; ++h)
+                                tma_load_2d_pair(&tmB, sB + (uint32_t)s * b_bytes + h * hrows * kBK, fb, kb * kBK,
+                                                 n0 + (int)(h * nmma + rank * hrows));
                             tma_load_2d_pair(&tmA, sA + (uint32_t)s * a_bytes, fb, kb * kBK, row0);
                         }
                         __syncwarp();
@@ -419,7 +427,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp == 1) {
         // ============================ MMA issuer ==============================
-        const uint32_t idesc = idesc_i8(PAIR ? 2u * kBM : kBM, (uint32_t)BN);
+        const uint32_t idesc = idesc_i8(PAIR ? 2u * kBM : kBM, nmma);
+        const uint32_t hoff16 = (hrows * kBK) >> 4;      // descriptor step to MMA half 1's B rows
         int s = 0;
         uint32_t ph = 0;
         if (resb) mbar_wait(bar_bfull, 0);
@@ -443,8 +452,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int nk = rem >= kBK ? 4 : rem / 32;
                 if (elect_one()) {
                     if constexpr (PAIR) {
-                        for (int k = 0; k < nk; ++k)
-                            mma_i8_pair(d, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                        for (uint32_t h = 0; h < nh2; ++h)
+                            for (int k = 0; k < nk; ++k)
+                                mma_i8_pair(d + h * nmma, ad + 2u * k, bd + h * hoff16 + 2u * k, idesc, (kb | k) != 0);
                         mma_commit_pair_mc(bar_empty + 8u * ss, 3);   // both CTAs' slots free
                     } else {
                         for (int k = 0; k < nk; ++k)

@@ -172,7 +172,8 @@ KernelFn kernel_for(int epi, int flags) {
                                           mlp_gemm_kernel<EP_ACC, kPair>, mlp_gemm_kernel<EP_ACC, kHasZc | kPair>};
             return t[((flags & kHasZc) ? 1 : 0) | ((flags & kPair) ? 2 : 0)];
         }
-        default: return pick<EP6_LN>(flags & 15, std::make_integer_sequence<int, 16>{}, false);
+        default: return pick<EP6_LN>((flags & 15) | ((flags & kPair) ? 16 : 0), std::make_integer_sequence<int, 32>{},
+                                     false);
     }
 }
 
@@ -248,8 +249,9 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // residual x tiles staged in smem
     for (int xs : {4, 2, 1, 0}) {   // op #6 x tile buffers: one per group, one shared, none
     if (epi != EP6_LN && xs != 0) continue;
-    for (int G : {4, 2}) {
+    for (int G : {4, 2, 1}) {
         if (G * pl.BN > 512) continue;
+        if (G == 1 && !pl.pair) continue;   // (one accumulator buffer: the pair op #6 plan only)
         if (xs > 1 && xs != G) continue;
         const uint32_t rbb = rb ? resb_bytes : 0u;
         const int bn_b = pl.pair ? pl.BN / 2 : pl.BN;   // B rows per stage in one CTA
@@ -282,6 +284,19 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
     pl.ebytes = ebytes;
     pl.threads = kernel_threads(epi);
     if (full_row) {
+        // op #6 on a CTA pair (cta_group::2, M = 256): the whole row (BN = N <= 512, two
+        // N/2 MMAs past 256) in each CTA's TMEM, each CTA streaming half of every W2
+        // K-block -- fewer operand bytes per MAC than the column-split cluster, but one
+        // accumulator buffer (the LayerNorm drain is exposed) and a 2-deep ring.  Measured
+        // slower (Swin-B b128 stack 2.03 ms vs 1.87 ms; C = 512: 27 us per tile pair), so
+        // opt-in: SWIN_MLP_LN_PAIR=1 (read per create).
+        const char* lp = std::getenv("SWIN_MLP_LN_PAIR");
+        const bool ln_pair = lp && *lp == '1';
+        if (ln_pair && N <= 512 && N > 256 && N % 64 == 0) {
+            pl.BN = N; pl.CS = 1; pl.n_groups = 1; pl.pair = 1;
+            if (fit_smem(epi, pl, 2, K)) return true;
+            pl.pair = 0;
+        }
         for (int cs : {1, 2, 4, 8}) {
             if (N % cs) continue;
             const int bn = N / cs;
@@ -654,14 +669,17 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     if (d.x_zero_point) H_TRY(upload(h, zc1, &h->zc1));
     if (d.h_zero_point) H_TRY(upload(h, zc2, &h->zc2));
     H_TRY(encode_2d(&h->tm_w1, h->w1, H, C, C, (uint32_t)(h->p1.pair ? h->p1.BN / 2 : h->p1.BN)));
-    H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H, (uint32_t)h->p2.BN));
+    // W2 boxes: BN rows, or (pair) the BN/4 or BN/2 rows a CTA holds per MMA half
+    H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H,
+                    (uint32_t)(h->p2.pair ? (h->p2.BN > 256 ? h->p2.BN / 4 : h->p2.BN / 2) : h->p2.BN)));
     // |A1| <= (128 + |z_x|) * 127 * C: below 2^22 the exact magic-number int->float applies
     const bool small_k1 = (int64_t)(128 + std::abs(d.x_zero_point)) * 127 * C < (int64_t(1) << 22);
     h->p1.fn = kernel_for(epi1,
                           (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (d.h_zero_point ? kZqNz : 0) |
                           (small_k1 ? kSmallK : 0) | (h->p1.pair ? kPair : 0));
     h->p2.fn = kernel_for(EP6_LN, (d.b2 ? kHasB : 0) | (d.h_zero_point ? kHasZc : 0) |
-                                      (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0));
+                                      (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0) |
+                                      (h->p2.pair ? kPair : 0));
     H_TRY(prepare(h->p1, h->num_sms));
     H_TRY(prepare(h->p2, h->num_sms));
     if (h->unfused) {
@@ -672,10 +690,11 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     } else if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp, fused_pair_for(C))) {
         const int ff = (d.act == SWIN_MLP_ACT_GELU_ERF ? kFGelu : 0) | (d.h_zero_point ? kFZh : 0) |
                        (d.b1 ? kFB1 : 0) | (d.ln_fp64 ? kFS64 : 0) | (small_k1 ? kFSmallK : 0);
-        // op #6 register path when a thread's half row is at most kFRegCh chunks of 16
-        // (SWIN_MLP_FUSED_REG=0 disables: A/B switch)
-        static const char* re = std::getenv("SWIN_MLP_FUSED_REG");
-        const bool reg = !(re && *re == '0') && !d.ln_fp64 && C / 2 <= 16 * kFRegCh;
+        // op #6 register path when a thread's half row is at most kFRegCh chunks of 16:
+        // opt-in (SWIN_MLP_FUSED_REG=1) -- measured no faster at C = 96 (op #6 is not bound
+        // by the TMEM park / reload it removes)
+        const char* re = std::getenv("SWIN_MLP_FUSED_REG");
+        const bool reg = re && *re == '1' && !d.ln_fp64 && C / 2 <= 16 * kFRegCh;
         const int fpair = h->fp.pair ? kFPair : 0;
         h->fp.fn = fused_kernel_for(ff | (reg && !fpair ? kFReg : 0) | fpair);
         h->fp_dbg = fused_kernel_for(ff | kFTaps | fpair);
@@ -730,6 +749,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         a.inv_h = h->inv_h; a.z_h = h->d.h_zero_point; a.inv_y = h->inv_y; a.z_y = h->d.y_zero_point;
         a.s_x = h->d.x_scale; a.z_x = h->d.x_zero_point; a.eps = h->d.ln_eps;
         a.x = x; a.resid = residual; a.resid_out = residual_out;
+        { const char* e = std::getenv("SWIN_MLP_FUSED_ROT"); a.rotate = (e && *e == '0') ? 0 : 1; }
         if (dbg) { a.acc1_tap = acc1; a.hid_tap = hidden; a.acc2_tap = acc2; a.ln_tap = ln_out; }
         a.trace = h->trace; a.trace_cta = h->trace_cta;
         a.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
@@ -799,8 +819,8 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.eg = h->p2.eg;
     { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; } a2.xstage = h->p2.xstage; a2.x = x;
     a2.out_w = h->p2.out_w;
-    a2.resb = h->p2.resb; a2.mt_major = 1;   // op #6: one n-group per cluster
-    a2.n_groups = 1; a2.num_units = m_tiles; a2.ldo = C;
+    a2.resb = h->p2.resb; a2.mt_major = h->p2.pair ? 0 : 1;   // op #6: one n-group per cluster
+    a2.n_groups = 1; a2.num_units = h->p2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
     a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
     a2.resid = residual; a2.resid_out = residual_out;

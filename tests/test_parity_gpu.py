@@ -168,6 +168,21 @@ def test_fused_opt_in_plans(dev, C, T, pair, monkeypatch):
     _run_and_check(dev, _layer(C, 8600 + C, act=1, bias=True, zx=3, zh=-128, zy=1), min(T, 400), e2e=False)
 
 
+@pytest.mark.parametrize("C,T", [(384, 148 * 256 * 2 + 77), (512, 148 * 256 + 300), (448, 1000), (320, 129)])
+def test_ln_pair_plan(dev, C, T, monkeypatch):
+    """FC2 + op #6 on a CTA pair (opt-in SWIN_MLP_LN_PAIR: cta_group::2, M = 256, whole row in
+    each CTA's TMEM, one accumulator buffer): several tiles per CTA (accumulator phase), odd
+    m-tile counts."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    monkeypatch.setenv("SWIN_MLP_LN_PAIR", "1")
+    L = _layer(C, 8800 + C)
+    pl = SwinMlpInt8Layer(L, device=0).plan()
+    assert pl["fused"] == 0 and pl["fc2_cs"] == 1 and pl["fc2_bn"] == C, pl
+    _run_and_check(dev, L, T, e2e=False)
+    _run_and_check(dev, _layer(C, 8900 + C, act=1, bias=True, zx=-3, zh=5, zy=2), min(T, 700), e2e=False,
+                   resid=True)
+
+
 def test_t_zero_is_noop(dev):
     from paper_2402_01169_b200 import SwinMlpInt8Layer
     layer = SwinMlpInt8Layer(_layer(96, 1), device=0)

@@ -1,5 +1,5 @@
 """Pipeline timeline of one CTA (debug trace) for a Swin-T batch-64 stage MLP.
-usage: python tools/trace_layer.py <stage> [cta]"""
+usage: python tools/trace_layer.py <stage | CxT> [cta]"""
 import sys
 
 import numpy as np
@@ -9,9 +9,13 @@ sys.path.insert(0, ".")
 import synth
 from paper_2402_01169_b200 import SwinMlpInt8Layer
 
-stage = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+arg = sys.argv[1] if len(sys.argv) > 1 else "0"
 cta = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-L, T, xs = synth.swin_t_batch64_layers()[stage]
+if "x" in arg:   # "<C>x<T>": any layer shape
+    C_, T_ = (int(v) for v in arg.split("x"))
+    L, T, xs = synth.make_layer(C_, 11), T_, 12
+else:
+    L, T, xs = synth.swin_t_batch64_layers()[int(arg)]
 layer = SwinMlpInt8Layer(L, device=0)
 x = torch.from_numpy(synth.make_activations(L, T, xs)).cuda()
 y = torch.empty((T, L.C), dtype=torch.int8, device="cuda")
