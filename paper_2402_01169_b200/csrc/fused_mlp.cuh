@@ -27,16 +27,14 @@
 //   warps 4-11   op #5: warp = (lane quadrant, 64-column half) of each acc1 chunk
 //   warps 12-19  op #6: warp = (lane quadrant, column half); a thread owns half a
 //                token row, the two halves combine their statistics pairwise
-//   warp 20      streamed weights: the W2 ring (its own warp, so the W1 items of the
-//                next chunks never queue behind a W2 slot still held by FC2)
 #pragma once
 #include "mlp_kernels.cuh"
 
 namespace swinmlp {
 
 constexpr int kFEp5W0 = 4, kFEp6W0 = 12;
-constexpr int kFW2Warp = 20;                 // streamed W2 producer
-constexpr int kFThreads = 32 * 21;          // 4 control + 8 op #5 + 8 op #6 + 1 W2 producer (96 regs each)
+constexpr int kFThreads = 32 * 20;          // 4 control + 8 op #5 + 8 op #6 warps (96 regs each; a 21st
+                                            // warp would cost 16 registers per thread: measured slower)
 constexpr int kFHc = 128;                    // hidden chunk = one 128-B K-block of FC2
 constexpr int kFMaxNB1 = 3, kFMaxNH = 4, kFMaxStages = 8;
 constexpr uint32_t kKB = (uint32_t)kBM * kBK;   // one [128 rows][128 B] box
@@ -263,6 +261,10 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     // the CTAs' streamed weight reads over different chunks (different L2 lines) instead
     // of every SM requesting the same chunk at the same time.
     const uint32_t rot = p.rotate ? cid % NJ : 0u;
+    // producer lookahead (chunks): the W1 items of FC1(q) are issued before the W2 items of
+    // FC2(q - LA); LA <= NB1 - 1 keeps every wait satisfiable by earlier work, LA <= NJ keeps
+    // the X-slot wait of the next tile behind the W2 loads it depends on
+    const uint32_t LA = min(NB1 - 1u, NJ);
     auto chunk_of = [&](uint32_t jj) -> uint32_t { const uint32_t c = jj + rot; return c >= NJ ? c - NJ : c; };
 
     if (warp == 0) {
@@ -291,10 +293,12 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         }
         pdl_wait();   // X: produced by the previous kernel
         // cursors advance incrementally (no runtime division in the role loops)
-        uint32_t i = 0, j = 0;             // FC1 tile / chunk of q
+        uint32_t i = 0, j = 0, j2 = 0;     // FC1 tile / chunk of q; FC2 chunk position of q - LA
         uint32_t xs = 0, xph = 0;          // X slot of tile i, its phase
-        for (uint32_t q = 0; q < U; ++q) {
-            {                                  // operands of FC1(q) (W2: warp kFW2Warp)
+        uint32_t s2 = 0, ph2 = 0;          // W2 ring
+        const uint32_t w2items = C > 256 ? 2u : 1u;
+        for (uint32_t q = 0; q < U + LA; ++q) {
+            if (q < U) {                       // operands of FC1(q)
                 if (j == 0) {
                     mbar_wait(bar_xempty + 8u * xs, xph ^ 1u);
                     if (elect_one()) {
@@ -329,14 +333,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                     if (++xs == NX) { xs = 0; xph ^= 1u; }
                 }
             }
-        }
-    } else if (warp == (uint32_t)kFW2Warp) {
-        // ====================== W2 producer (streamed weights) ======================
-        if (!resident) {
-            const uint32_t w2rows = C > 256 ? (uint32_t)C / 2u : (uint32_t)C;   // rows per FC2 MMA
-            const uint32_t w2items = C > 256 ? 2u : 1u;
-            uint32_t s2 = 0, ph2 = 0, j2 = 0;
-            for (uint32_t u = 0; u < U; ++u) {   // operands of FC2(u), in FC2's order
+            if (q >= LA && !resident) {        // operands of FC2(q - LA), in FC2's order
                 for (uint32_t h = 0; h < w2items; ++h) {   // one ring item per FC2 MMA half
                     mbar_wait(bar_w2empty + 8u * s2, ph2 ^ 1u);
                     if (elect_one()) {

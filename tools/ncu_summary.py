@@ -94,10 +94,20 @@ lines.append("|---|---|---|---|---|---|---|---|---|---|---|")
 specs = synth.swin_t_batch64_layers()
 for st in range(4):
     rep = os.path.join(ROOT, "gpurun_out", f"full_stage{st}.ncu-rep")
-    if not os.path.exists(rep):
+    raw_csv = os.path.join(ROOT, "gpurun_out", f"full_stage{st}_raw.csv")   # exported on the box
+    if os.path.exists(raw_csv):
+        raw = open(raw_csv).read()
+        shutil.copy(raw_csv, os.path.join(out, f"{tag}_full_stage{st}_raw.csv"))
+        det = raw_csv.replace("_raw.csv", "_details.csv")
+        if os.path.exists(det):
+            shutil.copy(det, os.path.join(out, f"{tag}_full_stage{st}_details.csv"))
+        if os.path.exists(rep):
+            shutil.copy(rep, os.path.join(out, f"{tag}_full_stage{st}.ncu-rep"))
+    elif os.path.exists(rep):
+        shutil.copy(rep, os.path.join(out, f"{tag}_full_stage{st}.ncu-rep"))
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    else:
         continue
-    shutil.copy(rep, os.path.join(out, f"{tag}_full_stage{st}.ncu-rep"))
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rr[0], rr[1], rr[2:]
     L, T, _ = specs[st]

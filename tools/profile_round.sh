@@ -5,9 +5,9 @@ set -u
 tag=${1:-r1}
 o=gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > $o/build_$tag.log 2>&1 || exit 1
-python bench.py --steps 2 --warmup 3 --pairs 1 --no-cpu > $o/plain_bench_$tag.log 2>&1 || exit 2
+python bench.py --steps 2 --warmup 3 --pairs 1 --no-cpu --no-stack > $o/plain_bench_$tag.log 2>&1 || exit 2
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches_$tag.csv \
-    python bench.py --steps 2 --warmup 3 --pairs 1 --no-cpu > $o/ncu_launch_$tag.log 2>&1
+    python bench.py --steps 2 --warmup 3 --pairs 1 --no-cpu --no-stack > $o/ncu_launch_$tag.log 2>&1
 for s in 0 1 2 3; do
   python tools/prof_layer.py $s 2 > $o/plain_${tag}_$s.log 2>&1 || continue
   # stages 0/1 run the one-kernel plan (1 launch per run), stages 2/3 two kernels
@@ -18,4 +18,18 @@ done
 for s in 2 3; do python tools/trace_layer.py $s > $o/trace_${tag}_$s.log 2>&1; done
 python tools/trace_fused.py 96 200704 > $o/trace_${tag}_0.log 2>&1
 python tools/trace_fused.py 192 50176 > $o/trace_${tag}_1.log 2>&1
+
+# FasterTransformer-layout arm (NEXT-1): launch list with DRAM bytes
+python tools/prof_ft.py gelu 1 > $o/plain_ft_$tag.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file $o/ft_launches_$tag.csv python tools/prof_ft.py gelu 1 > $o/ncu_ft_$tag.log 2>&1
+# bring-back budget (gpurun merges <= 64 MiB): raw + source CSV exports of every capture,
+# the .ncu-rep only for the dominant stage-0 kernel
+for s in 0 1 2 3; do
+  [ -f $o/full_stage$s.ncu-rep ] || continue
+  ncu -i $o/full_stage$s.ncu-rep --page raw --csv > $o/full_stage${s}_raw.csv 2>/dev/null
+  ncu -i $o/full_stage$s.ncu-rep --page details --csv > $o/full_stage${s}_details.csv 2>/dev/null
+  [ $s -gt 0 ] && rm -f $o/full_stage$s.ncu-rep
+done
+du -sh $o
 echo done
