@@ -109,6 +109,9 @@ struct GemmArgs {
     int32_t dbg;                      // debug experiments (0 in production)
     int32_t eg;                       // op #5 epilogue groups (1: all 16 warps drain every tile; or G)
     int32_t* acc_out;                 // EP_ACC: [M][ldo] int32 A1 (the unfused plan's GEMM output)
+    int32_t yin;                      // op #6 with xstage == G: Y staged over its own x tile (no
+                                      // separate output staging; the x buffer is released to the
+                                      // loader by the store warp once the stores have read Y)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -129,22 +132,25 @@ __host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages
 // eg: epilogue groups (G ping-pong groups, or 1: all 16 warps per tile), 4/eg column parts
 __host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int stages, int G, int ebytes = 4,
                                                   int xstage = 1, uint32_t resb_bytes = 0, int bn_b = 0,
-                                                  int eg = 0) {
+                                                  int eg = 0, int yin = 0, int csh = 0) {
     SmemLayout L;
     const uint32_t tile = (uint32_t)BN * kBM;
     L.a = 0;
     L.b = L.a + (uint32_t)stages * kBM * kBK;
     L.bres = L.b + (resb_bytes ? 0u : (uint32_t)stages * (uint32_t)(bn_b ? bn_b : BN) * kBK);
     L.out = L.bres + resb_bytes;                                   // [G] output staging tiles
-    L.xres = L.out + (epi == EP_ACC ? 0u : (uint32_t)G * tile);   // (EP_ACC stores from registers)                           // op #6: [G] residual x tiles
+    L.xres = L.out + (epi == EP_ACC || yin ? 0u : (uint32_t)G * tile);   // yin: out aliases xres   // (EP_ACC stores from registers)                           // op #6: [G] residual x tiles
     L.consts = L.xres + (epi == EP6_LN ? (uint32_t)xstage * tile : 0u);       // [G][kNConst][BN] fp32
-    L.bars = L.consts + (uint32_t)G * kNConst * (uint32_t)BN * 4u;
+    // csh: every tile of the CTA has the same columns (op #6, one column group) -> one
+    // constant buffer shared by the accumulator buffers
+    L.bars = L.consts + (csh ? 1u : (uint32_t)G) * kNConst * (uint32_t)BN * 4u;
     L.tmem_slot = L.bars + 8u * kNumBars(stages);
     const uint32_t eb = (uint32_t)ebytes;
     const uint32_t parts = 4u / (uint32_t)(eg ? eg : G);
+    const uint32_t npass = eb == 8u ? 2u : 1u;  // fp64 statistics: two exchange passes; fp32: one
     L.red = (L.tmem_slot + 8 + 15) & ~15u;      // op #6: [G][pass][part][val][row] (parts > 1 only)
-    L.xbuf = L.red + (epi == EP6_LN && parts > 1 ? (uint32_t)G * 2u * parts * 2u * kBM * eb : 0u);
-    L.total = L.xbuf + (epi == EP6_LN && CS > 1 ? (uint32_t)G * 2u * (uint32_t)CS * 2u * kBM * eb : 0u);
+    L.xbuf = L.red + (epi == EP6_LN && parts > 1 ? (uint32_t)G * npass * parts * 2u * kBM * eb : 0u);
+    L.total = L.xbuf + (epi == EP6_LN && CS > 1 ? (uint32_t)G * npass * (uint32_t)CS * 2u * kBM * eb : 0u);
     return L;
 }
 
@@ -247,7 +253,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t nh2 = (PAIR && BN > 256) ? 2u : 1u;
     const uint32_t nmma = (uint32_t)BN / nh2;            // UMMA N
     const uint32_t hrows = PAIR ? nmma / 2u : nmma;      // B rows per MMA half in this CTA
-    const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage, resb_bytes, bn_b, p.eg);
+    const bool csh = IS_LN && p.n_groups == 1;           // one shared constant buffer (see smem_layout)
+    constexpr uint32_t NPASS = STATS64 ? 2u : 1u;         // row-statistics exchange passes
+    const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage, resb_bytes, bn_b, p.eg,
+                                     IS_LN ? p.yin : 0, csh ? 1 : 0);
+    const bool yin = IS_LN && p.yin != 0;                 // Y staged over its x tile (xstage == G)
     const uint32_t tile_bytes = (uint32_t)BN * kBM;
     const uint32_t sA = base + L.a, sB = base + L.b;
     const uint32_t bar_full = base + L.bars;              // [stages] operands landed (count 1 + tx)
@@ -290,7 +300,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_init(bar_sfull + 8u * i, tile_warps);
             mbar_init(bar_sfree + 8u * i, 1);
             mbar_init(bar_xfull + 8u * i, 1);
-            mbar_init(bar_xfree + 8u * i, tile_warps);
+            mbar_init(bar_xfree + 8u * i, yin ? 1u : tile_warps);   // yin: the store warp frees it
             mbar_init(bar_xst + 16u * i, 1);
             mbar_init(bar_xst + 16u * i + 8u, 1);
         }
@@ -516,6 +526,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 bulk_wait_read<0>();              // the stores have read the staging tile
                 if (trc && it < 64) trc[2048 + 16 * it + 9] = gtimer();
                 mbar_arrive(bar_sfree + 8u * sb);
+                if (yin && p.resid == nullptr) mbar_arrive(bar_xfree + 8u * sb);   // (x tile == staging tile)
             }
             __syncwarp();
         }
@@ -548,7 +559,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
             mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);
             if (trc && lane == 0 && it < 512) trc[3072 + 2 * it] = gtimer();
-            float* cb = consts + (size_t)buf * kNConst * BN;
+            float* cb = consts + (size_t)(csh ? 0u : buf) * kNConst * BN;
+            if (!csh || it == 0)
             for (int c = (int)lane; c < BN; c += 32) {
                 const int n = n0 + c;
                 cb[0 * BN + c] = __ldg(p.m + n);
@@ -603,7 +615,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const int64_t row = (int64_t)m_tile * kBM + rit;
             const bool valid = row < p.M;
             const uint32_t tb = tmem_base + ((quad * 32u) << 16) + buf * (uint32_t)BN;
-            const float* cm = consts + (size_t)buf * kNConst * BN;
+            const float* cm = consts + (size_t)(csh ? 0u : buf) * kNConst * BN;
 
             // dQ (+bias) of one 16-column chunk, two columns per f32x2 op:
             // y = fl(fmaf(fl(acc - zc), m, b))  (bit-identical to the scalar form)
@@ -793,7 +805,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (!(p.dbg & 4)) tmem_st16(tb + (uint32_t)cl, r);
                 });
                 tmem_wait_st();
-                if (x_smem) {   // the x tile has been consumed: let the loader prefetch the next one
+                if (x_smem && !yin) {   // the x tile has been consumed: let the loader prefetch the next one
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bar_xfree + 8u * xbuf_of(it));
                 }
@@ -867,7 +879,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     const float q1 = nw > 0.f ? __fdiv_rn(S1, nw) : 0.f;
                     float m = __fadd_rn(K, q1), M2 = __fsub_rn(S2, __fmul_rn(S1, q1)), n = nw;
                     if (P > 1) {
-                        const uint32_t slot = (buf * 2u * P) * 2u;      // [G][pass 0][part][val]
+                        const uint32_t slot = (buf * NPASS * P) * 2u;   // [G][pass 0][part][val]
                         red[(slot + part * 2u) * kBM + rit] = m;
                         red[(slot + part * 2u + 1u) * kBM + rit] = M2;
                         named_bar_sync(1u + buf, 32u * tile_warps);
@@ -890,11 +902,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         n = na;
                     }
                     if (CS > 1) {
-                        const uint32_t sid = buf * 2u;
+                        const uint32_t sid = buf * 2u, sidd = buf * NPASS;   // barrier / data slot
                         const uint32_t xb = bar_xst + 8u * sid;
                         if (part == 0) {
                             if (grp_leader) mbar_arrive_expect_tx(xb, CS * kBM * 2u * (uint32_t)sizeof(acc_t));
-                            const uint32_t d0 = smem_u32(xbuf + (((size_t)sid * CS + rank) * 2u) * kBM + rit);
+                            const uint32_t d0 = smem_u32(xbuf + (((size_t)sidd * CS + rank) * 2u) * kBM + rit);
                             for (uint32_t r = 0; r < CS; ++r) {
                                 st_async_val(mapa(d0, r), (acc_t)m, mapa(xb, r));
                                 st_async_val(mapa(d0 + kBM * (uint32_t)sizeof(acc_t), r), (acc_t)M2, mapa(xb, r));
@@ -903,13 +915,13 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         mbar_wait_cluster(xb, aph);
                         float msum = 0.f, qsum = 0.f;
                         for (uint32_t r = 0; r < CS; ++r) {
-                            msum = __fadd_rn(msum, (float)xbuf[(((size_t)sid * CS + r) * 2u) * kBM + rit]);
-                            qsum = __fadd_rn(qsum, (float)xbuf[(((size_t)sid * CS + r) * 2u + 1u) * kBM + rit]);
+                            msum = __fadd_rn(msum, (float)xbuf[(((size_t)sidd * CS + r) * 2u) * kBM + rit]);
+                            qsum = __fadd_rn(qsum, (float)xbuf[(((size_t)sidd * CS + r) * 2u + 1u) * kBM + rit]);
                         }
                         const float mean = __fdiv_rn(msum, (float)CS);
                         float dsq = 0.f;
                         for (uint32_t r = 0; r < CS; ++r) {
-                            const float dr = __fsub_rn((float)xbuf[(((size_t)sid * CS + r) * 2u) * kBM + rit], mean);
+                            const float dr = __fsub_rn((float)xbuf[(((size_t)sidd * CS + r) * 2u) * kBM + rit], mean);
                             dsq = __fmaf_rn(dr, dr, dsq);
                         }
                         m = mean;

@@ -81,7 +81,7 @@ swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
 struct Plan {
     void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
     int epi = 0, threads = 0;
-    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0;
+    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0, yin = 0;
     int eg = 2;     // epilogue groups: G ping-pong groups, or 1 (all 16 warps drain every tile)
     int pair = 0;   // CTA pair (cta_group::2): clusters of 2 CTAs on m-tiles 2u, 2u+1 (CS == 1)
     uint32_t smem = 0;
@@ -247,18 +247,33 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // output staging: G ping-pong groups / accumulator buffers / staging tiles, 4 when
     // 4*BN TMEM columns fit (more tiles in flight), else 2; op #6 also prefers its
     // residual x tiles staged in smem
+    // SWIN_MLP_XS_MAX caps the op #6 x tile buffers (A/B switch: trades them for ring stages)
+    static const char* xs_env = std::getenv("SWIN_MLP_XS_MAX");
+    const int xs_max = xs_env && *xs_env ? atoi(xs_env) : 4;
     for (int xs : {4, 2, 1, 0}) {   // op #6 x tile buffers: one per group, one shared, none
     if (epi != EP6_LN && xs != 0) continue;
-    for (int G : {4, 2, 1}) {
+    if (xs > xs_max) continue;
+    // (op #6 prefers two accumulator buffers: at C = 512 G = 4 with a 3-deep ring measured
+    // 54.7 us vs 51.7 us for G = 2 with 4 stages)
+    static const int kGOrderLn[3] = {2, 4, 1}, kGOrder[3] = {4, 2, 1};
+    for (int gi = 0; gi < 3; ++gi) {
+        const int G = epi == EP6_LN ? kGOrderLn[gi] : kGOrder[gi];
         if (G * pl.BN > 512) continue;
         if (G == 1 && !pl.pair) continue;   // (one accumulator buffer: the pair op #6 plan only)
         if (xs > 1 && xs != G) continue;
         const uint32_t rbb = rb ? resb_bytes : 0u;
         const int bn_b = pl.pair ? pl.BN / 2 : pl.BN;   // B rows per stage in one CTA
+        // op #6 with one x tile per group: Y staged over its x tile (yin) frees G output tiles of
+        // smem for ring stages; SWIN_MLP_NO_YIN=1 keeps separate staging (A/B switch)
+        static const bool no_yin = std::getenv("SWIN_MLP_NO_YIN") != nullptr;
+        for (int yin : {1, 0}) {
+        if (yin && (epi != EP6_LN || xs != G || no_yin)) continue;
         for (int eg : {epilogue_groups(epi, G), G}) {
         pl.eg = eg;
+        pl.yin = yin;
         const uint32_t stage = (uint32_t)(kBM * kBK) + (rb ? 0u : (uint32_t)bn_b * kBK);
-        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb, bn_b, pl.eg).total + 1024;
+        const int csh = epi == EP6_LN && pl.n_groups == 1;
+        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb, bn_b, pl.eg, yin, csh).total + 1024;
         if (extra >= kSmemBudget) continue;
         int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
         if (stages > 8) stages = 8;
@@ -269,8 +284,9 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         pl.G = G;
         pl.xstage = xs;
         pl.resb = rb;
-        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb, bn_b, pl.eg).total + 1024;
+        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb, bn_b, pl.eg, yin, csh).total + 1024;
         if (pl.smem <= kSmemBudget) return true;
+        }
         }
     }
     }
@@ -297,8 +313,11 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
             if (fit_smem(epi, pl, 2, K)) return true;
             pl.pair = 0;
         }
+        // SWIN_MLP_LN_CS forces the op #6 cluster size (A/B switch)
+        static const char* cs_env = std::getenv("SWIN_MLP_LN_CS");
+        const int cs_force = cs_env && *cs_env ? atoi(cs_env) : 0;
         for (int cs : {1, 2, 4, 8}) {
-            if (N % cs) continue;
+            if (N % cs || (cs_force && cs != cs_force)) continue;
             const int bn = N / cs;
             if (bn > 256 || bn % 16) continue;
             pl.BN = bn; pl.CS = cs; pl.n_groups = 1;
@@ -817,7 +836,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
 
     GemmArgs a2 = {};
     a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.eg = h->p2.eg;
-    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; } a2.xstage = h->p2.xstage; a2.x = x;
+    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; } a2.xstage = h->p2.xstage; a2.yin = h->p2.yin; a2.x = x;
     a2.out_w = h->p2.out_w;
     a2.resb = h->p2.resb; a2.mt_major = h->p2.pair ? 0 : 1;   // op #6: one n-group per cluster
     a2.n_groups = 1; a2.num_units = h->p2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;

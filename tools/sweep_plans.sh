@@ -1,0 +1,7 @@
+# A/B sweep of plan switches on the Swin-B / Swin-T two-kernel shapes (GPU box; output in gpurun_out/sweep.log)
+o=gpurun_out/sweep.log; : > $o
+for CT in "512 25088" "1024 6272" "384 12544" "768 3136"; do
+  timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
+  SWIN_MLP_NO_YIN=1 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
+  SWIN_MLP_LN_CS=4 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
+done
