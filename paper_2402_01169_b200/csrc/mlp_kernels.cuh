@@ -112,6 +112,9 @@ struct GemmArgs {
     int32_t yin;                      // op #6 with xstage == G: Y staged over its own x tile (no
                                       // separate output staging; the x buffer is released to the
                                       // loader by the store warp once the stores have read Y)
+    int32_t dst;                      // op #5: Hq stored straight from registers to `out` (16-B
+                                      // st.global per chunk; no staging tiles, no store warp work)
+    int8_t* out;                      // [M][ldo] int8 output for dst
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -132,14 +135,14 @@ __host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages
 // eg: epilogue groups (G ping-pong groups, or 1: all 16 warps per tile), 4/eg column parts
 __host__ __device__ inline SmemLayout smem_layout(int epi, int BN, int CS, int stages, int G, int ebytes = 4,
                                                   int xstage = 1, uint32_t resb_bytes = 0, int bn_b = 0,
-                                                  int eg = 0, int yin = 0, int csh = 0) {
+                                                  int eg = 0, int yin = 0, int csh = 0, int dst = 0) {
     SmemLayout L;
     const uint32_t tile = (uint32_t)BN * kBM;
     L.a = 0;
     L.b = L.a + (uint32_t)stages * kBM * kBK;
     L.bres = L.b + (resb_bytes ? 0u : (uint32_t)stages * (uint32_t)(bn_b ? bn_b : BN) * kBK);
     L.out = L.bres + resb_bytes;                                   // [G] output staging tiles
-    L.xres = L.out + (epi == EP_ACC || yin ? 0u : (uint32_t)G * tile);   // yin: out aliases xres   // (EP_ACC stores from registers)                           // op #6: [G] residual x tiles
+    L.xres = L.out + (epi == EP_ACC || yin || dst ? 0u : (uint32_t)G * tile);   // yin: out aliases xres   // (EP_ACC stores from registers)                           // op #6: [G] residual x tiles
     L.consts = L.xres + (epi == EP6_LN ? (uint32_t)xstage * tile : 0u);       // [G][kNConst][BN] fp32
     // csh: every tile of the CTA has the same columns (op #6, one column group) -> one
     // constant buffer shared by the accumulator buffers
@@ -256,7 +259,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const bool csh = IS_LN && p.n_groups == 1;           // one shared constant buffer (see smem_layout)
     constexpr uint32_t NPASS = STATS64 ? 2u : 1u;         // row-statistics exchange passes
     const SmemLayout L = smem_layout(EPI, BN, p.CS, stages, p.G, (int)sizeof(acc_t), p.xstage, resb_bytes, bn_b, p.eg,
-                                     IS_LN ? p.yin : 0, csh ? 1 : 0);
+                                     IS_LN ? p.yin : 0, csh ? 1 : 0, p.dst);
+    const bool dst = !IS_LN && EPI != EP_ACC && p.dst != 0;   // op #5 direct global stores
     const bool yin = IS_LN && p.yin != 0;                 // Y staged over its x tile (xstage == G)
     const uint32_t tile_bytes = (uint32_t)BN * kBM;
     const uint32_t sA = base + L.a, sB = base + L.b;
@@ -509,7 +513,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     } else if (warp == 2) {
         // ============================ output store warp =========================
         pdl_wait();   // outputs may overwrite what the previous kernel still reads
-        for (uint32_t it = 0; it < my_tiles; ++it) {
+        for (uint32_t it = 0; it < (dst ? 0u : my_tiles); ++it) {
             const uint32_t sb = it & (G - 1u), sph = (it >> lgG) & 1u;
             mbar_wait(bar_sfull + 8u * sb, sph);
             if (trc && lane == 0 && it < 64) trc[2048 + 16 * it + 8] = gtimer();
@@ -607,7 +611,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const int n0 = n0_of(ng);
             const uint32_t buf = it & (G - 1u), aph = (it >> lgG) & 1u;
             const uint32_t sbuf = base + L.out + buf * tile_bytes;
-            mbar_wait(bar_sfree + 8u * buf, aph ^ 1u);   // staging tile read by its last stores
+            if (!dst) mbar_wait(bar_sfree + 8u * buf, aph ^ 1u);   // staging tile read by its last stores
             mbar_wait(bar_cfull + 8u * buf, aph);
             mbar_wait(bar_tfull + 8u * buf, aph);
             tc_fence_after();
@@ -713,7 +717,12 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                     uint32_t w[4];
                     quant_pack16<EPI == EP5_RELU, ZQNZ>(v, p.zq, w);
-                    st_shared_v4(sbuf + gran(ch), w[0], w[1], w[2], w[3]);
+                    if (dst) {
+                        if (valid) st_v4(p.out + row * (int64_t)p.ldo + n0 + cl,
+                                         make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]));
+                    } else {
+                        st_shared_v4(sbuf + gran(ch), w[0], w[1], w[2], w[3]);
+                    }
                 });
             } else {
                 // ---------------- fused op #6: dQ, bias, +residual, LayerNorm, Q ----------------
@@ -989,7 +998,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (rank == 0) mbar_arrive(bar_ptempty + 8u * buf);
                     else mbar_arrive_cluster(mapa(bar_ptempty + 8u * buf, 0));
                 }
-                mbar_arrive(bar_sfull + 8u * buf);    // this warp's part of the tile is staged
+                if (!dst) mbar_arrive(bar_sfull + 8u * buf);    // this warp's part of the tile is staged
             }
             if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 7] = gtimer();
         }

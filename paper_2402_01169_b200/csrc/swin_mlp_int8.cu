@@ -81,7 +81,7 @@ swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
 struct Plan {
     void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
     int epi = 0, threads = 0;
-    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0, yin = 0;
+    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0, yin = 0, dst = 0;
     int eg = 2;     // epilogue groups: G ping-pong groups, or 1 (all 16 warps drain every tile)
     int pair = 0;   // CTA pair (cta_group::2): clusters of 2 CTAs on m-tiles 2u, 2u+1 (CS == 1)
     uint32_t smem = 0;
@@ -266,14 +266,22 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         // op #6 with one x tile per group: Y staged over its x tile (yin) frees G output tiles of
         // smem for ring stages; SWIN_MLP_NO_YIN=1 keeps separate staging (A/B switch)
         static const bool no_yin = std::getenv("SWIN_MLP_NO_YIN") != nullptr;
+        // op #5: Hq stored from registers (no staging tiles, deeper ring), opt-in SWIN_MLP_DST=1:
+        // measured slower (C = 512 FC1 43.7 us with 6 stages vs 39.2 us staged with 4; the
+        // drain, not the ring, gates FC1 there)
+        static const char* dst_env = std::getenv("SWIN_MLP_DST");
+        static const bool no_dst = !(dst_env && *dst_env == '1');
+        for (int dst : {1, 0}) {
+        if (dst && (epi == EP6_LN || epi == EP_ACC || no_dst)) continue;
         for (int yin : {1, 0}) {
         if (yin && (epi != EP6_LN || xs != G || no_yin)) continue;
         for (int eg : {epilogue_groups(epi, G), G}) {
         pl.eg = eg;
         pl.yin = yin;
+        pl.dst = dst;
         const uint32_t stage = (uint32_t)(kBM * kBK) + (rb ? 0u : (uint32_t)bn_b * kBK);
         const int csh = epi == EP6_LN && pl.n_groups == 1;
-        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb, bn_b, pl.eg, yin, csh).total + 1024;
+        const uint32_t extra = smem_layout(epi, pl.BN, pl.CS, 0, G, pl.ebytes, xs, rbb, bn_b, pl.eg, yin, csh, dst).total + 1024;
         if (extra >= kSmemBudget) continue;
         int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
         if (stages > 8) stages = 8;
@@ -284,8 +292,9 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         pl.G = G;
         pl.xstage = xs;
         pl.resb = rb;
-        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb, bn_b, pl.eg, yin, csh).total + 1024;
+        pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb, bn_b, pl.eg, yin, csh, dst).total + 1024;
         if (pl.smem <= kSmemBudget) return true;
+        }
         }
         }
     }
@@ -691,8 +700,16 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     // W2 boxes: BN rows, or (pair) the BN/4 or BN/2 rows a CTA holds per MMA half
     H_TRY(encode_2d(&h->tm_w2, h->w2, C, H, H,
                     (uint32_t)(h->p2.pair ? (h->p2.BN > 256 ? h->p2.BN / 4 : h->p2.BN / 2) : h->p2.BN)));
-    // |A1| <= (128 + |z_x|) * 127 * C: below 2^22 the exact magic-number int->float applies
-    const bool small_k1 = (int64_t)(128 + std::abs(d.x_zero_point)) * 127 * C < (int64_t(1) << 22);
+    // |A1[t][n]| = |sum_k (X - z_x) W1[n][k]| <= (128 + |z_x|) * max_n sum_k |W1[n][k]| (a rigorous
+    // bound from the actual weights, tighter than 127 * C): below 2^22 the exact magic-number
+    // int->float applies (for max-abs-quantised Gaussian weights this holds up to C ~ 768)
+    int64_t w1_rowabs = 0;
+    for (int n = 0; n < H; ++n) {
+        int64_t s = 0;
+        for (int k = 0; k < C; ++k) s += std::abs((int)w1[(size_t)n * C + k]);
+        w1_rowabs = std::max(w1_rowabs, s);
+    }
+    const bool small_k1 = (int64_t)(128 + std::abs(d.x_zero_point)) * w1_rowabs < (int64_t(1) << 22);
     h->p1.fn = kernel_for(epi1,
                           (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (d.h_zero_point ? kZqNz : 0) |
                           (small_k1 ? kSmallK : 0) | (h->p1.pair ? kPair : 0));
@@ -830,6 +847,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a1.acc_tap = dbg ? acc1 : nullptr;
     int32_t* a1ws = h->unfused ? reinterpret_cast<int32_t*>(hq + ((T * H + 127) / 128 * 128)) : nullptr;
     a1.acc_out = a1ws;
+    a1.dst = h->p1.dst; a1.out = hq;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
     a1.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
     { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }

@@ -329,6 +329,39 @@ def test_parity_extreme_accumulators(dev, C):
     _tier_int8(taps["y"].cpu().numpy(), oracle.mlp(L, X), what="Y extreme")
 
 
+@pytest.mark.parametrize("C,zx", [(512, 0), (768, 0), (768, -3)])
+def test_parity_weight_bound_small_k(dev, C, zx):
+    """The exact magic-number int->float path of op #5 is chosen from the weights' own bound
+    (128 + |z_x|) * max_n sum_k |W1[n][k]| < 2^22.  Hidden unit 0 sits just under that bound and
+    is driven to it (|A1| = 4194176 or the largest multiple the zero point allows); unit 1 is just
+    over it for the bound-free path's sake on a second handle.  acc1 and Hq bit-exact."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(C, 9300 + C, zx=zx)
+    lim = (1 << 22) // (128 + abs(zx))            # row |sum| must stay below this
+    row = np.zeros(C, np.int8)
+    n127 = (lim - 1) // 127
+    row[:n127] = 127
+    row[n127] = (lim - 1) - 127 * n127            # sum |W1[0]| = lim - 1
+    L.w1[0] = row
+    L.w1[1] = -row
+    T = 260
+    X = synth.make_activations(L, T, 3)
+    X[:130, :n127 + 1] = -128                    # drives A1[:, 0] to -(128 + z_x) * (lim - 1)
+    X[130:, :n127 + 1] = 127
+    for variant in (0, 1):
+        if variant:
+            L.w1[2] = 127                          # bound exceeded: the I2F path
+        layer = SwinMlpInt8Layer(L, device=0)
+        taps = layer.run_debug(torch.from_numpy(X).to(dev))
+        torch.cuda.synchronize()
+        a1 = oracle.gemm_i8(X, L.w1, L.z_x)
+        if not variant:
+            assert np.abs(a1).max() < (1 << 22) and np.abs(a1[:, 0]).max() >= (1 << 22) - 2 * 255 * 128
+        np.testing.assert_array_equal(taps["acc1"].cpu().numpy(), a1)
+        m1, ih, m2, iy = oracle.fold_constants(L.s_x, L.s_w1, L.s_h, L.s_w2, L.s_y)
+        np.testing.assert_array_equal(taps["hidden"].cpu().numpy(), oracle.ep5(a1, m1, L.b1, ih, L.z_h))
+
+
 # ---- one-kernel plan (fused_mlp.cuh, C <= 256) vs the two-kernel plan ---------------------------
 
 @pytest.mark.parametrize("C,fused", [(96, 1), (128, 1), (192, 1), (256, 1), (384, 0), (512, 0), (768, 0)])

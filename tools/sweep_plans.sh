@@ -2,6 +2,5 @@
 o=gpurun_out/sweep.log; : > $o
 for CT in "512 25088" "1024 6272" "384 12544" "768 3136"; do
   timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
-  SWIN_MLP_NO_YIN=1 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
-  SWIN_MLP_LN_CS=4 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
+  SWIN_MLP_EP5_GROUPS=1 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
 done
