@@ -196,7 +196,8 @@ swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_
 
 /* Introspection: the launch plan of this layer, out10[20] = {FC1 BN, FC1 cluster size,
  * FC1 stages, FC1 max co-resident clusters, FC2 BN, FC2 cluster size, FC2 stages,
- * FC2 max clusters, FC1 epilogue groups, FC2 epilogue groups, FC1 resident weights,
+ * FC2 max clusters, FC1 epilogue groups, FC2 epilogue groups, FC1 resident weights (1: all,
+ * 2: each cluster's own column slice),
  * FC2 resident weights, one-kernel plan used (C <= 256, H % 128 == 0; 1/0), its weight
  * ring depth (0 = weights resident in smem), its hidden-tile buffers, its FC1 TMEM
  * buffers, FC1 CTA pair (cta_group::2 MMA, M = 256; 1/0), 0, 0, 0}.  Entries 0-11 and 16

@@ -115,6 +115,9 @@ struct GemmArgs {
     int32_t dst;                      // op #5: Hq stored straight from registers to `out` (16-B
                                       // st.global per chunk; no staging tiles, no store warp work)
     int8_t* out;                      // [M][ldo] int8 output for dst
+    int32_t wsl;                      // weight-stationary slice (op #5): each cluster owns ONE
+                                      // column group, keeps that B slice resident in smem (its half
+                                      // for a pair) and streams only A tiles through the ring
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -249,8 +252,10 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t lgEG = EG == 4u ? 2u : EG == 2u ? 1u : 0u;
     const uint32_t tile_warps = kEpiWarps / EG;
     using acc_t = typename std::conditional<STATS64, double, float>::type;   // LN statistics type
-    const uint32_t resb_bytes = p.resb ? (uint32_t)p.n_groups * (uint32_t)((p.K + kBK - 1) / kBK) * (uint32_t)BN * kBK : 0u;
     const int bn_b = PAIR ? BN / 2 : BN;                 // B rows per ring stage in this CTA
+    const bool wsl = !IS_LN && p.wsl != 0;               // weight-stationary slice (see GemmArgs)
+    const uint32_t resb_bytes = p.resb ? (uint32_t)p.n_groups * (uint32_t)((p.K + kBK - 1) / kBK) * (uint32_t)BN * kBK
+                              : wsl ? (uint32_t)((p.K + kBK - 1) / kBK) * (uint32_t)bn_b * kBK : 0u;
     // pair with BN > 256: two MMAs of N = BN/2 per K step; each CTA holds, per MMA half h,
     // B rows [h BN/2 + rank BN/4, + BN/4) as [h][BN/4 rows][128 B]
     const uint32_t nh2 = (PAIR && BN > 256) ? 2u : 1u;
@@ -339,10 +344,19 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // is reused across them; required by resident B).  Otherwise the (m, n) units
     // are dealt round-robin (more parallelism when there are few m-tiles).
     const uint32_t my_m = cid < m_tiles ? (m_tiles - cid + nclus - 1) / nclus : 0u;
-    const uint32_t my_tiles = p.mt_major ? my_m * n_groups
+    // weight-stationary slice: cluster cid owns column group g = cid % n_groups and the m units
+    // li, li + cnt, ... of it (cnt clusters share the group)
+    const uint32_t wg = cid % n_groups, wli = cid / n_groups;
+    const uint32_t wcnt = (nclus - wg + n_groups - 1) / n_groups;
+    const uint32_t my_tiles = wsl ? (wli < m_tiles ? (m_tiles - wli + wcnt - 1) / wcnt : 0u)
+                            : p.mt_major ? my_m * n_groups
                                          : (cid < num_units ? (num_units - cid + nclus - 1) / nclus : 0u);
     auto tile_at = [&](uint32_t it, uint32_t& m_tile, uint32_t& ng) {
-        if (p.mt_major) {
+        if (wsl) {
+            const uint32_t u = wli + it * wcnt;
+            m_tile = PAIR ? 2u * u + rank : u;
+            ng = wg;
+        } else if (p.mt_major) {
             m_tile = cid + (it / n_groups) * nclus;
             ng = it % n_groups;
         } else {
@@ -398,6 +412,40 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (++s == stages) { s = 0; ph ^= 1u; }
                 }
             }
+        } else if (wsl) {
+            // this cluster's B slice (this CTA's half rows for a pair), loaded once; the bytes
+            // of both CTAs of a pair complete on the leader's barrier
+            if (elect_one()) {
+                const uint32_t bb = PAIR ? mapa(bar_bfull, 0) : bar_bfull;
+                if (!PAIR || rank == 0) mbar_arrive_expect_tx(bar_bfull, (PAIR ? 2u : 1u) * (uint32_t)num_kb * b_bytes);
+                const int n0 = n0_of(wg) + (PAIR ? (int)(rank * hrows) : 0);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    if constexpr (PAIR) tma_load_2d_pair(&tmB, base + L.bres + (uint32_t)kb * b_bytes, bb, kb * kBK, n0);
+                    else tma_load_2d(&tmB, base + L.bres + (uint32_t)kb * b_bytes, bb, kb * kBK, n0);
+                }
+            }
+            __syncwarp();
+            pdl_wait();   // activations: produced by the previous kernel
+            for (uint32_t it = 0; it < my_tiles; ++it) {
+                uint32_t m_tile, ng;
+                tile_at(it, m_tile, ng);
+                const int row0 = (int)(m_tile * kBM);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(bar_empty + 8u * s, ph ^ 1u);
+                    if (elect_one()) {
+                        if (trc && kb == 0 && it < 512) trc[2 * it] = gtimer();
+                        if constexpr (PAIR) {
+                            if (rank == 0) mbar_arrive_expect_tx(bar_full + 8u * s, 2u * a_bytes);
+                            tma_load_2d_pair(&tmA, sA + (uint32_t)s * a_bytes, mapa(bar_full + 8u * s, 0), kb * kBK, row0);
+                        } else {
+                            mbar_arrive_expect_tx(bar_full + 8u * s, a_bytes);
+                            tma_load_2d(&tmA, sA + (uint32_t)s * a_bytes, bar_full + 8u * s, kb * kBK, row0);
+                        }
+                    }
+                    __syncwarp();
+                    if (++s == stages) { s = 0; ph ^= 1u; }
+                }
+            }
         } else {
             pdl_wait();   // activations: produced by the previous kernel
             for (uint32_t it = 0; it < my_tiles; ++it) {
@@ -445,7 +493,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t hoff16 = (hrows * kBK) >> 4;      // descriptor step to MMA half 1's B rows
         int s = 0;
         uint32_t ph = 0;
-        if (resb) mbar_wait(bar_bfull, 0);
+        if (resb || (wsl && (!PAIR || rank == 0))) mbar_wait(bar_bfull, 0);
         // one tile: MMAs over its k-blocks starting at ring slot (s0, ph0); with resident B
         // the n-groups of an m-tile share the A slots (waited by the first, released by the last)
         auto mma_tile = [&](uint32_t it, uint32_t ng, bool first, bool last, int& ss, uint32_t& pp) {
@@ -461,6 +509,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if (trc && lane == 0 && it < 256 && kb == 0) trc[1024 + 4 * it + 1] = gtimer();
                 const uint64_t ad = umma_desc_k128(sA + (uint32_t)ss * a_bytes);
                 const uint64_t bd = umma_desc_k128(resb ? base + L.bres + (ng * (uint32_t)num_kb + (uint32_t)kb) * b_bytes
+                                                   : wsl ? base + L.bres + (uint32_t)kb * b_bytes
                                                         : sB + (uint32_t)ss * b_bytes);
                 const int rem = p.K - kb * kBK;
                 const int nk = rem >= kBK ? 4 : rem / 32;

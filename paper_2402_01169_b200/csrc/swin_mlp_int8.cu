@@ -81,7 +81,7 @@ swin_mlp_status_t fail(swin_mlp_status_t st, const char* fmt, ...) {
 struct Plan {
     void (*fn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs) = nullptr;
     int epi = 0, threads = 0;
-    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0, yin = 0, dst = 0;
+    int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0, yin = 0, dst = 0, wsl = 0;
     int eg = 2;     // epilogue groups: G ping-pong groups, or 1 (all 16 warps drain every tile)
     int pair = 0;   // CTA pair (cta_group::2): clusters of 2 CTAs on m-tiles 2u, 2u+1 (CS == 1)
     uint32_t smem = 0;
@@ -239,16 +239,27 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // Resident B: the CTA's whole weight slice stays in smem and the ring streams
     // A (activations) only -- 2x deeper prefetch per byte of smem, and the weights
     // are read from L2 once per CTA instead of once per tile.  Tried first.
-    const uint32_t resb_bytes = (uint32_t)pl.n_groups * (uint32_t)num_kb * (uint32_t)pl.BN * kBK;
+    // Weight-stationary slice (op #5, mode 2): each cluster keeps only ITS column group's
+    // weights resident (half of them per CTA of a pair) and streams A tiles only -- half the
+    // operand bytes per MAC of the streamed plan.  Tried after whole-B residency.
     static const bool no_resb = std::getenv("SWIN_MLP_NO_RESB") != nullptr;   // debug / A-B switch
-    for (int rb : {1, 0}) {
-    if (rb && no_resb) continue;
-    if (rb && pl.pair) continue;   // pair: B streams (half per CTA)
+    // (opt-in SWIN_MLP_WSL=1: measured no faster -- C = 512 FC1 40.0 vs 41.0 us, C = 384
+    // 22.4 vs 20.7 us; halving the operand bytes does not move FC1, whose tiles are gated by
+    // the op #5 drain of the accumulator they reuse)
+    const char* wsl_env = std::getenv("SWIN_MLP_WSL");   // (read per create)
+    const bool no_wsl = !(wsl_env && *wsl_env == '1');
+    for (int mode : {1, 2, 0}) {   // 1: whole B resident, 2: this cluster's B slice, 0: streamed
+    const int rb = mode != 0;
+    if (mode == 1 && (no_resb || pl.pair)) continue;   // pair: B halves (mode 2 or streamed)
+    if (mode == 2 && (no_wsl || epi == EP6_LN || epi == EP_ACC || pl.CS != 1 || (pl.pair && pl.BN > 256))) continue;
+    const int bn_rows = pl.pair ? pl.BN / 2 : pl.BN;
+    const uint32_t resb_bytes = mode == 1 ? (uint32_t)pl.n_groups * (uint32_t)num_kb * (uint32_t)pl.BN * kBK
+                                          : (uint32_t)num_kb * (uint32_t)bn_rows * kBK;
     // output staging: G ping-pong groups / accumulator buffers / staging tiles, 4 when
     // 4*BN TMEM columns fit (more tiles in flight), else 2; op #6 also prefers its
     // residual x tiles staged in smem
     // SWIN_MLP_XS_MAX caps the op #6 x tile buffers (A/B switch: trades them for ring stages)
-    static const char* xs_env = std::getenv("SWIN_MLP_XS_MAX");
+    const char* xs_env = std::getenv("SWIN_MLP_XS_MAX");   // (read per create)
     const int xs_max = xs_env && *xs_env ? atoi(xs_env) : 4;
     for (int xs : {4, 2, 1, 0}) {   // op #6 x tile buffers: one per group, one shared, none
     if (epi != EP6_LN && xs != 0) continue;
@@ -259,18 +270,18 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     for (int gi = 0; gi < 3; ++gi) {
         const int G = epi == EP6_LN ? kGOrderLn[gi] : kGOrder[gi];
         if (G * pl.BN > 512) continue;
-        if (G == 1 && !pl.pair) continue;   // (one accumulator buffer: the pair op #6 plan only)
+        if (G == 1 && (!pl.pair || epi != EP6_LN)) continue;   // (one accumulator buffer: the pair op #6 plan only)
         if (xs > 1 && xs != G) continue;
         const uint32_t rbb = rb ? resb_bytes : 0u;
         const int bn_b = pl.pair ? pl.BN / 2 : pl.BN;   // B rows per stage in one CTA
         // op #6 with one x tile per group: Y staged over its x tile (yin) frees G output tiles of
         // smem for ring stages; SWIN_MLP_NO_YIN=1 keeps separate staging (A/B switch)
-        static const bool no_yin = std::getenv("SWIN_MLP_NO_YIN") != nullptr;
+        const bool no_yin = std::getenv("SWIN_MLP_NO_YIN") != nullptr;   // (read per create)
         // op #5: Hq stored from registers (no staging tiles, deeper ring), opt-in SWIN_MLP_DST=1:
         // measured slower (C = 512 FC1 43.7 us with 6 stages vs 39.2 us staged with 4; the
         // drain, not the ring, gates FC1 there)
-        static const char* dst_env = std::getenv("SWIN_MLP_DST");
-        static const bool no_dst = !(dst_env && *dst_env == '1');
+        const char* dst_env = std::getenv("SWIN_MLP_DST");   // (read per create)
+        const bool no_dst = !(dst_env && *dst_env == '1');
         for (int dst : {1, 0}) {
         if (dst && (epi == EP6_LN || epi == EP_ACC || no_dst)) continue;
         for (int yin : {1, 0}) {
@@ -286,12 +297,14 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         int stages = (int)((kSmemBudget - extra - 64u * 8u) / stage);
         if (stages > 8) stages = 8;
         int need = min_stages;
-        if (rb) need = std::max(need, pl.n_groups > 1 ? num_kb + 2 : 3);   // an m-tile's k-blocks stay resident
+        if (mode == 1) need = std::max(need, pl.n_groups > 1 ? num_kb + 2 : 3);   // an m-tile's k-blocks stay resident
+        if (mode == 2) need = std::max(need, 3);
         if (stages < need) continue;
         pl.stages = stages;
         pl.G = G;
         pl.xstage = xs;
-        pl.resb = rb;
+        pl.resb = mode == 1;
+        pl.wsl = mode == 2;
         pl.smem = smem_layout(epi, pl.BN, pl.CS, stages, G, pl.ebytes, xs, rbb, bn_b, pl.eg, yin, csh, dst).total + 1024;
         if (pl.smem <= kSmemBudget) return true;
         }
@@ -323,7 +336,7 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
             pl.pair = 0;
         }
         // SWIN_MLP_LN_CS forces the op #6 cluster size (A/B switch)
-        static const char* cs_env = std::getenv("SWIN_MLP_LN_CS");
+        const char* cs_env = std::getenv("SWIN_MLP_LN_CS");   // (read per create)
         const int cs_force = cs_env && *cs_env ? atoi(cs_env) : 0;
         for (int cs : {1, 2, 4, 8}) {
             if (N % cs || (cs_force && cs != cs_force)) continue;
@@ -438,6 +451,8 @@ swin_mlp_status_t launch(const Plan& pl, const CUtensorMap& ta, const CUtensorMa
     // independent work items: m-tiles in m-major order, (m, n) units otherwise
     const int64_t units = a.mt_major ? a.num_units / a.n_groups : a.num_units;
     int64_t clusters = units < pl.max_clusters ? units : pl.max_clusters;
+    // weight-stationary slices: the same number of clusters on every column group
+    if (a.wsl && clusters > a.n_groups) clusters -= clusters % a.n_groups;
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
     const int cl = pl.pair ? 2 : pl.CS;   // CTAs per cluster
@@ -847,7 +862,8 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a1.acc_tap = dbg ? acc1 : nullptr;
     int32_t* a1ws = h->unfused ? reinterpret_cast<int32_t*>(hq + ((T * H + 127) / 128 * 128)) : nullptr;
     a1.acc_out = a1ws;
-    a1.dst = h->p1.dst; a1.out = hq;
+    a1.dst = h->p1.dst; a1.out = hq; a1.wsl = h->p1.wsl;
+    if (h->p1.wsl) a1.mt_major = 0;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
     a1.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
     { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }
@@ -1127,7 +1143,7 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
     out10[0] = h->p1.BN; out10[1] = h->p1.CS; out10[2] = h->p1.stages; out10[3] = h->p1.max_clusters;
     out10[4] = h->p2.BN; out10[5] = h->p2.CS; out10[6] = h->p2.stages; out10[7] = h->p2.max_clusters;
     out10[8] = h->p1.G; out10[9] = h->p2.G;
-    out10[10] = h->p1.resb; out10[11] = h->p2.resb;
+    out10[10] = h->p1.resb ? 1 : h->p1.wsl ? 2 : 0; out10[11] = h->p2.resb;
     out10[12] = h->fp.on ? 1 : 0; out10[13] = h->fp.stages; out10[14] = h->fp.NH; out10[15] = h->fp.NB1;
     out10[16] = h->p1.pair; out10[17] = h->fp.NX; out10[18] = h->fp.stages2; out10[19] = h->unfused ? 1 : 0;
     return 0;

@@ -403,3 +403,29 @@ def test_fc1_cta_pair(dev, C, T):
     assert SwinMlpInt8Layer(L, device=0).plan()["fc1_pair"] == 1
     _run_and_check(dev, L, T, e2e=False)
     _run_and_check(dev, _layer(C, 9600 + C, act=1, bias=True, zx=-5, zh=-3, zy=2), T, e2e=False)
+
+
+@pytest.mark.parametrize("C,T,env", [
+    (512, 20 * 128 + 77, {"SWIN_MLP_WSL": "1"}),                      # weight-stationary slices, pair
+    (384, 13 * 128 + 5, {"SWIN_MLP_WSL": "1"}),                       # ... single CTA
+    (768, 3 * 128 - 51, {"SWIN_MLP_DST": "1"}),                       # op #5 stores from registers
+    (512, 9 * 128 + 1, {"SWIN_MLP_NO_YIN": "1"}),                     # op #6 separate Y staging
+    (512, 9 * 128 + 1, {"SWIN_MLP_LN_CS": "4"}),                      # op #6 4-CTA column split
+    (1024, 7 * 128 + 100, {}),                                        # op #6 yin at cs = 4, BN = 256
+])
+def test_gemm_plan_variants(dev, C, T, env, monkeypatch):
+    """Two-kernel plan variants: opt-in FC1 weight-stationary slices and
+    direct Hq stores, op #6 with and without Y staged over its x tile, forced cluster sizes;
+    ReLU paper mode and GELU with bias and zero points, bit-exact / tiered against the oracle."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    L = _layer(C, 9700 + C)
+    plan = SwinMlpInt8Layer(L, device=0).plan()
+    assert plan["fused"] == 0
+    if "SWIN_MLP_WSL" in env:
+        assert plan["fc1_resb"] == 2
+    if "SWIN_MLP_LN_CS" in env:
+        assert plan["fc2_cs"] == int(env["SWIN_MLP_LN_CS"])
+    _run_and_check(dev, L, T, e2e=False)
+    _run_and_check(dev, _layer(C, 9800 + C, act=1, bias=True, zx=-5, zh=-3, zy=2), T, e2e=False)
