@@ -361,8 +361,11 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
     // SWIN_MLP_PAIR=1 / 0 forces it on / off.
     static const char* pair_env = std::getenv("SWIN_MLP_PAIR");
     const bool want_pair = pair_env ? (*pair_env == '1') : K >= 512;
-    if (epi != EP6_LN && want_pair && N % 256 == 0) {
-        pl.BN = 256; pl.CS = 1; pl.n_groups = N / 256; pl.pair = 1;
+    // SWIN_MLP_PAIR_BN = 128 / 192: narrower pair tiles (more accumulator buffers) -- A/B switch
+    const char* pbn_env = std::getenv("SWIN_MLP_PAIR_BN");   // (read per create)
+    const int pbn = pbn_env && *pbn_env ? atoi(pbn_env) : 256;
+    if (epi != EP6_LN && want_pair && (pbn == 128 || pbn == 192 || pbn == 256) && N % pbn == 0) {
+        pl.BN = pbn; pl.CS = 1; pl.n_groups = N / pbn; pl.pair = 1;
         if (fit_smem(epi, pl, 3, K)) return true;
         pl.pair = 0;
     }

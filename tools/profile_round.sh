@@ -19,17 +19,24 @@ for s in 2 3; do python tools/trace_layer.py $s > $o/trace_${tag}_$s.log 2>&1; d
 python tools/trace_fused.py 96 200704 > $o/trace_${tag}_0.log 2>&1
 python tools/trace_fused.py 192 50176 > $o/trace_${tag}_1.log 2>&1
 
+# north-star stage: Swin-B b128 stage 3 layer (C = 512, T = 25088), both kernels
+python tools/layer_sweep.py 512 25088 3 > $o/plain_swinb3_$tag.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:mlp_gemm_kernel -s 6 -c 2 -o $o/full_swinb3 -f \
+    python tools/layer_sweep.py 512 25088 3 > $o/ncu_full_swinb3_$tag.log 2>&1
+python tools/stack_bench.py 4 3 --steps 10 > $o/stack_$tag.log 2>&1
+
 # FasterTransformer-layout arm (NEXT-1): launch list with DRAM bytes
 python tools/prof_ft.py gelu 1 > $o/plain_ft_$tag.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $o/ft_launches_$tag.csv python tools/prof_ft.py gelu 1 > $o/ncu_ft_$tag.log 2>&1
 # bring-back budget (gpurun merges <= 64 MiB): raw + source CSV exports of every capture,
 # the .ncu-rep only for the dominant stage-0 kernel
-for s in 0 1 2 3; do
-  [ -f $o/full_stage$s.ncu-rep ] || continue
+for s in 0 1 2 3 swinb3; do
+  [ -f $o/full_stage$s.ncu-rep ] || [ -f $o/full_$s.ncu-rep ] || continue
+  [ -f $o/full_$s.ncu-rep ] && mv $o/full_$s.ncu-rep $o/full_stage$s.ncu-rep
   ncu -i $o/full_stage$s.ncu-rep --page raw --csv > $o/full_stage${s}_raw.csv 2>/dev/null
   ncu -i $o/full_stage$s.ncu-rep --page details --csv > $o/full_stage${s}_details.csv 2>/dev/null
-  [ $s -gt 0 ] && rm -f $o/full_stage$s.ncu-rep
+  [ "$s" != 0 ] && rm -f $o/full_stage$s.ncu-rep
 done
 du -sh $o
 echo done
