@@ -396,6 +396,11 @@ def main():
                                        "int8_peak_tops", "stages", "l2")}
         torch.cuda.empty_cache()
 
+    # ---- NEXT-2 row: proj GEMM + fused op #4 (+LN2), one kernel per layer --------
+    proj = None
+    if rank == 0 and not args.no_stack:
+        proj = proj_rows(max(3, min(args.steps, 20)))
+
     # ---- CPU baseline: the oracle as it stands on this host (rank 0, N=1 only) ----------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -418,12 +423,50 @@ def main():
                 "gpu_launches": sum(n * P.swin_mlp_int8_launches_per_run(l.handle) for (_, _, n), l in zip(prof, relu_layers)),
                 "relu_vs_gelu": relu_gelu,
                 "north_star_stack": stack,
+                "proj_op4": proj,
                 "tensor_frac_of_step": roofline["step_frac"],
                 "clocks": sampler.result()}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def proj_rows(steps):
+    """Proj GEMM + op #4 (+LN2) (swin_proj_int8_run) at the Swin-T b64 stage shapes and the Swin-B
+    b128 stage-3 shape: CUDA events on the launching stream around `steps` back-to-back launches,
+    L2 flushed before each; ops = 2*T*C*C per launch (int8 tensor roof)."""
+    import torch
+    import synth
+    from paper_2402_01169_b200 import SwinProjInt8Layer
+    peak = 2.0 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    rows = []
+    for C, T in ((96, 200704), (192, 50176), (384, 12544), (768, 3136), (512, 25088)):
+        Pl = synth.make_proj(C, synth.layer_seed(2, 0, 90) + C)
+        layer = SwinProjInt8Layer(Pl, device=0)
+        a = torch.from_numpy(synth.make_attn_out(Pl, T, 5)).cuda()
+        r = torch.from_numpy(synth.make_residual(T, C, 6)).cuda()
+        y = torch.empty_like(a)
+        z = torch.empty_like(r)
+        for _ in range(3):
+            layer(a, r, y=y, residual_out=z)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for k in range(steps):
+            flush.fill_(k & 0xff)
+            ev[k][0].record()
+            layer(a, r, y=y, residual_out=z)
+            ev[k][1].record()
+        torch.cuda.synchronize()
+        us = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in ev)[steps // 2]
+        tops = 2.0 * T * C * C / (us * 1e-6) / 1e12
+        rows.append({"C": C, "T": T, "us_median": round(us, 2), "tokens_per_s": T / (us * 1e-6),
+                     "tops": round(tops, 1), "tensor_frac": round(tops / peak, 3),
+                     "hbm_gbs": round((2 * C + 8 * C) * T / (us * 1e-6) / 1e9, 1), "plan": layer.plan()})
+        del layer
+    return {"what": "swin_proj_int8_run: Proj GEMM + op #4 + LN2 (PAPER.md Fig. 1 lines 63-70, reading R18)",
+            "bytes_per_token": "C (a) + 4C (residual) + C (y) + 4C (z)", "rows": rows, "steps": steps}
 
 
 if __name__ == "__main__":

@@ -208,6 +208,59 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
 /* Release the handle's device memory.  No run may be in flight. NULL is OK. */
 swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h);
 
+/* ------------------------------------------------------------------------------------
+ * the attention projection GEMM + fused op #4 (Fig. 1,
+ * lines 63-70: Proj GEMM -> dQ -> Proj Bias -> Add (Residual) -> Q), the step that
+ * produces the MLP sub-layer's input.  For T tokens of C channels:
+ *
+ *   Proj GEMM  A[t][c] = sum_k (Xa[t][k] - z_a) * W[c][k]          int32 (exact)
+ *   op #4      d = fmaf(fl(A), m[c], b[c] or 0),  m[c] = fl(a_scale * w_scale[c])
+ *              z = fl(d + residual[t][c])             (residual: the block's fp32 shortcut)
+ *              yhat = LayerNorm2(z) (as op #6: fp64 or fp32 statistics, biased variance)
+ *              Y = clamp(rne(fl(yhat * inv_y)) + y_zero_point, -128, 127)
+ *
+ * Reading (R18): Fig. 1 draws op #4 as dQ/bias/add/Q with no LayerNorm, but the
+ * Swin block is pre-norm: FC1 consumes LN2(x + proj), so LN2 is fused into op #4's
+ * epilogue here -- Y is the int8 MLP input, residual_out = z is the fp32 residual stream the
+ * MLP sub-layer adds back (its `residual` argument).  The arithmetic is op #6's with K = C.
+ *
+ * Errors, ownership, layout and alignment follow swin_mlp_int8_* (Xa, Y [T][C] int8 row-major;
+ * W [C][C] int8 nn.Linear [out][in], symmetric, per-output-channel scales).  `residual` is
+ * required (op #4 always adds the shortcut).  No workspace. */
+typedef struct swin_proj_int8_s* swin_proj_int8_t;
+
+typedef struct {
+    int32_t C;                  /* channels; C % 32 == 0, 32 <= C <= 1536                  */
+    float   a_scale;            /* attention-output (Proj GEMM input) scale > 0           */
+    int32_t a_zero_point;       /* in [-128, 127]                                          */
+    const int8_t* w;            /* [C][C] proj weights                                     */
+    const float*  w_scale;      /* [C], > 0                                                */
+    const float*  b;            /* [C] proj bias or NULL                                   */
+    const float*  ln_gamma;     /* [C] LN2                                                 */
+    const float*  ln_beta;      /* [C]                                                     */
+    float   ln_eps;             /* > 0                                                     */
+    float   y_scale;            /* output (MLP input) scale > 0                            */
+    int32_t y_zero_point;       /* in [-128, 127]                                          */
+    int32_t device;
+    int32_t ln_fp64;            /* as swin_mlp_int8_desc_t.ln_fp64                         */
+} swin_proj_int8_desc_t;
+
+swin_mlp_status_t swin_proj_int8_create(const swin_proj_int8_desc_t* desc, swin_proj_int8_t* out);
+/*   a            [T][C] int8, device, 16-byte aligned (the V*att output, quantized)
+ *   residual     [T][C] fp32, device, 16-byte aligned, required
+ *   y            [T][C] int8, device, 16-byte aligned
+ *   residual_out [T][C] fp32, device, or NULL: receives z
+ * T >= 0 (0: no launch).  One kernel launch, stream-ordered, asynchronous. */
+swin_mlp_status_t swin_proj_int8_run(swin_proj_int8_t h, const int8_t* a, const float* residual, int8_t* y,
+                                     float* residual_out, int64_t T, void* stream);
+/* run + debug taps (device, any may be NULL): acc [T][C] int32 (A), ln_out [T][C] fp32 (yhat). */
+swin_mlp_status_t swin_proj_int8_run_debug(swin_proj_int8_t h, const int8_t* a, const float* residual, int8_t* y,
+                                           float* residual_out, int64_t T, void* stream, int32_t* acc,
+                                           float* ln_out);
+/* Launch plan: out4 = {BN, cluster size, ring stages, CTA pair}.  Returns 0, or -1 on NULL. */
+int32_t swin_proj_int8_plan(swin_proj_int8_t h, int32_t* out4);
+swin_mlp_status_t swin_proj_int8_destroy(swin_proj_int8_t h);
+
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* swin_mlp_int8_last_error(void);
 

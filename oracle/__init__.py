@@ -132,6 +132,21 @@ def ep6(A2, m2, b2, X, s_x, z_x, gamma, beta, eps, inv_y, z_y, R=None):
     return Y, yh, z
 
 
+def proj_op4(P, A_in, R):
+    """SURVEY.md §8(f) NEXT-2, Fig. 1 lines 63-70 (Proj GEMM -> fused op #4: dQ -> Proj
+    Bias -> Add (Residual) -> Q), with LN2 before the Q (reading R18: the Swin block is
+    pre-norm, so FC1's input is LN2(x + proj)).  Composition of the pinned steps, in this order:
+      O3  A[t,c] = sum_k (A_in[t,k] - z_a) * W[c,k]             (gemm_i8)
+      O0  m[c] = fl(s_a * s_w[c]), inv_y = fl(1/s_y)              (fold_constants, h-slot = s_a)
+      O4-O6 with the fp32 shortcut R: z = fl(fmaf(fl(A), m, b) + R); yhat = LN2(z); Y = Q_y(yhat)
+    Returns (Y int8, yhat fp32, z fp32, A int32)."""
+    A = gemm_i8(A_in, P.w, P.z_a)
+    C = P.C
+    _, _, m, inv_y = fold_constants(1.0, np.ones(C, np.float32), P.s_a, P.s_w, P.s_y)
+    Y, yhat, z = ep6(A, m, P.b, np.zeros_like(A_in), 1.0, 0, P.gamma, P.beta, P.eps, inv_y, P.z_y, R=R)
+    return Y, yhat, z, A
+
+
 class _Layer(ctypes.Structure):
     _fields_ = [("C", ctypes.c_int32), ("H", ctypes.c_int32), ("act", ctypes.c_int32),
                 ("s_x", ctypes.c_float), ("z_x", ctypes.c_int32),

@@ -32,6 +32,8 @@ EXPORTS = [
     "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end", "swin_mlp_int8_set_trace",
     "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
     "swin_mlp_int8_host_batch_workspace_bytes", "swin_mlp_int8_run_host_batch",
+    "swin_proj_int8_create", "swin_proj_int8_run", "swin_proj_int8_run_debug", "swin_proj_int8_plan",
+    "swin_proj_int8_destroy",
 ]
 
 
@@ -46,6 +48,16 @@ class swin_mlp_int8_desc_t(ctypes.Structure):
         ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32),
         ("device", ctypes.c_int32), ("ln_fp64", ctypes.c_int32),
         ("op5_unfused", ctypes.c_int32),
+    ]
+
+
+class swin_proj_int8_desc_t(ctypes.Structure):
+    _fields_ = [
+        ("C", ctypes.c_int32), ("a_scale", ctypes.c_float), ("a_zero_point", ctypes.c_int32),
+        ("w", ctypes.c_void_p), ("w_scale", ctypes.c_void_p), ("b", ctypes.c_void_p),
+        ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
+        ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32),
+        ("device", ctypes.c_int32), ("ln_fp64", ctypes.c_int32),
     ]
 
 
@@ -97,6 +109,16 @@ def lib():
     L.swin_mlp_int8_host_batch_workspace_bytes.restype = sz
     L.swin_mlp_int8_run_host_batch.argtypes = [i32, P, P, P, P, P, sz, P]
     L.swin_mlp_int8_run_host_batch.restype = i32
+    L.swin_proj_int8_create.argtypes = [ctypes.POINTER(swin_proj_int8_desc_t), ctypes.POINTER(P)]
+    L.swin_proj_int8_create.restype = i32
+    L.swin_proj_int8_run.argtypes = [P, P, P, P, P, i64, P]
+    L.swin_proj_int8_run.restype = i32
+    L.swin_proj_int8_run_debug.argtypes = [P, P, P, P, P, i64, P, P, P]
+    L.swin_proj_int8_run_debug.restype = i32
+    L.swin_proj_int8_plan.argtypes = [P, P]
+    L.swin_proj_int8_plan.restype = i32
+    L.swin_proj_int8_destroy.argtypes = [P]
+    L.swin_proj_int8_destroy.restype = i32
     L.swin_mlp_int8_last_error.argtypes = []
     L.swin_mlp_int8_last_error.restype = ctypes.c_char_p
     _lib = L
@@ -173,6 +195,24 @@ def swin_mlp_int8_launches_per_run(h) -> int:
 
 def swin_mlp_int8_last_error() -> str:
     return last_error()
+
+
+def swin_proj_int8_create(desc: swin_proj_int8_desc_t) -> int:
+    h = ctypes.c_void_p()
+    _check(lib().swin_proj_int8_create(ctypes.byref(desc), ctypes.byref(h)))
+    return h.value
+
+
+def swin_proj_int8_run(h, a, residual, y, residual_out, T, stream):
+    _check(lib().swin_proj_int8_run(h, a, residual, y, residual_out, T, stream))
+
+
+def swin_proj_int8_run_debug(h, a, residual, y, residual_out, T, stream, acc, ln_out):
+    _check(lib().swin_proj_int8_run_debug(h, a, residual, y, residual_out, T, stream, acc, ln_out))
+
+
+def swin_proj_int8_destroy(h):
+    _check(lib().swin_proj_int8_destroy(h))
 
 
 # ---- torch-facing convenience (device memory + streams only) ---------------------
@@ -306,3 +346,65 @@ class SwinMlpInt8Layer:
         swin_mlp_int8_run_host(self.handle, _ptr(x_host), _ptr(residual_host), _ptr(y_host), T,
                                _ptr(ws), ws.numel(), ctypes.c_void_p(s))
         return y_host
+
+
+class SwinProjInt8Layer:
+    """Proj GEMM + fused op #4 (+ LN2) handle (include/swin_mlp_int8.h).
+    `layer` has the fields of synth.ProjLayer (C, s_a, z_a, w, s_w, b, gamma, beta, eps, s_y, z_y)."""
+
+    def __init__(self, layer, device: int = 0, ln_fp64: bool = False):
+        import numpy as np
+        import torch
+        keep = []
+
+        def hp(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a.ctypes.data_as(ctypes.c_void_p).value
+
+        d = swin_proj_int8_desc_t()
+        d.C = int(layer.C)
+        d.a_scale, d.a_zero_point = float(layer.s_a), int(layer.z_a)
+        d.w, d.w_scale, d.b = hp(layer.w, np.int8), hp(layer.s_w, np.float32), hp(layer.b, np.float32)
+        d.ln_gamma, d.ln_beta, d.ln_eps = hp(layer.gamma, np.float32), hp(layer.beta, np.float32), float(layer.eps)
+        d.y_scale, d.y_zero_point = float(layer.s_y), int(layer.z_y)
+        d.device, d.ln_fp64 = int(device), int(bool(ln_fp64))
+        self.C, self.device = d.C, device
+        self.handle = swin_proj_int8_create(d)
+        self._torch = torch
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                lib().swin_proj_int8_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def plan(self):
+        out = (ctypes.c_int32 * 4)()
+        lib().swin_proj_int8_plan(self.handle, out)
+        return {"bn": out[0], "cs": out[1], "stages": out[2], "pair": out[3]}
+
+    def __call__(self, a, residual, y=None, residual_out=None):
+        torch = self._torch
+        T = a.shape[0]
+        if y is None:
+            y = torch.empty((T, self.C), dtype=torch.int8, device=a.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)
+        swin_proj_int8_run(self.handle, _ptr(a), _ptr(residual), _ptr(y), _ptr(residual_out), T, stream)
+        return y
+
+    def run_debug(self, a, residual, residual_out=None):
+        torch = self._torch
+        T = a.shape[0]
+        y = torch.empty((T, self.C), dtype=torch.int8, device=a.device)
+        acc = torch.empty((T, self.C), dtype=torch.int32, device=a.device)
+        ln = torch.empty((T, self.C), dtype=torch.float32, device=a.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)
+        swin_proj_int8_run_debug(self.handle, _ptr(a), _ptr(residual), _ptr(y), _ptr(residual_out), T, stream,
+                                 _ptr(acc), _ptr(ln))
+        return {"y": y, "acc": acc, "ln_out": ln}

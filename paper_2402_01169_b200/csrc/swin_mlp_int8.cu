@@ -1140,6 +1140,169 @@ swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h) {
     return SWIN_MLP_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// NEXT-2: Proj GEMM + fused op #4 (+ LN2), Fig. 1 lines 63-70.  Kernel 2 of the
+// two-kernel plan (mlp_gemm_kernel<EP6_LN>) with K = C: the handle is an MLP handle whose
+// FC2 slot holds W_proj and whose "hidden" quantizer is the attention-output quantizer.
+struct swin_proj_int8_s {
+    swin_mlp_int8_s m;
+};
+
+swin_mlp_status_t swin_proj_int8_create(const swin_proj_int8_desc_t* desc, swin_proj_int8_t* out) {
+    g_last_error.clear();
+    if (!desc || !out) return fail(SWIN_MLP_EINVAL, "desc and out must be non-NULL");
+    const swin_proj_int8_desc_t& d = *desc;
+    if (d.C < 32 || d.C % 32) return fail(SWIN_MLP_EINVAL, "C=%d must be a multiple of 32 and >= 32", d.C);
+    if (d.C > 1536) return fail(SWIN_MLP_EUNSUPPORTED, "C=%d exceeds 1536", d.C);
+    if (!normal_positive(d.a_scale) || !normal_positive(d.y_scale))
+        return fail(SWIN_MLP_EINVAL, "activation scales must be finite, normal and > 0");
+    if (!(d.ln_eps > 0.0f) || !std::isfinite(d.ln_eps)) return fail(SWIN_MLP_EINVAL, "ln_eps must be > 0");
+    for (int32_t z : {d.a_zero_point, d.y_zero_point})
+        if (z < -128 || z > 127) return fail(SWIN_MLP_EINVAL, "zero point %d outside [-128, 127]", z);
+    if (!d.w || !d.w_scale || !d.ln_gamma || !d.ln_beta)
+        return fail(SWIN_MLP_EINVAL, "w, w_scale, ln_gamma, ln_beta are required");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (d.device < 0 || d.device >= ndev) return fail(SWIN_MLP_EINVAL, "device %d of %d", d.device, ndev);
+    DeviceGuard guard(d.device);
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, d.device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(SWIN_MLP_EUNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)", d.device,
+                    prop.major, prop.minor);
+    const int C = d.C;
+    std::vector<int8_t> w;
+    std::vector<float> sw, b, g, bt;
+    ST_TRY(fetch(d.w, (size_t)C * C, w, "w"));
+    ST_TRY(fetch(d.w_scale, (size_t)C, sw, "w_scale"));
+    ST_TRY(fetch(d.ln_gamma, (size_t)C, g, "ln_gamma"));
+    ST_TRY(fetch(d.ln_beta, (size_t)C, bt, "ln_beta"));
+    if (d.b) ST_TRY(fetch(d.b, (size_t)C, b, "b"));
+
+    auto ph = new swin_proj_int8_s();
+    swin_mlp_int8_s* h = &ph->m;
+    auto bail = [&](swin_mlp_status_t st) {
+        delete ph;
+        return st;
+    };
+    h->d = swin_mlp_int8_desc_t{};
+    h->d.C = C; h->d.H = C; h->d.act = SWIN_MLP_ACT_RELU;
+    h->d.x_scale = 1.0f; h->d.x_zero_point = 0;                       // (no FC1 / no dQ(x) residual)
+    h->d.h_scale = d.a_scale; h->d.h_zero_point = d.a_zero_point;     // the GEMM input quantizer
+    h->d.ln_eps = d.ln_eps; h->d.y_scale = d.y_scale; h->d.y_zero_point = d.y_zero_point;
+    h->d.device = d.device; h->d.ln_fp64 = d.ln_fp64;
+    h->device = d.device;
+    h->num_sms = prop.multiProcessorCount;
+    // O0 for op #4: m[c] = fl(a_scale * w_scale[c]), inv_y = fl(1/y_scale); zero-point correction
+    h->hm2.resize(C);
+    for (int c = 0; c < C; ++c) {
+        if (!normal_positive(sw[c])) return bail(fail(SWIN_MLP_EINVAL, "w_scale[%d] not finite/normal/positive", c));
+        volatile float m = d.a_scale * sw[c];
+        h->hm2[c] = m;
+        if (!normal_positive(h->hm2[c])) return bail(fail(SWIN_MLP_EINVAL, "a_scale*w_scale[%d] not normal", c));
+    }
+    {
+        volatile float one = 1.0f;
+        h->inv_y = one / d.y_scale;
+    }
+    if (!normal_positive(h->inv_y)) return bail(fail(SWIN_MLP_EINVAL, "1/y_scale not normal"));
+    h->hws2.assign(C, 0);
+    std::vector<int32_t> zc(C);
+    for (int c = 0; c < C; ++c) {
+        int64_t s = 0;
+        for (int k = 0; k < C; ++k) {
+            if (w[(size_t)c * C + k] == -128) return bail(fail(SWIN_MLP_EINVAL, "w must be symmetric (-128 not allowed)"));
+            s += w[(size_t)c * C + k];
+        }
+        h->hws2[c] = (int32_t)s;
+        zc[c] = (int32_t)(s * d.a_zero_point);
+    }
+    if (!make_plan(EP6_LN, C, C, true, h->p2, d.ln_fp64 ? 8 : 4))
+        return bail(fail(SWIN_MLP_EUNSUPPORTED, "no proj tile plan for C=%d", C));
+    swin_mlp_status_t st;
+#define H_TRY(expr)                                   \
+    do {                                              \
+        if ((st = (expr)) != SWIN_MLP_OK) return bail(st); \
+    } while (0)
+    H_TRY(upload(h, w, &h->w2));
+    H_TRY(upload(h, h->hm2, &h->m2));
+    H_TRY(upload(h, g, &h->gamma));
+    H_TRY(upload(h, bt, &h->beta));
+    if (d.b) H_TRY(upload(h, b, &h->b2));
+    if (d.a_zero_point) H_TRY(upload(h, zc, &h->zc2));
+    H_TRY(encode_2d(&h->tm_w2, h->w2, C, C, C,
+                    (uint32_t)(h->p2.pair ? (h->p2.BN > 256 ? h->p2.BN / 4 : h->p2.BN / 2) : h->p2.BN)));
+    h->p2.fn = kernel_for(EP6_LN, (d.b ? kHasB : 0) | (d.a_zero_point ? kHasZc : 0) | (d.y_zero_point ? kZqNz : 0) |
+                                      (d.ln_fp64 ? kS64 : 0) | (h->p2.pair ? kPair : 0));
+    H_TRY(prepare(h->p2, h->num_sms));
+#undef H_TRY
+    *out = ph;
+    return SWIN_MLP_OK;
+}
+
+static swin_mlp_status_t proj_run_impl(swin_proj_int8_t ph, const int8_t* a, const float* residual, int8_t* y,
+                                       float* residual_out, int64_t T, void* stream, int32_t* acc, float* ln_out,
+                                       bool dbg) {
+    if (!ph) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    swin_mlp_int8_s* h = &ph->m;
+    if (T < 0) return fail(SWIN_MLP_EINVAL, "T=%lld < 0", (long long)T);
+    if (T == 0) return SWIN_MLP_OK;
+    if (T > (int64_t)1 << 31) return fail(SWIN_MLP_EUNSUPPORTED, "T=%lld too large", (long long)T);
+    if (!a || !y || !residual) return fail(SWIN_MLP_EINVAL, "a, residual and y are required");
+    if (!aligned16(a) || !aligned16(y) || !aligned16(residual) || (residual_out && !aligned16(residual_out)))
+        return fail(SWIN_MLP_EINVAL, "a/y/residual/residual_out must be 16-byte aligned");
+    if ((const void*)a == (const void*)y) return fail(SWIN_MLP_EINVAL, "y may not alias a");
+    const int C = h->d.C;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto swz = [](int w) {
+        return w == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : w == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+             : w == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    };
+    CUtensorMap tm_a, tm_y;
+    ST_TRY(encode_cached(h, &tm_a, a, T, C, C, (uint32_t)(kBM / h->p2.CS)));
+    ST_TRY(encode_cached(h, &tm_y, y, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
+    const int64_t m_tiles = (T + kBM - 1) / kBM;
+    GemmArgs a2 = {};
+    a2.M = T; a2.K = C; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.eg = h->p2.eg;
+    a2.xstage = h->p2.xstage; a2.yin = h->p2.yin; a2.x = nullptr;
+    a2.out_w = h->p2.out_w;
+    a2.resb = h->p2.resb; a2.mt_major = h->p2.pair ? 0 : 1;
+    a2.n_groups = 1; a2.num_units = h->p2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;
+    a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
+    a2.s_x = 1.0f; a2.z_x = 0;
+    a2.resid = residual; a2.resid_out = residual_out;
+    a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
+    a2.acc_tap = dbg ? acc : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
+    return launch(h->p2, tm_a, h->tm_w2, tm_y, tm_y, a2, s);
+}
+
+swin_mlp_status_t swin_proj_int8_run(swin_proj_int8_t h, const int8_t* a, const float* residual, int8_t* y,
+                                     float* residual_out, int64_t T, void* stream) {
+    return proj_run_impl(h, a, residual, y, residual_out, T, stream, nullptr, nullptr, false);
+}
+
+swin_mlp_status_t swin_proj_int8_run_debug(swin_proj_int8_t h, const int8_t* a, const float* residual, int8_t* y,
+                                           float* residual_out, int64_t T, void* stream, int32_t* acc,
+                                           float* ln_out) {
+    return proj_run_impl(h, a, residual, y, residual_out, T, stream, acc, ln_out, true);
+}
+
+int32_t swin_proj_int8_plan(swin_proj_int8_t h, int32_t* out4) {
+    if (!h || !out4) return -1;
+    out4[0] = h->m.p2.BN; out4[1] = h->m.p2.CS; out4[2] = h->m.p2.stages; out4[3] = h->m.p2.pair;
+    return 0;
+}
+
+swin_mlp_status_t swin_proj_int8_destroy(swin_proj_int8_t h) {
+    if (!h) return SWIN_MLP_OK;
+    {
+        DeviceGuard guard(h->m.device);
+        delete h;
+    }
+    return SWIN_MLP_OK;
+}
+
 // Test/bench introspection: the launch plan chosen for this layer.
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
     if (!h || !out10) return -1;  // out10 holds 20 entries

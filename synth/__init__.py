@@ -154,3 +154,41 @@ def config_layers(config: int, act: int = ACT_RELU, batch: Optional[int] = None)
     depths = (1, 1, 1, 1) if config == 2 else SWIN[name]["depths"]
     toks = stage_tokens(b, img=img)
     return [(C0 << s, toks[s], depths[s]) for s in range(4)]
+
+
+@dataclass
+class ProjLayer:
+    """Attention projection + op #4 (+ LN2) parameters.  Field names
+    follow swin_proj_int8_desc_t."""
+    C: int
+    s_a: float                  # attention-output (V*att) scale
+    z_a: int
+    w: np.ndarray               # int8 [C][C]
+    s_w: np.ndarray             # fp32 [C]
+    b: Optional[np.ndarray]     # fp32 [C] or None
+    gamma: np.ndarray
+    beta: np.ndarray
+    eps: float
+    s_y: float
+    z_y: int
+    seed: int = 0
+
+
+def make_proj(C: int, seed: int, bias: bool = True, z_a: int = 0, z_y: int = 0) -> ProjLayer:
+    """The same recipe as make_layer for a C x C projection: N(0, 0.02^2) weights under per-channel
+    max-abs PTQ, N(0, 0.02^2) bias, LN2 gamma = 1 + 0.1 N, beta = 0.1 N.  The attention output is
+    a convex mix of V rows, ~N(0, 1) without outlier channels: s_a = 4.5 sigma / 127; s_y = 5/127."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    w, s_w = _quant_weights(rng, C, C)
+    b = (rng.standard_normal(C, dtype=np.float32) * np.float32(0.02)) if bias else None
+    gamma = (np.float32(1.0) + np.float32(0.1) * rng.standard_normal(C, dtype=np.float32)).astype(np.float32)
+    beta = (np.float32(0.1) * rng.standard_normal(C, dtype=np.float32)).astype(np.float32)
+    return ProjLayer(C=C, s_a=float(np.float32(4.5 / 127.0)), z_a=z_a, w=w, s_w=s_w, b=b, gamma=gamma,
+                     beta=beta, eps=1e-5, s_y=float(np.float32(5.0 / 127.0)), z_y=z_y, seed=seed)
+
+
+def make_attn_out(P: ProjLayer, T: int, seed: int) -> np.ndarray:
+    """int8 [T][C] attention outputs: N(0, 1) quantized with s_a, z_a (RNE, saturating)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = rng.standard_normal((T, P.C), dtype=np.float32)
+    return np.clip(np.rint(x * np.float32(1.0 / P.s_a)) + P.z_a, -128, 127).astype(np.int8)

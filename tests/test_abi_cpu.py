@@ -24,7 +24,7 @@ def P():
 def _declared():
     src = open(os.path.join(ROOT, "include", "swin_mlp_int8.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(swin_mlp_int8_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(swin_(?:mlp|proj)_int8_[a-z_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(P):

@@ -376,3 +376,38 @@ def test_ep6_residual_added_with_one_rounding():
             assert z[t, c] == f32(exact), (t, c)
             differs += np.float32(np.float32(np.float32(int(X[t, c]) - z_x) * s_x) + d) != z[t, c]
     assert differs > 0   # the case actually distinguishes one rounding from two
+
+
+# ---------------------------------------------------------------- NEXT-2: proj GEMM + op #4 (+ LN2)
+def test_proj_op4_pins():
+    """oracle.proj_op4 (Fig. 1 lines 63-70; R18): (i) A is the brute-force
+    integer product with the input zero point; (ii) power-of-two scales make every fp32 op exact:
+    z == A * s_a * s_w + b + R in float64; (iii) yhat == torch float64 layer_norm(z) (LN2),
+    Y == clamp(rne(fl(yhat * 1/s_y)) + z_y); (iv) W = 0 and a constant shortcut row give
+    yhat == beta exactly (the bias and the residual enter once, before LN2)."""
+    import torch
+    C, T = 64, 9
+    P = synth.make_proj(C, 31, z_a=-3, z_y=2)
+    P.s_a = 2.0 ** -4
+    P.s_w = np.full(C, 2.0 ** -6, np.float32)
+    P.b = (RNG.integers(-64, 64, C) * 2.0 ** -10).astype(np.float32)
+    P.s_y = 2.0 ** -5
+    A_in = RNG.integers(-128, 128, (T, C), dtype=np.int8)
+    R = (RNG.integers(-4096, 4096, (T, C)) * 2.0 ** -10).astype(np.float32)
+    Y, yh, z, A = oracle.proj_op4(P, A_in, R)
+    np.testing.assert_array_equal(A, _triple_loop(A_in, P.w, -3))
+    exact = A.astype(np.float64) * 2.0 ** -10 + P.b.astype(np.float64) + R.astype(np.float64)
+    np.testing.assert_array_equal(z.astype(np.float64), exact)
+    ref = torch.nn.functional.layer_norm(torch.tensor(z, dtype=torch.float64), (C,),
+                                         torch.tensor(P.gamma, dtype=torch.float64),
+                                         torch.tensor(P.beta, dtype=torch.float64), eps=P.eps).numpy()
+    np.testing.assert_allclose(yh, ref.astype(np.float32), rtol=0, atol=2e-6)
+    v = (yh * np.float32(32.0)).astype(np.float64)
+    np.testing.assert_array_equal(Y, np.clip(np.rint(v) + 2, -128, 127).astype(np.int8))
+    P.w = np.zeros((C, C), np.int8)
+    P.b = None
+    Rc = np.full((3, C), 1.25, np.float32)
+    _, yh, z, A = oracle.proj_op4(P, A_in[:3], Rc)
+    assert (A == 0).all()
+    np.testing.assert_array_equal(z, Rc)
+    np.testing.assert_array_equal(yh, np.broadcast_to(P.gamma * 0 + P.beta, (3, C)))

@@ -429,3 +429,63 @@ def test_gemm_plan_variants(dev, C, T, env, monkeypatch):
         assert plan["fc2_cs"] == int(env["SWIN_MLP_LN_CS"])
     _run_and_check(dev, L, T, e2e=False)
     _run_and_check(dev, _layer(C, 9800 + C, act=1, bias=True, zx=-5, zh=-3, zy=2), T, e2e=False)
+
+
+# ---- NEXT-2: proj GEMM + fused op #4 (+ LN2) ---------------------------------------------------
+
+@pytest.mark.parametrize("C,T,za,zy,bias,ln64", [
+    (96, 3000, 0, 0, True, False), (128, 129, -3, 2, False, False), (192, 1000, 0, 0, True, True),
+    (256, 257, 5, -1, True, False), (384, 1500, 0, 0, True, False), (512, 20 * 128 + 77, 0, 0, True, False),
+    (768, 300, -7, 0, True, True), (1024, 7 * 128 + 100, 0, 0, True, False),
+])
+def test_parity_proj_op4(dev, C, T, za, zy, bias, ln64):
+    """swin_proj_int8_* (Fig. 1 lines 63-70, reading R18) against oracle.proj_op4:
+    A int32 and z (the fp32 residual stream handed to the MLP) bit-exact, yhat and Y in tier."""
+    from paper_2402_01169_b200 import SwinProjInt8Layer
+    P = synth.make_proj(C, 9900 + C, bias=bias, z_a=za, z_y=zy)
+    A_in = synth.make_attn_out(P, T, 17)
+    R = synth.make_residual(T, C, 18)
+    layer = SwinProjInt8Layer(P, device=0, ln_fp64=ln64)
+    zo = torch.empty((T, C), dtype=torch.float32, device=dev)
+    taps = layer.run_debug(torch.from_numpy(A_in).to(dev), torch.from_numpy(R).to(dev), residual_out=zo)
+    torch.cuda.synchronize()
+    Y, yh, z, A = oracle.proj_op4(P, A_in, R)
+    np.testing.assert_array_equal(taps["acc"].cpu().numpy(), A)
+    np.testing.assert_array_equal(zo.cpu().numpy(), z)
+    _tier_yhat(taps["ln_out"].cpu().numpy(), yh)
+    _tier_int8(taps["y"].cpu().numpy(), Y, what=f"proj Y C={C}")
+    y2 = layer(torch.from_numpy(A_in).to(dev), torch.from_numpy(R).to(dev))   # plain run == debug run
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y2.cpu().numpy(), taps["y"].cpu().numpy())
+
+
+def test_proj_op4_feeds_mlp(dev):
+    """One Swin MLP half-block end to end on the GPU: proj + op #4 (+LN2) -> MLP with the fp32
+    residual stream z, against the oracle composition (bit-exact z chain, Y in tier)."""
+    from paper_2402_01169_b200 import SwinProjInt8Layer, SwinMlpInt8Layer
+    C, T = 384, 700
+    P = synth.make_proj(C, 9950)
+    L = synth.make_layer(C, 9951)
+    L.s_x = P.s_y          # the MLP consumes op #4's quantized LN2 output
+    A_in = synth.make_attn_out(P, T, 19)
+    R = synth.make_residual(T, C, 20)
+    proj, mlp = SwinProjInt8Layer(P, device=0), SwinMlpInt8Layer(L, device=0)
+    z1 = torch.empty((T, C), dtype=torch.float32, device=dev)
+    x = proj(torch.from_numpy(A_in).to(dev), torch.from_numpy(R).to(dev), residual_out=z1)
+    z2 = torch.empty((T, C), dtype=torch.float32, device=dev)
+    y = mlp(x, residual=z1, residual_out=z2)
+    torch.cuda.synchronize()
+    Yp, _, zp, _ = oracle.proj_op4(P, A_in, R)
+    _tier_int8(x.cpu().numpy(), Yp, what="op #4 Y")
+    xin = x.cpu().numpy()                          # the MLP oracle on the GPU's own int8 input
+    np.testing.assert_array_equal(z1.cpu().numpy(), zp)
+    _tier_int8(y.cpu().numpy(), oracle.mlp(L, xin, R=zp), what="MLP Y")
+
+
+def test_proj_requires_residual(dev):
+    from paper_2402_01169_b200 import SwinProjInt8Layer, SwinMlpError
+    P = synth.make_proj(96, 9960)
+    layer = SwinProjInt8Layer(P, device=0)
+    a = torch.zeros((10, 96), dtype=torch.int8, device=dev)
+    with pytest.raises(SwinMlpError):
+        layer(a, None)
