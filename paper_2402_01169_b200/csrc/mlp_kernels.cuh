@@ -610,6 +610,15 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 __syncwarp();
             }
+            if (IS_LN && p.resid != nullptr && !(p.dbg & 8)) {
+                // fp32 residual rows of this tile -> L2 ahead of pass 1 (its per-chunk loads are
+                // otherwise HBM-latency bound: one dependent load round trip per 16 columns)
+                if (it == 0) pdl_wait();
+                for (uint32_t r = lane; r < (uint32_t)kBM; r += 32u) {
+                    const int64_t row = (int64_t)m_tile * kBM + r;
+                    if (row < p.M) bulk_prefetch_l2(p.resid + row * (int64_t)p.ldo + n0, (uint32_t)BN * 4u);
+                }
+            }
             mbar_wait(bar_tempty + 8u * buf, aph ^ 1u);
             if (trc && lane == 0 && it < 512) trc[3072 + 2 * it] = gtimer();
             float* cb = consts + (size_t)(csh ? 0u : buf) * kNConst * BN;

@@ -1274,6 +1274,7 @@ static swin_mlp_status_t proj_run_impl(swin_proj_int8_t ph, const int8_t* a, con
     a2.resid = residual; a2.resid_out = residual_out;
     a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
     a2.acc_tap = dbg ? acc : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
+    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; }
     return launch(h->p2, tm_a, h->tm_w2, tm_y, tm_y, a2, s);
 }
 
