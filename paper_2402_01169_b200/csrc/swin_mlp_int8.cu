@@ -316,7 +316,8 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     return false;
 }
 
-bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
+// ln_pair: -1 = the SWIN_MLP_LN_PAIR switch, 1 = only the CTA-pair op #6 plan, 0 = never it
+bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, int ln_pair_mode = -1) {
     pl = Plan();
     pl.epi = epi;
     pl.ebytes = ebytes;
@@ -329,12 +330,13 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4) {
         // slower (Swin-B b128 stack 2.03 ms vs 1.87 ms; C = 512: 27 us per tile pair), so
         // opt-in: SWIN_MLP_LN_PAIR=1 (read per create).
         const char* lp = std::getenv("SWIN_MLP_LN_PAIR");
-        const bool ln_pair = lp && *lp == '1';
+        const bool ln_pair = ln_pair_mode < 0 ? (lp && *lp == '1') : ln_pair_mode == 1;
         if (ln_pair && N <= 512 && N > 256 && N % 64 == 0) {
             pl.BN = N; pl.CS = 1; pl.n_groups = 1; pl.pair = 1;
             if (fit_smem(epi, pl, 2, K)) return true;
             pl.pair = 0;
         }
+        if (ln_pair_mode == 1) return false;
         // SWIN_MLP_LN_CS forces the op #6 cluster size (A/B switch)
         const char* cs_env = std::getenv("SWIN_MLP_LN_CS");   // (read per create)
         const int cs_force = cs_env && *cs_env ? atoi(cs_env) : 0;
@@ -502,6 +504,13 @@ struct swin_mlp_int8_s {
     std::vector<int32_t> hws1, hws2;
     float inv_h = 0.f, inv_y = 0.f;
     CUtensorMap tm_w1, tm_w2;
+    // few-tile alternative for op #6 (256 < C <= 512): the CTA-pair whole-row plan, used when
+    // the run has at most 2 * p2b.max_clusters m-tiles (one wave of pairs) -- measured faster
+    // there (C = 384, T = 12544: 22.7 vs 25.4 us; C = 512, T = 12544: 28.8 vs 30.9 us) and
+    // slower for more tiles (C = 512, T = 25088: 47.2 vs 39.9 us)
+    Plan p2b;
+    bool has_p2b = false;
+    CUtensorMap tm_w2b;
     std::vector<void*> allocs;
     // native profiling (bench roofline): event triples per recorded run
     bool prof_on = false;
@@ -736,6 +745,16 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
                                       (h->p2.pair ? kPair : 0));
     H_TRY(prepare(h->p1, h->num_sms));
     H_TRY(prepare(h->p2, h->num_sms));
+    {
+        const char* lp = std::getenv("SWIN_MLP_LN_PAIR");   // '0': never the pair plan
+        if (!h->p2.pair && !(lp && *lp == '0') && make_plan(EP6_LN, C, H, true, h->p2b, d.ln_fp64 ? 8 : 4, 1)) {
+            H_TRY(encode_2d(&h->tm_w2b, h->w2, C, H, H, (uint32_t)(h->p2b.BN > 256 ? h->p2b.BN / 4 : h->p2b.BN / 2)));
+            h->p2b.fn = kernel_for(EP6_LN, (d.b2 ? kHasB : 0) | (d.h_zero_point ? kHasZc : 0) |
+                                               (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0) | kPair);
+            H_TRY(prepare(h->p2b, h->num_sms));
+            h->has_p2b = true;
+        }
+    }
     if (h->unfused) {
         h->op5_fn = op5_kernel_for(d.act == SWIN_MLP_ACT_GELU_ERF, d.b1 != nullptr, d.h_zero_point != 0);
         int per_sm = 0;
@@ -841,19 +860,22 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         return SWIN_MLP_OK;
     }
 
+    const int64_t m_tiles = (T + kBM - 1) / kBM;
+    const bool use_b = h->has_p2b && m_tiles <= 2 * (int64_t)h->p2b.max_clusters;
+    const Plan& P2 = use_b ? h->p2b : h->p2;
+    const CUtensorMap& tmw2 = use_b ? h->tm_w2b : h->tm_w2;
     CUtensorMap tm_x, tm_h, tm_ho, tm_y, tm_xr;
     ST_TRY(encode_cached(h, &tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
-    ST_TRY(encode_cached(h, &tm_h, hq, T, H, H, (uint32_t)(kBM / h->p2.CS)));
+    ST_TRY(encode_cached(h, &tm_h, hq, T, H, H, (uint32_t)(kBM / P2.CS)));
     // epilogue output maps: [128 rows][W B] boxes with the W-byte swizzle the staging uses
     auto swz = [](int w) {
         return w == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : w == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
              : w == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
     };
     ST_TRY(encode_cached(h, &tm_ho, hq, T, H, H, kBM, (uint32_t)h->p1.out_w, swz(h->p1.out_w)));
-    ST_TRY(encode_cached(h, &tm_y, y, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
+    ST_TRY(encode_cached(h, &tm_y, y, T, C, C, kBM, (uint32_t)P2.out_w, swz(P2.out_w)));
     // op #6 residual source x, staged by TMA with the output tile's box and swizzle
-    ST_TRY(encode_cached(h, &tm_xr, x, T, C, C, kBM, (uint32_t)h->p2.out_w, swz(h->p2.out_w)));
-    const int64_t m_tiles = (T + kBM - 1) / kBM;
+    ST_TRY(encode_cached(h, &tm_xr, x, T, C, C, kBM, (uint32_t)P2.out_w, swz(P2.out_w)));
 
     GemmArgs a1 = {};
     a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.G = h->p1.G; a1.resb = h->p1.resb;
@@ -872,11 +894,11 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }
 
     GemmArgs a2 = {};
-    a2.M = T; a2.K = H; a2.BN = h->p2.BN; a2.CS = h->p2.CS; a2.stages = h->p2.stages; a2.G = h->p2.G; a2.eg = h->p2.eg;
-    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; } a2.xstage = h->p2.xstage; a2.yin = h->p2.yin; a2.x = x;
-    a2.out_w = h->p2.out_w;
-    a2.resb = h->p2.resb; a2.mt_major = h->p2.pair ? 0 : 1;   // op #6: one n-group per cluster
-    a2.n_groups = 1; a2.num_units = h->p2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;
+    a2.M = T; a2.K = H; a2.BN = P2.BN; a2.CS = P2.CS; a2.stages = P2.stages; a2.G = P2.G; a2.eg = P2.eg;
+    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; } a2.xstage = P2.xstage; a2.yin = P2.yin; a2.x = x;
+    a2.out_w = P2.out_w;
+    a2.resb = P2.resb; a2.mt_major = P2.pair ? 0 : 1;   // op #6: one n-group per cluster
+    a2.n_groups = 1; a2.num_units = P2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
     a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
     a2.resid = residual; a2.resid_out = residual_out;
@@ -908,7 +930,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     }
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
     if (dbg && hidden) CUDA_TRY(cudaMemcpyAsync(hidden, hq, (size_t)T * H, cudaMemcpyDeviceToDevice, s));
-    ST_TRY(launch(h->p2, tm_h, h->tm_w2, tm_y, tm_xr, a2, s));
+    ST_TRY(launch(P2, tm_h, tmw2, tm_y, tm_xr, a2, s));
     if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
     return SWIN_MLP_OK;
 }

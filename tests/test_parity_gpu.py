@@ -409,8 +409,10 @@ def test_fc1_cta_pair(dev, C, T):
     (512, 20 * 128 + 77, {"SWIN_MLP_WSL": "1"}),                      # weight-stationary slices, pair
     (384, 13 * 128 + 5, {"SWIN_MLP_WSL": "1"}),                       # ... single CTA
     (768, 3 * 128 - 51, {"SWIN_MLP_DST": "1"}),                       # op #5 stores from registers
-    (512, 9 * 128 + 1, {"SWIN_MLP_NO_YIN": "1"}),                     # op #6 separate Y staging
-    (512, 9 * 128 + 1, {"SWIN_MLP_LN_CS": "4"}),                      # op #6 4-CTA column split
+    (512, 9 * 128 + 1, {"SWIN_MLP_NO_YIN": "1", "SWIN_MLP_LN_PAIR": "0"}),   # op #6 separate Y staging
+    (512, 9 * 128 + 1, {"SWIN_MLP_LN_CS": "4", "SWIN_MLP_LN_PAIR": "0"}),    # op #6 4-CTA column split
+    (384, 98 * 128, {}),                                              # few tiles: the pair op #6 plan
+    (384, 150 * 128 + 3, {}),                                         # more: the column-split plan
     (1024, 7 * 128 + 100, {}),                                        # op #6 yin at cs = 4, BN = 256
 ])
 def test_gemm_plan_variants(dev, C, T, env, monkeypatch):
