@@ -400,6 +400,10 @@ def main():
     proj = None
     if rank == 0 and not args.no_stack:
         proj = proj_rows(max(3, min(args.steps, 20)))
+    # ---- BASELINE configs[0]: one 7x7 window of the Swin-T stage-4 MLP (T = 49), latency ------------
+    cfg1 = None
+    if rank == 0 and not args.no_stack:
+        cfg1 = window_latency(max(10, min(args.steps, 50)))
 
     # ---- CPU baseline: the oracle as it stands on this host (rank 0, N=1 only) ----------------------
     cpu = None
@@ -424,12 +428,79 @@ def main():
                 "relu_vs_gelu": relu_gelu,
                 "north_star_stack": stack,
                 "proj_op4": proj,
+                "config0_window": cfg1,
                 "tensor_frac_of_step": roofline["step_frac"],
                 "clocks": sampler.result()}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def window_latency(steps):
+    """BASELINE configs[0]: Swin-T stage-4 MLP (C = 768 -> 3072 -> 768) on
+    one 7x7 window, T = 49 tokens, batch 1.  Latency-bound: reported as us per layer, cold (L2
+    flushed before each run: the 4.7 MB of weights come from HBM) and hot (back to back), the
+    hot time per layer inside a CUDA graph of `steps` layer runs (launch overhead removed), and
+    the fraction of the HBM roof for the cold run's algorithmic bytes (weights + 2C per token)."""
+    import torch
+    import synth
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    peak_gbs = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    L = synth.make_layer(768, synth.layer_seed(1, 3, 0))
+    layer = SwinMlpInt8Layer(L, device=0)
+    T = 49
+    x = torch.from_numpy(synth.make_activations(L, T, 3)).cuda()
+    y = torch.empty_like(x)
+    ws = layer.workspace(T)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(5):
+        layer(x, y=y, workspace=ws)
+    torch.cuda.synchronize()
+
+    def run(cold):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for k in range(steps):
+            if cold:
+                flush.fill_(k & 0xff)
+            ev[k][0].record()
+            layer(x, y=y, workspace=ws)
+            ev[k][1].record()
+        torch.cuda.synchronize()
+        return sorted(a.elapsed_time(b) * 1e3 for a, b in ev)[steps // 2]
+
+    cold, hot = run(True), run(False)
+    try:
+        graph_us = graph_time(torch, layer, x, y, ws, steps)
+    except Exception as e:   # (reported, never fatal to the bench line)
+        graph_us = f"capture failed: {e}"[:200]
+    bytes_cold = 2 * 4 * 768 * 768 + 2 * 768 * T
+    return {"workload": "configs[0]: Swin-T stage-4 MLP, one 7x7 window (T = 49), batch 1, int8",
+            "us_cold_l2": round(cold, 2), "us_hot_l2": round(hot, 2),
+            "us_hot_in_cuda_graph": round(graph_us, 2) if isinstance(graph_us, float) else graph_us,
+            "hbm_frac_cold": round(bytes_cold / (cold * 1e-6) / 1e9 / peak_gbs, 3),
+            "algorithmic_bytes": bytes_cold, "plan": layer.plan(), "parallelism": "replicas only (DESIGN.md §2.6)"}
+
+
+def graph_time(torch, layer, x, y, ws, steps):
+    """Per-layer time of `steps` layer runs captured in one CUDA graph (no launch overhead)."""
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        layer(x, y=y, workspace=ws)   # (warm the map cache on this stream)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(steps):
+                layer(x, y=y, workspace=ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / steps
 
 
 def proj_rows(steps):
