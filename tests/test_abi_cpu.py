@@ -113,6 +113,50 @@ def test_null_handle_paths(P):
     assert L.swin_mlp_int8_launches_per_run(None) == 0
 
 
+def _proj_desc(P, **kw):
+    d = P.swin_proj_int8_desc_t()
+    C = kw.get("C", 96)
+    keep = []
+
+    def arr(a):
+        keep.append(a)
+        return a.ctypes.data_as(ctypes.c_void_p).value
+
+    d.C = C
+    d.a_scale, d.a_zero_point = kw.get("a_scale", 0.035), kw.get("a_zero_point", 0)
+    d.w = None if kw.get("null_w") else arr(np.ones((C, C), np.int8))
+    d.w_scale = arr(np.full(C, 0.01, np.float32))
+    d.b = None
+    d.ln_gamma = arr(np.ones(C, np.float32)); d.ln_beta = arr(np.zeros(C, np.float32))
+    d.ln_eps = kw.get("ln_eps", 1e-5)
+    d.y_scale, d.y_zero_point = kw.get("y_scale", 0.04), kw.get("y_zero_point", 0)
+    d.device = 0
+    return d, keep
+
+
+@pytest.mark.parametrize("kw,frag", [
+    (dict(C=100), "multiple of 32"), (dict(a_scale=0.0), "scales"), (dict(y_scale=float("nan")), "scales"),
+    (dict(ln_eps=-1.0), "ln_eps"), (dict(a_zero_point=-129), "zero point"), (dict(null_w=True), "required"),
+])
+def test_proj_create_rejects_invalid(P, kw, frag):
+    """swin_proj_int8_create validates before touching the device (NEXT-2 entry points)."""
+    d, keep = _proj_desc(P, **kw)
+    h = ctypes.c_void_p()
+    assert P.lib().swin_proj_int8_create(ctypes.byref(d), ctypes.byref(h)) == P.SWIN_MLP_EINVAL
+    assert frag in P.last_error()
+    assert h.value is None
+    d, keep = _proj_desc(P, C=2048)
+    assert P.lib().swin_proj_int8_create(ctypes.byref(d), ctypes.byref(h)) == P.SWIN_MLP_EUNSUPPORTED
+
+
+def test_proj_null_handle_paths(P):
+    L = P.lib()
+    assert L.swin_proj_int8_run(None, None, None, None, None, 10, None) == P.SWIN_MLP_EINVAL
+    assert "NULL handle" in P.last_error()
+    assert L.swin_proj_int8_plan(None, None) == -1
+    assert L.swin_proj_int8_destroy(None) == P.SWIN_MLP_OK
+
+
 def test_no_cpu_fallback_in_product_path():
     """The product package never imports the oracle (or numpy-based math) — a CPU
     fallback would void every parity claim."""
