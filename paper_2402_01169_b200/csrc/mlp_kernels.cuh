@@ -1054,7 +1054,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 mbar_arrive(bar_tempty + 8u * buf);   // TMEM free: the next MMA may start
                 if constexpr (PAIR) {                 // (pair: the leader's MMA waits on both CTAs)
                     if (rank == 0) mbar_arrive(bar_ptempty + 8u * buf);
-                    else mbar_arrive_cluster(mapa(bar_ptempty + 8u * buf, 0));
+                    else if (p.dbg & 16) mbar_arrive_cluster(mapa(bar_ptempty + 8u * buf, 0));   // (A/B: release)
+                    else mbar_arrive_cluster_relaxed(mapa(bar_ptempty + 8u * buf, 0));
                 }
                 if (!dst) mbar_arrive(bar_sfull + 8u * buf);    // this warp's part of the tile is staged
             }

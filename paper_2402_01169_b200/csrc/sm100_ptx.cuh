@@ -231,6 +231,13 @@ __device__ __forceinline__ void tma_load_2d_pair(const void* tmap, uint32_t dst,
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
+// Relaxed remote arrive: no release fence (a release at cluster scope compiles to
+// MEMBAR.ALL.GPU + ERRBAR, i.e. a wait for every outstanding memory operation of the
+// thread).  For signals that order nothing but completed tcgen05.ld (TMEM drained:
+// tcgen05.wait::ld + tcgen05.fence::before_thread_sync precede it), a WAR hazard on TMEM.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 
 // Arrive (once) on `bar` when all previously issued tcgen05 ops complete.
 __device__ __forceinline__ void mma_commit(uint32_t bar) {

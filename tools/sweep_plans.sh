@@ -1,9 +1,6 @@
-# A/B sweep of plan switches for the one-window config (T = 49) (GPU box; output in gpurun_out/sweep.log)
+# A/B: relaxed vs release remote arrive of the pair's TMEM-drained signal (GPU box; gpurun_out/sweep.log)
 o=gpurun_out/sweep.log; : > $o
-for CT in "768 49" "768 3136"; do
+for CT in "512 25088" "768 3136" "1024 6272" "512 12544"; do
   timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
-  SWIN_MLP_LN_CS=8 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
-  SWIN_MLP_PAIR=0 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
-  SWIN_MLP_PAIR=0 SWIN_MLP_LN_CS=8 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
-  SWIN_MLP_PAIR=0 SWIN_MLP_LN_CS=8 SWIN_MLP_NO_RESB=1 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
+  SWIN_MLP_DBG1=16 timeout 120 python tools/layer_sweep.py $CT >> $o 2>&1
 done
