@@ -317,7 +317,11 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
 }
 
 // ln_pair: -1 = the SWIN_MLP_LN_PAIR switch, 1 = only the CTA-pair op #6 plan, 0 = never it
-bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, int ln_pair_mode = -1) {
+// small_bn > 0: the few-tile plan for runs of one or two m-tiles (a 7x7 window, T = 49):
+// FC1 single-CTA tiles of small_bn columns (more CTAs on the same few rows), op #6 the
+// widest cluster that covers the row (CS = 8 first), so more SMs share each weight stream.
+bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, int ln_pair_mode = -1,
+               int small_bn = 0) {
     pl = Plan();
     pl.epi = epi;
     pl.ebytes = ebytes;
@@ -337,6 +341,14 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, i
             pl.pair = 0;
         }
         if (ln_pair_mode == 1) return false;
+        if (small_bn > 0) {
+            for (int cs : {8, 4}) {
+                if (N % cs || N / cs > 256 || (N / cs) % 16) continue;
+                pl.BN = N / cs; pl.CS = cs; pl.n_groups = 1;
+                if (fit_smem(epi, pl, 3, K) || fit_smem(epi, pl, 2, K)) return true;
+            }
+            return false;
+        }
         // SWIN_MLP_LN_CS forces the op #6 cluster size (A/B switch)
         const char* cs_env = std::getenv("SWIN_MLP_LN_CS");   // (read per create)
         const int cs_force = cs_env && *cs_env ? atoi(cs_env) : 0;
@@ -361,6 +373,11 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, i
     // ring).  Measured on the Swin-T stages: FC1 at C = 768 2 us faster, at C = 384
     // 0.5 us slower (there the single-CTA ring already holds a whole tile's K).
     // SWIN_MLP_PAIR=1 / 0 forces it on / off.
+    if (small_bn > 0) {
+        if (N % small_bn) return false;
+        pl.BN = small_bn; pl.CS = 1; pl.n_groups = N / small_bn;
+        return fit_smem(epi, pl, 3, K) || fit_smem(epi, pl, 2, K);
+    }
     static const char* pair_env = std::getenv("SWIN_MLP_PAIR");
     const bool want_pair = pair_env ? (*pair_env == '1') : K >= 512;
     // SWIN_MLP_PAIR_BN = 128 / 192: narrower pair tiles (more accumulator buffers) -- A/B switch
@@ -511,6 +528,13 @@ struct swin_mlp_int8_s {
     Plan p2b;
     bool has_p2b = false;
     CUtensorMap tm_w2b;
+    // few-tile plans (make_plan small_bn): used when the default plans would put both
+    // GEMMs of the run on fewer than num_sms / 4 CTAs (configs[0]: one 7x7 window, T = 49,
+    // C = 768 -- FC1 12 CTA pairs, op #6 one cluster of 4).  SWIN_MLP_SMALL=0 disables,
+    // SWIN_MLP_SMALL_BN picks the FC1 tile width (default 64).
+    Plan p1s, p2s;
+    bool has_small = false;
+    CUtensorMap tm_w1s, tm_w2s;
     std::vector<void*> allocs;
     // native profiling (bench roofline): event triples per recorded run
     bool prof_on = false;
@@ -755,6 +779,24 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
             h->has_p2b = true;
         }
     }
+    {
+        const char* se = std::getenv("SWIN_MLP_SMALL");       // (read per create)
+        const char* sb = std::getenv("SWIN_MLP_SMALL_BN");
+        const int sbn = sb && *sb ? atoi(sb) : 64;
+        if (!h->unfused && !(se && *se == '0') && sbn >= 16 && sbn % 16 == 0 &&
+            make_plan(epi1, H, C, false, h->p1s, 4, -1, sbn) &&
+            make_plan(EP6_LN, C, H, true, h->p2s, d.ln_fp64 ? 8 : 4, 0, sbn)) {
+            H_TRY(encode_2d(&h->tm_w1s, h->w1, H, C, C, (uint32_t)h->p1s.BN));
+            H_TRY(encode_2d(&h->tm_w2s, h->w2, C, H, H, (uint32_t)h->p2s.BN));
+            h->p1s.fn = kernel_for(epi1, (d.b1 ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) |
+                                             (d.h_zero_point ? kZqNz : 0) | (small_k1 ? kSmallK : 0));
+            h->p2s.fn = kernel_for(EP6_LN, (d.b2 ? kHasB : 0) | (d.h_zero_point ? kHasZc : 0) |
+                                               (d.y_zero_point ? kZqNz : 0) | (d.ln_fp64 ? kS64 : 0));
+            H_TRY(prepare(h->p1s, h->num_sms));
+            H_TRY(prepare(h->p2s, h->num_sms));
+            h->has_small = true;
+        }
+    }
     if (h->unfused) {
         h->op5_fn = op5_kernel_for(d.act == SWIN_MLP_ACT_GELU_ERF, d.b1 != nullptr, d.h_zero_point != 0);
         int per_sm = 0;
@@ -861,34 +903,39 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     }
 
     const int64_t m_tiles = (T + kBM - 1) / kBM;
-    const bool use_b = h->has_p2b && m_tiles <= 2 * (int64_t)h->p2b.max_clusters;
-    const Plan& P2 = use_b ? h->p2b : h->p2;
-    const CUtensorMap& tmw2 = use_b ? h->tm_w2b : h->tm_w2;
+    const int64_t units1 = (h->p1.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p1.n_groups;
+    const int64_t units2 = (h->p2.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p2.CS;
+    const bool use_s = h->has_small && units1 + units2 < h->num_sms / 4;
+    const bool use_b = !use_s && h->has_p2b && m_tiles <= 2 * (int64_t)h->p2b.max_clusters;
+    const Plan& P1 = use_s ? h->p1s : h->p1;
+    const CUtensorMap& tmw1 = use_s ? h->tm_w1s : h->tm_w1;
+    const Plan& P2 = use_s ? h->p2s : use_b ? h->p2b : h->p2;
+    const CUtensorMap& tmw2 = use_s ? h->tm_w2s : use_b ? h->tm_w2b : h->tm_w2;
     CUtensorMap tm_x, tm_h, tm_ho, tm_y, tm_xr;
-    ST_TRY(encode_cached(h, &tm_x, x, T, C, C, (uint32_t)(kBM / h->p1.CS)));
+    ST_TRY(encode_cached(h, &tm_x, x, T, C, C, (uint32_t)(kBM / P1.CS)));
     ST_TRY(encode_cached(h, &tm_h, hq, T, H, H, (uint32_t)(kBM / P2.CS)));
     // epilogue output maps: [128 rows][W B] boxes with the W-byte swizzle the staging uses
     auto swz = [](int w) {
         return w == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : w == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
              : w == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
     };
-    ST_TRY(encode_cached(h, &tm_ho, hq, T, H, H, kBM, (uint32_t)h->p1.out_w, swz(h->p1.out_w)));
+    ST_TRY(encode_cached(h, &tm_ho, hq, T, H, H, kBM, (uint32_t)P1.out_w, swz(P1.out_w)));
     ST_TRY(encode_cached(h, &tm_y, y, T, C, C, kBM, (uint32_t)P2.out_w, swz(P2.out_w)));
     // op #6 residual source x, staged by TMA with the output tile's box and swizzle
     ST_TRY(encode_cached(h, &tm_xr, x, T, C, C, kBM, (uint32_t)P2.out_w, swz(P2.out_w)));
 
     GemmArgs a1 = {};
-    a1.M = T; a1.K = C; a1.BN = h->p1.BN; a1.CS = h->p1.CS; a1.stages = h->p1.stages; a1.G = h->p1.G; a1.resb = h->p1.resb;
-    a1.mt_major = h->p1.resb ? 1 : 0;   // resident B needs the m-major order; otherwise deal (m, n) units
-    a1.out_w = h->p1.out_w;
-    a1.n_groups = h->p1.n_groups; a1.num_units = (h->p1.pair ? (m_tiles + 1) / 2 : m_tiles) * h->p1.n_groups;
-    a1.eg = h->p1.eg; a1.ldo = H;
+    a1.M = T; a1.K = C; a1.BN = P1.BN; a1.CS = P1.CS; a1.stages = P1.stages; a1.G = P1.G; a1.resb = P1.resb;
+    a1.mt_major = P1.resb ? 1 : 0;   // resident B needs the m-major order; otherwise deal (m, n) units
+    a1.out_w = P1.out_w;
+    a1.n_groups = P1.n_groups; a1.num_units = (P1.pair ? (m_tiles + 1) / 2 : m_tiles) * P1.n_groups;
+    a1.eg = P1.eg; a1.ldo = H;
     a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = h->inv_h; a1.zq = h->d.h_zero_point;
     a1.acc_tap = dbg ? acc1 : nullptr;
     int32_t* a1ws = h->unfused ? reinterpret_cast<int32_t*>(hq + ((T * H + 127) / 128 * 128)) : nullptr;
     a1.acc_out = a1ws;
-    a1.dst = h->p1.dst; a1.out = hq; a1.wsl = h->p1.wsl;
-    if (h->p1.wsl) a1.mt_major = 0;
+    a1.dst = P1.dst; a1.out = hq; a1.wsl = P1.wsl;
+    if (P1.wsl) a1.mt_major = 0;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
     a1.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
     { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }
@@ -910,7 +957,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     cudaEvent_t* ev = nullptr;
     if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
-    ST_TRY(launch(h->p1, tm_x, h->tm_w1, tm_ho, tm_ho, a1, s));
+    ST_TRY(launch(P1, tm_x, tmw1, tm_ho, tm_ho, a1, s));
     if (h->unfused) {   // the separate op #5 kernel (PDL-chained like the GEMMs)
         if (dbg && acc1) CUDA_TRY(cudaMemcpyAsync(acc1, a1ws, (size_t)T * H * 4, cudaMemcpyDeviceToDevice, s));
         Op5Args o = {};

@@ -206,10 +206,14 @@ def test_folded_constants_match_oracle(dev):
     np.testing.assert_array_equal(w2, L.w2.astype(np.int64).sum(1))
 
 
-def test_shard_concat_equals_unsharded(dev):
+def test_shard_concat_equals_unsharded(dev, monkeypatch):
     """Tokens are independent rows: running shards separately and
-    concatenating equals the unsharded run bit-exactly (the multi-GPU invariant)."""
+    concatenating equals the unsharded run bit-exactly (the multi-GPU invariant) while the
+    shards run the same launch plan.  The plan is a function of T (the few-tile plans for
+    runs of at most a few m-tiles), so this arm pins the many-tile plans
+    (SWIN_MLP_SMALL=0); the next test covers a plan switch."""
     from paper_2402_01169_b200 import SwinMlpInt8Layer
+    monkeypatch.setenv("SWIN_MLP_SMALL", "0")
     L = _layer(384, 7000)
     T = 1000
     X = torch.from_numpy(synth.make_activations(L, T, 9)).to(dev)
@@ -222,6 +226,41 @@ def test_shard_concat_equals_unsharded(dev):
     perm = torch.randperm(T, generator=torch.Generator().manual_seed(1))
     yp = layer(X[perm.to(dev)].contiguous()).cpu()
     assert torch.equal(yp, full[perm])
+
+
+@pytest.mark.parametrize("ln_fp64", [False, True])
+def test_shard_concat_across_plan_switch(dev, ln_fp64):
+    """Shards small enough for the few-tile plans (FC1 BN = 64 tiles, op #6 on an 8-CTA
+    cluster) against the unsharded many-tile run: Hq is integer/elementwise work and the
+    same bit for bit under any tiling; Y differs only in the LayerNorm statistics' fp32
+    summation order (the row split across 8 instead of 2 CTAs), so it is within the Y tier
+    (R15) with fp32 statistics and bit-exact with ln_fp64."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(384, 7001)
+    T = 1000
+    X = torch.from_numpy(synth.make_activations(L, T, 10)).to(dev)
+    layer = SwinMlpInt8Layer(L, device=0, ln_fp64=ln_fp64)
+    full = layer.run_debug(X)
+    cuts = ((0, 49), (49, 177), (177, 1000))
+    parts = [layer.run_debug(X[a:b].contiguous()) for a, b in cuts]
+    torch.cuda.synchronize()
+    hq = torch.cat([p["hidden"].cpu() for p in parts])
+    assert torch.equal(full["hidden"].cpu(), hq)
+    y = torch.cat([p["y"].cpu() for p in parts]).numpy()
+    if ln_fp64:
+        np.testing.assert_array_equal(full["y"].cpu().numpy(), y)
+    else:
+        _tier_int8(y, full["y"].cpu().numpy(), what="Y across plans")
+
+
+@pytest.mark.parametrize("C,T", [(384, 49), (512, 49), (768, 49), (768, 128), (768, 200), (1024, 49),
+                                 (1536, 49), (384, 1), (768, 17)])
+def test_parity_few_tile_plans(dev, C, T):
+    """The few-tile plans chosen per run for one or two m-tiles (configs[0]: one 7x7
+    window, T = 49, C = 768) against the oracle, every output element."""
+    _run_and_check(dev, _layer(C, 7100 + C + T), T, x_seed=T)
+    _run_and_check(dev, _layer(C, 7200 + C + T, act=1, bias=True, zx=-5, zh=3, zy=2), T, x_seed=T + 1,
+                   resid=True, e2e=False)
 
 
 def test_run_host_matches_device(dev):
