@@ -412,7 +412,7 @@ def main():
         cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
                "sample": f"every {args.cpu_stride}th token of each of the 4 layers ({tok} tokens, {t:.1f} s)"}
 
-    plans = [l.plan() for l in relu_layers]
+    plans = [l.plan(T) for (_, T, _), l in zip(spec, relu_layers)]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -479,7 +479,7 @@ def window_latency(steps):
             "us_cold_l2": round(cold, 2), "us_hot_l2": round(hot, 2),
             "us_hot_in_cuda_graph": round(graph_us, 2) if isinstance(graph_us, float) else graph_us,
             "hbm_frac_cold": round(bytes_cold / (cold * 1e-6) / 1e9 / peak_gbs, 3),
-            "algorithmic_bytes": bytes_cold, "plan": layer.plan(), "parallelism": "replicas only (DESIGN.md §2.6)"}
+            "algorithmic_bytes": bytes_cold, "plan": layer.plan(T), "parallelism": "replicas only (DESIGN.md §2.6)"}
 
 
 def graph_time(torch, layer, x, y, ws, steps):

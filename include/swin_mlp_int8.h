@@ -205,6 +205,14 @@ swin_mlp_status_t swin_mlp_int8_set_trace(swin_mlp_int8_t h, void* trace, int32_
  * Returns 0, or -1 on a NULL argument. */
 int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
 
+/* Introspection: the plans a run of T tokens actually launches (the two-kernel path
+ * chooses per run: the few-tile plans for one or two m-tiles, the CTA-pair op #6 for at
+ * most one wave of pairs, else the defaults).  Same 20-entry layout as
+ * swin_mlp_int8_plan with entries 0-11 and 16 describing the chosen plans, and entry 19 =
+ * op5_unfused | (choice << 1), choice 0 = default, 1 = CTA-pair op #6, 2 = few-tile.
+ * Host-only, no launch.  Returns 0, or -1 on a NULL argument or T < 0. */
+int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20);
+
 /* Release the handle's device memory.  No run may be in flight. NULL is OK. */
 swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h);
 

@@ -29,6 +29,7 @@ EXPORTS = [
     "swin_mlp_int8_create", "swin_mlp_int8_workspace_bytes", "swin_mlp_int8_run",
     "swin_mlp_int8_run_debug", "swin_mlp_int8_host_workspace_bytes", "swin_mlp_int8_run_host",
     "swin_mlp_int8_get_constants", "swin_mlp_int8_launches_per_run", "swin_mlp_int8_plan",
+    "swin_mlp_int8_plan_for",
     "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end", "swin_mlp_int8_set_trace",
     "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
     "swin_mlp_int8_host_batch_workspace_bytes", "swin_mlp_int8_run_host_batch",
@@ -97,6 +98,8 @@ def lib():
     L.swin_mlp_int8_launches_per_run.restype = i32
     L.swin_mlp_int8_plan.argtypes = [P, P]
     L.swin_mlp_int8_plan.restype = i32
+    L.swin_mlp_int8_plan_for.argtypes = [P, ctypes.c_int64, P]
+    L.swin_mlp_int8_plan_for.restype = i32
     L.swin_mlp_int8_profile_begin.argtypes = [P, i32]
     L.swin_mlp_int8_profile_begin.restype = i32
     L.swin_mlp_int8_profile_end.argtypes = [P, P, P, P]
@@ -267,9 +270,13 @@ class SwinMlpInt8Layer:
                 pass
             self.handle = None
 
-    def plan(self):
+    def plan(self, T=None):
+        """The layer's launch plan; with T, the plans a run of T tokens launches."""
         out = (ctypes.c_int32 * 20)()
-        lib().swin_mlp_int8_plan(self.handle, out)
+        if T is None:
+            lib().swin_mlp_int8_plan(self.handle, out)
+        elif lib().swin_mlp_int8_plan_for(self.handle, int(T), out) != 0:
+            raise ValueError(f"swin_mlp_int8_plan_for: bad T = {T}")
         if out[12]:
             return {"fused": 1, "stages": out[13], "hq_buffers": out[14], "acc1_buffers": out[15],
                     "x_slots": out[17], "w2_stages": out[18],
@@ -277,7 +284,8 @@ class SwinMlpInt8Layer:
         return {"fused": 0, "fc1_bn": out[0], "fc1_cs": out[1], "fc1_stages": out[2], "fc1_max_clusters": out[3],
                 "fc2_bn": out[4], "fc2_cs": out[5], "fc2_stages": out[6], "fc2_max_clusters": out[7],
                 "fc1_groups": out[8], "fc2_groups": out[9], "fc1_resb": out[10], "fc2_resb": out[11],
-                "fc1_pair": out[16], "op5_unfused": out[19]}
+                "fc1_pair": out[16], "op5_unfused": out[19] & 1,
+                **({"run_plan": ("default", "ln_pair", "few_tile")[out[19] >> 1]} if T is not None else {})}
 
     def set_trace(self, buf=None, cta=0):
         """buf: int64 device tensor of >= 9216 elements (see swin_mlp_int8_set_trace), or None."""

@@ -566,6 +566,18 @@ struct swin_mlp_int8_s {
     }
 };
 
+// Which plan pair a run of T tokens takes (two-kernel path): 0 = the default plans,
+// 1 = the CTA-pair op #6 (p2b, at most one wave of pairs), 2 = the few-tile plans
+// (p1s/p2s: the defaults would put both GEMMs on fewer than num_sms / 4 CTAs).
+static int plan_choice(const swin_mlp_int8_s* h, int64_t T) {
+    const int64_t m_tiles = (T + kBM - 1) / kBM;
+    const int64_t units1 = (h->p1.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p1.n_groups;
+    const int64_t units2 = (h->p2.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p2.CS;
+    if (h->has_small && units1 + units2 < h->num_sms / 4) return 2;
+    if (h->has_p2b && m_tiles <= 2 * (int64_t)h->p2b.max_clusters) return 1;
+    return 0;
+}
+
 namespace {
 
 // encode_2d through the handle's cache of activation maps
@@ -903,10 +915,8 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     }
 
     const int64_t m_tiles = (T + kBM - 1) / kBM;
-    const int64_t units1 = (h->p1.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p1.n_groups;
-    const int64_t units2 = (h->p2.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p2.CS;
-    const bool use_s = h->has_small && units1 + units2 < h->num_sms / 4;
-    const bool use_b = !use_s && h->has_p2b && m_tiles <= 2 * (int64_t)h->p2b.max_clusters;
+    const int run_plan = plan_choice(h, T);
+    const bool use_s = run_plan == 2, use_b = run_plan == 1;
     const Plan& P1 = use_s ? h->p1s : h->p1;
     const CUtensorMap& tmw1 = use_s ? h->tm_w1s : h->tm_w1;
     const Plan& P2 = use_s ? h->p2s : use_b ? h->p2b : h->p2;
@@ -1384,5 +1394,20 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
     out10[16] = h->p1.pair; out10[17] = h->fp.NX; out10[18] = h->fp.stages2; out10[19] = h->unfused ? 1 : 0;
     return 0;
 }
+
+int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20) {
+    if (!h || !out20 || T < 0) return -1;
+    swin_mlp_int8_plan(h, out20);
+    const int c = plan_choice(h, T);
+    const Plan& P1 = c == 2 ? h->p1s : h->p1;
+    const Plan& P2 = c == 2 ? h->p2s : c == 1 ? h->p2b : h->p2;
+    out20[0] = P1.BN; out20[1] = P1.CS; out20[2] = P1.stages; out20[3] = P1.max_clusters;
+    out20[4] = P2.BN; out20[5] = P2.CS; out20[6] = P2.stages; out20[7] = P2.max_clusters;
+    out20[8] = P1.G; out20[9] = P2.G;
+    out20[10] = P1.resb ? 1 : P1.wsl ? 2 : 0; out20[11] = P2.resb; out20[16] = P1.pair;
+    out20[19] = (h->unfused ? 1 : 0) | (c << 1);
+    return 0;
+}
+
 
 }  // extern "C"

@@ -111,6 +111,8 @@ def test_null_handle_paths(P):
     assert L.swin_mlp_int8_workspace_bytes(None, 10) == 0
     assert L.swin_mlp_int8_destroy(None) == P.SWIN_MLP_OK
     assert L.swin_mlp_int8_launches_per_run(None) == 0
+    out = (ctypes.c_int32 * 20)()
+    assert L.swin_mlp_int8_plan_for(None, 49, out) == -1
 
 
 def _proj_desc(P, **kw):

@@ -530,3 +530,15 @@ def test_proj_requires_residual(dev):
     a = torch.zeros((10, 96), dtype=torch.int8, device=dev)
     with pytest.raises(SwinMlpError):
         layer(a, None)
+
+
+def test_plan_for_reports_the_run_plan(dev):
+    """swin_mlp_int8_plan_for: a one-window run (T = 49) at C = 768 takes the few-tile plans
+    (FC1 BN = 64 single-CTA tiles, op #6 on an 8-CTA cluster), a full-stage run the defaults."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    layer = SwinMlpInt8Layer(_layer(768, 7300), device=0)
+    small, big = layer.plan(49), layer.plan(200704)
+    assert small["run_plan"] == "few_tile" and small["fc1_bn"] == 64 and small["fc1_pair"] == 0
+    assert small["fc2_cs"] == 8 and small["fc2_bn"] == 96
+    assert big["run_plan"] == "default"
+    assert {k: v for k, v in big.items() if k != "run_plan"} == layer.plan()

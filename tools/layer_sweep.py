@@ -44,4 +44,4 @@ print(json.dumps({"C": C, "T": T, "env": env, "layer_us_median": round(us[len(us
                   "fc1_us": round(f1 / max(n, 1) * 1e3, 2), "fc2_us": round(f2 / max(n, 1) * 1e3, 2),
                   "fc1_tops": round(ops / (f1 / max(n, 1) * 1e-3) / 1e12, 1) if f1 else None,
                   "fc2_tops": round(ops / (f2 / max(n, 1) * 1e-3) / 1e12, 1) if f2 else None,
-                  "layer_tops": round(2 * ops / (us[len(us) // 2] * 1e-6) / 1e12, 1), "plan": h.plan()}), flush=True)
+                  "layer_tops": round(2 * ops / (us[len(us) // 2] * 1e-6) / 1e12, 1), "plan": h.plan(T)}), flush=True)
