@@ -158,8 +158,10 @@ void oracle_ep5(const int32_t* A1, int64_t nrows, int32_t H, const float* m1,
  * then Q (reading R4).
  *   d = fmaf(fl(A2), m2[c], b2[c] or 0)
  *   z = fl(d + R[t][c])                          with an fp32 residual, else
- *   z = fmaf(fl(X[t][c] - z_x), s_x, d)          the residual dQ(X) added with one
- *                                                rounding (reading R3)
+ *   r = fl(fl(X[t][c] - z_x) * s_x)              dQ(X) (the dQ node), then
+ *   z = fl(d + r)                                the Add node (Fig. 1, PAPER.md:82-86:
+ *                                                dQ -> FC2 Bias -> Add, each its own step;
+ *                                                reading R3)
  *   mu  = (sum_c z) / C          double, ascending c
  *   var = (sum_c (z-mu)^2) / C   double, ascending c, biased (R9)
  *   rstd = 1 / sqrt(var + eps)   double
@@ -180,8 +182,10 @@ void oracle_ep6(const int32_t* A2, int64_t nrows, int32_t C, const float* m2,
             float d = fmaf((float)A2[i * C + c], m2[c], b2 ? b2[c] : 0.0f);
             if (R)
                 z[c] = d + R[i * C + c];
-            else
-                z[c] = fmaf((float)((int32_t)X[i * C + c] - z_x), s_x, d);
+            else {
+                float r = (float)((int32_t)X[i * C + c] - z_x) * s_x;   /* dQ(X) */
+                z[c] = d + r;                                              /* Add  */
+            }
             if (z_out) z_out[i * C + c] = z[c];
         }
         double sum = 0.0;

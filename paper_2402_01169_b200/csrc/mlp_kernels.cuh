@@ -811,7 +811,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             rr[2 * j4 + 1] = make_float2(v.z, v.w);
                         }
                     } else {
-                        // x - z_x as float (then z = fl((x - z_x) * s_x + d)).  Exact int8 -> float without the
+                        // x - z_x as float (then z = fl(d + fl((x - z_x) * s_x))).  Exact int8 -> float without the
                         // 1/8-rate I2F.S8: with u = x ^ 0x80 (offset binary) the bits
                         // 0x4B0000uu are the float 2^23 + u, and
                         // (2^23 + u) - (2^23 + 128 + z_x) = x - z_x exactly.
@@ -838,8 +838,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     tap_acc(r, n0 + cl);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        // z = fl(d + R), or fl((x - z_x) * s_x + d) with one rounding (R3)
-                        z[j] = x_res ? f2_fma(rr[j], sx2, z[j]) : f2_add(z[j], rr[j]);
+                        // z = fl(d + R), or fl(d + fl((x - z_x) * s_x)): dQ(x) then Add (R3)
+                        z[j] = f2_add(z[j], x_res ? f2_mul(rr[j], sx2) : rr[j]);
                         if constexpr (STATS64) {
                             s1d = __dadd_rn(s1d, (double)z[j].x);
                             s1d = __dadd_rn(s1d, (double)z[j].y);

@@ -349,9 +349,11 @@ def test_recipe_non_degenerate():
         assert (np.abs(X.astype(int)).sum(1) > 0).all()
 
 
-def test_ep6_residual_added_with_one_rounding():
-    """Reading R3: with residual == NULL, z = fl((X - z_x) * s_x + d) rounded ONCE (an fma),
-    pinned against exact rational arithmetic (not against another float formula)."""
+def test_ep6_residual_dq_then_add():
+    """Reading R3 / Fig. 1 (dQ -> FC2 Bias -> Add, each node its own step): with
+    residual == NULL the residual is dQ(X) = fl(fl(X - z_x) * s_x) (the dQ of PAPER.md:124) and
+    z = fl(d + dQ(X)) -- two roundings, pinned against exact rational arithmetic (each rounding
+    done on the exact rational value, not by another float formula)."""
     from fractions import Fraction
 
     def f32(q):   # exact round-to-nearest-even of a rational to float32
@@ -372,10 +374,11 @@ def test_ep6_residual_added_with_one_rounding():
         for c in range(C):
             d = f32(Fraction(float(np.float32(A2[t, c]))) * Fraction(float(m2[c])) +
                     Fraction(float(b2[c])))                         # fmaf(fl(A2), m2, b2)
-            exact = Fraction(int(X[t, c]) - z_x) * Fraction(float(s_x)) + Fraction(float(d))
-            assert z[t, c] == f32(exact), (t, c)
-            differs += np.float32(np.float32(np.float32(int(X[t, c]) - z_x) * s_x) + d) != z[t, c]
-    assert differs > 0   # the case actually distinguishes one rounding from two
+            r = f32(Fraction(int(X[t, c]) - z_x) * Fraction(float(s_x)))   # dQ(X)
+            assert z[t, c] == f32(Fraction(float(d)) + Fraction(float(r))), (t, c)
+            one = f32(Fraction(int(X[t, c]) - z_x) * Fraction(float(s_x)) + Fraction(float(d)))
+            differs += one != z[t, c]
+    assert differs > 0   # the case actually distinguishes two roundings from one (an fma)
 
 
 # ---------------------------------------------------------------- NEXT-2: proj GEMM + op #4 (+ LN2)
