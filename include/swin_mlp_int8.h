@@ -210,8 +210,22 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
  * most one wave of pairs, else the defaults).  Same 20-entry layout as
  * swin_mlp_int8_plan with entries 0-11 and 16 describing the chosen plans, and entry 19 =
  * op5_unfused | (choice << 1), choice 0 = default, 1 = CTA-pair op #6, 2 = few-tile.
+ * The plan hint (swin_mlp_int8_set_plan_hint), when set, replaces T.  For a one-kernel
+ * handle (entry 12 = 1) the result equals swin_mlp_int8_plan: one launch serves every T.
  * Host-only, no launch.  Returns 0, or -1 on a NULL argument or T < 0. */
 int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20);
+
+/* Plan hint (batch invariance, reading R20).  The two-kernel path chooses its
+ * launch plans per run from T (few-tile plans for one or two m-tiles, the CTA-pair op #6
+ * for one wave of pairs, else the defaults), and with fp32 LayerNorm statistics
+ * (ln_fp64 = 0) Y can differ by 1 LSB between plans because the row statistics are summed
+ * in a different order (within the R15 tier).  With T_hint > 0 every later run/run_debug
+ * on this handle chooses its plans as a run of T_hint tokens would, so the shards of a
+ * batch of T_hint tokens (multi-GPU token sharding, chunked serving) reproduce the
+ * unsharded run bit for bit.  T_hint = 0 restores the per-run choice.  run_host and
+ * run_host_batch always plan every chunk for the whole call's T (or the hint when set).
+ * Host-only.  Returns OK, or EINVAL on a NULL handle or T_hint < 0. */
+swin_mlp_status_t swin_mlp_int8_set_plan_hint(swin_mlp_int8_t h, int64_t T_hint);
 
 /* Release the handle's device memory.  No run may be in flight. NULL is OK. */
 swin_mlp_status_t swin_mlp_int8_destroy(swin_mlp_int8_t h);

@@ -29,7 +29,7 @@ EXPORTS = [
     "swin_mlp_int8_create", "swin_mlp_int8_workspace_bytes", "swin_mlp_int8_run",
     "swin_mlp_int8_run_debug", "swin_mlp_int8_host_workspace_bytes", "swin_mlp_int8_run_host",
     "swin_mlp_int8_get_constants", "swin_mlp_int8_launches_per_run", "swin_mlp_int8_plan",
-    "swin_mlp_int8_plan_for",
+    "swin_mlp_int8_plan_for", "swin_mlp_int8_set_plan_hint",
     "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end", "swin_mlp_int8_set_trace",
     "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
     "swin_mlp_int8_host_batch_workspace_bytes", "swin_mlp_int8_run_host_batch",
@@ -100,6 +100,8 @@ def lib():
     L.swin_mlp_int8_plan.restype = i32
     L.swin_mlp_int8_plan_for.argtypes = [P, ctypes.c_int64, P]
     L.swin_mlp_int8_plan_for.restype = i32
+    L.swin_mlp_int8_set_plan_hint.argtypes = [P, ctypes.c_int64]
+    L.swin_mlp_int8_set_plan_hint.restype = i32
     L.swin_mlp_int8_profile_begin.argtypes = [P, i32]
     L.swin_mlp_int8_profile_begin.restype = i32
     L.swin_mlp_int8_profile_end.argtypes = [P, P, P, P]
@@ -286,6 +288,10 @@ class SwinMlpInt8Layer:
                 "fc1_groups": out[8], "fc2_groups": out[9], "fc1_resb": out[10], "fc2_resb": out[11],
                 "fc1_pair": out[16], "op5_unfused": out[19] & 1,
                 **({"run_plan": ("default", "ln_pair", "few_tile")[out[19] >> 1]} if T is not None else {})}
+
+    def set_plan_hint(self, T_hint=0):
+        """Choose launch plans as for a run of T_hint tokens (0: per run); see the header."""
+        _check(lib().swin_mlp_int8_set_plan_hint(self.handle, int(T_hint)))
 
     def set_trace(self, buf=None, cta=0):
         """buf: int64 device tensor of >= 9216 elements (see swin_mlp_int8_set_trace), or None."""

@@ -1,13 +1,13 @@
 // fused_mlp.cu — instantiations of the one-kernel MLP (fused_mlp.cuh).  Compiled
 // once per -DFUSED_PART=k (parallel build), each object holding the 16 variants whose
-// flags have (flags >> 4) == k: k = 0..5 single-CTA, 8..11 CTA pair (kFPair = 128); the
-// host picks one by flags.
+// flags have (flags >> 4) == k: k = 0..3 (flags 0..63: GELU, hidden zero point, FC1 bias,
+// fp64 LN, small-K conversion, taps); the host picks one by flags.
 #include <utility>
 
 #include "fused_mlp.cuh"
 
 #ifndef FUSED_PART
-#error "compile with -DFUSED_PART=<0..5 | 8..11>"
+#error "compile with -DFUSED_PART=<0..3>"
 #endif
 
 namespace swinmlp {

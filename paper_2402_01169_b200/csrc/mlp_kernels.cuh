@@ -106,7 +106,6 @@ struct GemmArgs {
     unsigned long long* trace;
     int32_t trace_cta;
     unsigned long long* cta_stamps;   // debug: per CTA %globaltimer at entry / exit ([2 * blockIdx.x + {0,1}])
-    int32_t dbg;                      // debug experiments (0 in production)
     int32_t eg;                       // op #5 epilogue groups (1: all 16 warps drain every tile; or G)
     int32_t* acc_out;                 // EP_ACC: [M][ldo] int32 A1 (the unfused plan's GEMM output)
     int32_t yin;                      // op #6 with xstage == G: Y staged over its own x tile (no
@@ -472,8 +471,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (elect_one()) {
                         if (trc && kb == 0 && it < 512) trc[2 * it] = gtimer();
                         if (trc && it < 4 && kb < 16) trc[2048 + 16 * (40 + it) + kb] = gtimer();
-                        mbar_arrive_expect_tx(bar_full + 8u * s, (p.dbg & 1) ? a_bytes : a_bytes + b_bytes);
-                        if (!(p.dbg & 1)) tma_load_2d(&tmB, sB + (uint32_t)s * b_bytes, bar_full + 8u * s, kb * kBK, n0);
+                        mbar_arrive_expect_tx(bar_full + 8u * s, a_bytes + b_bytes);
+                        tma_load_2d(&tmB, sB + (uint32_t)s * b_bytes, bar_full + 8u * s, kb * kBK, n0);
                         load_a(kb, row0);
                     }
                     __syncwarp();
@@ -572,7 +571,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int n0 = n0_of(ng);
                 const int32_t row0 = (int32_t)(m_tile * kBM);
                 const uint32_t src = base + L.out + sb * tile_bytes;
-                if (EPI != EP_ACC && !(p.dbg & 2))
+                if (EPI != EP_ACC)
                 for (uint32_t sub = 0; sub < ((uint32_t)BN >> lgW); ++sub)
                     tma_store_2d(&tmO, src + (sub << (lgW + 7u)), n0 + (int)(sub << lgW), row0);
                 bulk_commit();
@@ -610,7 +609,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
                 __syncwarp();
             }
-            if (IS_LN && p.resid != nullptr && !(p.dbg & 8)) {
+            if (IS_LN && p.resid != nullptr) {
                 // fp32 residual rows of this tile -> L2 ahead of pass 1 (its per-chunk loads are
                 // otherwise HBM-latency bound: one dependent load round trip per 16 columns)
                 if (it == 0) pdl_wait();
@@ -869,7 +868,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             *reinterpret_cast<float4*>(zrow + 4 * j4) =
                                 make_float4(z[2 * j4].x, z[2 * j4].y, z[2 * j4 + 1].x, z[2 * j4 + 1].y);
                     }
-                    if (!(p.dbg & 4)) tmem_st16(tb + (uint32_t)cl, r);
+                    tmem_st16(tb + (uint32_t)cl, r);
                 });
                 tmem_wait_st();
                 if (x_smem && !yin) {   // the x tile has been consumed: let the loader prefetch the next one
@@ -1054,7 +1053,6 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 mbar_arrive(bar_tempty + 8u * buf);   // TMEM free: the next MMA may start
                 if constexpr (PAIR) {                 // (pair: the leader's MMA waits on both CTAs)
                     if (rank == 0) mbar_arrive(bar_ptempty + 8u * buf);
-                    else if (p.dbg & 16) mbar_arrive_cluster(mapa(bar_ptempty + 8u * buf, 0));   // (A/B: release)
                     else mbar_arrive_cluster_relaxed(mapa(bar_ptempty + 8u * buf, 0));
                 }
                 if (!dst) mbar_arrive(bar_sfull + 8u * buf);    // this warp's part of the tile is staged

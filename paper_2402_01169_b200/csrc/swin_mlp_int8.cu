@@ -28,28 +28,16 @@ using namespace swinmlp;
 
 namespace swinmlp {
 using FusedFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, FusedArgs);
-FusedFn fused_kernel_part0(int flags);   // fused_mlp.cu, -DFUSED_PART=0..5 (flags >> 4)
+FusedFn fused_kernel_part0(int flags);   // fused_mlp.cu, -DFUSED_PART=0..3 (flags >> 4)
 FusedFn fused_kernel_part1(int flags);
 FusedFn fused_kernel_part2(int flags);
 FusedFn fused_kernel_part3(int flags);
-FusedFn fused_kernel_part4(int flags);
-FusedFn fused_kernel_part5(int flags);
-FusedFn fused_kernel_part8(int flags);   // CTA-pair variants (kFPair)
-FusedFn fused_kernel_part9(int flags);
-FusedFn fused_kernel_part10(int flags);
-FusedFn fused_kernel_part11(int flags);
 inline FusedFn fused_kernel_for(int flags) {
     switch (flags >> 4) {
         case 0: return fused_kernel_part0(flags);
         case 1: return fused_kernel_part1(flags);
         case 2: return fused_kernel_part2(flags);
-        case 3: return fused_kernel_part3(flags);
-        case 4: return fused_kernel_part4(flags);
-        case 5: return fused_kernel_part5(flags);
-        case 8: return fused_kernel_part8(flags);
-        case 9: return fused_kernel_part9(flags);
-        case 10: return fused_kernel_part10(flags);
-        default: return fused_kernel_part11(flags);
+        default: return fused_kernel_part3(flags);
     }
 }
 }  // namespace swinmlp
@@ -218,19 +206,10 @@ swin_mlp_status_t prepare(Plan& pl, int num_sms) {
 // full_row: the epilogue needs whole rows (LayerNorm) -> the cluster must
 // cover all N columns (CS * BN == N); otherwise column groups are independent.
 // The first candidate whose shared-memory plan fits wins.
-// Epilogue groups for G accumulator buffers: G ping-pong groups (default), or one
-// group of all 16 warps per tile.  Measured on the Swin-T stages: no gain for op #5
-// (its drain is issue-bound, the same SM-wide rate either way) and op #6 slower by
-// ~1 us (the 4-part statistics combine).  SWIN_MLP_EP5_GROUPS / SWIN_MLP_EP6_GROUPS
-// = 1, 2 or 4 (dividing G) select another split; a plan that does not fit falls back
-// to G.
-int epilogue_groups(int epi, int G) {
-    static const char* e5 = std::getenv("SWIN_MLP_EP5_GROUPS");
-    static const char* e6 = std::getenv("SWIN_MLP_EP6_GROUPS");
-    const char* e = epi == EP6_LN ? e6 : e5;
-    const int want = e ? atoi(e) : G;
-    return (want == 1 || want == 2 || want == 4) && G % want == 0 ? want : G;
-}
+// Epilogue groups: G ping-pong groups, one per accumulator buffer.  (Round 1 measured one
+// group of all 16 warps per tile: no gain for op #5, its drain is issue-bound at the same
+// SM-wide rate, and op #6 ~1 us slower from the 4-part statistics combine; removed.)
+int epilogue_groups(int, int G) { return G; }
 
 bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // output TMA box width: widest swizzle span dividing BN (full 128-B lines when possible)
@@ -242,12 +221,10 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // Weight-stationary slice (op #5, mode 2): each cluster keeps only ITS column group's
     // weights resident (half of them per CTA of a pair) and streams A tiles only -- half the
     // operand bytes per MAC of the streamed plan.  Tried after whole-B residency.
-    static const bool no_resb = std::getenv("SWIN_MLP_NO_RESB") != nullptr;   // debug / A-B switch
-    // (opt-in SWIN_MLP_WSL=1: measured no faster -- C = 512 FC1 40.0 vs 41.0 us, C = 384
-    // 22.4 vs 20.7 us; halving the operand bytes does not move FC1, whose tiles are gated by
-    // the op #5 drain of the accumulator they reuse)
-    const char* wsl_env = std::getenv("SWIN_MLP_WSL");   // (read per create)
-    const bool no_wsl = !(wsl_env && *wsl_env == '1');
+    // (Round 1 also measured weight-stationary column slices -- each cluster keeping its W1
+    // slice resident: C = 512 FC1 40.0 vs 41.0 us, C = 384 22.4 vs 20.7 us, no faster because
+    // FC1's tiles are gated by the op #5 drain, DESIGN.md §2.3 -- so that mode is not planned.)
+    const bool no_resb = false, no_wsl = true;
     for (int mode : {1, 2, 0}) {   // 1: whole B resident, 2: this cluster's B slice, 0: streamed
     const int rb = mode != 0;
     if (mode == 1 && (no_resb || pl.pair)) continue;   // pair: B halves (mode 2 or streamed)
@@ -258,9 +235,7 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     // output staging: G ping-pong groups / accumulator buffers / staging tiles, 4 when
     // 4*BN TMEM columns fit (more tiles in flight), else 2; op #6 also prefers its
     // residual x tiles staged in smem
-    // SWIN_MLP_XS_MAX caps the op #6 x tile buffers (A/B switch: trades them for ring stages)
-    const char* xs_env = std::getenv("SWIN_MLP_XS_MAX");   // (read per create)
-    const int xs_max = xs_env && *xs_env ? atoi(xs_env) : 4;
+    const int xs_max = 4;
     for (int xs : {4, 2, 1, 0}) {   // op #6 x tile buffers: one per group, one shared, none
     if (epi != EP6_LN && xs != 0) continue;
     if (xs > xs_max) continue;
@@ -277,11 +252,10 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         // op #6 with one x tile per group: Y staged over its x tile (yin) frees G output tiles of
         // smem for ring stages; SWIN_MLP_NO_YIN=1 keeps separate staging (A/B switch)
         const bool no_yin = std::getenv("SWIN_MLP_NO_YIN") != nullptr;   // (read per create)
-        // op #5: Hq stored from registers (no staging tiles, deeper ring), opt-in SWIN_MLP_DST=1:
-        // measured slower (C = 512 FC1 43.7 us with 6 stages vs 39.2 us staged with 4; the
-        // drain, not the ring, gates FC1 there)
-        const char* dst_env = std::getenv("SWIN_MLP_DST");   // (read per create)
-        const bool no_dst = !(dst_env && *dst_env == '1');
+        // (op #5 storing Hq from registers to free the staging tiles for ring stages measured
+        // slower in round 1 -- C = 512 FC1 43.7 us with 6 stages vs 39.2 us staged with 4 -- and is
+        // not planned)
+        const bool no_dst = true;
         for (int dst : {1, 0}) {
         if (dst && (epi == EP6_LN || epi == EP_ACC || no_dst)) continue;
         for (int yin : {1, 0}) {
@@ -372,17 +346,13 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, i
     // its A rows and half of B, 2/3 of the single-CTA operand bytes per MAC in a 4-deep
     // ring).  Measured on the Swin-T stages: FC1 at C = 768 2 us faster, at C = 384
     // 0.5 us slower (there the single-CTA ring already holds a whole tile's K).
-    // SWIN_MLP_PAIR=1 / 0 forces it on / off.
     if (small_bn > 0) {
         if (N % small_bn) return false;
         pl.BN = small_bn; pl.CS = 1; pl.n_groups = N / small_bn;
         return fit_smem(epi, pl, 3, K) || fit_smem(epi, pl, 2, K);
     }
-    static const char* pair_env = std::getenv("SWIN_MLP_PAIR");
-    const bool want_pair = pair_env ? (*pair_env == '1') : K >= 512;
-    // SWIN_MLP_PAIR_BN = 128 / 192: narrower pair tiles (more accumulator buffers) -- A/B switch
-    const char* pbn_env = std::getenv("SWIN_MLP_PAIR_BN");   // (read per create)
-    const int pbn = pbn_env && *pbn_env ? atoi(pbn_env) : 256;
+    const bool want_pair = K >= 512;
+    const int pbn = 256;   // (128-wide pair tiles with 4 accumulator buffers measured slower: 50.5 vs 36.7 us)
     if (epi != EP6_LN && want_pair && (pbn == 128 || pbn == 192 || pbn == 256) && N % pbn == 0) {
         pl.BN = pbn; pl.CS = 1; pl.n_groups = N / pbn; pl.pair = 1;
         if (fit_smem(epi, pl, 3, K)) return true;
@@ -398,25 +368,19 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, i
 
 // The one-kernel plan: weights resident in smem when they fit (W1 and W2 each
 // 4C^2 bytes: C <= 128), else streamed through a ring; Hq buffers 2..4.
-// CTA-pair one-kernel plan (streamed weights, C > 128), opt-in: SWIN_MLP_FUSED_PAIR=1.
-// Measured (back-to-back launches, Swin-T b64): C = 192 41.7 us vs 30.2 us single-CTA,
-// C = 384 40.6 vs 35.1 -- halving each SM's weight stream does not pay for the per-chunk
-// cross-CTA handshakes (peer op #5 -> leader MMA), so the single-CTA plan is the default.
-int fused_pair_for(int C) {
-    const char* e = std::getenv("SWIN_MLP_FUSED_PAIR");   // (read per create)
-    return (e && *e == '1' && C > 128) ? 1 : 0;
-}
+// (A CTA-pair one-kernel plan measured slower in round 1 -- C = 192 41.7 us vs 30.2 us
+// single-CTA, C = 384 40.6 vs 35.1: halving each SM's weight stream does not pay for the
+// per-chunk cross-CTA handshakes -- and is not built.)
+int fused_pair_for(int) { return 0; }
 
 bool make_fused(int C, int H, int ebytes, FusedPlan& fp, int pair) {
     fp = FusedPlan();
     fp.pair = pair;
     const char* no = std::getenv("SWIN_MLP_NO_FUSED");   // A/B switch (read per create)
     if (no && *no && *no != '0') return false;
-    // C <= 256 by default; SWIN_MLP_FUSED_MAXC=384 admits 256 < C <= 384 (single acc1, FC2
-    // as two N = C/2 MMAs) -- measured at C = 384, T = 12544: 35.1 us vs 33.4 us for the
-    // two-kernel plan, so not the default
-    const char* mc = std::getenv("SWIN_MLP_FUSED_MAXC");   // (read per create)
-    const int maxc = mc && *mc ? std::min(384, atoi(mc)) : 256;
+    // C <= 256 (256 < C <= 384 -- a single acc1, FC2 as two N = C/2 MMAs -- measured at
+    // C = 384, T = 12544: 35.1 us vs 33.4 us for the two-kernel plan, so not planned)
+    const int maxc = 256;
     if (C > maxc || H % kFHc) return false;
     fp.KBC = (C + kBK - 1) / kBK;
     fp.NJ = H / kFHc;
@@ -447,8 +411,7 @@ bool make_fused(int C, int H, int ebytes, FusedPlan& fp, int pair) {
     // chunks load while FC2 still holds W2 items; Y staged over its X slot (frees a Y
     // buffer); the W1 ring as deep as fits (measured at C = 192: a 2-CTA cluster
     // multicasting the weight items, or W2 split in two items, did not help)
-    const char* yie = std::getenv("SWIN_MLP_FUSED_YIN");
-    const int yin = (yie && *yie == '0') ? 0 : 1;
+    const int yin = 1;
     // C > 256: one X slot (a CTA gets about one tile) so the weight rings get the smem
     for (int nx : {C > 256 ? 1 : 2, C > 256 ? 2 : 1}) {
     // W2 ring: up to two chunks of items (C > 256: two half-chunk items per chunk), then the
@@ -557,6 +520,9 @@ struct swin_mlp_int8_s {
     // run_host pipeline: copy-in and copy-out streams + per-chunk events (created lazily)
     cudaStream_t io_in = nullptr, io_out = nullptr;
     std::vector<cudaEvent_t> io_ev;
+    // plan hint (swin_mlp_int8_set_plan_hint): > 0 = runs choose their launch plans as a run of
+    // plan_hint tokens would, so shards / chunks of one batch run the batch's plan
+    int64_t plan_hint = 0;
     ~swin_mlp_int8_s() {
         for (void* p : allocs) cudaFree(p);
         for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
@@ -793,8 +759,7 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     }
     {
         const char* se = std::getenv("SWIN_MLP_SMALL");       // (read per create)
-        const char* sb = std::getenv("SWIN_MLP_SMALL_BN");
-        const int sbn = sb && *sb ? atoi(sb) : 64;
+        const int sbn = 64;   // (BN = 32 / 128 measured no better at the layer level)
         if (!h->unfused && !(se && *se == '0') && sbn >= 16 && sbn % 16 == 0 &&
             make_plan(epi1, H, C, false, h->p1s, 4, -1, sbn) &&
             make_plan(EP6_LN, C, H, true, h->p2s, d.ln_fp64 ? 8 : 4, 0, sbn)) {
@@ -817,13 +782,9 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     } else if (make_fused(C, H, d.ln_fp64 ? 8 : 4, h->fp, fused_pair_for(C))) {
         const int ff = (d.act == SWIN_MLP_ACT_GELU_ERF ? kFGelu : 0) | (d.h_zero_point ? kFZh : 0) |
                        (d.b1 ? kFB1 : 0) | (d.ln_fp64 ? kFS64 : 0) | (small_k1 ? kFSmallK : 0);
-        // op #6 register path when a thread's half row is at most kFRegCh chunks of 16:
-        // opt-in (SWIN_MLP_FUSED_REG=1) -- measured no faster at C = 96 (op #6 is not bound
-        // by the TMEM park / reload it removes)
-        const char* re = std::getenv("SWIN_MLP_FUSED_REG");
-        const bool reg = re && *re == '1' && !d.ln_fp64 && C / 2 <= 16 * kFRegCh;
         const int fpair = h->fp.pair ? kFPair : 0;
-        h->fp.fn = fused_kernel_for(ff | (reg && !fpair ? kFReg : 0) | fpair);
+        h->fp.fn = fused_kernel_for(ff | fpair);
+        h->has_small = false;   // (the one-kernel plan serves every T: no per-run plans)
         h->fp_dbg = fused_kernel_for(ff | kFTaps | fpair);
         H_TRY(encode_2d(&h->tm_fw1, h->w1, H, C, C, (uint32_t)(h->fp.pair ? kFHc / 2 : kFHc)));
         H_TRY(encode_2d(&h->tm_fw2, h->w2, C, H, H, fused_w2_rows(C, h->fp.pair)));
@@ -842,9 +803,13 @@ size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T) {
     return h->unfused ? hq + (size_t)T * h->d.H * 4 : hq;   // unfused plan: + A1 int32 [T][H]
 }
 
+// plan_T: the token count the launch plans are chosen for (the run's own T, the handle's plan
+// hint, or -- run_host / run_host_batch -- the whole call's T, so every chunk of one call runs
+// one plan and the result does not depend on the chunking; R20)
 static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const float* residual, int8_t* y,
                                   float* residual_out, int64_t T, void* workspace, size_t ws_bytes, void* stream,
-                                  int32_t* acc1, int8_t* hidden, int32_t* acc2, float* ln_out, bool dbg) {
+                                  int32_t* acc1, int8_t* hidden, int32_t* acc2, float* ln_out, bool dbg,
+                                  int64_t plan_T = 0) {
     if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
     if (T < 0) return fail(SWIN_MLP_EINVAL, "T=%lld < 0", (long long)T);
     if (T == 0) return SWIN_MLP_OK;
@@ -876,7 +841,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         a.inv_h = h->inv_h; a.z_h = h->d.h_zero_point; a.inv_y = h->inv_y; a.z_y = h->d.y_zero_point;
         a.s_x = h->d.x_scale; a.z_x = h->d.x_zero_point; a.eps = h->d.ln_eps;
         a.x = x; a.resid = residual; a.resid_out = residual_out;
-        { const char* e = std::getenv("SWIN_MLP_FUSED_ROT"); a.rotate = (e && *e == '0') ? 0 : 1; }
+        a.rotate = 1;
         if (dbg) { a.acc1_tap = acc1; a.hid_tap = hidden; a.acc2_tap = acc2; a.ln_tap = ln_out; }
         a.trace = h->trace; a.trace_cta = h->trace_cta;
         a.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
@@ -915,7 +880,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     }
 
     const int64_t m_tiles = (T + kBM - 1) / kBM;
-    const int run_plan = plan_choice(h, T);
+    const int run_plan = plan_choice(h, plan_T > 0 ? plan_T : h->plan_hint > 0 ? h->plan_hint : T);
     const bool use_s = run_plan == 2, use_b = run_plan == 1;
     const Plan& P1 = use_s ? h->p1s : h->p1;
     const CUtensorMap& tmw1 = use_s ? h->tm_w1s : h->tm_w1;
@@ -948,11 +913,10 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     if (P1.wsl) a1.mt_major = 0;
     a1.trace = h->trace; a1.trace_cta = h->trace_cta;
     a1.cta_stamps = h->trace ? h->trace + 8192 : nullptr;
-    { static const char* e = std::getenv("SWIN_MLP_DBG1"); a1.dbg = e ? atoi(e) : 0; }
 
     GemmArgs a2 = {};
     a2.M = T; a2.K = H; a2.BN = P2.BN; a2.CS = P2.CS; a2.stages = P2.stages; a2.G = P2.G; a2.eg = P2.eg;
-    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; } a2.xstage = P2.xstage; a2.yin = P2.yin; a2.x = x;
+    a2.xstage = P2.xstage; a2.yin = P2.yin; a2.x = x;
     a2.out_w = P2.out_w;
     a2.resb = P2.resb; a2.mt_major = P2.pair ? 0 : 1;   // op #6: one n-group per cluster
     a2.n_groups = 1; a2.num_units = P2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;
@@ -997,6 +961,13 @@ swin_mlp_status_t swin_mlp_int8_run(swin_mlp_int8_t h, const int8_t* x, const fl
                                     void* stream) {
     return run_impl(h, x, residual, y, residual_out, T, workspace, workspace_bytes, stream, nullptr, nullptr,
                     nullptr, nullptr, false);
+}
+
+swin_mlp_status_t swin_mlp_int8_set_plan_hint(swin_mlp_int8_t h, int64_t T_hint) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (T_hint < 0) return fail(SWIN_MLP_EINVAL, "T_hint=%lld < 0", (long long)T_hint);
+    h->plan_hint = T_hint;
+    return SWIN_MLP_OK;
 }
 
 swin_mlp_status_t swin_mlp_int8_run_debug(swin_mlp_int8_t h, const int8_t* x, const float* residual, int8_t* y,
@@ -1045,11 +1016,11 @@ swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host
     if (!h->io_in) {
         CUDA_TRY(cudaStreamCreateWithFlags(&h->io_in, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&h->io_out, cudaStreamNonBlocking));
-        for (int i = 0; i < 2 * kMaxChunks + 2; ++i) {
-            cudaEvent_t e;
-            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            h->io_ev.push_back(e);
-        }
+    }
+    while (h->io_ev.size() < 2 * kMaxChunks + 2) {   // (run_host_batch may have created fewer)
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->io_ev.push_back(e);
     }
     cudaEvent_t ev_start = h->io_ev[2 * kMaxChunks], ev_done = h->io_ev[2 * kMaxChunks + 1];
     CUDA_TRY(cudaEventRecord(ev_start, s));
@@ -1063,7 +1034,8 @@ swin_mlp_status_t swin_mlp_int8_run_host(swin_mlp_int8_t h, const int8_t* x_host
         if (rd) CUDA_TRY(cudaMemcpyAsync(rd + off, residual_host + off, bytes * 4, cudaMemcpyHostToDevice, h->io_in));
         CUDA_TRY(cudaEventRecord(ev_in, h->io_in));
         CUDA_TRY(cudaStreamWaitEvent(s, ev_in, 0));
-        ST_TRY(swin_mlp_int8_run(h, xd + off, rd ? rd + off : nullptr, yd + off, nullptr, n, w, ws, stream));
+        ST_TRY(run_impl(h, xd + off, rd ? rd + off : nullptr, yd + off, nullptr, n, w, ws, stream, nullptr, nullptr,
+                        nullptr, nullptr, false, h->plan_hint > 0 ? h->plan_hint : T));
         CUDA_TRY(cudaEventRecord(ev_out, s));
         CUDA_TRY(cudaStreamWaitEvent(h->io_out, ev_out, 0));
         CUDA_TRY(cudaMemcpyAsync(y_host + off, yd + off, bytes, cudaMemcpyDeviceToHost, h->io_out));
@@ -1142,7 +1114,8 @@ swin_mlp_status_t swin_mlp_int8_run_host_batch(int32_t n, const swin_mlp_int8_t*
         CUDA_TRY(cudaMemcpyAsync(xd + o, x_hosts[l] + o, bytes, cudaMemcpyHostToDevice, h0->io_in));
         CUDA_TRY(cudaEventRecord(ev_in, h0->io_in));
         CUDA_TRY(cudaStreamWaitEvent(s, ev_in, 0));
-        ST_TRY(swin_mlp_int8_run(hs[l], xd + o, nullptr, yd + o, nullptr, rows, w, ws, stream));
+        ST_TRY(run_impl(hs[l], xd + o, nullptr, yd + o, nullptr, rows, w, ws, stream, nullptr, nullptr, nullptr,
+                        nullptr, false, hs[l]->plan_hint > 0 ? hs[l]->plan_hint : Ts[l]));
         CUDA_TRY(cudaEventRecord(ev_out, s));
         CUDA_TRY(cudaStreamWaitEvent(h0->io_out, ev_out, 0));
         CUDA_TRY(cudaMemcpyAsync(y_hosts[l] + o, yd + o, bytes, cudaMemcpyDeviceToHost, h0->io_out));
@@ -1353,7 +1326,6 @@ static swin_mlp_status_t proj_run_impl(swin_proj_int8_t ph, const int8_t* a, con
     a2.resid = residual; a2.resid_out = residual_out;
     a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
     a2.acc_tap = dbg ? acc : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
-    { static const char* e = std::getenv("SWIN_MLP_DBG2"); a2.dbg = e ? atoi(e) : 0; }
     return launch(h->p2, tm_a, h->tm_w2, tm_y, tm_y, a2, s);
 }
 
@@ -1398,7 +1370,8 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10) {
 int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20) {
     if (!h || !out20 || T < 0) return -1;
     swin_mlp_int8_plan(h, out20);
-    const int c = plan_choice(h, T);
+    if (h->fp.on) return 0;   // the one-kernel plan: the same launch for every T
+    const int c = plan_choice(h, h->plan_hint > 0 ? h->plan_hint : T);
     const Plan& P1 = c == 2 ? h->p1s : h->p1;
     const Plan& P2 = c == 2 ? h->p2s : c == 1 ? h->p2b : h->p2;
     out20[0] = P1.BN; out20[1] = P1.CS; out20[2] = P1.stages; out20[3] = P1.max_clusters;
