@@ -760,8 +760,8 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                         z[2 * j4] = f2_add(d0, rr[2 * j4]);
                         z[2 * j4 + 1] = f2_add(d1, rr[2 * j4 + 1]);
                     } else {                     // z = fl(d + fl((x - z_x) * s_x))
-                        z[2 * j4] = f2_add(d0, f2_mul(rr[2 * j4], sx2));       // dQ(x), then Add (R3)
-                        z[2 * j4 + 1] = f2_add(d1, f2_mul(rr[2 * j4 + 1], sx2));
+                        z[2 * j4] = f2_add(d0, f2_mul_nc(rr[2 * j4], sx2));       // dQ(x), then Add (R3)
+                        z[2 * j4 + 1] = f2_add(d1, f2_mul_nc(rr[2 * j4 + 1], sx2));
                     }
                 }
             };

@@ -838,7 +838,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         // z = fl(d + R), or fl(d + fl((x - z_x) * s_x)): dQ(x) then Add (R3)
-                        z[j] = f2_add(z[j], x_res ? f2_mul(rr[j], sx2) : rr[j]);
+                        z[j] = f2_add(z[j], x_res ? f2_mul_nc(rr[j], sx2) : rr[j]);   // (_nc: ptxas would fuse mul+add)
                         if constexpr (STATS64) {
                             s1d = __dadd_rn(s1d, (double)z[j].x);
                             s1d = __dadd_rn(s1d, (double)z[j].y);
