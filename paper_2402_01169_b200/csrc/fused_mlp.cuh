@@ -69,6 +69,7 @@ struct FusedArgs {
     float inv_h; int32_t z_h;
     float inv_y; int32_t z_y;
     float s_x; int32_t z_x; float eps;
+    float one;                                              // 1.0f (host-set), see GemmArgs::one
     const int8_t* x;                                        // [M][C] layer input (op #6 residual dQ(x))
     const float* resid; float* resid_out;                   // [M][C] fp32 or nullptr
     int32_t* acc1_tap; int8_t* hid_tap; int32_t* acc2_tap; float* ln_tap;   // debug taps
@@ -668,6 +669,7 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         };
         const float2 inv2 = make_float2(p.inv_y, p.inv_y);
         const float2 sx2 = make_float2(p.s_x, p.s_x);
+        const float2 one2 = make_float2(p.one, p.one);
         const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
         const float2 xoff2 = make_float2(xoff, xoff);
         auto goff = [&](int c) -> uint32_t {       // this row's granule of column c (multiple of 16)
@@ -760,8 +762,9 @@ fused_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                         z[2 * j4] = f2_add(d0, rr[2 * j4]);
                         z[2 * j4 + 1] = f2_add(d1, rr[2 * j4 + 1]);
                     } else {                     // z = fl(d + fl((x - z_x) * s_x))
-                        z[2 * j4] = f2_add(d0, f2_mul_nc(rr[2 * j4], sx2));       // dQ(x), then Add (R3)
-                        z[2 * j4 + 1] = f2_add(d1, f2_mul_nc(rr[2 * j4 + 1], sx2));
+                        // dQ(x), then Add (R3): fl(fl(r * s_x) * 1 + d), see GemmArgs::one
+                        z[2 * j4] = f2_fma(f2_mul(rr[2 * j4], sx2), one2, d0);
+                        z[2 * j4 + 1] = f2_fma(f2_mul(rr[2 * j4 + 1], sx2), one2, d1);
                     }
                 }
             };

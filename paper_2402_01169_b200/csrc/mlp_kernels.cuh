@@ -98,6 +98,8 @@ struct GemmArgs {
     const float* gamma;
     const float* beta;
     float eps;
+    float one;             // 1.0f (host-set): z = fma(dQ(x), one, d) keeps ptxas from fusing the
+                           // dQ product into the Add (it contracts mul.rn.f32x2 + add.rn.f32x2)
     // debug taps
     int32_t* acc_tap;      // [M][ldo] int32 accumulators (incl. zero-point term)
     float* ln_tap;         // [M][ldo] fp32 yhat (EP6)
@@ -790,6 +792,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 if (x_smem) mbar_wait(bar_xfull + 8u * xbuf_of(it), xph_of(it));   // residual x tile landed
                 if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 6] = gtimer();
                 const float2 sx2 = make_float2(p.s_x, p.s_x);
+                const float2 one2 = make_float2(p.one, p.one);
                 const float xoff = 8388608.0f + 128.0f + (float)p.z_x;   // exact: |z_x| <= 128
                 const float2 xoff2 = make_float2(xoff, xoff);
                 // pass 1: z = fl(fl(fmaf(fl(A2), m2, b2)) + r); park z in TMEM; row statistics:
@@ -838,7 +841,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         // z = fl(d + R), or fl(d + fl((x - z_x) * s_x)): dQ(x) then Add (R3)
-                        z[j] = f2_add(z[j], x_res ? f2_mul_nc(rr[j], sx2) : rr[j]);   // (_nc: ptxas would fuse mul+add)
+                        z[j] = x_res ? f2_fma(f2_mul(rr[j], sx2), one2, z[j]) : f2_add(z[j], rr[j]);   // (see GemmArgs::one)
                         if constexpr (STATS64) {
                             s1d = __dadd_rn(s1d, (double)z[j].x);
                             s1d = __dadd_rn(s1d, (double)z[j].y);

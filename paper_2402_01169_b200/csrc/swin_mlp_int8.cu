@@ -839,7 +839,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         a.m2 = h->m2; a.b2 = h->b2; a.zc2 = h->zc2;
         a.gamma = h->gamma; a.beta = h->beta;
         a.inv_h = h->inv_h; a.z_h = h->d.h_zero_point; a.inv_y = h->inv_y; a.z_y = h->d.y_zero_point;
-        a.s_x = h->d.x_scale; a.z_x = h->d.x_zero_point; a.eps = h->d.ln_eps;
+        a.s_x = h->d.x_scale; a.z_x = h->d.x_zero_point; a.eps = h->d.ln_eps; a.one = 1.0f;
         a.x = x; a.resid = residual; a.resid_out = residual_out;
         a.rotate = 1;
         if (dbg) { a.acc1_tap = acc1; a.hid_tap = hidden; a.acc2_tap = acc2; a.ln_tap = ln_out; }
@@ -921,7 +921,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a2.resb = P2.resb; a2.mt_major = P2.pair ? 0 : 1;   // op #6: one n-group per cluster
     a2.n_groups = 1; a2.num_units = P2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
-    a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point;
+    a2.s_x = h->d.x_scale; a2.z_x = h->d.x_zero_point; a2.one = 1.0f;
     a2.resid = residual; a2.resid_out = residual_out;
     a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
     a2.acc_tap = dbg ? acc2 : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
@@ -1322,7 +1322,7 @@ static swin_mlp_status_t proj_run_impl(swin_proj_int8_t ph, const int8_t* a, con
     a2.resb = h->p2.resb; a2.mt_major = h->p2.pair ? 0 : 1;
     a2.n_groups = 1; a2.num_units = h->p2.pair ? (m_tiles + 1) / 2 : m_tiles; a2.ldo = C;
     a2.m = h->m2; a2.b = h->b2; a2.zc = h->zc2; a2.inv_q = h->inv_y; a2.zq = h->d.y_zero_point;
-    a2.s_x = 1.0f; a2.z_x = 0;
+    a2.s_x = 1.0f; a2.z_x = 0; a2.one = 1.0f;
     a2.resid = residual; a2.resid_out = residual_out;
     a2.gamma = h->gamma; a2.beta = h->beta; a2.eps = h->d.ln_eps;
     a2.acc_tap = dbg ? acc : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
