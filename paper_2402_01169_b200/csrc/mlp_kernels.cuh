@@ -119,6 +119,18 @@ struct GemmArgs {
     int32_t wsl;                      // weight-stationary slice (op #5): each cluster owns ONE
                                       // column group, keeps that B slice resident in smem (its half
                                       // for a pair) and streams only A tiles through the ring
+    // op #6 split-K (runs of few m-tiles): the units are (m-tile, split) pairs, one per cluster;
+    // split s accumulates k-blocks [s kb_per, (s+1) kb_per).  Splits 1..S-1 add their int32
+    // partial tiles into kacc with bulk reduce-add and count in; split 0 (the reducer) waits for
+    // the S-1 arrivals, adds kacc to its own accumulator and runs op #6.  Integer sums are exact
+    // in any order, so A2 -- and Y -- are bit-identical to the unsplit plan.
+    int32_t ksplit;                   // S (<= 1: no split)
+    int32_t kb_per;                   // k-blocks per split
+    int32_t* kacc;                    // [M][ldo] int32 (zeroed by the preceding FC1 launch)
+    int32_t* kcnt;                    // [m_tiles][CS] arrival counters (zeroed with kacc)
+    // FC1: words of `zero_ptr` to clear (after griddepcontrol.wait) for the next launch's split-K
+    int32_t* zero_ptr;
+    int64_t zero_words;               // multiple of 4, zero_ptr 16-byte aligned
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -333,6 +345,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t CL = PAIR ? 2u : CS;                   // CTAs per cluster
     const uint32_t cid = blockIdx.x / CL, nclus = gridDim.x / CL;
     const uint32_t num_units = (uint32_t)p.num_units, n_groups = (uint32_t)p.n_groups;
+    const uint32_t KS = (IS_LN && p.ksplit > 1) ? (uint32_t)p.ksplit : 1u;   // split-K (op #6 only)
     const uint32_t m_tiles = num_units / n_groups;
     const int num_kb = (p.K + kBK - 1) / kBK;
     const uint32_t a_bytes = kBM * kBK, b_bytes = (uint32_t)bn_b * kBK;
@@ -361,10 +374,16 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             m_tile = cid + (it / n_groups) * nclus;
             ng = it % n_groups;
         } else {
-            const uint32_t u = cid + it * nclus;
+            const uint32_t u = KS > 1u ? (cid + it * nclus) / KS : cid + it * nclus;
             m_tile = PAIR ? 2u * (u / n_groups) + rank : u / n_groups;   // pair: units are m-tile pairs
             ng = u % n_groups;
         }
+    };
+    // split-K: this unit's split and k-block range (split 0 reduces)
+    auto split_of = [&](uint32_t it) -> uint32_t { return KS > 1u ? (cid + it * nclus) % KS : 0u; };
+    auto kb_range = [&](uint32_t it, int& kb0, int& kb1) {
+        kb0 = KS > 1u ? (int)split_of(it) * p.kb_per : 0;
+        kb1 = KS > 1u ? min(num_kb, kb0 + p.kb_per) : num_kb;
     };
     auto n0_of = [&](uint32_t ng) -> int { return (int)((PAIR ? ng : ng * CS + rank) * (uint32_t)BN); };
     // op #6 x tile buffer of tile `it` and its phase (xstage buffers: 1 or G, powers of two)
@@ -453,7 +472,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 uint32_t m_tile, ng;
                 tile_at(it, m_tile, ng);
                 const int n0 = n0_of(ng), row0 = (int)(m_tile * kBM);
-                for (int kb = 0; kb < num_kb; ++kb) {
+                int kbA, kbB;
+                kb_range(it, kbA, kbB);
+                for (int kb = kbA; kb < kbB; ++kb) {
                     mbar_wait(bar_empty + 8u * s, ph ^ 1u);
                     if constexpr (PAIR) {
                         // both CTAs load their halves; the bytes complete on the leader's barrier
@@ -503,7 +524,9 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             tc_fence_after();
             if (trc && lane == 0 && it < 256) trc[1024 + 4 * it] = gtimer();
             const uint32_t d = tmem_base + buf * (uint32_t)BN;
-            for (int kb = 0; kb < num_kb; ++kb) {
+            int kbA, kbB;
+            kb_range(it, kbA, kbB);
+            for (int kb = kbA; kb < kbB; ++kb) {
                 if (first) mbar_wait(bar_full + 8u * ss, pp);
                 tc_fence_after();
                 if (trc && lane == 0 && it < 4 && kb < 16) trc[2048 + 16 * (44 + it) + kb] = gtimer();
@@ -518,11 +541,11 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if constexpr (PAIR) {
                         for (uint32_t h = 0; h < nh2; ++h)
                             for (int k = 0; k < nk; ++k)
-                                mma_i8_pair(d + h * nmma, ad + 2u * k, bd + h * hoff16 + 2u * k, idesc, (kb | k) != 0);
+                                mma_i8_pair(d + h * nmma, ad + 2u * k, bd + h * hoff16 + 2u * k, idesc, (kb != kbA) | (k != 0));
                         mma_commit_pair_mc(bar_empty + 8u * ss, 3);   // both CTAs' slots free
                     } else {
                         for (int k = 0; k < nk; ++k)
-                            mma_i8(d, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                            mma_i8(d, ad + 2u * k, bd + 2u * k, idesc, (kb != kbA) | (k != 0));
                         if (last) {
                             if (CS == 1) mma_commit(bar_empty + 8u * ss);
                             else mma_commit_mc(bar_empty + 8u * ss, cmask);
@@ -564,6 +587,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // ============================ output store warp =========================
         pdl_wait();   // outputs may overwrite what the previous kernel still reads
         for (uint32_t it = 0; it < (dst ? 0u : my_tiles); ++it) {
+            if (split_of(it) != 0u) continue;   // split-K partial: nothing to store
             const uint32_t sb = it & (G - 1u), sph = (it >> lgG) & 1u;
             mbar_wait(bar_sfull + 8u * sb, sph);
             if (trc && lane == 0 && it < 64) trc[2048 + 16 * it + 8] = gtimer();
@@ -592,9 +616,19 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // Per tile: (op #6) TMA the residual x[rows][cols] tile into xres[buf] as soon
         // as the previous user of that buffer finished pass 1 (xfree), then copy the
         // per-column constants once the buffer's previous tile is fully drained (tempty).
+        if (p.zero_ptr) {
+            // clear the next launch's split-K partial sums and counters (after the previous
+            // grid -- whose op #6 may still read them -- has completed)
+            pdl_wait();
+            int4* zp = reinterpret_cast<int4*>(p.zero_ptr);
+            const int64_t n4 = p.zero_words >> 2;
+            for (int64_t i = (int64_t)blockIdx.x * 32 + lane; i < n4; i += (int64_t)gridDim.x * 32)
+                zp[i] = make_int4(0, 0, 0, 0);
+        }
         const bool load_x = IS_LN && (p.resid == nullptr) && p.xstage;
         if (load_x) pdl_wait();
         for (uint32_t it = 0; it < my_tiles; ++it) {
+            if (split_of(it) != 0u) continue;   // split-K partial: no constants / residual needed
             uint32_t m_tile, ng;
             tile_at(it, m_tile, ng);
             const int n0 = n0_of(ng);
@@ -669,6 +703,37 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             tile_at(it, m_tile, ng);
             const int n0 = n0_of(ng);
             const uint32_t buf = it & (G - 1u), aph = (it >> lgG) & 1u;
+            if (IS_LN && KS > 1u && split_of(it) != 0u) {
+                // ---- split-K partial: TMEM -> smem (row-major int32, in the operand ring,
+                // free once every MMA of this cluster's only unit has completed) -> bulk
+                // reduce-add into kacc; then count in for the reducer
+                mbar_wait(bar_tfull + 8u * buf, aph);
+                tc_fence_after();
+                const int64_t prow = (int64_t)m_tile * kBM + rit;
+                const uint32_t tbp = tmem_base + ((quad * 32u) << 16) + buf * (uint32_t)BN;
+                const uint32_t stg = base + L.a + rit * (uint32_t)BN * 4u;
+                for (int ch = ch_lo; ch < ch_hi; ++ch) {
+                    uint32_t r[16];
+                    tmem_ld16(tbp + (uint32_t)(ch * kChunk), r);
+                    tmem_wait_ld_dep(r);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        st_shared_v4(stg + (uint32_t)ch * 64u + 16u * q, r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                }
+                fence_proxy_async_smem();
+                if (prow < p.M && ch_hi > ch_lo) {
+                    bulk_reduce_add_s32(p.kacc + prow * (int64_t)p.ldo + n0 + ch_lo * kChunk,
+                                        stg + (uint32_t)ch_lo * 64u, (uint32_t)(ch_hi - ch_lo) * 64u);
+                    bulk_commit();
+                    bulk_wait_all();
+                    fence_proxy_async_global();
+                }
+                __threadfence();
+                tc_fence_before();
+                named_bar_sync(1u + buf, 32u * tile_warps);
+                if (grp_leader) red_release_gpu_add(p.kcnt + m_tile * CS + rank, 1);
+                continue;
+            }
             const uint32_t sbuf = base + L.out + buf * tile_bytes;
             if (!dst) mbar_wait(bar_sfree + 8u * buf, aph ^ 1u);   // staging tile read by its last stores
             mbar_wait(bar_cfull + 8u * buf, aph);
@@ -790,6 +855,13 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const bool x_smem = x_res && p.xstage;
                 const uint32_t xtile = base + L.xres + xbuf_of(it) * tile_bytes;
                 if (x_smem) mbar_wait(bar_xfull + 8u * xbuf_of(it), xph_of(it));   // residual x tile landed
+                if (KS > 1u) {   // split-K reducer: the S-1 partial tiles of these columns are in kacc
+                    const int32_t* cnt = p.kcnt + m_tile * CS + rank;
+                    if (lane == 0)
+                        while (ld_acquire_gpu(cnt) < (int32_t)KS - 1) __nanosleep(64);
+                    __syncwarp();
+                    (void)ld_acquire_gpu(cnt);
+                }
                 if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 6] = gtimer();
                 const float2 sx2 = make_float2(p.s_x, p.s_x);
                 const float2 one2 = make_float2(p.one, p.one);
@@ -833,6 +905,15 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                                            __uint_as_float(__byte_perm(ob, 0x4B000000u, 0x7653)));
                             rr[2 * q] = f2_sub(f01, xoff2);      // x - z_x, exact
                             rr[2 * q + 1] = f2_sub(f23, xoff2);
+                        }
+                    }
+                    if (KS > 1u && valid) {   // + the other splits' partial sums (exact int32)
+                        const int4* kp = reinterpret_cast<const int4*>(p.kacc + row * (int64_t)C + n0 + cl);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int4 v = __ldcg(kp + q);
+                            r[4 * q] += (uint32_t)v.x; r[4 * q + 1] += (uint32_t)v.y;
+                            r[4 * q + 2] += (uint32_t)v.z; r[4 * q + 3] += (uint32_t)v.w;
                         }
                     }
                     float2 z[8];

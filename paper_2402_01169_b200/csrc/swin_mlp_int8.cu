@@ -796,11 +796,39 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     return SWIN_MLP_OK;
 }
 
+// op #6 split-K region of the workspace: int32 partial sums [rows][C] + counters [m_tiles][CS],
+// for runs of at most kSplitRowsCap rows (the split is only taken when the unsplit op #6 grid would
+// fill at most half the SMs: m_tiles * CS <= num_sms / 2, so m_tiles <= num_sms / 2)
+static int64_t split_rows_cap(const swin_mlp_int8_s* h) { return (int64_t)(h->num_sms / 2) * kBM; }
+static size_t split_region_bytes(const swin_mlp_int8_s* h, int64_t T) {
+    const int64_t rows = std::min<int64_t>(T, split_rows_cap(h));
+    const int64_t words = (rows * h->d.C + 3) / 4 * 4 + ((rows + kBM - 1) / kBM * 8 + 3) / 4 * 4;
+    return (size_t)((words * 4 + 127) / 128 * 128);
+}
+
+// Split-K factor of op #6 for a run of T tokens on plan P2 (1 = none): only when the unsplit grid
+// fills at most half the SMs, with every (m-tile, split) unit on its own co-resident cluster (the
+// reducer waits for its partners) and the int32 partial tile fitting the operand ring.
+static int ksplit_for(const swin_mlp_int8_s* h, const Plan& P2, int64_t T, int& kb_per) {
+    kb_per = 0;
+    if (h->unfused || P2.pair || P2.resb) return 1;
+    const int64_t m_tiles = (T + kBM - 1) / kBM;
+    if (m_tiles * P2.CS * 2 > h->num_sms || m_tiles > h->num_sms / 2) return 1;
+    const int num_kb = (h->d.H + kBK - 1) / kBK;
+    int64_t S = std::min<int64_t>(num_kb, P2.max_clusters / std::max<int64_t>(m_tiles, 1));
+    if (S < 2) return 1;
+    kb_per = (int)((num_kb + S - 1) / S);
+    S = (num_kb + kb_per - 1) / kb_per;
+    if ((uint64_t)P2.stages * ((uint64_t)kBM * kBK + (uint64_t)P2.BN * kBK) < (uint64_t)kBM * P2.BN * 4u) return 1;
+    return (int)S;
+}
+
 size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T) {
     if (!h || T <= 0) return 0;
     if (h->fp.on) return 0;   // one kernel: the hidden tile never leaves the SM
     const size_t hq = (size_t)(((T * h->d.H) + 127) / 128 * 128);
-    return h->unfused ? hq + (size_t)T * h->d.H * 4 : hq;   // unfused plan: + A1 int32 [T][H]
+    if (h->unfused) return hq + (size_t)T * h->d.H * 4;   // unfused plan: + A1 int32 [T][H]
+    return hq + split_region_bytes(h, T);                  // + op #6 split-K partials (small T)
 }
 
 // plan_T: the token count the launch plans are chosen for (the run's own T, the handle's plan
@@ -927,6 +955,19 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     a2.acc_tap = dbg ? acc2 : nullptr; a2.ln_tap = dbg ? ln_out : nullptr;
     a2.trace = h->trace ? h->trace + 4096 : nullptr; a2.trace_cta = h->trace_cta;
     a2.cta_stamps = h->trace ? h->trace + 8192 + 512 : nullptr;
+    // op #6 split-K for runs of few m-tiles: partial sums + counters after Hq in the workspace,
+    // cleared by this run's FC1 launch
+    int kb_per = 0;
+    const int ks = ksplit_for(h, P2, T, kb_per);
+    if (ks > 1) {
+        int32_t* kacc = reinterpret_cast<int32_t*>(hq + ((T * H + 127) / 128 * 128));
+        const int64_t acc_words = (T * C + 3) / 4 * 4;
+        a2.ksplit = ks; a2.kb_per = kb_per; a2.kacc = kacc; a2.kcnt = kacc + acc_words;
+        a2.mt_major = 0;
+        a2.num_units = m_tiles * ks;
+        a1.zero_ptr = kacc;
+        a1.zero_words = acc_words + (m_tiles * P2.CS + 3) / 4 * 4;
+    }
 
     cudaEvent_t* ev = nullptr;
     if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
