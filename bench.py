@@ -166,8 +166,17 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def refuse_plan_switches():
+    """The library reads SWIN_MLP_* A/B switches (plan variants, PDL off, sync checks) at create
+    time; a bench number taken under any of them is not the product's, so refuse to run."""
+    bad = sorted(k for k in os.environ if k.startswith("SWIN_MLP_"))
+    if bad:
+        raise SystemExit(f"bench.py: refusing to run with plan/debug switches set: {', '.join(bad)}")
+
+
 def main():
     args = parse()
+    refuse_plan_switches()
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)
@@ -400,6 +409,14 @@ def main():
     proj = None
     if rank == 0 and not args.no_stack:
         proj = proj_rows(max(3, min(args.steps, 20)))
+    # ---- BASELINE configs[2] / configs[3] as the target states them: a FIXED global batch sharded by
+    # whole images over the N ranks (strong scaling; per-GPU T shrinks as N grows), weights broadcast
+    # once over NCCL, no collective inside the timed region, max over ranks ------------------------
+    sharded = None
+    if not args.no_stack:
+        sharded = [sharded_stack(cfg, ws, rank, dev, max(3, min(args.steps, 10)), barrier, max_over_ranks)
+                   for cfg in (3, 4)]
+        torch.cuda.empty_cache()
     # ---- BASELINE configs[0]: one 7x7 window of the Swin-T stage-4 MLP (T = 49), latency ------------
     cfg1 = None
     if rank == 0 and not args.no_stack:
@@ -427,6 +444,7 @@ def main():
                 "gpu_launches": sum(n * P.swin_mlp_int8_launches_per_run(l.handle) for (_, _, n), l in zip(prof, relu_layers)),
                 "relu_vs_gelu": relu_gelu,
                 "north_star_stack": stack,
+                "sharded_fixed_batch": sharded,
                 "proj_op4": proj,
                 "config0_window": cfg1,
                 "tensor_frac_of_step": roofline["step_frac"],
@@ -435,6 +453,82 @@ def main():
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def sharded_stack(config, ws, rank, dev, steps, barrier, max_over_ranks):
+    """BASELINE configs[2] (synth config 3: Swin-S MLP stack, batch 256) and configs[3] (config 4:
+    Swin-B, batch 1024) with the global batch FIXED and split by whole images over the ws ranks
+    (paper_2402_01169_b200.dist.shard_range): rank r runs every layer of the stack on its images'
+    tokens.  Weights: rank 0's, broadcast once over NCCL before timing (the only collective; a
+    checksum all-gathered afterwards proves every rank holds the same bytes).  Timed: `steps` stack
+    passes, L2 flushed before each, CUDA events on the launching stream, job time = max over ranks;
+    tokens/s counts the whole batch's layer-tokens.  "scaling": "strong"."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import synth
+    from paper_2402_01169_b200 import SwinMlpInt8Layer, swin_mlp_int8_workspace_bytes
+    from paper_2402_01169_b200.dist import broadcast_layer, shard_range
+    full_batch = {3: 256, 4: 1024}[config]
+    lo, hi = shard_range(full_batch, rank, ws)
+    stages_full = synth.config_layers(config)
+    stages = synth.config_layers(config, batch=hi - lo)
+    layers, bufs, wsb, csum = [], [], 128, 0
+    for s_i, (C, T, n) in enumerate(stages):
+        L0 = synth.make_layer(C, synth.layer_seed(config, s_i, 0))
+        a = torch.from_numpy(synth.make_activations(L0, T, synth.layer_seed(config, s_i, 0) + 50 + 7919 * rank)).to(dev)
+        bufs.append((a, torch.empty_like(a)))
+        for l_i in range(n):
+            L = synth.make_layer(C, synth.layer_seed(config, s_i, l_i))
+            if ws > 1:
+                broadcast_layer(L, dev)
+                csum += int(L.w1.to(torch.int64).sum().item()) * 3 + int(L.w2.to(torch.int64).sum().item())
+            h = SwinMlpInt8Layer(L, device=dev.index)
+            layers.append((h, s_i, l_i, T))
+            wsb = max(wsb, swin_mlp_int8_workspace_bytes(h.handle, T))
+    work = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for h, s_i, l_i, T in layers:
+            a, b = bufs[s_i]
+            x, y = (a, b) if l_i % 2 == 0 else (b, a)
+            h(x, y=y, workspace=work)
+
+    for _ in range(3):
+        step()
+    barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        flush.fill_(k & 0xff)
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs))
+    checks_equal = True
+    if ws > 1:
+        allc = [None] * ws
+        dist.all_gather_object(allc, csum)
+        checks_equal = len(set(allc)) == 1
+    tokens = sum(T * n for (C, T, n) in stages_full)
+    ops = sum(16.0 * C * C * T * n for (C, T, n) in stages_full)
+    peak = 2.0 * load_peaks()["bf16_burst"]
+    t = ms / steps / 1e3
+    out = {"config": f"BASELINE configs[{config - 1}]", "workload": {3: "Swin-S MLP stack (24 layers)",
+                                                                     4: "Swin-B MLP stack (24 layers)"}[config],
+           "global_batch": full_batch, "images_per_gpu": hi - lo, "n_gpus": ws, "scaling": "strong",
+           "per_gpu_T": [T for (_, T, _) in stages], "C": [C for (C, _, _) in stages],
+           "ms_per_step": ms / steps, "tokens_per_s": tokens / t, "layer_tokens_per_step": tokens,
+           "tensor_frac_per_gpu": ops / t / 1e12 / ws / peak,
+           "weights": "rank 0's, broadcast once over NCCL before timing" if ws > 1 else "local (1 GPU)",
+           "weights_checksum_equal_across_ranks": checks_equal,
+           "hot_path_collectives": 0, "l2": "flushed between steps",
+           "plans": [h.plan(T)["run_plan"] if not h.plan()["fused"] else "fused" for h, _, l_i, T in layers if l_i == 0]}
+    del layers
+    return out
 
 
 def window_latency(steps):

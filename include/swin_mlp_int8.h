@@ -209,7 +209,9 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
  * chooses per run: the few-tile plans for one or two m-tiles, the CTA-pair op #6 for at
  * most one wave of pairs, else the defaults).  Same 20-entry layout as
  * swin_mlp_int8_plan with entries 0-11 and 16 describing the chosen plans, and entry 19 =
- * op5_unfused | (choice << 1), choice 0 = default, 1 = CTA-pair op #6, 2 = few-tile.
+ * op5_unfused | (choice << 1), choice 0 = default, 1 = CTA-pair op #6, 2 = few-tile, and
+ * entry 13 = the op #6 split-K factor S of this run (1 = none; S > 1 splits FC2's K = H
+ * over S clusters per m-tile when the unsplit grid would fill at most half the SMs).
  * The plan hint (swin_mlp_int8_set_plan_hint), when set, replaces T.  For a one-kernel
  * handle (entry 12 = 1) the result equals swin_mlp_int8_plan: one launch serves every T.
  * Host-only, no launch.  Returns 0, or -1 on a NULL argument or T < 0. */

@@ -142,7 +142,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct SmemLayout {
     uint32_t a, b, bres, out, xres, consts, bars, tmem_slot, red, xbuf, total;
 };
-__host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages + 7u * kGMax + 2u * kGMax + 1u + kGMax; }
+__host__ __device__ constexpr uint32_t kNumBars(int stages) { return 2u * stages + 7u * kGMax + 2u * kGMax + 1u + kGMax + 1u; }
+// split-K: row stride (bytes) of an int32 partial tile staged in the operand ring (16 B of padding
+// per row: consecutive rows start in different 16-B bank groups)
+__host__ __device__ constexpr uint32_t ksplit_row_bytes(int BN) { return (uint32_t)BN * 4u + 16u; }
 
 // ebytes: size of one exchanged row statistic (4: fp32 LN, 8: fp64 LN);
 // xstage: op #6 stages the residual x tiles in smem (else pass 1 reads x from global)
@@ -294,6 +297,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t bar_xst = bar_xfree + 8u * kGMax;      // [G][pass] op #6 DSMEM row stats (1 + tx)
     const uint32_t bar_bfull = bar_xst + 16u * kGMax;     // resident B landed (count 1 + tx)
     const uint32_t bar_ptempty = bar_bfull + 8u;          // [G] pair: accumulator drained in both CTAs
+    const uint32_t bar_kfull = bar_ptempty + 8u * kGMax;  // split-K reducer: partial sums staged (1 + tx)
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(gbase + L.tmem_slot);
     float* consts = reinterpret_cast<float*>(gbase + L.consts);
     acc_t* red = reinterpret_cast<acc_t*>(gbase + L.red);
@@ -328,6 +332,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
         mbar_init(bar_bfull, 1);
         for (uint32_t i = 0; i < (uint32_t)kGMax; ++i) mbar_init(bar_ptempty + 8u * i, 2u * tile_warps);
+        mbar_init(bar_kfull, 1);
         fence_mbar_init();
     }
     if (warp == 2) {
@@ -670,6 +675,25 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
             if (trc && lane == 0 && it < 512) trc[3072 + 2 * it + 1] = gtimer();
             mbar_arrive(bar_cfull + 8u * buf);
+            if (IS_LN && KS > 1u) {
+                // split-K reducer: once the S-1 partners have counted in and this CTA's own MMAs
+                // have completed (the operand ring is free: one unit per cluster), bulk-copy the
+                // summed partial rows kacc[rows][n0, n0 + BN) into the ring, one row per copy
+                const int32_t* cnt = p.kcnt + m_tile * CS + rank;
+                if (lane == 0)
+                    while (ld_acquire_gpu(cnt) < (int32_t)KS - 1) __nanosleep(32);
+                __syncwarp();
+                (void)ld_acquire_gpu(cnt);
+                fence_proxy_async_global();   // (the copies below read through the async proxy)
+                mbar_wait(bar_tfull + 8u * buf, aph);
+                const int64_t r0 = (int64_t)m_tile * kBM;
+                const uint32_t nrows = (uint32_t)min((int64_t)kBM, p.M - r0);
+                if (lane == 0) mbar_arrive_expect_tx(bar_kfull, nrows * (uint32_t)BN * 4u);
+                __syncwarp();
+                for (uint32_t r = lane; r < nrows; r += 32u)
+                    bulk_load_g2s(base + L.a + r * ksplit_row_bytes(BN), p.kacc + (r0 + r) * (int64_t)p.ldo + n0,
+                                  (uint32_t)BN * 4u, bar_kfull);
+            }
         }
     } else {
         // ============================ epilogue ================================
@@ -711,7 +735,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 tc_fence_after();
                 const int64_t prow = (int64_t)m_tile * kBM + rit;
                 const uint32_t tbp = tmem_base + ((quad * 32u) << 16) + buf * (uint32_t)BN;
-                const uint32_t stg = base + L.a + rit * (uint32_t)BN * 4u;
+                const uint32_t stg = base + L.a + rit * ksplit_row_bytes(BN);
                 for (int ch = ch_lo; ch < ch_hi; ++ch) {
                     uint32_t r[16];
                     tmem_ld16(tbp + (uint32_t)(ch * kChunk), r);
@@ -855,13 +879,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const bool x_smem = x_res && p.xstage;
                 const uint32_t xtile = base + L.xres + xbuf_of(it) * tile_bytes;
                 if (x_smem) mbar_wait(bar_xfull + 8u * xbuf_of(it), xph_of(it));   // residual x tile landed
-                if (KS > 1u) {   // split-K reducer: the S-1 partial tiles of these columns are in kacc
-                    const int32_t* cnt = p.kcnt + m_tile * CS + rank;
-                    if (lane == 0)
-                        while (ld_acquire_gpu(cnt) < (int32_t)KS - 1) __nanosleep(64);
-                    __syncwarp();
-                    (void)ld_acquire_gpu(cnt);
-                }
+                if (KS > 1u) mbar_wait(bar_kfull, 0);   // split-K reducer: the partners' sums staged in smem
                 if (trc && grp_leader && it < 64) trc[2048 + 16 * it + 6] = gtimer();
                 const float2 sx2 = make_float2(p.s_x, p.s_x);
                 const float2 one2 = make_float2(p.one, p.one);
@@ -908,12 +926,12 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         }
                     }
                     if (KS > 1u && valid) {   // + the other splits' partial sums (exact int32)
-                        const int4* kp = reinterpret_cast<const int4*>(p.kacc + row * (int64_t)C + n0 + cl);
+                        const uint32_t kp = base + L.a + rit * ksplit_row_bytes(BN) + (uint32_t)cl * 4u;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const int4 v = __ldcg(kp + q);
-                            r[4 * q] += (uint32_t)v.x; r[4 * q + 1] += (uint32_t)v.y;
-                            r[4 * q + 2] += (uint32_t)v.z; r[4 * q + 3] += (uint32_t)v.w;
+                            uint32_t v[4];
+                            ld_shared_v4(kp + 16u * q, v);
+                            r[4 * q] += v[0]; r[4 * q + 1] += v[1]; r[4 * q + 2] += v[2]; r[4 * q + 3] += v[3];
                         }
                     }
                     float2 z[8];

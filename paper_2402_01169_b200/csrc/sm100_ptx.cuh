@@ -339,6 +339,11 @@ __device__ __forceinline__ void bulk_reduce_add_s32(int32_t* gdst, uint32_t src,
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.s32 [%0], [%1], %2;"
                  ::"l"(gdst), "r"(src), "r"(bytes) : "memory");
 }
+// Bulk (non-tensor) copy of `bytes` (multiple of 16) global -> this CTA's smem, completing on `bar`.
+__device__ __forceinline__ void bulk_load_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
 // Order this thread's completed async-proxy global writes before its later generic accesses.
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void red_release_gpu_add(int32_t* p, int32_t v) {

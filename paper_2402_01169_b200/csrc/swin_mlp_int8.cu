@@ -523,6 +523,8 @@ struct swin_mlp_int8_s {
     // plan hint (swin_mlp_int8_set_plan_hint): > 0 = runs choose their launch plans as a run of
     // plan_hint tokens would, so shards / chunks of one batch run the batch's plan
     int64_t plan_hint = 0;
+    // op #6 split-K for runs of few m-tiles (SWIN_MLP_KSPLIT=0 disables; A/B switch read per create)
+    bool ksplit_on = true;
     ~swin_mlp_int8_s() {
         for (void* p : allocs) cudaFree(p);
         for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
@@ -758,6 +760,10 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
         }
     }
     {
+        const char* ke = std::getenv("SWIN_MLP_KSPLIT");      // (read per create)
+        h->ksplit_on = !(ke && *ke == '0');
+    }
+    {
         const char* se = std::getenv("SWIN_MLP_SMALL");       // (read per create)
         const int sbn = 64;   // (BN = 32 / 128 measured no better at the layer level)
         if (!h->unfused && !(se && *se == '0') && sbn >= 16 && sbn % 16 == 0 &&
@@ -797,9 +803,8 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
 }
 
 // op #6 split-K region of the workspace: int32 partial sums [rows][C] + counters [m_tiles][CS],
-// for runs of at most kSplitRowsCap rows (the split is only taken when the unsplit op #6 grid would
-// fill at most half the SMs: m_tiles * CS <= num_sms / 2, so m_tiles <= num_sms / 2)
-static int64_t split_rows_cap(const swin_mlp_int8_s* h) { return (int64_t)(h->num_sms / 2) * kBM; }
+// for runs of at most two m-tiles (the only runs ksplit_for splits)
+static int64_t split_rows_cap(const swin_mlp_int8_s*) { return 2 * (int64_t)kBM; }
 static size_t split_region_bytes(const swin_mlp_int8_s* h, int64_t T) {
     const int64_t rows = std::min<int64_t>(T, split_rows_cap(h));
     const int64_t words = (rows * h->d.C + 3) / 4 * 4 + ((rows + kBM - 1) / kBM * 8 + 3) / 4 * 4;
@@ -811,15 +816,18 @@ static size_t split_region_bytes(const swin_mlp_int8_s* h, int64_t T) {
 // reducer waits for its partners) and the int32 partial tile fitting the operand ring.
 static int ksplit_for(const swin_mlp_int8_s* h, const Plan& P2, int64_t T, int& kb_per) {
     kb_per = 0;
-    if (h->unfused || P2.pair || P2.resb) return 1;
+    if (!h->ksplit_on || h->unfused || P2.pair || P2.resb) return 1;
     const int64_t m_tiles = (T + kBM - 1) / kBM;
-    if (m_tiles * P2.CS * 2 > h->num_sms || m_tiles > h->num_sms / 2) return 1;
+    // (measured: a win for one m-tile -- C = 768 / 1024 / 1536 at T = 49: 31.6 -> 29.7, 37.9 -> 31.7,
+    // 48.2 -> 35.9 us per layer -- a loss from 13 m-tiles on: C = 768, T = 1568 36 -> 42 us, the
+    // partials' global reduce-add and the reducer's wait outweigh the shorter K loops)
+    if (m_tiles > 2 || m_tiles * P2.CS * 2 > h->num_sms) return 1;
     const int num_kb = (h->d.H + kBK - 1) / kBK;
     int64_t S = std::min<int64_t>(num_kb, P2.max_clusters / std::max<int64_t>(m_tiles, 1));
     if (S < 2) return 1;
     kb_per = (int)((num_kb + S - 1) / S);
     S = (num_kb + kb_per - 1) / kb_per;
-    if ((uint64_t)P2.stages * ((uint64_t)kBM * kBK + (uint64_t)P2.BN * kBK) < (uint64_t)kBM * P2.BN * 4u) return 1;
+    if ((uint64_t)P2.stages * ((uint64_t)kBM * kBK + (uint64_t)P2.BN * kBK) < (uint64_t)kBM * ksplit_row_bytes(P2.BN)) return 1;
     return (int)S;
 }
 
@@ -1420,6 +1428,8 @@ int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20) {
     out20[8] = P1.G; out20[9] = P2.G;
     out20[10] = P1.resb ? 1 : P1.wsl ? 2 : 0; out20[11] = P2.resb; out20[16] = P1.pair;
     out20[19] = (h->unfused ? 1 : 0) | (c << 1);
+    int kb_per = 0;   // op #6 split-K factor of this run (two-kernel handles only; 1 = none)
+    out20[13] = ksplit_for(h, P2, T, kb_per);
     return 0;
 }
 

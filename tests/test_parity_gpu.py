@@ -521,7 +521,8 @@ def test_plan_for_reports_the_run_plan(dev):
     assert small["run_plan"] == "few_tile" and small["fc1_bn"] == 64 and small["fc1_pair"] == 0
     assert small["fc2_cs"] == 8 and small["fc2_bn"] == 96
     assert big["run_plan"] == "default"
-    assert {k: v for k, v in big.items() if k != "run_plan"} == layer.plan()
+    assert big["fc2_ksplit"] == 1 and small["fc2_ksplit"] > 1   # split-K: one m-tile only
+    assert {k: v for k, v in big.items() if k not in ("run_plan", "fc2_ksplit")} == layer.plan()
 
 
 # ---- round-to-nearest-even ties forced through the GPU (reading R2) --------------------------
