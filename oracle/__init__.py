@@ -51,6 +51,21 @@ def lib():
         L.oracle_q.restype = None
         L.oracle_dq.argtypes = [P, i64, f32, i32, P]
         L.oracle_dq.restype = None
+        # attention half (oracle_attn.c)
+        L.oracle_window_src_row.argtypes = [i64, i32, i32, i32, i32]
+        L.oracle_window_src_row.restype = i64
+        L.oracle_op1.argtypes = [P, i32, i32, i32, i32, i32, i32, P, P, f32, f32, i32, P, i64, P, P]
+        L.oracle_op1.restype = None
+        L.oracle_qkv.argtypes = [P, i64, i32, i32, P, P, P, f32, f32, f32, f32, P, P]
+        L.oracle_qkv.restype = None
+        L.oracle_rel_bias.argtypes = [P, i32, i32, P]
+        L.oracle_rel_bias.restype = None
+        L.oracle_shift_mask.argtypes = [i32, i32, i32, i32, P]
+        L.oracle_shift_mask.restype = None
+        L.oracle_attn_fold.argtypes = [f32, f32, f32, f32, i32, P, P, P]
+        L.oracle_attn_fold.restype = None
+        L.oracle_attn.argtypes = [P, i64, i32, i32, i32, i32, i32, i32, f32, P, P, f32, f32, i32, P, i64, P, P]
+        L.oracle_attn.restype = None
         _lib = L
     return _lib
 
@@ -194,3 +209,82 @@ def mlp(layer, X, R=None, rows=None, nthreads=0, taps=False):
     if taps:
         return {"acc1": a1, "hidden": h, "acc2": a2, "yhat": yh, "z": z, "y": Y}
     return Y
+
+
+# ---- attention half of the block (oracle_attn.c) -------------
+
+def window_src_row(r, Hs, Ws, M, s):
+    """Raster row (b*Hs*Ws + y*Ws + x) of window-ordered row r (readings R21, R22)."""
+    return int(lib().oracle_window_src_row(int(r), int(Hs), int(Ws), int(M), int(s)))
+
+
+def op1(x, gamma, beta, eps, s_q, z_q, M, shift, rows=None, return_yhat=False):
+    """Fused op #1: LayerNorm -> window shift -> Q.  x: fp32 [B][Hs][Ws][C].
+    Returns int8 [nrows][C] in window order (all B*Hs*Ws rows when rows is None)."""
+    x = _c(x, np.float32)
+    B, Hs, Ws, C = x.shape
+    gamma = _c(gamma, np.float32); beta = _c(beta, np.float32)
+    r = None if rows is None else _c(rows, np.int64)
+    n = B * Hs * Ws if r is None else r.shape[0]
+    out = np.empty((n, C), np.int8)
+    yh = np.empty((n, C), np.float32) if return_yhat else None
+    inv = np.float32(1.0) / np.float32(s_q)
+    lib().oracle_op1(_p(x), B, Hs, Ws, C, int(M), int(shift), _p(gamma), _p(beta), float(eps), float(inv), int(z_q),
+                     _p(r), n, _p(out), _p(yh))
+    return (out, yh) if return_yhat else out
+
+
+def qkv(X, W, s_w, b, s_x, z_x, s_q, s_k, s_v, return_acc=False):
+    """QKV GEMM + fused op #2.  X int8 [T][C], W int8 [3C][C] -> int8 [T][3C]."""
+    X = _c(X, np.int8); W = _c(W, np.int8); s_w = _c(s_w, np.float32); b = _c(b, np.float32)
+    T, C = X.shape
+    out = np.empty((T, 3 * C), np.int8)
+    acc = np.empty((T, 3 * C), np.int32) if return_acc else None
+    lib().oracle_qkv(_p(X), T, C, int(z_x), _p(W), _p(s_w), _p(b), float(s_x), float(s_q), float(s_k), float(s_v),
+                     _p(acc), _p(out))
+    return (out, acc) if return_acc else out
+
+
+def rel_bias(table, M, heads):
+    """Relative position bias [heads][N][N] from the [(2M-1)^2][heads] table (reading R24)."""
+    table = _c(table, np.float32)
+    N = M * M
+    out = np.empty((heads, N, N), np.float32)
+    lib().oracle_rel_bias(_p(table), int(M), int(heads), _p(out))
+    return out
+
+
+def shift_mask(Hs, Ws, M, shift):
+    """Shifted-window mask [nW][N][N] of 0 / -100 (reading R25)."""
+    N, nW = M * M, (Hs // M) * (Ws // M)
+    out = np.empty((nW, N, N), np.float32)
+    lib().oracle_shift_mask(int(Hs), int(Ws), int(M), int(shift), _p(out))
+    return out
+
+
+def attn_fold(s_q, s_k, s_v, s_a, D=32):
+    """(m3, inv_p, m_o): op #3's dequant multiplier with the attention scale, the probability
+    quantizer's reciprocal and the V.att requant multiplier (R23, R26, R27)."""
+    o = np.empty(3, np.float32)
+    lib().oracle_attn_fold(float(s_q), float(s_k), float(s_v), float(s_a), int(D), _p(o[0:]), _p(o[1:]), _p(o[2:]))
+    return float(o[0]), float(o[1]), float(o[2])
+
+
+def attn(qkv_q, A, B, wins=None, return_p=False):
+    """Q.K GEMM -> fused op #3 -> V.att GEMM for the windows `wins` (all when None).  qkv_q: int8
+    [B*Hs*Ws][3C] in window order; A: synth.AttnLayer.  Returns int8 [B*Hs*Ws][C] in raster order
+    (rows of windows not computed are left 0) and, with return_p, Pq [nwins][heads][N][N]."""
+    qkv_q = _c(qkv_q, np.int8)
+    C, heads, M, Hs, Ws, s = A.C, A.heads, A.M, A.Hs, A.Ws, A.shift
+    N = M * M
+    n_win = qkv_q.shape[0] // N
+    m3, inv_p, m_o = attn_fold(A.s_q, A.s_k, A.s_v, A.s_a, C // heads)
+    bias = rel_bias(A.table, M, heads)
+    mask = shift_mask(Hs, Ws, M, s) if s else None
+    w = None if wins is None else _c(wins, np.int64)
+    nw = n_win if w is None else w.shape[0]
+    out = np.zeros((qkv_q.shape[0], C), np.int8)
+    pt = np.empty((nw, heads, N, N), np.int8) if return_p else None
+    lib().oracle_attn(_p(qkv_q), n_win, C, heads, M, Hs, Ws, int(s), float(m3), _p(bias), _p(mask), float(inv_p),
+                      float(m_o), int(A.z_a), _p(w), nw, _p(out), _p(pt))
+    return (out, pt) if return_p else out

@@ -192,3 +192,71 @@ def make_attn_out(P: ProjLayer, T: int, seed: int) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed))
     x = rng.standard_normal((T, P.C), dtype=np.float32)
     return np.clip(np.rint(x * np.float32(1.0 / P.s_a)) + P.z_a, -128, 127).astype(np.int8)
+
+
+@dataclass
+class AttnLayer:
+    """Attention half of one Swin block (Fig. 1 nodes
+    a1-d5): op #1 LayerNorm parameters and output quantizer, the QKV weights, the q/k/v and
+    attention-output quantizers, the relative position bias table and the window geometry.
+    Field names follow swin_attn_int8_desc_t / swin_op1_int8_desc_t."""
+    C: int
+    heads: int
+    M: int                      # window side (7; 12 for Swin-L at 384)
+    Hs: int                     # feature map height / width (multiples of M)
+    Ws: int
+    shift: int                  # 0 or M // 2
+    gamma1: np.ndarray          # fp32 [C] (op #1 LayerNorm)
+    beta1: np.ndarray
+    eps: float
+    s_x: float                  # op #1 output quantizer (the QKV GEMM input)
+    z_x: int
+    w_qkv: np.ndarray           # int8 [3C][C]
+    s_wqkv: np.ndarray          # fp32 [3C]
+    b_qkv: Optional[np.ndarray]  # fp32 [3C]
+    s_q: float
+    s_k: float
+    s_v: float
+    table: np.ndarray           # fp32 [(2M-1)^2][heads]
+    s_a: float                  # attention-output (V.att) quantizer, the Proj GEMM input
+    z_a: int
+    seed: int = 0
+
+
+def make_attn_layer(C: int, Hs: int, Ws: int, seed: int, M: int = 7, shift: Optional[int] = None,
+                    heads: Optional[int] = None, z_x: int = 0, z_a: int = 0, qk_std: float = 1.5) -> AttnLayer:
+    """Recipe: head dim 32 (Swin), LN params as the MLP's, QKV weights with the
+    std that gives q and k ~ N(0, qk_std^2) and v ~ N(0, 1) on the LN output (logits
+    q.k / sqrt(32) ~ N(0, qk_std^4), so the softmax is neither uniform nor one-hot), per-channel
+    max-abs PTQ, 4-sigma clip points for s_q / s_k / s_v, relative position table N(0, 0.5^2)."""
+    heads = C // 32 if heads is None else heads
+    shift = M // 2 if shift is None else shift
+    rng = np.random.Generator(np.random.PCG64(seed))
+    gamma1 = (np.float32(1.0) + np.float32(0.1) * rng.standard_normal(C, dtype=np.float32)).astype(np.float32)
+    beta1 = (np.float32(0.1) * rng.standard_normal(C, dtype=np.float32)).astype(np.float32)
+    wq, sq_w = _quant_weights(rng, C, C, std=qk_std / np.sqrt(C))
+    wk, sk_w = _quant_weights(rng, C, C, std=qk_std / np.sqrt(C))
+    wv, sv_w = _quant_weights(rng, C, C, std=1.0 / np.sqrt(C))
+    w_qkv = np.concatenate([wq, wk, wv]).astype(np.int8)
+    s_wqkv = np.concatenate([sq_w, sk_w, sv_w]).astype(np.float32)
+    b_qkv = (np.float32(0.02) * rng.standard_normal(3 * C, dtype=np.float32)).astype(np.float32)
+    table = (np.float32(0.5) * rng.standard_normal(((2 * M - 1) ** 2, heads), dtype=np.float32)).astype(np.float32)
+    return AttnLayer(C=C, heads=heads, M=M, Hs=Hs, Ws=Ws, shift=shift, gamma1=gamma1, beta1=beta1, eps=1e-5,
+                     s_x=float(np.float32(5.0 / 127.0)), z_x=z_x, w_qkv=w_qkv, s_wqkv=s_wqkv, b_qkv=b_qkv,
+                     s_q=float(np.float32(4.0 * qk_std / 127.0)), s_k=float(np.float32(4.0 * qk_std / 127.0)),
+                     s_v=float(np.float32(4.0 / 127.0)), table=table, s_a=float(np.float32(3.0 / 127.0)),
+                     z_a=z_a, seed=seed)
+
+
+def make_block_input(B: int, Hs: int, Ws: int, C: int, seed: int) -> np.ndarray:
+    """fp32 [B][Hs][Ws][C] block input (residual stream): N(0,1) with 2 % x6 outlier channels
+    and a per-token offset N(0, 0.5^2) (LayerNorm has a mean to remove)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    gain = np.ones(C, np.float32)
+    gain[rng.choice(C, max(1, int(round(0.02 * C))), replace=False)] = np.float32(6.0)
+    out = np.empty((B, Hs, Ws, C), np.float32)
+    for b in range(B):
+        x = rng.standard_normal((Hs, Ws, C), dtype=np.float32) * gain
+        x += np.float32(0.5) * rng.standard_normal((Hs, Ws, 1), dtype=np.float32)
+        out[b] = x
+    return out
