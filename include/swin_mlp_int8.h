@@ -18,8 +18,9 @@
  *   ReLU: v = fl(max(y,0) * inv_h)         GELU: v = fl(gelu_erf(y) * inv_h)
  *   Hq = clamp(rne(v) + h_zero_point, -128, 127),  inv_h = fl(1/h_scale)
  *   d  = fmaf(fl(A2), m2[c], b2[c] or 0),  m2[c] = fl(h_scale*w2_scale[c])
- *   z  = fl(d + residual[t][c])  or, when residual == NULL, the residual dQ(X) added
- *        with one rounding: z = fmaf(fl(X[t][c] - z_x), x_scale, d);
+ *   z  = fl(d + residual[t][c])  or, when residual == NULL, the residual dQ(X) then the
+ *        Add, each its own rounding (Fig. 1 node order, reading R3):
+ *        r = fl(fl(X[t][c] - z_x) * x_scale),  z = fl(d + r);
  *   mu, var (biased), rstd = 1/sqrt(var+eps) in double;
  *   yhat = fl(((z-mu)*rstd)*gamma[c] + beta[c])  (double ops; desc.ln_fp64 = 1 —
  *   with ln_fp64 = 0 the same formula is evaluated in fp32 with one fmaf);

@@ -33,6 +33,9 @@ EXPORTS = [
     "swin_mlp_int8_profile_begin", "swin_mlp_int8_profile_end", "swin_mlp_int8_set_trace",
     "swin_mlp_int8_destroy", "swin_mlp_int8_last_error",
     "swin_mlp_int8_host_batch_workspace_bytes", "swin_mlp_int8_run_host_batch",
+    "swin_op1_int8_create", "swin_op1_int8_run", "swin_op1_int8_destroy",
+    "swin_attn_int8_create", "swin_attn_int8_workspace_bytes", "swin_attn_int8_run", "swin_attn_int8_run_debug",
+    "swin_attn_int8_get_constants", "swin_attn_int8_destroy",
     "swin_proj_int8_create", "swin_proj_int8_run", "swin_proj_int8_run_debug", "swin_proj_int8_plan",
     "swin_proj_int8_destroy",
 ]
@@ -59,6 +62,29 @@ class swin_proj_int8_desc_t(ctypes.Structure):
         ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
         ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32),
         ("device", ctypes.c_int32), ("ln_fp64", ctypes.c_int32),
+    ]
+
+
+class swin_op1_int8_desc_t(ctypes.Structure):
+    """include/swin_attn_int8.h (fused op #1, NEXT-4)."""
+    _fields_ = [
+        ("C", ctypes.c_int32), ("M", ctypes.c_int32), ("shift", ctypes.c_int32),
+        ("Hs", ctypes.c_int32), ("Ws", ctypes.c_int32),
+        ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
+        ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32), ("device", ctypes.c_int32),
+    ]
+
+
+class swin_attn_int8_desc_t(ctypes.Structure):
+    """include/swin_attn_int8.h (QKV GEMM + op #2 -> Q.K + op #3 -> V.att, NEXT-3)."""
+    _fields_ = [
+        ("C", ctypes.c_int32), ("heads", ctypes.c_int32), ("M", ctypes.c_int32), ("shift", ctypes.c_int32),
+        ("Hs", ctypes.c_int32), ("Ws", ctypes.c_int32),
+        ("x_scale", ctypes.c_float), ("x_zero_point", ctypes.c_int32),
+        ("w_qkv", ctypes.c_void_p), ("w_qkv_scale", ctypes.c_void_p), ("b_qkv", ctypes.c_void_p),
+        ("q_scale", ctypes.c_float), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float),
+        ("rel_bias_table", ctypes.c_void_p),
+        ("a_scale", ctypes.c_float), ("a_zero_point", ctypes.c_int32), ("device", ctypes.c_int32),
     ]
 
 
@@ -124,6 +150,24 @@ def lib():
     L.swin_proj_int8_plan.restype = i32
     L.swin_proj_int8_destroy.argtypes = [P]
     L.swin_proj_int8_destroy.restype = i32
+    L.swin_op1_int8_create.argtypes = [ctypes.POINTER(swin_op1_int8_desc_t), ctypes.POINTER(P)]
+    L.swin_op1_int8_create.restype = i32
+    L.swin_op1_int8_run.argtypes = [P, P, i64, P, P]
+    L.swin_op1_int8_run.restype = i32
+    L.swin_op1_int8_destroy.argtypes = [P]
+    L.swin_op1_int8_destroy.restype = i32
+    L.swin_attn_int8_create.argtypes = [ctypes.POINTER(swin_attn_int8_desc_t), ctypes.POINTER(P)]
+    L.swin_attn_int8_create.restype = i32
+    L.swin_attn_int8_workspace_bytes.argtypes = [P, i64]
+    L.swin_attn_int8_workspace_bytes.restype = sz
+    L.swin_attn_int8_run.argtypes = [P, P, i64, P, P, sz, P]
+    L.swin_attn_int8_run.restype = i32
+    L.swin_attn_int8_run_debug.argtypes = [P, P, i64, P, P, sz, P, P, P, P]
+    L.swin_attn_int8_run_debug.restype = i32
+    L.swin_attn_int8_get_constants.argtypes = [P, P, P]
+    L.swin_attn_int8_get_constants.restype = i32
+    L.swin_attn_int8_destroy.argtypes = [P]
+    L.swin_attn_int8_destroy.restype = i32
     L.swin_mlp_int8_last_error.argtypes = []
     L.swin_mlp_int8_last_error.restype = ctypes.c_char_p
     _lib = L
@@ -423,3 +467,158 @@ class SwinProjInt8Layer:
         swin_proj_int8_run_debug(self.handle, _ptr(a), _ptr(residual), _ptr(y), _ptr(residual_out), T, stream,
                                  _ptr(acc), _ptr(ln))
         return {"y": y, "acc": acc, "ln_out": ln}
+
+
+# ---- attention half (include/swin_attn_int8.h) -------------------
+
+def swin_op1_int8_create(desc: swin_op1_int8_desc_t) -> int:
+    h = ctypes.c_void_p()
+    _check(lib().swin_op1_int8_create(ctypes.byref(desc), ctypes.byref(h)))
+    return h.value
+
+
+def swin_op1_int8_run(h, x, B, y, stream):
+    _check(lib().swin_op1_int8_run(h, x, B, y, stream))
+
+
+def swin_op1_int8_destroy(h):
+    _check(lib().swin_op1_int8_destroy(h))
+
+
+def swin_attn_int8_create(desc: swin_attn_int8_desc_t) -> int:
+    h = ctypes.c_void_p()
+    _check(lib().swin_attn_int8_create(ctypes.byref(desc), ctypes.byref(h)))
+    return h.value
+
+
+def swin_attn_int8_workspace_bytes(h, B) -> int:
+    return int(lib().swin_attn_int8_workspace_bytes(h, B))
+
+
+def swin_attn_int8_run(h, xw, B, a, workspace, workspace_bytes, stream):
+    _check(lib().swin_attn_int8_run(h, xw, B, a, workspace, workspace_bytes, stream))
+
+
+def swin_attn_int8_run_debug(h, xw, B, a, workspace, workspace_bytes, stream, qkv, acc, p):
+    _check(lib().swin_attn_int8_run_debug(h, xw, B, a, workspace, workspace_bytes, stream, qkv, acc, p))
+
+
+def swin_attn_int8_destroy(h):
+    _check(lib().swin_attn_int8_destroy(h))
+
+
+def _host_ptr(keep, a, dt):
+    import numpy as np
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=dt)
+    keep.append(a)
+    return a.ctypes.data_as(ctypes.c_void_p).value
+
+
+class SwinOp1Int8:
+    """Fused op #1 handle (LayerNorm -> window shift -> Q).  `layer`: synth.AttnLayer (or any
+    object with C, M, shift, Hs, Ws, gamma1, beta1, eps, s_x, z_x)."""
+
+    def __init__(self, layer, device: int = 0):
+        import numpy as np
+        import torch
+        keep = []
+        d = swin_op1_int8_desc_t()
+        d.C, d.M, d.shift, d.Hs, d.Ws = int(layer.C), int(layer.M), int(layer.shift), int(layer.Hs), int(layer.Ws)
+        d.ln_gamma, d.ln_beta = _host_ptr(keep, layer.gamma1, np.float32), _host_ptr(keep, layer.beta1, np.float32)
+        d.ln_eps, d.y_scale, d.y_zero_point, d.device = float(layer.eps), float(layer.s_x), int(layer.z_x), int(device)
+        self.C, self.Hs, self.Ws = d.C, d.Hs, d.Ws
+        self.handle = swin_op1_int8_create(d)
+        self._torch = torch
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                lib().swin_op1_int8_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def __call__(self, x, y=None):
+        """x: fp32 [B][Hs][Ws][C] device tensor -> int8 [B*Hs*Ws][C] (window order)."""
+        torch = self._torch
+        B = x.shape[0]
+        if y is None:
+            y = torch.empty((B * self.Hs * self.Ws, self.C), dtype=torch.int8, device=x.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+        swin_op1_int8_run(self.handle, _ptr(x), B, _ptr(y), stream)
+        return y
+
+
+class SwinAttnInt8Layer:
+    """QKV GEMM + op #2 -> Q.K + op #3 -> V.att handle.  `layer`: synth.AttnLayer."""
+
+    def __init__(self, layer, device: int = 0):
+        import numpy as np
+        import torch
+        keep = []
+        d = swin_attn_int8_desc_t()
+        d.C, d.heads, d.M, d.shift = int(layer.C), int(layer.heads), int(layer.M), int(layer.shift)
+        d.Hs, d.Ws = int(layer.Hs), int(layer.Ws)
+        d.x_scale, d.x_zero_point = float(layer.s_x), int(layer.z_x)
+        d.w_qkv = _host_ptr(keep, layer.w_qkv, np.int8)
+        d.w_qkv_scale = _host_ptr(keep, layer.s_wqkv, np.float32)
+        d.b_qkv = _host_ptr(keep, layer.b_qkv, np.float32)
+        d.q_scale, d.k_scale, d.v_scale = float(layer.s_q), float(layer.s_k), float(layer.s_v)
+        d.rel_bias_table = _host_ptr(keep, layer.table, np.float32)
+        d.a_scale, d.a_zero_point, d.device = float(layer.s_a), int(layer.z_a), int(device)
+        self.C, self.heads, self.M, self.Hs, self.Ws = d.C, d.heads, d.M, d.Hs, d.Ws
+        self.handle = swin_attn_int8_create(d)
+        self._torch = torch
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                lib().swin_attn_int8_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def workspace(self, B, device=None):
+        n = max(swin_attn_int8_workspace_bytes(self.handle, B), 128)
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = self._torch.empty(n, dtype=self._torch.uint8, device=device or "cuda")
+        return self._ws
+
+    def constants(self):
+        import numpy as np
+        c = np.empty(3, np.float32)
+        N = self.M * self.M
+        bias = np.empty((self.heads, N, N), np.float32)
+        _check(lib().swin_attn_int8_get_constants(self.handle, c.ctypes.data_as(ctypes.c_void_p),
+                                                  bias.ctypes.data_as(ctypes.c_void_p)))
+        return {"m3": float(c[0]), "inv_p": float(c[1]), "m_o": float(c[2]), "bias": bias}
+
+    def __call__(self, xw, B, a=None, workspace=None):
+        """xw: int8 [B*Hs*Ws][C] window order (op #1's output) -> int8 [B*Hs*Ws][C] raster order."""
+        torch = self._torch
+        T = xw.shape[0]
+        if a is None:
+            a = torch.empty((T, self.C), dtype=torch.int8, device=xw.device)
+        ws = workspace if workspace is not None else self.workspace(B, xw.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(xw.device).cuda_stream)
+        swin_attn_int8_run(self.handle, _ptr(xw), B, _ptr(a), _ptr(ws), ws.numel(), stream)
+        return a
+
+    def run_debug(self, xw, B):
+        torch = self._torch
+        T = xw.shape[0]
+        N = self.M * self.M
+        a = torch.empty((T, self.C), dtype=torch.int8, device=xw.device)
+        qkv = torch.empty((T, 3 * self.C), dtype=torch.int8, device=xw.device)
+        acc = torch.empty((T, 3 * self.C), dtype=torch.int32, device=xw.device)
+        p = torch.empty((T // N, self.heads, N, N), dtype=torch.int8, device=xw.device)
+        ws = self.workspace(B, xw.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(xw.device).cuda_stream)
+        swin_attn_int8_run_debug(self.handle, _ptr(xw), B, _ptr(a), _ptr(ws), ws.numel(), stream,
+                                 _ptr(qkv), _ptr(acc), _ptr(p))
+        return {"a": a, "qkv": qkv, "acc": acc, "p": p}

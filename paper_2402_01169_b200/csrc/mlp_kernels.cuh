@@ -10,6 +10,8 @@
 //   EP5_GELU  FC1 + fused op #5 with exact-erf GELU (the control the paper removes)
 //   EP6_LN    FC2 + fused op #6: dQ, FC2 bias, residual add, LayerNorm, Q
 //             (trailing Q per DESIGN.md reading R4)
+//   EP2_QKV   QKV GEMM + fused op #2: dQ, QKV bias, Q with a per-column output scale (the q, k and
+//             v thirds each on their own quantizer)
 //   EP_ACC    FC1 alone, the int32 accumulators A1 (zero-point term included) written
 //             to global memory: the FasterTransformer layout the paper starts from,
 //             where op #5 is a separate kernel (SURVEY.md
@@ -55,7 +57,7 @@
 
 namespace swinmlp {
 
-enum Epi : int { EP5_RELU = 0, EP5_GELU = 1, EP6_LN = 2, EP_ACC = 3 };
+enum Epi : int { EP5_RELU = 0, EP5_GELU = 1, EP6_LN = 2, EP_ACC = 3, EP2_QKV = 4 };
 
 constexpr int kBM = 128;             // rows per tile (UMMA M, TMEM lanes)
 constexpr int kBK = 128;             // K bytes per pipeline stage (one 128-B swizzle row)
@@ -95,7 +97,7 @@ struct GemmArgs {
     int32_t z_x;
     const float* resid;    // [M][ldo] fp32 residual or nullptr (nullptr: r = dQ(x), x via tmX)
     float* resid_out;      // [M][ldo] fp32 z or nullptr
-    const float* gamma;
+    const float* gamma;    // EP6: LN gamma; EP2_QKV: [N] per-column output quantizer reciprocal
     const float* beta;
     float eps;
     float one;             // 1.0f (host-set): z = fma(dQ(x), one, d) keeps ptxas from fusing the
@@ -672,6 +674,7 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     cb[3 * BN + c] = __ldg(p.gamma + n);
                     cb[4 * BN + c] = __ldg(p.beta + n);
                 }
+                if (EPI == EP2_QKV) cb[3 * BN + c] = __ldg(p.gamma + n);   // 1/s of this column's quantizer
             }
             if (trc && lane == 0 && it < 512) trc[3072 + 2 * it + 1] = gtimer();
             mbar_arrive(bar_cfull + 8u * buf);
@@ -859,6 +862,8 @@ mlp_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     for (int j = 0; j < 8; ++j) {
                         float2 t;
                         if constexpr (EPI == EP5_RELU) t = f2_mul(y[j], inv2);   // ReLU folds into the pack
+                        else if constexpr (EPI == EP2_QKV)   // op #2: fl(y * fl(1/s_q|k|v)) per column
+                            t = f2_mul(y[j], *reinterpret_cast<const float2*>(cm + 3 * BN + cl + 2 * j));
                         else t = f2_mul(make_float2(gelu_erf_f32(y[j].x), gelu_erf_f32(y[j].y)), inv2);
                         v[2 * j] = t.x;
                         v[2 * j + 1] = t.y;

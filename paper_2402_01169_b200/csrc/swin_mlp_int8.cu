@@ -20,7 +20,9 @@
 #include <vector>
 
 #include "../../include/swin_mlp_int8.h"
+#include "../../include/swin_attn_int8.h"
 #include "mlp_kernels.cuh"
+#include "attn_kernels.cuh"
 #include "fused_mlp.cuh"
 #include "op5_unfused.cuh"
 
@@ -159,6 +161,19 @@ KernelFn kernel_for(int epi, int flags) {
             static const KernelFn t[4] = {mlp_gemm_kernel<EP_ACC, 0>, mlp_gemm_kernel<EP_ACC, kHasZc>,
                                           mlp_gemm_kernel<EP_ACC, kPair>, mlp_gemm_kernel<EP_ACC, kHasZc | kPair>};
             return t[((flags & kHasZc) ? 1 : 0) | ((flags & kPair) ? 2 : 0)];
+        }
+        case EP2_QKV: {   // op #2: bias, input zero point, small-K conversion, CTA pair
+            static const KernelFn t[16] = {
+#define Q2(f) mlp_gemm_kernel<EP2_QKV, (f)>
+                Q2(0), Q2(kHasB), Q2(kHasZc), Q2(kHasB | kHasZc),
+                Q2(kSmallK), Q2(kSmallK | kHasB), Q2(kSmallK | kHasZc), Q2(kSmallK | kHasB | kHasZc),
+                Q2(kPair), Q2(kPair | kHasB), Q2(kPair | kHasZc), Q2(kPair | kHasB | kHasZc),
+                Q2(kPair | kSmallK), Q2(kPair | kSmallK | kHasB), Q2(kPair | kSmallK | kHasZc),
+                Q2(kPair | kSmallK | kHasB | kHasZc)
+#undef Q2
+            };
+            return t[((flags & kHasB) ? 1 : 0) | ((flags & kHasZc) ? 2 : 0) | ((flags & kSmallK) ? 4 : 0) |
+                     ((flags & kPair) ? 8 : 0)];
         }
         default: return pick<EP6_LN>((flags & 15) | ((flags & kPair) ? 16 : 0), std::make_integer_sequence<int, 32>{},
                                      false);
@@ -1433,5 +1448,370 @@ int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20) {
     return 0;
 }
 
+// ---------------------------------------------------------------------------------------
+// NEXT-4: fused op #1 (LayerNorm -> window shift -> Q), Fig. 1 lines 39-43.
+struct swin_op1_int8_s {
+    swin_op1_int8_desc_t d;
+    int device = 0, num_sms = 0, blocks_per_sm = 1, U = 1;
+    void (*fn)(Op1Args) = nullptr;
+    float* gamma = nullptr;
+    float* beta = nullptr;
+    float inv_s = 0.f;
+    ~swin_op1_int8_s() {
+        if (gamma) cudaFree(gamma);
+        if (beta) cudaFree(beta);
+    }
+};
+
+swin_mlp_status_t swin_op1_int8_create(const swin_op1_int8_desc_t* desc, swin_op1_int8_t* out) {
+    g_last_error.clear();
+    if (!desc || !out) return fail(SWIN_MLP_EINVAL, "desc and out must be non-NULL");
+    const swin_op1_int8_desc_t& d = *desc;
+    if (d.C < 4 || d.C % 4) return fail(SWIN_MLP_EINVAL, "C=%d must be a positive multiple of 4", d.C);
+    if (d.C > 1536) return fail(SWIN_MLP_EUNSUPPORTED, "C=%d exceeds 1536", d.C);
+    if (d.M < 1 || d.M > 16) return fail(SWIN_MLP_EINVAL, "window M=%d outside [1, 16]", d.M);
+    if (d.shift < 0 || d.shift >= d.M) return fail(SWIN_MLP_EINVAL, "shift=%d outside [0, M)", d.shift);
+    if (d.Hs < d.M || d.Ws < d.M || d.Hs % d.M || d.Ws % d.M)
+        return fail(SWIN_MLP_EINVAL, "Hs=%d, Ws=%d must be positive multiples of M=%d", d.Hs, d.Ws, d.M);
+    if (!normal_positive(d.y_scale)) return fail(SWIN_MLP_EINVAL, "y_scale must be finite, normal and > 0");
+    if (!(d.ln_eps > 0.0f) || !std::isfinite(d.ln_eps)) return fail(SWIN_MLP_EINVAL, "ln_eps must be > 0");
+    if (d.y_zero_point < -128 || d.y_zero_point > 127) return fail(SWIN_MLP_EINVAL, "zero point outside [-128, 127]");
+    if (!d.ln_gamma || !d.ln_beta) return fail(SWIN_MLP_EINVAL, "ln_gamma and ln_beta are required");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (d.device < 0 || d.device >= ndev) return fail(SWIN_MLP_EINVAL, "device %d of %d", d.device, ndev);
+    DeviceGuard guard(d.device);
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, d.device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(SWIN_MLP_EUNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)", d.device,
+                    prop.major, prop.minor);
+    std::vector<float> g, b;
+    ST_TRY(fetch(d.ln_gamma, (size_t)d.C, g, "ln_gamma"));
+    ST_TRY(fetch(d.ln_beta, (size_t)d.C, b, "ln_beta"));
+    auto h = new swin_op1_int8_s();
+    h->d = d;
+    h->d.ln_gamma = h->d.ln_beta = nullptr;
+    h->device = d.device;
+    h->num_sms = prop.multiProcessorCount;
+    auto bail = [&](swin_mlp_status_t st) { delete h; return st; };
+    {
+        volatile float one = 1.0f;
+        h->inv_s = one / d.y_scale;
+    }
+    if (!normal_positive(h->inv_s)) return bail(fail(SWIN_MLP_EINVAL, "1/y_scale not normal"));
+    // float4 per lane (C <= 128 VPL) and rows in flight per warp (~8 float4 loads per lane)
+    const int vpl = (d.C + 127) / 128;
+    switch (vpl) {
+        case 1: h->fn = op1_kernel<1, 8>; h->U = 8; break;
+        case 2: h->fn = op1_kernel<2, 4>; h->U = 4; break;
+        case 3: h->fn = op1_kernel<3, 2>; h->U = 2; break;
+        case 4: h->fn = op1_kernel<4, 2>; h->U = 2; break;
+        case 5: case 6: h->fn = op1_kernel<6, 1>; h->U = 1; break;
+        case 7: case 8: h->fn = op1_kernel<8, 1>; h->U = 1; break;
+        default: h->fn = op1_kernel<12, 1>; h->U = 1; break;
+    }
+    cudaError_t e = cudaMalloc(&h->gamma, sizeof(float) * d.C);
+    if (e == cudaSuccess) e = cudaMalloc(&h->beta, sizeof(float) * d.C);
+    if (e == cudaSuccess) e = cudaMemcpy(h->gamma, g.data(), sizeof(float) * d.C, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->beta, b.data(), sizeof(float) * d.C, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->blocks_per_sm, h->fn, 256, 0);
+    if (e != cudaSuccess) return bail(fail(SWIN_MLP_ECUDA, "op1 create: %s", cudaGetErrorString(e)));
+    h->blocks_per_sm = std::max(1, h->blocks_per_sm);
+    *out = h;
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_op1_int8_run(swin_op1_int8_t h, const float* x, int64_t B, int8_t* y, void* stream) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (B < 0) return fail(SWIN_MLP_EINVAL, "B=%lld < 0", (long long)B);
+    if (B == 0) return SWIN_MLP_OK;
+    if (!x || !y) return fail(SWIN_MLP_EINVAL, "x and y are required");
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) || (reinterpret_cast<uintptr_t>(y) & 3u))
+        return fail(SWIN_MLP_EINVAL, "x must be 16-byte and y 4-byte aligned");
+    const int64_t rows = B * (int64_t)h->d.Hs * h->d.Ws;
+    if (rows > ((int64_t)1 << 40)) return fail(SWIN_MLP_EUNSUPPORTED, "B=%lld too large", (long long)B);
+    DeviceGuard guard(h->device);
+    Op1Args a = {};
+    a.x = x; a.y = y; a.rows = rows;
+    a.C = h->d.C; a.Hs = h->d.Hs; a.Ws = h->d.Ws; a.M = h->d.M; a.shift = h->d.shift;
+    a.gamma = h->gamma; a.beta = h->beta; a.eps = h->d.ln_eps; a.inv_s = h->inv_s; a.z = h->d.y_zero_point;
+    const int64_t warps = (rows + h->U - 1) / h->U;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)h->num_sms * h->blocks_per_sm));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, h->fn, a));
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_op1_int8_destroy(swin_op1_int8_t h) {
+    if (!h) return SWIN_MLP_OK;
+    DeviceGuard guard(h->device);
+    delete h;
+    return SWIN_MLP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// NEXT-3: QKV GEMM + op #2 -> Q.K + op #3 -> V.att, Fig. 1 lines 45-62.  The QKV GEMM
+// is the MLP's GEMM skeleton with the op #2 epilogue (mlp_gemm_kernel<EP2_QKV>); the attention
+// core is attn_core_kernel<M> (attn_kernels.cuh).
+struct swin_attn_int8_s {
+    swin_mlp_int8_s m;          // the QKV GEMM: p1 / tm_w1 / w1 (Wqkv) / m1 / b1 / zc1, map cache
+    swin_attn_int8_desc_t d;
+    float* inv_cols = nullptr;  // [3C] fl(1/s_q | 1/s_k | 1/s_v) per column
+    float* bias = nullptr;      // [heads][N][N]
+    float* mask = nullptr;      // [nW][N][N] or nullptr (shift == 0)
+    std::vector<float> hbias;
+    float m3 = 0.f, inv_p = 0.f, m_o = 0.f;
+    int N = 0, nW = 0, core_smem = 0, core_blocks_per_sm = 1;
+    void (*core)(AttnArgs) = nullptr;
+};
+
+swin_mlp_status_t swin_attn_int8_create(const swin_attn_int8_desc_t* desc, swin_attn_int8_t* out) {
+    g_last_error.clear();
+    if (!desc || !out) return fail(SWIN_MLP_EINVAL, "desc and out must be non-NULL");
+    const swin_attn_int8_desc_t& d = *desc;
+    if (d.heads < 1 || d.C != 32 * d.heads) return fail(SWIN_MLP_EINVAL, "C=%d must be 32 * heads (heads=%d)", d.C, d.heads);
+    if (d.C < 64) return fail(SWIN_MLP_EINVAL, "C=%d < 64", d.C);
+    if (d.C > 1536) return fail(SWIN_MLP_EUNSUPPORTED, "C=%d exceeds 1536", d.C);
+    if (d.M != 7 && d.M != 12) return fail(SWIN_MLP_EUNSUPPORTED, "window M=%d (built: 7, 12)", d.M);
+    if (d.shift < 0 || d.shift >= d.M) return fail(SWIN_MLP_EINVAL, "shift=%d outside [0, M)", d.shift);
+    if (d.Hs < d.M || d.Ws < d.M || d.Hs % d.M || d.Ws % d.M)
+        return fail(SWIN_MLP_EINVAL, "Hs=%d, Ws=%d must be positive multiples of M=%d", d.Hs, d.Ws, d.M);
+    if (!normal_positive(d.x_scale) || !normal_positive(d.q_scale) || !normal_positive(d.k_scale) ||
+        !normal_positive(d.v_scale) || !normal_positive(d.a_scale))
+        return fail(SWIN_MLP_EINVAL, "scales must be finite, normal and > 0");
+    for (int32_t z : {d.x_zero_point, d.a_zero_point})
+        if (z < -128 || z > 127) return fail(SWIN_MLP_EINVAL, "zero point %d outside [-128, 127]", z);
+    if (!d.w_qkv || !d.w_qkv_scale || !d.rel_bias_table)
+        return fail(SWIN_MLP_EINVAL, "w_qkv, w_qkv_scale and rel_bias_table are required");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (d.device < 0 || d.device >= ndev) return fail(SWIN_MLP_EINVAL, "device %d of %d", d.device, ndev);
+    DeviceGuard guard(d.device);
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, d.device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(SWIN_MLP_EUNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)", d.device,
+                    prop.major, prop.minor);
+    const int C = d.C, N3 = 3 * d.C, M = d.M, N = M * M, heads = d.heads;
+    const int nW = (d.Hs / M) * (d.Ws / M);
+    std::vector<int8_t> w;
+    std::vector<float> sw, b, table;
+    ST_TRY(fetch(d.w_qkv, (size_t)N3 * C, w, "w_qkv"));
+    ST_TRY(fetch(d.w_qkv_scale, (size_t)N3, sw, "w_qkv_scale"));
+    ST_TRY(fetch(d.rel_bias_table, (size_t)(2 * M - 1) * (2 * M - 1) * heads, table, "rel_bias_table"));
+    if (d.b_qkv) ST_TRY(fetch(d.b_qkv, (size_t)N3, b, "b_qkv"));
+
+    auto ah = new swin_attn_int8_s();
+    swin_mlp_int8_s* h = &ah->m;
+    auto bail = [&](swin_mlp_status_t st) {
+        delete ah;
+        return st;
+    };
+    ah->d = d;
+    ah->d.w_qkv = nullptr; ah->d.w_qkv_scale = ah->d.b_qkv = ah->d.rel_bias_table = nullptr;
+    ah->N = N; ah->nW = nW;
+    h->d = swin_mlp_int8_desc_t{};
+    h->d.C = C; h->d.H = N3; h->d.x_scale = d.x_scale; h->d.x_zero_point = d.x_zero_point;
+    h->d.device = d.device;
+    h->device = d.device;
+    h->num_sms = prop.multiProcessorCount;
+    // op #2 folded constants: m[n] = fl(s_x * s_w[n]), inv per column; zero-point correction
+    h->hm1.resize(N3);
+    std::vector<float> inv(N3);
+    float inv3[3];
+    {
+        volatile float one = 1.0f;
+        inv3[0] = one / d.q_scale; inv3[1] = one / d.k_scale; inv3[2] = one / d.v_scale;
+    }
+    std::vector<int32_t> zc(N3);
+    int64_t rowabs = 0;
+    for (int n = 0; n < N3; ++n) {
+        if (!normal_positive(sw[n])) return bail(fail(SWIN_MLP_EINVAL, "w_qkv_scale[%d] not finite/normal/positive", n));
+        volatile float m = d.x_scale * sw[n];
+        h->hm1[n] = m;
+        if (!normal_positive(h->hm1[n])) return bail(fail(SWIN_MLP_EINVAL, "x_scale*w_qkv_scale[%d] not normal", n));
+        inv[n] = inv3[n / C];
+        int64_t s = 0, sa = 0;
+        for (int k = 0; k < C; ++k) {
+            const int8_t v = w[(size_t)n * C + k];
+            if (v == -128) return bail(fail(SWIN_MLP_EINVAL, "w_qkv must be symmetric (-128 not allowed)"));
+            s += v;
+            sa += std::abs((int)v);
+        }
+        zc[n] = (int32_t)(s * d.x_zero_point);
+        rowabs = std::max(rowabs, sa);
+    }
+    for (float v : inv3)
+        if (!normal_positive(v)) return bail(fail(SWIN_MLP_EINVAL, "1/q|k|v_scale not normal"));
+    // op #3 and V.att constants (one fp32 rounding each, as written in the header)
+    {
+        volatile float rs = (float)(1.0 / std::sqrt(32.0));
+        volatile float sqk = d.q_scale * d.k_scale;
+        volatile float m3 = sqk * rs;
+        volatile float one = 1.0f;
+        volatile float s_p = one / 127.0f;
+        volatile float inv_p = one / s_p;
+        volatile float spv = s_p * d.v_scale;
+        volatile float inv_a = one / d.a_scale;
+        volatile float m_o = spv * inv_a;
+        ah->m3 = m3; ah->inv_p = inv_p; ah->m_o = m_o;
+    }
+    if (!normal_positive(ah->m3) || !normal_positive(ah->m_o)) return bail(fail(SWIN_MLP_EINVAL, "folded op #3 constants not normal"));
+    // relative position bias [heads][N][N] and the shifted-window mask [nW][N][N]
+    ah->hbias.resize((size_t)heads * N * N);
+    for (int hh = 0; hh < heads; ++hh)
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) {
+                const int dy = i / M - j / M + M - 1, dx = i % M - j % M + M - 1;
+                ah->hbias[((size_t)hh * N + i) * N + j] = table[(size_t)(dy * (2 * M - 1) + dx) * heads + hh];
+            }
+    std::vector<float> hmask;
+    if (d.shift > 0) {
+        hmask.assign((size_t)nW * N * N, 0.0f);
+        const int nWx = d.Ws / M;
+        std::vector<int> reg(N);
+        for (int wv = 0; wv < nW; ++wv) {
+            for (int p = 0; p < N; ++p) {
+                const int y = (wv / nWx) * M + p / M, x = (wv % nWx) * M + p % M;
+                const int ry = y < d.Hs - M ? 0 : y < d.Hs - d.shift ? 1 : 2;
+                const int rx = x < d.Ws - M ? 0 : x < d.Ws - d.shift ? 1 : 2;
+                reg[p] = ry * 3 + rx;
+            }
+            for (int i = 0; i < N; ++i)
+                for (int j = 0; j < N; ++j) hmask[((size_t)wv * N + i) * N + j] = reg[i] == reg[j] ? 0.0f : -100.0f;
+        }
+    }
+    // QKV GEMM plan (op #2 epilogue)
+    if (!make_plan(EP2_QKV, N3, C, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no QKV GEMM plan for C=%d", C));
+    swin_mlp_status_t st;
+#define A_TRY(expr)                                        \
+    do {                                                   \
+        if ((st = (expr)) != SWIN_MLP_OK) return bail(st); \
+    } while (0)
+    A_TRY(upload(h, w, &h->w1));
+    A_TRY(upload(h, h->hm1, &h->m1));
+    A_TRY(upload(h, inv, &ah->inv_cols));   // (device copies are owned by h->allocs)
+    if (d.b_qkv) A_TRY(upload(h, b, &h->b1));
+    if (d.x_zero_point) A_TRY(upload(h, zc, &h->zc1));
+    A_TRY(upload(h, ah->hbias, &ah->bias));
+    if (d.shift > 0) A_TRY(upload(h, hmask, &ah->mask));
+    A_TRY(encode_2d(&h->tm_w1, h->w1, N3, C, C, (uint32_t)(h->p1.pair ? h->p1.BN / 2 : h->p1.BN)));
+    const bool small_k = (int64_t)(128 + std::abs(d.x_zero_point)) * rowabs < (int64_t(1) << 22);
+    h->p1.fn = kernel_for(EP2_QKV, (d.b_qkv ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (small_k ? kSmallK : 0) |
+                                       (h->p1.pair ? kPair : 0));
+    A_TRY(prepare(h->p1, h->num_sms));
+    // attention core: one warp per (window, head), kAttnWarps warps per CTA
+    ah->core = M == 7 ? attn_core_kernel<7> : attn_core_kernel<12>;
+    ah->core_smem = kAttnWarps * (M == 7 ? AttnGeom<7>::BYTES : AttnGeom<12>::BYTES);
+    CUDA_TRY(cudaFuncSetAttribute(ah->core, cudaFuncAttributeMaxDynamicSharedMemorySize, ah->core_smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ah->core_blocks_per_sm, ah->core, 32 * kAttnWarps,
+                                                           ah->core_smem));
+    ah->core_blocks_per_sm = std::max(1, ah->core_blocks_per_sm);
+#undef A_TRY
+    *out = ah;
+    return SWIN_MLP_OK;
+}
+
+size_t swin_attn_int8_workspace_bytes(swin_attn_int8_t h, int64_t B) {
+    if (!h || B <= 0) return 0;
+    const int64_t T = B * (int64_t)h->d.Hs * h->d.Ws;
+    return (size_t)((T * 3 * h->d.C + 127) / 128 * 128);
+}
+
+static swin_mlp_status_t attn_run_impl(swin_attn_int8_t ah, const int8_t* xw, int64_t B, int8_t* aout, void* workspace,
+                                       size_t ws_bytes, void* stream, int8_t* qkv_tap, int32_t* acc_tap, int8_t* p_tap) {
+    if (!ah) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (B < 0) return fail(SWIN_MLP_EINVAL, "B=%lld < 0", (long long)B);
+    if (B == 0) return SWIN_MLP_OK;
+    swin_mlp_int8_s* h = &ah->m;
+    const int C = ah->d.C, N3 = 3 * C;
+    const int64_t T = B * (int64_t)ah->d.Hs * ah->d.Ws;
+    if (T > ((int64_t)1 << 31)) return fail(SWIN_MLP_EUNSUPPORTED, "B=%lld too large", (long long)B);
+    const size_t need = swin_attn_int8_workspace_bytes(ah, B);
+    if (!xw || !aout || !workspace) return fail(SWIN_MLP_EINVAL, "xw, a and workspace are required");
+    if (ws_bytes < need) return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", ws_bytes, need);
+    if (!aligned16(xw) || (reinterpret_cast<uintptr_t>(aout) & 1u) || (reinterpret_cast<uintptr_t>(workspace) & 127u))
+        return fail(SWIN_MLP_EINVAL, "xw 16-byte, a 2-byte and workspace 128-byte aligned");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int8_t* qkv = static_cast<int8_t*>(workspace);
+    const Plan& P1 = h->p1;
+    auto swz = [](int w) {
+        return w == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : w == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+             : w == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    };
+    CUtensorMap tm_x, tm_o;
+    ST_TRY(encode_cached(h, &tm_x, xw, T, C, C, (uint32_t)(kBM / P1.CS)));
+    ST_TRY(encode_cached(h, &tm_o, qkv, T, N3, N3, kBM, (uint32_t)P1.out_w, swz(P1.out_w)));
+    const int64_t m_tiles = (T + kBM - 1) / kBM;
+    GemmArgs a1 = {};
+    a1.M = T; a1.K = C; a1.BN = P1.BN; a1.CS = P1.CS; a1.stages = P1.stages; a1.G = P1.G; a1.resb = P1.resb;
+    a1.mt_major = P1.resb ? 1 : 0;
+    a1.out_w = P1.out_w;
+    a1.n_groups = P1.n_groups; a1.num_units = (P1.pair ? (m_tiles + 1) / 2 : m_tiles) * P1.n_groups;
+    a1.eg = P1.eg; a1.ldo = N3;
+    a1.m = h->m1; a1.b = h->b1; a1.zc = h->zc1; a1.inv_q = 1.0f; a1.zq = 0;
+    a1.gamma = ah->inv_cols;
+    a1.acc_tap = acc_tap;
+    a1.out = qkv;
+    ST_TRY(launch(P1, tm_x, h->tm_w1, tm_o, tm_o, a1, s));
+    if (qkv_tap) CUDA_TRY(cudaMemcpyAsync(qkv_tap, qkv, (size_t)T * N3, cudaMemcpyDeviceToDevice, s));
+
+    AttnArgs c = {};
+    c.qkv = qkv; c.out = aout;
+    c.n_items = (T / ah->N) * ah->d.heads;
+    c.C = C; c.heads = ah->d.heads; c.Hs = ah->d.Hs; c.Ws = ah->d.Ws; c.shift = ah->d.shift; c.nW = ah->nW;
+    c.bias = ah->bias; c.mask = ah->mask;
+    c.m3 = ah->m3; c.inv_p = ah->inv_p; c.m_o = ah->m_o; c.z_a = ah->d.a_zero_point;
+    c.p_tap = p_tap;
+    const int64_t blocks = std::max<int64_t>(
+        1, std::min<int64_t>((c.n_items + kAttnWarps - 1) / kAttnWarps, (int64_t)h->num_sms * ah->core_blocks_per_sm));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(32 * kAttnWarps);
+    cfg.dynamicSmemBytes = (size_t)ah->core_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = (pdl_enabled() && !qkv_tap) ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, ah->core, c));
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_attn_int8_run(swin_attn_int8_t h, const int8_t* xw, int64_t B, int8_t* a, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    return attn_run_impl(h, xw, B, a, workspace, workspace_bytes, stream, nullptr, nullptr, nullptr);
+}
+
+swin_mlp_status_t swin_attn_int8_run_debug(swin_attn_int8_t h, const int8_t* xw, int64_t B, int8_t* a,
+                                           void* workspace, size_t workspace_bytes, void* stream, int8_t* qkv,
+                                           int32_t* acc, int8_t* p) {
+    return attn_run_impl(h, xw, B, a, workspace, workspace_bytes, stream, qkv, acc, p);
+}
+
+swin_mlp_status_t swin_attn_int8_get_constants(swin_attn_int8_t h, float* m3_invp_mo, float* bias) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    if (m3_invp_mo) { m3_invp_mo[0] = h->m3; m3_invp_mo[1] = h->inv_p; m3_invp_mo[2] = h->m_o; }
+    if (bias) std::memcpy(bias, h->hbias.data(), h->hbias.size() * sizeof(float));
+    return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_attn_int8_destroy(swin_attn_int8_t h) {
+    if (!h) return SWIN_MLP_OK;
+    DeviceGuard guard(h->m.device);
+    delete h;
+    return SWIN_MLP_OK;
+}
 
 }  // extern "C"

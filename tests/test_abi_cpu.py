@@ -22,9 +22,13 @@ def P():
 
 
 def _declared():
-    src = open(os.path.join(ROOT, "include", "swin_mlp_int8.h")).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(swin_(?:mlp|proj)_int8_[a-z_]+)\s*\(", src)))
+    names = set()
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        if h.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", h)).read()
+            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+            names |= set(re.findall(r"\b(swin_(?:mlp|proj|op1|attn)_int8_[a-z_]+)\s*\(", src))
+    return sorted(names)
 
 
 def test_exports_every_declared_symbol(P):
@@ -54,6 +58,10 @@ def test_sm100a_code_only():
         name = f.split()[0]
         if "op5_unfused_kernel" in name:   # the unfused plan's elementwise op #5 (NEXT-1)
             assert "LDG" in f and "STG" in f and "F2I" in f, name
+        elif "op1_kernel" in name:         # op #1: HBM-bound LayerNorm + gather + Q (NEXT-4)
+            assert "LDG" in f and "STG" in f and "SHFL" in f, name
+        elif "attn_core_kernel" in name:   # op #3 core: warp mma.sync (IMMA) on 49 / 144-token windows
+            assert "IMMA" in f and "MUFU.EX2" in f and "LDS" in f, name
         elif "mlp_gemm_kernelILi3E" in name:   # EP_ACC: FC1 storing int32 A1 from registers
             assert "UTCIMMA" in f and "LDTM" in f and "STG" in f, name
         else:
@@ -168,3 +176,24 @@ def test_no_cpu_fallback_in_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 s = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in s and "from oracle" not in s and "oracle_mlp" not in s, f
+
+
+def test_attn_null_handle_paths(P):
+    """NEXT-3 / NEXT-4 entry points: NULL handles and invalid descriptions fail before any launch."""
+    L = P.lib()
+    assert L.swin_op1_int8_run(None, None, 1, None, None) == P.SWIN_MLP_EINVAL
+    assert "NULL handle" in P.last_error()
+    assert L.swin_op1_int8_destroy(None) == P.SWIN_MLP_OK
+    assert L.swin_attn_int8_run(None, None, 1, None, None, 0, None) == P.SWIN_MLP_EINVAL
+    assert L.swin_attn_int8_workspace_bytes(None, 4) == 0
+    assert L.swin_attn_int8_get_constants(None, None, None) == P.SWIN_MLP_EINVAL
+    assert L.swin_attn_int8_destroy(None) == P.SWIN_MLP_OK
+    d = P.swin_op1_int8_desc_t()
+    d.C, d.M, d.shift, d.Hs, d.Ws, d.ln_eps, d.y_scale = 96, 7, 7, 14, 14, 1e-5, 0.04
+    h = ctypes.c_void_p()
+    assert L.swin_op1_int8_create(ctypes.byref(d), ctypes.byref(h)) == P.SWIN_MLP_EINVAL
+    assert "shift" in P.last_error()
+    a = P.swin_attn_int8_desc_t()
+    a.C, a.heads, a.M, a.Hs, a.Ws = 96, 2, 7, 14, 14
+    assert L.swin_attn_int8_create(ctypes.byref(a), ctypes.byref(h)) == P.SWIN_MLP_EINVAL
+    assert "heads" in P.last_error()
