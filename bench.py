@@ -141,6 +141,35 @@ def cpu_oracle_rate(spec, stride, offset=0, nthreads=0):
     return tok / t_total, tok, t_total, nthreads
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_per_c_table():
+    """SURVEY.md §8(d) oracle timing: tokens/s of the oracle as it stands per distinct C, on 2048
+    rows with every host core and on 128 rows with one thread (cost is linear in T)."""
+    import numpy as np
+    import oracle
+    import synth
+    out = []
+    for C in (96, 192, 384, 768):
+        L = synth.make_layer(C, synth.layer_seed(2, 0, 0) + C)
+        X = synth.make_activations(L, 2048, 5)
+        row = {"C": C}
+        for key, n, nth in (("all_cores", 2048, os.cpu_count()), ("one_thread", 128, 1)):
+            t0 = time.perf_counter()
+            oracle.mlp(L, X, rows=np.arange(n, dtype=np.int64), nthreads=nth)
+            row[key + "_tokens_per_s"] = n / (time.perf_counter() - t0)
+        out.append(row)
+    return out
+
+
 def run_reference(args, ws, rank):
     """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
     if rank != 0:
@@ -417,6 +446,13 @@ def main():
         sharded = [sharded_stack(cfg, ws, rank, dev, max(3, min(args.steps, 10)), barrier, max_over_ranks)
                    for cfg in (3, 4)]
         torch.cuda.empty_cache()
+    # ---- NEXT-3 / NEXT-4 rows: op #1, QKV GEMM + op #2, window-attention core at the
+    # Swin-T b64 stage shapes (the attention half of the same blocks) ---------------------------------
+    attn_half = None
+    if rank == 0 and not args.no_stack:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import attn_bench
+        attn_half = attn_bench.run("swin_t", max(5, min(args.steps, 20)))
     # ---- BASELINE configs[0]: one 7x7 window of the Swin-T stage-4 MLP (T = 49), latency ------------
     cfg1 = None
     if rank == 0 and not args.no_stack:
@@ -427,7 +463,8 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu:
         rate, tok, t, nth = cpu_oracle_rate(layers_spec(args.batch, synth.ACT_RELU), args.cpu_stride)
         cpu = {"value": rate, "unit": "tokens/s", "cores": nth, "kind": "oracle",
-               "sample": f"every {args.cpu_stride}th token of each of the 4 layers ({tok} tokens, {t:.1f} s)"}
+               "sample": f"every {args.cpu_stride}th token of each of the 4 layers ({tok} tokens, {t:.1f} s)",
+               "cpu_model": cpu_model(), "per_C": oracle_per_c_table()}
 
     plans = [l.plan(T) for (_, T, _), l in zip(spec, relu_layers)]
     if rank == 0:
@@ -446,6 +483,7 @@ def main():
                 "north_star_stack": stack,
                 "sharded_fixed_batch": sharded,
                 "proj_op4": proj,
+                "attention_half": attn_half,
                 "config0_window": cfg1,
                 "tensor_frac_of_step": roofline["step_frac"],
                 "clocks": sampler.result()}

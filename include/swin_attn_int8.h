@@ -22,11 +22,12 @@
  *              (the oracle's statistics are in double: Y within 1 LSB on <= 0.01 %)
  *   op #2      y = fmaf(fl(A), fl(s_x * s_w[n]), b[n] or 0); qkv = clamp(rne(fl(y * fl(1/s))), -128, 127),
  *              s = q_scale / k_scale / v_scale for the three C-column thirds (zero point 0)
- *   op #3      l = fl(fl(fl(S) * m3) + B[h][i][j]) (+ mask, one more rounding), m3 =
- *              fl(fl(q_scale * k_scale) * fl(1/sqrt(32))); B from the (2M-1)^2 x heads table by
- *              the relative (row, col) displacement; mask 0 / -100 across the shifted regions
- *              (shift > 0 only); p = softmax_j(l) (fp32 on the GPU, ex2 of the max-shifted
- *              logits); Pq = clamp(rne(fl(p * 127)), -128, 127)   (s_p = 1/127)
+ *   op #3      l = S * m3 + B[h][i][j] (+ mask), m3 = fl(fl(q_scale * k_scale) * fl(1/sqrt(32)));
+ *              B from the (2M-1)^2 x heads table by the relative (row, col) displacement; mask
+ *              0 / -100 across the shifted regions (shift > 0 only); p = softmax_j(l);
+ *              Pq = clamp(rne(p * 127), 0, 127)   (s_p = 1/127).  The oracle rounds each step in
+ *              fp32 and takes the softmax in double; the GPU uses one fma for l, ex2 of the
+ *              max-shifted logits and one product e * fl(127 / sum): Pq within 1 LSB on <= 0.01 %
  *   V.att      a = clamp(rne(fl(fl(O) * m_o)) + z_a, -128, 127), O = sum_j Pq v (int32 exact),
  *              m_o = fl(fl(fl(1/127) * v_scale) * fl(1/a_scale))
  * Layout: x fp32 [B][Hs][Ws][C]; window-ordered and raster tensors [B*Hs*Ws][C] (int8);
@@ -90,7 +91,7 @@ swin_mlp_status_t swin_attn_int8_create(const swin_attn_int8_desc_t* desc, swin_
 /* Device workspace bytes for a run of B images: qkv [B*Hs*Ws][3C] int8 (128-byte aligned). */
 size_t swin_attn_int8_workspace_bytes(swin_attn_int8_t h, int64_t B);
 /*   xw  [B*Hs*Ws][C] int8, device, 16-byte aligned, window order (op #1's output)
- *   a   [B*Hs*Ws][C] int8, device, 2-byte aligned, RASTER order (the Proj GEMM input)
+ *   a   [B*Hs*Ws][C] int8, device, 16-byte aligned, RASTER order (the Proj GEMM input)
  * Two launches (QKV GEMM + op #2, then the attention core), PDL-chained, asynchronous. */
 swin_mlp_status_t swin_attn_int8_run(swin_attn_int8_t h, const int8_t* xw, int64_t B, int8_t* a, void* workspace,
                                      size_t workspace_bytes, void* stream);
@@ -101,6 +102,11 @@ swin_mlp_status_t swin_attn_int8_run_debug(swin_attn_int8_t h, const int8_t* xw,
                                            int32_t* acc, int8_t* p);
 /* Folded constants (host): {m3, inv_p, m_o} and the expanded bias [heads][N][N] (may be NULL). */
 swin_mlp_status_t swin_attn_int8_get_constants(swin_attn_int8_t h, float* m3_invp_mo, float* bias);
+/* Native per-kernel timing (bench / tools): CUDA events around the QKV GEMM and the attention
+ * core of the next max_runs runs on their launching stream; _end synchronizes on the events and
+ * returns the summed milliseconds of each kernel.  Host-only; EINVAL on a NULL handle. */
+swin_mlp_status_t swin_attn_int8_profile_begin(swin_attn_int8_t h, int32_t max_runs);
+swin_mlp_status_t swin_attn_int8_profile_end(swin_attn_int8_t h, float* qkv_ms, float* core_ms, int32_t* runs);
 swin_mlp_status_t swin_attn_int8_destroy(swin_attn_int8_t h);
 
 #ifdef __cplusplus

@@ -35,7 +35,8 @@ EXPORTS = [
     "swin_mlp_int8_host_batch_workspace_bytes", "swin_mlp_int8_run_host_batch",
     "swin_op1_int8_create", "swin_op1_int8_run", "swin_op1_int8_destroy",
     "swin_attn_int8_create", "swin_attn_int8_workspace_bytes", "swin_attn_int8_run", "swin_attn_int8_run_debug",
-    "swin_attn_int8_get_constants", "swin_attn_int8_destroy",
+    "swin_attn_int8_get_constants", "swin_attn_int8_profile_begin", "swin_attn_int8_profile_end",
+    "swin_attn_int8_destroy",
     "swin_proj_int8_create", "swin_proj_int8_run", "swin_proj_int8_run_debug", "swin_proj_int8_plan",
     "swin_proj_int8_destroy",
 ]
@@ -166,6 +167,10 @@ def lib():
     L.swin_attn_int8_run_debug.restype = i32
     L.swin_attn_int8_get_constants.argtypes = [P, P, P]
     L.swin_attn_int8_get_constants.restype = i32
+    L.swin_attn_int8_profile_begin.argtypes = [P, i32]
+    L.swin_attn_int8_profile_begin.restype = i32
+    L.swin_attn_int8_profile_end.argtypes = [P, P, P, P]
+    L.swin_attn_int8_profile_end.restype = i32
     L.swin_attn_int8_destroy.argtypes = [P]
     L.swin_attn_int8_destroy.restype = i32
     L.swin_mlp_int8_last_error.argtypes = []
@@ -608,6 +613,15 @@ class SwinAttnInt8Layer:
         stream = ctypes.c_void_p(torch.cuda.current_stream(xw.device).cuda_stream)
         swin_attn_int8_run(self.handle, _ptr(xw), B, _ptr(a), _ptr(ws), ws.numel(), stream)
         return a
+
+    def profile_begin(self, max_runs):
+        _check(lib().swin_attn_int8_profile_begin(self.handle, int(max_runs)))
+
+    def profile_end(self):
+        """(qkv_gemm_ms_total, core_ms_total, runs) of the runs recorded since profile_begin."""
+        a, b, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
+        _check(lib().swin_attn_int8_profile_end(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
+        return a.value, b.value, n.value
 
     def run_debug(self, xw, B):
         torch = self._torch

@@ -1452,7 +1452,7 @@ int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20) {
 // NEXT-4: fused op #1 (LayerNorm -> window shift -> Q), Fig. 1 lines 39-43.
 struct swin_op1_int8_s {
     swin_op1_int8_desc_t d;
-    int device = 0, num_sms = 0, blocks_per_sm = 1, U = 1;
+    int device = 0, num_sms = 0, blocks_per_sm = 1, U = 1, L = 32;
     void (*fn)(Op1Args) = nullptr;
     float* gamma = nullptr;
     float* beta = nullptr;
@@ -1500,17 +1500,21 @@ swin_mlp_status_t swin_op1_int8_create(const swin_op1_int8_desc_t* desc, swin_op
         h->inv_s = one / d.y_scale;
     }
     if (!normal_positive(h->inv_s)) return bail(fail(SWIN_MLP_EINVAL, "1/y_scale not normal"));
-    // float4 per lane (C <= 128 VPL) and rows in flight per warp (~8 float4 loads per lane)
-    const int vpl = (d.C + 127) / 128;
-    switch (vpl) {
-        case 1: h->fn = op1_kernel<1, 8>; h->U = 8; break;
-        case 2: h->fn = op1_kernel<2, 4>; h->U = 4; break;
-        case 3: h->fn = op1_kernel<3, 2>; h->U = 2; break;
-        case 4: h->fn = op1_kernel<4, 2>; h->U = 2; break;
-        case 5: case 6: h->fn = op1_kernel<6, 1>; h->U = 1; break;
-        case 7: case 8: h->fn = op1_kernel<8, 1>; h->U = 1; break;
-        default: h->fn = op1_kernel<12, 1>; h->U = 1; break;
+    // a row on L lanes (8, 16 or 32: 32 / L rows per warp instruction), VPL float4 per lane, U row
+    // groups per warp in flight (~8 float4 loads per lane)
+    const int c4 = d.C / 4;
+    const int L = c4 <= 32 ? 8 : c4 <= 64 ? 16 : 32;
+    const int vpl = (c4 + L - 1) / L;
+#define OP1(LL, V, UU) do { h->fn = op1_kernel<LL, V, UU>; h->U = UU; h->L = LL; } while (0)
+    if (L == 8) {
+        if (vpl == 1) OP1(8, 1, 8); else if (vpl == 2) OP1(8, 2, 4); else if (vpl == 3) OP1(8, 3, 2); else OP1(8, 4, 2);
+    } else if (L == 16) {
+        if (vpl == 3) OP1(16, 3, 2); else OP1(16, 4, 2);   // (c4 in 33..64)
+    } else {
+        if (vpl <= 3) OP1(32, 3, 2); else if (vpl == 4) OP1(32, 4, 2); else if (vpl <= 6) OP1(32, 6, 1);
+        else if (vpl <= 8) OP1(32, 8, 1); else OP1(32, 12, 1);
     }
+#undef OP1
     cudaError_t e = cudaMalloc(&h->gamma, sizeof(float) * d.C);
     if (e == cudaSuccess) e = cudaMalloc(&h->beta, sizeof(float) * d.C);
     if (e == cudaSuccess) e = cudaMemcpy(h->gamma, g.data(), sizeof(float) * d.C, cudaMemcpyHostToDevice);
@@ -1530,13 +1534,18 @@ swin_mlp_status_t swin_op1_int8_run(swin_op1_int8_t h, const float* x, int64_t B
     if ((reinterpret_cast<uintptr_t>(x) & 15u) || (reinterpret_cast<uintptr_t>(y) & 3u))
         return fail(SWIN_MLP_EINVAL, "x must be 16-byte and y 4-byte aligned");
     const int64_t rows = B * (int64_t)h->d.Hs * h->d.Ws;
-    if (rows > ((int64_t)1 << 40)) return fail(SWIN_MLP_EUNSUPPORTED, "B=%lld too large", (long long)B);
+    if (rows >= ((int64_t)1 << 31)) return fail(SWIN_MLP_EUNSUPPORTED, "B=%lld too large", (long long)B);
     DeviceGuard guard(h->device);
     Op1Args a = {};
     a.x = x; a.y = y; a.rows = rows;
     a.C = h->d.C; a.Hs = h->d.Hs; a.Ws = h->d.Ws; a.M = h->d.M; a.shift = h->d.shift;
     a.gamma = h->gamma; a.beta = h->beta; a.eps = h->d.ln_eps; a.inv_s = h->inv_s; a.z = h->d.y_zero_point;
-    const int64_t warps = (rows + h->U - 1) / h->U;
+    a.divN = make_fastdiv((uint32_t)(h->d.M * h->d.M));
+    a.divNW = make_fastdiv((uint32_t)((h->d.Hs / h->d.M) * (h->d.Ws / h->d.M)));
+    a.divNWx = make_fastdiv((uint32_t)(h->d.Ws / h->d.M));
+    a.divM = make_fastdiv((uint32_t)h->d.M);
+    const int64_t per_warp = (int64_t)h->U * (32 / h->L);
+    const int64_t warps = (rows + per_warp - 1) / per_warp;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)h->num_sms * h->blocks_per_sm));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
@@ -1566,11 +1575,10 @@ struct swin_attn_int8_s {
     swin_mlp_int8_s m;          // the QKV GEMM: p1 / tm_w1 / w1 (Wqkv) / m1 / b1 / zc1, map cache
     swin_attn_int8_desc_t d;
     float* inv_cols = nullptr;  // [3C] fl(1/s_q | 1/s_k | 1/s_v) per column
-    float* bias = nullptr;      // [heads][N][N]
-    float* mask = nullptr;      // [nW][N][N] or nullptr (shift == 0)
-    std::vector<float> hbias;
+    float* bias = nullptr;      // [heads][MT*16][NT*8] padded (-inf at columns >= N, 0 at rows >= N)
+    std::vector<float> hbias;   // [heads][N][N] (get_constants)
     float m3 = 0.f, inv_p = 0.f, m_o = 0.f;
-    int N = 0, nW = 0, core_smem = 0, core_blocks_per_sm = 1;
+    int N = 0, nW = 0, core_smem = 0, core_blocks_per_sm = 1, qrows = 0, np = 0;
     void (*core)(AttnArgs) = nullptr;
 };
 
@@ -1674,22 +1682,16 @@ swin_mlp_status_t swin_attn_int8_create(const swin_attn_int8_desc_t* desc, swin_
                 const int dy = i / M - j / M + M - 1, dx = i % M - j % M + M - 1;
                 ah->hbias[((size_t)hh * N + i) * N + j] = table[(size_t)(dy * (2 * M - 1) + dx) * heads + hh];
             }
-    std::vector<float> hmask;
-    if (d.shift > 0) {
-        hmask.assign((size_t)nW * N * N, 0.0f);
-        const int nWx = d.Ws / M;
-        std::vector<int> reg(N);
-        for (int wv = 0; wv < nW; ++wv) {
-            for (int p = 0; p < N; ++p) {
-                const int y = (wv / nWx) * M + p / M, x = (wv % nWx) * M + p % M;
-                const int ry = y < d.Hs - M ? 0 : y < d.Hs - d.shift ? 1 : 2;
-                const int rx = x < d.Ws - M ? 0 : x < d.Ws - d.shift ? 1 : 2;
-                reg[p] = ry * 3 + rx;
-            }
-            for (int i = 0; i < N; ++i)
-                for (int j = 0; j < N; ++j) hmask[((size_t)wv * N + i) * N + j] = reg[i] == reg[j] ? 0.0f : -100.0f;
-        }
-    }
+    // the kernel's padded tile per head: [MT*16][NT*8], -inf beyond column N (those logits vanish
+    // in the softmax), 0 on the padding rows (finite, discarded)
+    ah->qrows = M == 7 ? AttnGeom<7>::QROWS : AttnGeom<12>::QROWS;
+    ah->np = M == 7 ? AttnGeom<7>::NP : AttnGeom<12>::NP;
+    std::vector<float> pbias((size_t)heads * ah->qrows * ah->np, 0.0f);
+    for (int hh = 0; hh < heads; ++hh)
+        for (int i = 0; i < ah->qrows; ++i)
+            for (int j = 0; j < ah->np; ++j)
+                pbias[((size_t)hh * ah->qrows + i) * ah->np + j] =
+                    j >= N ? -INFINITY : i >= N ? 0.0f : ah->hbias[((size_t)hh * N + i) * N + j];
     // QKV GEMM plan (op #2 epilogue)
     if (!make_plan(EP2_QKV, N3, C, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no QKV GEMM plan for C=%d", C));
     swin_mlp_status_t st;
@@ -1702,8 +1704,7 @@ swin_mlp_status_t swin_attn_int8_create(const swin_attn_int8_desc_t* desc, swin_
     A_TRY(upload(h, inv, &ah->inv_cols));   // (device copies are owned by h->allocs)
     if (d.b_qkv) A_TRY(upload(h, b, &h->b1));
     if (d.x_zero_point) A_TRY(upload(h, zc, &h->zc1));
-    A_TRY(upload(h, ah->hbias, &ah->bias));
-    if (d.shift > 0) A_TRY(upload(h, hmask, &ah->mask));
+    A_TRY(upload(h, pbias, &ah->bias));
     A_TRY(encode_2d(&h->tm_w1, h->w1, N3, C, C, (uint32_t)(h->p1.pair ? h->p1.BN / 2 : h->p1.BN)));
     const bool small_k = (int64_t)(128 + std::abs(d.x_zero_point)) * rowabs < (int64_t(1) << 22);
     h->p1.fn = kernel_for(EP2_QKV, (d.b_qkv ? kHasB : 0) | (d.x_zero_point ? kHasZc : 0) | (small_k ? kSmallK : 0) |
@@ -1711,7 +1712,7 @@ swin_mlp_status_t swin_attn_int8_create(const swin_attn_int8_desc_t* desc, swin_
     A_TRY(prepare(h->p1, h->num_sms));
     // attention core: one warp per (window, head), kAttnWarps warps per CTA
     ah->core = M == 7 ? attn_core_kernel<7> : attn_core_kernel<12>;
-    ah->core_smem = kAttnWarps * (M == 7 ? AttnGeom<7>::BYTES : AttnGeom<12>::BYTES);
+    ah->core_smem = M == 7 ? AttnGeom<7>::SMEM : AttnGeom<12>::SMEM;
     CUDA_TRY(cudaFuncSetAttribute(ah->core, cudaFuncAttributeMaxDynamicSharedMemorySize, ah->core_smem));
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ah->core_blocks_per_sm, ah->core, 32 * kAttnWarps,
                                                            ah->core_smem));
@@ -1739,8 +1740,8 @@ static swin_mlp_status_t attn_run_impl(swin_attn_int8_t ah, const int8_t* xw, in
     const size_t need = swin_attn_int8_workspace_bytes(ah, B);
     if (!xw || !aout || !workspace) return fail(SWIN_MLP_EINVAL, "xw, a and workspace are required");
     if (ws_bytes < need) return fail(SWIN_MLP_EINVAL, "workspace %zu < %zu bytes", ws_bytes, need);
-    if (!aligned16(xw) || (reinterpret_cast<uintptr_t>(aout) & 1u) || (reinterpret_cast<uintptr_t>(workspace) & 127u))
-        return fail(SWIN_MLP_EINVAL, "xw 16-byte, a 2-byte and workspace 128-byte aligned");
+    if (!aligned16(xw) || !aligned16(aout) || (reinterpret_cast<uintptr_t>(workspace) & 127u))
+        return fail(SWIN_MLP_EINVAL, "xw and a 16-byte, workspace 128-byte aligned");
     DeviceGuard guard(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int8_t* qkv = static_cast<int8_t*>(workspace);
@@ -1763,18 +1764,26 @@ static swin_mlp_status_t attn_run_impl(swin_attn_int8_t ah, const int8_t* xw, in
     a1.gamma = ah->inv_cols;
     a1.acc_tap = acc_tap;
     a1.out = qkv;
+    cudaEvent_t* ev = nullptr;
+    if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
     ST_TRY(launch(P1, tm_x, h->tm_w1, tm_o, tm_o, a1, s));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
     if (qkv_tap) CUDA_TRY(cudaMemcpyAsync(qkv_tap, qkv, (size_t)T * N3, cudaMemcpyDeviceToDevice, s));
 
     AttnArgs c = {};
     c.qkv = qkv; c.out = aout;
-    c.n_items = (T / ah->N) * ah->d.heads;
+    c.n_win = T / ah->N;
     c.C = C; c.heads = ah->d.heads; c.Hs = ah->d.Hs; c.Ws = ah->d.Ws; c.shift = ah->d.shift; c.nW = ah->nW;
-    c.bias = ah->bias; c.mask = ah->mask;
+    c.bias = ah->bias;
     c.m3 = ah->m3; c.inv_p = ah->inv_p; c.m_o = ah->m_o; c.z_a = ah->d.a_zero_point;
     c.p_tap = p_tap;
-    const int64_t blocks = std::max<int64_t>(
-        1, std::min<int64_t>((c.n_items + kAttnWarps - 1) / kAttnWarps, (int64_t)h->num_sms * ah->core_blocks_per_sm));
+    // CTAs come in groups of `heads` (CTA c serves head c % heads): as many groups as the windows
+    // need (kAttnWarps per CTA) or as fit resident
+    const int64_t groups = std::max<int64_t>(
+        1, std::min<int64_t>((c.n_win + kAttnWarps - 1) / kAttnWarps,
+                             std::max<int64_t>(1, (int64_t)h->num_sms * ah->core_blocks_per_sm / ah->d.heads)));
+    const int64_t blocks = groups * ah->d.heads;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(32 * kAttnWarps);
@@ -1786,7 +1795,18 @@ static swin_mlp_status_t attn_run_impl(swin_attn_int8_t ah, const int8_t* xw, in
     cfg.attrs = at;
     cfg.numAttrs = 1;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, ah->core, c));
+    if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
     return SWIN_MLP_OK;
+}
+
+swin_mlp_status_t swin_attn_int8_profile_begin(swin_attn_int8_t h, int32_t max_runs) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    return swin_mlp_int8_profile_begin(&h->m, max_runs);
+}
+
+swin_mlp_status_t swin_attn_int8_profile_end(swin_attn_int8_t h, float* qkv_ms, float* core_ms, int32_t* runs) {
+    if (!h) return fail(SWIN_MLP_EINVAL, "NULL handle");
+    return swin_mlp_int8_profile_end(&h->m, qkv_ms, core_ms, runs);
 }
 
 swin_mlp_status_t swin_attn_int8_run(swin_attn_int8_t h, const int8_t* xw, int64_t B, int8_t* a, void* workspace,
