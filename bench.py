@@ -229,6 +229,7 @@ def main():
     spec = layers_spec(args.batch, synth.ACT_RELU)
     relu_layers, gelu_layers, xs_dev, xs_host, ys, T_list = [], [], [], [], [], []
     ft_gelu_layers, ft_relu_layers = [], []   # FasterTransformer layout: op #5 unfused (NEXT-1)
+    sg_layers = []   # the I-ViT shift-GELU control (NEXT-4; always unfused: it needs each row's max)
     for li, (L, T, xseed) in enumerate(spec):
         if ws > 1:
             broadcast_layer(L, dev)   # create() copies from the device tensors
@@ -237,6 +238,8 @@ def main():
         L.act = synth.ACT_GELU
         gelu_layers.append(SwinMlpInt8Layer(L, device=local))
         ft_gelu_layers.append(SwinMlpInt8Layer(L, device=local, op5_unfused=True))
+        L.act = synth.ACT_SHIFT_GELU
+        sg_layers.append(SwinMlpInt8Layer(L, device=local))
         L.act = synth.ACT_RELU
         X = synth.make_activations(L, T, xseed + 7919 * rank)
         xh = torch.from_numpy(X).pin_memory()
@@ -399,7 +402,10 @@ def main():
     #   gelu_ft  the paper's baseline layout: FC1 -> A1 int32 in HBM -> separate dQ/GELU/Q kernel
     #            -> FC2 (FasterTransformer)
     #   relu_ft  the same unfused layout with ReLU (separates the fusion gain from the activation)
-    arms = {"relu": relu_layers, "gelu": gelu_layers, "gelu_ft": ft_gelu_layers, "relu_ft": ft_relu_layers}
+    #   shift_gelu the I-ViT integer shift-GELU (the paper's other comparison):
+    #            FC1 -> A1 -> the row-max op #5 kernel -> FC2 (R28)
+    arms = {"relu": relu_layers, "gelu": gelu_layers, "gelu_ft": ft_gelu_layers, "relu_ft": ft_relu_layers,
+            "shift_gelu": sg_layers}
     for layers in arms.values():
         for _ in range(3):
             step(layers)
@@ -408,7 +414,7 @@ def main():
     names = list(arms)
     for i in range(args.pairs):
         res = {}
-        for k in names[i % 4:] + names[:i % 4]:
+        for k in names[i % len(names):] + names[:i % len(names)]:
             res[k] = 1e3 * timed(lambda: step(arms[k]), 1)[0]
         for k in names:
             samples[k].append(res[k])
@@ -417,6 +423,8 @@ def main():
     relu_gelu = {"relu_us_median": med["relu"], "gelu_us_median": med["gelu"],
                  "gelu_over_relu": med["gelu"] / med["relu"],
                  "gelu_ft_us_median": med["gelu_ft"], "relu_ft_us_median": med["relu_ft"],
+                 "shift_gelu_us_median": med["shift_gelu"],
+                 "latency_gain_vs_shift_gelu": 1.0 - med["relu"] / med["shift_gelu"],
                  "latency_gain_vs_ft_gelu": 1.0 - med["relu"] / med["gelu_ft"],
                  "latency_gain_vs_fused_gelu": 1.0 - med["relu"] / med["gelu"],
                  "paper_context": "RTX 4090, whole Swin model: >= 11% latency gain from GELU->ReLU (PAPER.md:13)",

@@ -59,7 +59,10 @@ typedef enum {
 
 typedef enum {
     SWIN_MLP_ACT_RELU = 0,      /* the paper's GELU-less block             */
-    SWIN_MLP_ACT_GELU_ERF = 1   /* control: exact erf GELU, 0.5*y*(1+erf(y/sqrt 2))       */
+    SWIN_MLP_ACT_GELU_ERF = 1,  /* control: exact erf GELU, 0.5*y*(1+erf(y/sqrt 2))       */
+    SWIN_MLP_ACT_SHIFT_GELU = 2 /* control: I-ViT's integer shift-GELU (R28), which needs
+                                 * the max of each token's FC1 row before any output: always
+                                 * the unfused plan (FC1 -> A1 -> row-max op #5 kernel -> FC2) */
 } swin_mlp_act_t;
 
 /* Layer description passed to swin_mlp_int8_create.  All pointers may be
@@ -98,6 +101,17 @@ typedef struct {
                                  *    to measure on B200 what fusing / deleting op #5 saves.  Uses
                                  *    the three-kernel plan for every C (the workspace grows by
                                  *    4*T*H bytes for A1). */
+    float gelu_in_scale;        /* act == SWIN_MLP_ACT_SHIFT_GELU only: s_g, the 16-bit integer grid
+                                 * of the shift-GELU input (I = clamp(rne(fl(y * fl(1/s_g))),
+                                 * +-32767)); finite, normal, > 0.  Ignored otherwise.  The
+                                 * control's arithmetic (reading R28):
+                                 *   Im = max_n I[t][n];  e = ShiftExp(I - Im), e_m = ShiftExp(min(-Im, 0))
+                                 *   sig = floor(e * floor((2^31-1) / min(e + e_m, 2^31-1)) / 2^24)
+                                 *   Hq = clamp(rne(fl(fl(I * sig) * fl(fl(s_g * inv_h) * 2^-7))) + z_h)
+                                 * ShiftExp(x <= 0): S = fl(1.702 s_g), x0 = floor(-1/S) (double),
+                                 *   p = max(x + floor(x/2) - floor(x/16), 15 x0), q = floor(p / x0),
+                                 *   e = max(floor((p - q x0 - 2 x0) * 2^(14 - q)), 0)
+                                 * (integer throughout: Hq bit-exact with the oracle). */
 } swin_mlp_int8_desc_t;
 
 /* Create a layer handle: validates the description, folds the fp32

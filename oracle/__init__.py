@@ -25,6 +25,7 @@ from . import build as _build
 
 ACT_RELU = 0
 ACT_GELU = 1
+ACT_SHIFT_GELU = 2
 
 _lib = None
 
@@ -44,6 +45,8 @@ def lib():
         L.oracle_ep5.restype = None
         L.oracle_ep6.argtypes = [P, i64, i32, P, P, P, P, f32, i32, P, P, f32, f32, i32, P, P, P]
         L.oracle_ep6.restype = None
+        L.oracle_ep5_shiftgelu.argtypes = [P, i64, i32, P, P, f32, f32, i32, P, P]
+        L.oracle_ep5_shiftgelu.restype = None
         L.oracle_mlp.argtypes = [P, P, P, P, i64, i32, P, P, P, P, P, P]
         L.oracle_mlp.restype = i32
         L.oracle_max_threads.restype = i32
@@ -135,6 +138,16 @@ def ep5(A1, m1, b1, inv_h, z_h, act=ACT_RELU, return_pre=False):
     return (Hq, pre) if return_pre else Hq
 
 
+def ep5_shiftgelu(A1, m1, b1, s_g, inv_h, z_h, return_I=False):
+    """O2'': the I-ViT shift-GELU control (R28): Hq from A1 with the per-row max."""
+    A1 = _c(A1, np.int32); m1 = _c(m1, np.float32); b1 = _c(b1, np.float32)
+    T, H = A1.shape
+    Hq = np.empty((T, H), np.int8)
+    I = np.empty((T, H), np.int32) if return_I else None
+    lib().oracle_ep5_shiftgelu(_p(A1), T, H, _p(m1), _p(b1), float(s_g), float(inv_h), int(z_h), _p(Hq), _p(I))
+    return (Hq, I) if return_I else Hq
+
+
 def ep6(A2, m2, b2, X, s_x, z_x, gamma, beta, eps, inv_y, z_y, R=None):
     """O4-O6: returns (Y int8, yhat fp32, z fp32)."""
     A2 = _c(A2, np.int32); m2 = _c(m2, np.float32); b2 = _c(b2, np.float32)
@@ -169,7 +182,7 @@ class _Layer(ctypes.Structure):
                 ("s_h", ctypes.c_float), ("z_h", ctypes.c_int32),
                 ("w2", ctypes.c_void_p), ("s_w2", ctypes.c_void_p), ("b2", ctypes.c_void_p),
                 ("gamma", ctypes.c_void_p), ("beta", ctypes.c_void_p), ("eps", ctypes.c_float),
-                ("s_y", ctypes.c_float), ("z_y", ctypes.c_int32)]
+                ("s_y", ctypes.c_float), ("z_y", ctypes.c_int32), ("s_g", ctypes.c_float)]
 
 
 def mlp(layer, X, R=None, rows=None, nthreads=0, taps=False):
@@ -191,7 +204,7 @@ def mlp(layer, X, R=None, rows=None, nthreads=0, taps=False):
     g = arr(layer.gamma, np.float32); bt = arr(layer.beta, np.float32)
     L = _Layer(C, H, int(layer.act), float(layer.s_x), int(layer.z_x), _p(w1), _p(s_w1), _p(b1),
                float(layer.s_h), int(layer.z_h), _p(w2), _p(s_w2), _p(b2), _p(g), _p(bt),
-               float(layer.eps), float(layer.s_y), int(layer.z_y))
+               float(layer.eps), float(layer.s_y), int(layer.z_y), float(getattr(layer, "s_g", 0.0) or 0.0))
     X = arr(X, np.int8); R = arr(R, np.float32)
     assert X.shape[1] == C
     r = None if rows is None else arr(rows, np.int64)

@@ -154,6 +154,76 @@ void oracle_ep5(const int32_t* A1, int64_t nrows, int32_t H, const float* m1,
 }
 
 /* ------------------------------------------------------------------ */
+/* O2'': the I-ViT shift-GELU control of SURVEY.md §8(f) NEXT-4 (the integer GELU the paper
+ * contrasts ReLU with: "needs to compute the maximum value of the input tensor",
+ * PAPER.md:182-186, 246).  The paper gives no formula; this follows I-ViT's ShiftGELU as read
+ * in DESIGN.md reading R28, every step integer except the two quantizer products:
+ *   y  = fmaf(fl(A1), m1[n], b1[n] or 0)                     dQ + bias, as op #5
+ *   I  = clamp(rne(fl(y * inv_g)), -32767, 32767)            the 16-bit GELU input grid s_g
+ *   Im = max_n I[t][n]                                        per token row (the tensor max)
+ *   e_x = ShiftExp(I - Im),  e_m = ShiftExp(min(-Im, 0))      2^(1.702 x s_g log2 e), integer
+ *   sig = floor(e_x * floor((2^31-1) / min(e_x + e_m, 2^31-1)) / 2^24)   in [0, 128]
+ *   G  = I * sig                                              GELU on the grid s_g * 2^-7
+ *   Hq = clamp(rne(fl(fl(G) * k_g)) + z_h, -128, 127),  k_g = fl(fl(s_g * inv_h) * 2^-7)
+ * ShiftExp(x <= 0), with S = fl(1.702 * s_g), x0 = floor(-1 / S) (double), n = 15:
+ *   p = x + floor(x / 2) - floor(x / 16)            (x log2 e, by shifts)
+ *   p = max(p, n * x0);  q = floor(p / x0);  r = p - q * x0        (r in (x0, 0])
+ *   e = max(floor((r - 2 x0) * 2^(n - q - 1)), 0)                   (2^(r/x0) ~ 1 + r/(2|x0|))  */
+/* ------------------------------------------------------------------ */
+#define ORACLE_ACT_SHIFT_GELU 2
+#define SHIFT_N 15
+
+static int64_t floor_div(int64_t a, int64_t b) {   /* floor(a / b), b != 0 */
+    int64_t q = a / b, r = a % b;
+    if (r != 0 && ((r < 0) != (b < 0))) --q;
+    return q;
+}
+
+static int64_t shift_exp(int64_t x, int64_t x0) {
+    int64_t p = x + floor_div(x, 2) - floor_div(x, 16);
+    if (p < SHIFT_N * x0) p = SHIFT_N * x0;
+    const int64_t q = floor_div(p, x0);
+    const int64_t r = p - q * x0;
+    const int64_t m = r - 2 * x0;                       /* > 0 */
+    int64_t e = SHIFT_N - q - 1 >= 0 ? m << (SHIFT_N - q - 1) : floor_div(m, 2);
+    return e > 0 ? e : 0;
+}
+
+void oracle_ep5_shiftgelu(const int32_t* A1, int64_t nrows, int32_t H, const float* m1,
+                          const float* b1 /*[H] or NULL*/, float s_g, float inv_h, int32_t z_h,
+                          int8_t* Hq /*[nrows][H]*/, int32_t* I_out /*[nrows][H] or NULL*/) {
+    const float inv_g = 1.0f / s_g;
+    const float S = 1.702f * s_g;
+    const int64_t x0 = (int64_t)floor(-1.0 / (double)S);
+    const float k_g = (s_g * inv_h) * 0.0078125f;
+    int32_t* I = (int32_t*)malloc(sizeof(int32_t) * (size_t)H);
+    for (int64_t i = 0; i < nrows; ++i) {
+        int32_t Im = -32768;
+        for (int32_t n = 0; n < H; ++n) {
+            const float y = fmaf((float)A1[i * H + n], m1[n], b1 ? b1[n] : 0.0f);
+            double r = nearbyint((double)(y * inv_g));
+            if (r > 32767.0) r = 32767.0;
+            if (r < -32767.0) r = -32767.0;
+            I[n] = (int32_t)r;
+            if (I[n] > Im) Im = I[n];
+            if (I_out) I_out[i * H + n] = I[n];
+        }
+        const int64_t e_m = shift_exp(-Im < 0 ? -(int64_t)Im : 0, x0);
+        for (int32_t n = 0; n < H; ++n) {
+            const int64_t e_x = shift_exp((int64_t)I[n] - Im, x0);
+            int64_t sum = e_x + e_m;
+            if (sum > 2147483647LL) sum = 2147483647LL;
+            const int64_t factor = sum > 0 ? 2147483647LL / sum : 0;
+            const int64_t sig = (e_x * factor) >> 24;
+            const int64_t G = (int64_t)I[n] * sig;
+            const float v = (float)G * k_g;
+            Hq[i * H + n] = quant_from_scaled(v, z_h);
+        }
+    }
+    free(I);
+}
+
+/* ------------------------------------------------------------------ */
 /* O4-O6: fused op #6: dQ -> FC2 bias -> Add & LayerNorm,
  * then Q (reading R4).
  *   d = fmaf(fl(A2), m2[c], b2[c] or 0)
@@ -223,6 +293,7 @@ typedef struct {
     const int8_t* w2; const float* s_w2; const float* b2;
     const float* gamma; const float* beta; float eps;
     float s_y; int32_t z_y;
+    float s_g;   /* shift-GELU input grid (act == 2 only) */
 } oracle_layer_t;
 
 int32_t oracle_mlp(const oracle_layer_t* L, const int8_t* X /*[T][C]*/,
@@ -248,7 +319,10 @@ int32_t oracle_mlp(const oracle_layer_t* L, const int8_t* X /*[T][C]*/,
         int8_t* h = (int8_t*)malloc((size_t)H);
         int32_t* a2 = (int32_t*)malloc(sizeof(int32_t) * (size_t)C);
         status |= oracle_gemm_i8(X + t * C, C, NULL, 1, C, L->w1, H, L->z_x, a1, -1);
-        oracle_ep5(a1, 1, H, m1, L->b1, inv_h, L->z_h, L->act, h, NULL);
+        if (L->act == ORACLE_ACT_SHIFT_GELU)
+            oracle_ep5_shiftgelu(a1, 1, H, m1, L->b1, L->s_g, inv_h, L->z_h, h, NULL);
+        else
+            oracle_ep5(a1, 1, H, m1, L->b1, inv_h, L->z_h, L->act, h, NULL);
         status |= oracle_gemm_i8(h, H, NULL, 1, H, L->w2, C, L->z_h, a2, -1);
         oracle_ep6(a2, 1, C, m2, L->b2, R ? R + t * C : NULL, X + t * C, L->s_x, L->z_x,
                    L->gamma, L->beta, L->eps, inv_y, L->z_y,

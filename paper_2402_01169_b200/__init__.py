@@ -52,7 +52,7 @@ class swin_mlp_int8_desc_t(ctypes.Structure):
         ("ln_gamma", ctypes.c_void_p), ("ln_beta", ctypes.c_void_p), ("ln_eps", ctypes.c_float),
         ("y_scale", ctypes.c_float), ("y_zero_point", ctypes.c_int32),
         ("device", ctypes.c_int32), ("ln_fp64", ctypes.c_int32),
-        ("op5_unfused", ctypes.c_int32),
+        ("op5_unfused", ctypes.c_int32), ("gelu_in_scale", ctypes.c_float),
     ]
 
 
@@ -306,6 +306,7 @@ class SwinMlpInt8Layer:
         d.device = int(device)
         d.ln_fp64 = int(bool(ln_fp64))
         d.op5_unfused = int(bool(op5_unfused))   # FT-style baseline: A1 through HBM, separate op #5
+        d.gelu_in_scale = float(getattr(layer, "s_g", 0.0) or 0.0)   # shift-GELU control only
         self.C, self.H, self.device = d.C, d.H, device
         self.handle = swin_mlp_int8_create(d)
         self._keep = []

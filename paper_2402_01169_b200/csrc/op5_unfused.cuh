@@ -96,4 +96,85 @@ __global__ void __launch_bounds__(kOp5Threads) op5_unfused_kernel(const __grid_c
     }
 }
 
+// ---- the I-ViT shift-GELU control (reading R28) ------------
+// Needs the max of each token's FC1 row before any of its outputs: one
+// warp per token row, two passes over A1 (the second from L2); integer arithmetic after the
+// two fp32 quantizer products, so Hq is bit-exact with the oracle.
+struct ShiftGeluArgs {
+    const int32_t* a1;   // [T][H]
+    int8_t* hq;          // [T][H]
+    const float* m1;     // [H]
+    const float* b1;     // [H] or nullptr
+    float inv_g;         // fl(1/s_g)
+    float k_g;           // fl(fl(s_g * inv_h) * 2^-7)
+    int32_t x0;          // floor(-1 / fl(1.702 s_g)) < 0
+    int32_t z_h;
+    int32_t H;
+    int64_t T;
+};
+
+__device__ __forceinline__ int32_t sg_quant_in(int32_t a, float m, float b, float inv_g) {
+    const float y = __fmaf_rn(__int2float_rn(a), m, b);
+    return (int32_t)fminf(fmaxf(rintf(__fmul_rn(y, inv_g)), -32767.f), 32767.f);   // rne, clamp
+}
+
+// ShiftExp(x <= 0) with n = 15 (see swin_mlp_int8.h): 2^(x S log2 e) on the scale 2^15 |x0|.
+__device__ __forceinline__ int64_t sg_shift_exp(int32_t x, int32_t x0) {
+    int32_t p = x + (x >> 1) - (x >> 4);             // arithmetic shifts: floor(x/2), floor(x/16)
+    p = max(p, 15 * x0);
+    const int32_t q = p / x0;                        // p <= 0, x0 < 0: truncation == floor
+    const int32_t m = p - q * x0 - 2 * x0;           // r - 2 x0 > 0
+    const int64_t e = 14 - q >= 0 ? (int64_t)m << (14 - q) : (int64_t)(m >> 1);
+    return e > 0 ? e : 0;
+}
+
+template <bool HAS_B, bool ZH>
+__global__ void __launch_bounds__(kOp5Threads) op5_shiftgelu_kernel(const __grid_constant__ ShiftGeluArgs p) {
+    using namespace sm100;
+    pdl_wait();   // A1 is the previous kernel's output
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * kOp5Threads + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * kOp5Threads) >> 5;
+    const int H4 = p.H >> 2;
+    for (int64_t t = warp; t < p.T; t += nwarps) {
+        const int4* row = reinterpret_cast<const int4*>(p.a1 + t * p.H);
+        int32_t im = -32768;
+        for (int k = lane; k < H4; k += 32) {   // pass 1: the row max of I
+            const int4 a = __ldg(row + k);
+            const float4 mv = __ldg(reinterpret_cast<const float4*>(p.m1) + k);
+            const float4 bv = HAS_B ? __ldg(reinterpret_cast<const float4*>(p.b1) + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            im = max(im, max(max(sg_quant_in(a.x, mv.x, bv.x, p.inv_g), sg_quant_in(a.y, mv.y, bv.y, p.inv_g)),
+                             max(sg_quant_in(a.z, mv.z, bv.z, p.inv_g), sg_quant_in(a.w, mv.w, bv.w, p.inv_g))));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) im = max(im, __shfl_xor_sync(0xffffffffu, im, o));
+        const int64_t e_m = sg_shift_exp(im > 0 ? -im : 0, p.x0);
+        uint32_t* out = reinterpret_cast<uint32_t*>(p.hq + t * p.H);
+        for (int k = lane; k < H4; k += 32) {   // pass 2 (A1 from L2)
+            const int4 a = __ldg(row + k);
+            const float4 mv = __ldg(reinterpret_cast<const float4*>(p.m1) + k);
+            const float4 bv = HAS_B ? __ldg(reinterpret_cast<const float4*>(p.b1) + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int32_t I[4] = {sg_quant_in(a.x, mv.x, bv.x, p.inv_g), sg_quant_in(a.y, mv.y, bv.y, p.inv_g),
+                                  sg_quant_in(a.z, mv.z, bv.z, p.inv_g), sg_quant_in(a.w, mv.w, bv.w, p.inv_g)};
+            int32_t qv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t e_x = sg_shift_exp(I[j] - im, p.x0);
+                const int64_t sum = min(e_x + e_m, (int64_t)2147483647);
+                // floor((2^31 - 1) / sum): the double quotient, corrected to the exact floor
+                int64_t f = 0;
+                if (sum > 0) {
+                    f = (int64_t)(2147483647.0 / (double)sum);
+                    if (f * sum > 2147483647LL) --f;
+                    else if ((f + 1) * sum <= 2147483647LL) ++f;
+                }
+                const int32_t sig = (int32_t)((e_x * f) >> 24);
+                const float v = __fmul_rn((float)(I[j] * sig), p.k_g);
+                qv[j] = ZH ? f2i_rn_sat16(v) + p.z_h : __float2int_rn(fminf(fmaxf(v, -1024.f), 1024.f));
+            }
+            out[k] = pack_sat_s8(qv[1], qv[0], pack_sat_s8(qv[3], qv[2], 0u));
+        }
+    }
+}
+
 }  // namespace swinmlp

@@ -489,6 +489,10 @@ struct swin_mlp_int8_s {
     bool unfused = false;       // desc.op5_unfused: FC1 (EP_ACC) -> op5_fn -> FC2 + op #6
     Op5Fn op5_fn = nullptr;
     int op5_grid = 0;
+    // the shift-GELU control (act == SWIN_MLP_ACT_SHIFT_GELU, always unfused): row-max op #5 kernel
+    void (*sg_fn)(ShiftGeluArgs) = nullptr;
+    ShiftGeluArgs sg = {};
+    int sg_grid = 0;
     CUtensorMap tm_fw1, tm_fw2;
     // device copies (handle-owned)
     int8_t *w1 = nullptr, *w2 = nullptr;
@@ -632,8 +636,13 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     if (d.C < 32 || d.C % 32) return fail(SWIN_MLP_EINVAL, "C=%d must be a multiple of 32 and >= 32", d.C);
     if (d.H < d.C || d.H % 32) return fail(SWIN_MLP_EINVAL, "H=%d must be a multiple of 32 and >= C", d.H);
     if (d.C > 1536 || d.H > 6144) return fail(SWIN_MLP_EUNSUPPORTED, "C=%d H=%d exceed 1536/6144", d.C, d.H);
-    if (d.act != SWIN_MLP_ACT_RELU && d.act != SWIN_MLP_ACT_GELU_ERF)
+    if (d.act != SWIN_MLP_ACT_RELU && d.act != SWIN_MLP_ACT_GELU_ERF && d.act != SWIN_MLP_ACT_SHIFT_GELU)
         return fail(SWIN_MLP_EINVAL, "unknown activation %d", (int)d.act);
+    if (d.act == SWIN_MLP_ACT_SHIFT_GELU) {
+        if (!normal_positive(d.gelu_in_scale)) return fail(SWIN_MLP_EINVAL, "gelu_in_scale must be finite, normal and > 0");
+        volatile float S = 1.702f * d.gelu_in_scale;
+        if (!(1.0 / (double)S < (double)(1 << 26))) return fail(SWIN_MLP_EINVAL, "gelu_in_scale too small (1/(1.702 s_g) >= 2^26)");
+    }
     if (d.op5_unfused != 0 && d.op5_unfused != 1) return fail(SWIN_MLP_EINVAL, "op5_unfused=%d must be 0 or 1", d.op5_unfused);
     if (!normal_positive(d.x_scale) || !normal_positive(d.h_scale) || !normal_positive(d.y_scale))
         return fail(SWIN_MLP_EINVAL, "activation scales must be finite, normal and > 0");
@@ -721,7 +730,7 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
     }
 
     // tile / cluster plans
-    h->unfused = d.op5_unfused != 0;
+    h->unfused = d.op5_unfused != 0 || d.act == SWIN_MLP_ACT_SHIFT_GELU;   // (shift-GELU: the row max)
     const int epi1 = h->unfused ? EP_ACC : d.act == SWIN_MLP_ACT_RELU ? EP5_RELU : EP5_GELU;
     if (!make_plan(epi1, H, C, false, h->p1)) return bail(fail(SWIN_MLP_EUNSUPPORTED, "no FC1 tile plan for H=%d", H));
     if (!make_plan(EP6_LN, C, H, true, h->p2, d.ln_fp64 ? 8 : 4))
@@ -795,7 +804,22 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
             h->has_small = true;
         }
     }
-    if (h->unfused) {
+    if (h->unfused && d.act == SWIN_MLP_ACT_SHIFT_GELU) {
+        static void (*const sgt[4])(ShiftGeluArgs) = {op5_shiftgelu_kernel<false, false>, op5_shiftgelu_kernel<false, true>,
+                                                      op5_shiftgelu_kernel<true, false>, op5_shiftgelu_kernel<true, true>};
+        h->sg_fn = sgt[(d.b1 ? 2 : 0) | (d.h_zero_point ? 1 : 0)];
+        volatile float one = 1.0f;
+        volatile float inv_g = one / d.gelu_in_scale;
+        volatile float S = 1.702f * d.gelu_in_scale;
+        volatile float sgih = d.gelu_in_scale * h->inv_h;
+        volatile float k_g = sgih * 0.0078125f;
+        h->sg.inv_g = inv_g; h->sg.k_g = k_g;
+        h->sg.x0 = (int32_t)std::floor(-1.0 / (double)S);
+        h->sg.z_h = d.h_zero_point;
+        int per_sm = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->sg_fn, kOp5Threads, 0));
+        h->sg_grid = std::max(1, per_sm) * h->num_sms;
+    } else if (h->unfused) {
         h->op5_fn = op5_kernel_for(d.act == SWIN_MLP_ACT_GELU_ERF, d.b1 != nullptr, d.h_zero_point != 0);
         int per_sm = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->op5_fn, kOp5Threads, 0));
@@ -996,7 +1020,21 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
     ST_TRY(launch(P1, tm_x, tmw1, tm_ho, tm_ho, a1, s));
-    if (h->unfused) {   // the separate op #5 kernel (PDL-chained like the GEMMs)
+    if (h->unfused && h->sg_fn) {   // the shift-GELU control's row-max op #5 kernel
+        if (dbg && acc1) CUDA_TRY(cudaMemcpyAsync(acc1, a1ws, (size_t)T * H * 4, cudaMemcpyDeviceToDevice, s));
+        ShiftGeluArgs o = h->sg;
+        o.a1 = a1ws; o.hq = hq; o.m1 = h->m1; o.b1 = h->b1; o.H = H; o.T = T;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((T + kOp5Threads / 32 - 1) / (kOp5Threads / 32), h->sg_grid)));
+        cfg.blockDim = dim3((unsigned)kOp5Threads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, h->sg_fn, o));
+    } else if (h->unfused) {   // the separate op #5 kernel (PDL-chained like the GEMMs)
         if (dbg && acc1) CUDA_TRY(cudaMemcpyAsync(acc1, a1ws, (size_t)T * H * 4, cudaMemcpyDeviceToDevice, s));
         Op5Args o = {};
         o.a1 = a1ws; o.hq = hq; o.m1 = h->m1; o.b1 = h->b1; o.inv_h = h->inv_h; o.z_h = h->d.h_zero_point;

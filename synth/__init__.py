@@ -20,6 +20,7 @@ import numpy as np
 BASE_SEED = 240201169
 ACT_RELU = 0
 ACT_GELU = 1
+ACT_SHIFT_GELU = 2   # the I-ViT shift-GELU control (R28)
 
 # Swin stage channel widths and the BASELINE.json configs.
 SWIN = {
@@ -60,6 +61,7 @@ class Layer:
     z_y: int
     seed: int = 0
     meta: dict = field(default_factory=dict)
+    s_g: float = 0.0            # shift-GELU input grid (act == ACT_SHIFT_GELU): 9 bits over +-8 sigma
 
 
 def _quant_weights(rng, n_out, n_in, std=0.02):
@@ -96,9 +98,12 @@ def make_layer(C: int, seed: int, act: int = ACT_RELU, fc1_bias: bool = False,
     levels = 255.0 if z_h == -128 else 127.0
     s_h = np.float32(4.0 * sig_h / levels)
     s_y = np.float32(5.0 / 127.0)
+    # shift-GELU input grid: 9 bits over +-8 sigma (|x0| = 1/(1.702 s_g) ~ 150, so the integer
+    # sigmoid keeps ~7 bits: floor((2^31-1)/(e + e_m)) >= ~2^7 with e <= 2^15 * 2|x0|)
+    s_g = np.float32(8.0 * sig_h / 511.0)
     return Layer(C=C, H=H, act=act, s_x=float(s_x), z_x=z_x, w1=w1, s_w1=s_w1, b1=b1,
                  s_h=float(s_h), z_h=z_h, w2=w2, s_w2=s_w2, b2=b2, gamma=gamma, beta=beta,
-                 eps=1e-5, s_y=float(s_y), z_y=z_y, seed=seed)
+                 eps=1e-5, s_y=float(s_y), z_y=z_y, seed=seed, s_g=float(s_g))
 
 
 def make_activations(layer: Layer, T: int, seed: int, outlier_frac: float = 0.02,

@@ -56,7 +56,7 @@ def test_sm100a_code_only():
     assert len(funcs) >= 16
     for f in funcs:
         name = f.split()[0]
-        if "op5_unfused_kernel" in name:   # the unfused plan's elementwise op #5 (NEXT-1)
+        if "op5_unfused_kernel" in name or "op5_shiftgelu_kernel" in name:   # separate op #5 (NEXT-1/4)
             assert "LDG" in f and "STG" in f and "F2I" in f, name
         elif "op1_kernel" in name:         # op #1: HBM-bound LayerNorm + gather + Q (NEXT-4)
             assert "LDG" in f and "STG" in f and "SHFL" in f, name

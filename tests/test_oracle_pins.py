@@ -414,3 +414,61 @@ def test_proj_op4_pins():
     assert (A == 0).all()
     np.testing.assert_array_equal(z, Rc)
     np.testing.assert_array_equal(yh, np.broadcast_to(P.gamma * 0 + P.beta, (3, C)))
+
+
+# ---- O2'': the I-ViT shift-GELU control (reading R28) -----------
+
+def _sg_layer():
+    import synth
+    return synth.make_layer(96, 5150, act=2)
+
+
+def _sg_run(L, y_row, extra=None):
+    """Hq of one row of pre-activations y (A1 built so fl(A1) * m1 = y exactly: m1 = 2^-10)."""
+    y = np.asarray(y_row, np.float64)
+    A1 = np.rint(y * 1024.0).astype(np.int32)[None, :]
+    m1 = np.full(A1.shape[1], 2.0 ** -10, np.float32)
+    inv_h = np.float32(1.0) / np.float32(L.s_h)
+    Hq, I = oracle.ep5_shiftgelu(A1, m1, None, L.s_g, inv_h, 0, return_I=True)
+    return Hq[0], I[0], A1[0] / 1024.0
+
+
+def test_shiftgelu_zero_argument_is_exactly_one():
+    """ShiftExp(0) = 2|x0| 2^14 and, with e_m ~ 0 (a large row max), sig = 127 or 128 at the max:
+    the max element passes through (Hq = rne(y / s_h) within 1 LSB)."""
+    L = _sg_layer()
+    sig = 0.02 * np.sqrt(96 * 1.7)
+    y = np.linspace(-2, 2, 384) * sig
+    y[17] = 7.0 * sig                                     # the row max
+    Hq, I, yq = _sg_run(L, y)
+    assert I.max() == I[17]
+    assert abs(int(Hq[17]) - int(np.clip(np.rint(yq[17] / L.s_h), -128, 127))) <= 1
+
+
+def test_shiftgelu_matches_x_sigmoid_1p702x():
+    """The shift approximations (x log2 e by shifts, 2^f ~ 1 + f/2 on f in (-1, 0]) stay within 7 %
+    of x * sigmoid(1.702 x) -- the form I-ViT approximates -- plus 2 quantization steps; a sign
+    or index error (wrong max, wrong operand) fails by tens of steps."""
+    L = _sg_layer()
+    sig = 0.02 * np.sqrt(96 * 1.7)
+    y = np.linspace(-6, 6, 384) * sig
+    Hq, I, yq = _sg_run(L, y)
+    x = I.astype(np.float64) * L.s_g
+    ref = x / (1.0 + np.exp(-1.702 * x)) / L.s_h
+    tol = 0.07 * np.abs(x) / L.s_h + 2.0
+    assert (np.abs(Hq - np.clip(ref, -128, 127)) <= tol).all(), np.abs(Hq - ref).max()
+    assert (np.diff(Hq[y > 0].astype(int)) >= -1).all()   # monotone right of 0 (up to rounding)
+
+
+def test_shiftgelu_depends_on_the_row_max_only_through_rounding():
+    """sigmoid(1.702 x) = e^{S(I-Im)} / (e^{S(I-Im)} + e^{-S Im}) for any Im: raising the row max
+    (another element) may move outputs by the integer approximations' rounding only."""
+    L = _sg_layer()
+    sig = 0.02 * np.sqrt(96 * 1.7)
+    y = np.linspace(-3, 3, 384) * sig
+    y2 = y.copy()
+    y2[0] = 7.5 * sig                                     # a new, larger row max elsewhere
+    Hq1, _, _ = _sg_run(L, y)
+    Hq2, _, _ = _sg_run(L, y2)
+    d = np.abs(Hq1[1:].astype(int) - Hq2[1:].astype(int))
+    assert d.max() <= 1 and (d > 0).mean() < 0.5

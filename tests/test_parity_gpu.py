@@ -64,9 +64,12 @@ def _run_and_check(dev, L, T, x_seed=5, resid=False, e2e=True, ln_fp64=False, op
     m1, ih, m2, iy = oracle.fold_constants(L.s_x, L.s_w1, L.s_h, L.s_w2, L.s_y)
     a1 = oracle.gemm_i8(X, L.w1, L.z_x, nthreads=0)
     np.testing.assert_array_equal(g["acc1"], a1, err_msg="acc1 (FC1 int32) not bit-exact")
-    h = oracle.ep5(g["acc1"], m1, L.b1, ih, L.z_h, act=L.act)
-    if L.act == synth.ACT_RELU:
-        np.testing.assert_array_equal(g["hidden"], h, err_msg="Hq (ReLU) not bit-exact")
+    if L.act == synth.ACT_SHIFT_GELU:
+        h = oracle.ep5_shiftgelu(g["acc1"], m1, L.b1, L.s_g, ih, L.z_h)
+    else:
+        h = oracle.ep5(g["acc1"], m1, L.b1, ih, L.z_h, act=L.act)
+    if L.act in (synth.ACT_RELU, synth.ACT_SHIFT_GELU):   # (shift-GELU: integer after two fp32 products)
+        np.testing.assert_array_equal(g["hidden"], h, err_msg="Hq (ReLU / shift-GELU) not bit-exact")
     else:
         _tier_int8(g["hidden"], h, what="Hq (GELU)")
     a2 = oracle.gemm_i8(g["hidden"], L.w2, L.z_h)
@@ -136,6 +139,18 @@ def test_parity_op5_unfused(dev, C, T, act, bias, zx, zh):
     L = _layer(C, 6000 + C, act=act, bias=bias, zx=zx, zh=zh)
     _run_and_check(dev, L, T, op5_unfused=True)
     assert SwinMlpInt8Layer(L, device=0, op5_unfused=True).plan()["fused"] == 0
+
+
+@pytest.mark.parametrize("C,T,bias,zh", [(96, 1000, False, 0), (384, 300, True, 0), (768, 129, False, -128),
+                                         (1536, 77, False, 0)])
+def test_parity_shift_gelu_control(dev, C, T, bias, zh):
+    """SURVEY.md §8(f) NEXT-4's third control: I-ViT's integer shift-GELU (R28), which needs
+    each token row's max before any output -- so it always runs unfused: FC1 -> A1 -> row-max op #5
+    kernel -> FC2.  A1, Hq, A2, z bit-exact; Y within the op #6 tier."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer, lib
+    L = _layer(C, 6200 + C, act=synth.ACT_SHIFT_GELU, bias=bias, zh=zh)
+    _run_and_check(dev, L, T)
+    assert lib().swin_mlp_int8_launches_per_run(SwinMlpInt8Layer(L, device=0).handle) == 3
 
 
 def test_op5_unfused_matches_fused_plan(dev):
