@@ -74,6 +74,7 @@ struct Plan {
     int BN = 0, CS = 1, stages = 0, n_groups = 1, G = 2, out_w = 16, ebytes = 4, xstage = 1, resb = 0, yin = 0, dst = 0, wsl = 0;
     int eg = 2;     // epilogue groups: G ping-pong groups, or 1 (all 16 warps drain every tile)
     int pair = 0;   // CTA pair (cta_group::2): clusters of 2 CTAs on m-tiles 2u, 2u+1 (CS == 1)
+    int one_group = 0;   // few-tile plans: every CTA drains ONE tile, so all 16 epilogue warps take it
     uint32_t smem = 0;
     int max_clusters = 0;
 };
@@ -275,7 +276,7 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
         if (dst && (epi == EP6_LN || epi == EP_ACC || no_dst)) continue;
         for (int yin : {1, 0}) {
         if (yin && (epi != EP6_LN || xs != G || no_yin)) continue;
-        for (int eg : {epilogue_groups(epi, G), G}) {
+        for (int eg : {pl.one_group ? 1 : epilogue_groups(epi, G), G}) {
         pl.eg = eg;
         pl.yin = yin;
         pl.dst = dst;
@@ -303,6 +304,12 @@ bool fit_smem(int epi, Plan& pl, int min_stages, int K) {
     }
     }
     return false;
+}
+
+// few-tile plans drain with one group of all 16 epilogue warps (SWIN_MLP_ONE_GROUP=0: G groups; A/B)
+static int one_group_env() {
+    const char* e = std::getenv("SWIN_MLP_ONE_GROUP");   // (read per create)
+    return (e && *e == '0') ? 0 : 1;
 }
 
 // ln_pair: -1 = the SWIN_MLP_LN_PAIR switch, 1 = only the CTA-pair op #6 plan, 0 = never it
@@ -333,7 +340,7 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, i
         if (small_bn > 0) {
             for (int cs : {8, 4}) {
                 if (N % cs || N / cs > 256 || (N / cs) % 16) continue;
-                pl.BN = N / cs; pl.CS = cs; pl.n_groups = 1;
+                pl.BN = N / cs; pl.CS = cs; pl.n_groups = 1; pl.one_group = one_group_env();
                 if (fit_smem(epi, pl, 3, K) || fit_smem(epi, pl, 2, K)) return true;
             }
             return false;
@@ -363,7 +370,7 @@ bool make_plan(int epi, int N, int K, bool full_row, Plan& pl, int ebytes = 4, i
     // 0.5 us slower (there the single-CTA ring already holds a whole tile's K).
     if (small_bn > 0) {
         if (N % small_bn) return false;
-        pl.BN = small_bn; pl.CS = 1; pl.n_groups = N / small_bn;
+        pl.BN = small_bn; pl.CS = 1; pl.n_groups = N / small_bn; pl.one_group = one_group_env();
         return fit_smem(epi, pl, 3, K) || fit_smem(epi, pl, 2, K);
     }
     const bool want_pair = K >= 512;
