@@ -136,6 +136,44 @@ for st in range(4):
                      f"{val('lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
                      f"{d.get('launch__registers_per_thread', '')} | {d.get('launch__grid_size', '')} | "
                      f"{d.get('launch__cluster_dim_x', '')} |")
+# extra captures: the north-star stage (Swin-B b128 stage 3, C = 512) and the attention half
+extra = {"swinb3": ("Swin-B b128 stage 3 layer (C=512, T=25088)", ["fc1_relu_q", "fc2_ln_q"]),
+         "attn0": ("attention half, Swin-T b64 stage 0 (C=96, T=200704)", ["op1", "qkv_op2", "attn_core"])}
+for key, (what, names) in extra.items():
+    raw_csv = os.path.join(ROOT, "gpurun_out", f"full_stage{key}_raw.csv")
+    if not os.path.exists(raw_csv):
+        continue
+    shutil.copy(raw_csv, os.path.join(out, f"{tag}_full_{key}_raw.csv"))
+    det = raw_csv.replace("_raw.csv", "_details.csv")
+    if os.path.exists(det):
+        shutil.copy(det, os.path.join(out, f"{tag}_full_{key}_details.csv"))
+    rr = list(csv.reader(open(raw_csv)))
+    hdr, units, data = rr[0], rr[1], rr[2:]
+    lines.append(f"\n### {what}\n")
+    lines.append("| kernel | us | DRAM read MB | DRAM write MB | tensor(imma) % | issue % | eligible warps/sched | regs | grid |")
+    lines.append("|---|---|---|---|---|---|---|---|---|")
+    for jj, row in enumerate(data):
+        d = {h: row[i] for i, h in enumerate(hdr)}
+        u = {h: units[i] for i, h in enumerate(hdr)}
+
+        def v2(m, scale_to=None):
+            try:
+                v = float(d.get(m, "nan").replace(",", "") or "nan")
+            except ValueError:
+                return float("nan")
+            un = u.get(m, "")
+            if scale_to == "MB":
+                return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1, "Gbyte": 1e3}.get(un, 1)
+            if scale_to == "us":
+                return v * {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(un, 1)
+            return v
+        nm = names[jj] if jj < len(names) else d.get("Kernel Name", "")[:40]
+        lines.append(f"| {nm} | {v2('gpu__time_duration.sum', 'us'):.1f} | {v2('dram__bytes_read.sum', 'MB'):.1f} | "
+                     f"{v2('dram__bytes_write.sum', 'MB'):.1f} | "
+                     f"{v2('sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active'):.1f} | "
+                     f"{v2('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
+                     f"{v2('smsp__warps_eligible.avg.per_cycle_active'):.2f} | "
+                     f"{d.get('launch__registers_per_thread', '')} | {d.get('launch__grid_size', '')} |")
 json.dump(traffic, open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
 open(os.path.join(out, f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))

@@ -29,9 +29,13 @@ python tools/stack_bench.py 4 3 --steps 10 > $o/stack_$tag.log 2>&1
 python tools/prof_ft.py gelu 1 > $o/plain_ft_$tag.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $o/ft_launches_$tag.csv python tools/prof_ft.py gelu 1 > $o/ncu_ft_$tag.log 2>&1
+# attention half (NEXT-3 / NEXT-4), Swin-T b64 stage 0: op #1, QKV GEMM + op #2, attention core
+python tools/attn_one.py 0 2 > $o/plain_attn_$tag.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"attn_core|op1_kernel|mlp_gemm_kernel" -s 3 -c 3 \
+    -o $o/full_attn0 -f python tools/attn_one.py 0 2 > $o/ncu_full_attn_$tag.log 2>&1
 # bring-back budget (gpurun merges <= 64 MiB): raw + source CSV exports of every capture,
 # the .ncu-rep only for the dominant stage-0 kernel
-for s in 0 1 2 3 swinb3; do
+for s in 0 1 2 3 swinb3 attn0; do
   [ -f $o/full_stage$s.ncu-rep ] || [ -f $o/full_$s.ncu-rep ] || continue
   [ -f $o/full_$s.ncu-rep ] && mv $o/full_$s.ncu-rep $o/full_stage$s.ncu-rep
   ncu -i $o/full_stage$s.ncu-rep --page raw --csv > $o/full_stage${s}_raw.csv 2>/dev/null
