@@ -337,7 +337,7 @@ class SwinMlpInt8Layer:
                 "fc2_bn": out[4], "fc2_cs": out[5], "fc2_stages": out[6], "fc2_max_clusters": out[7],
                 "fc1_groups": out[8], "fc2_groups": out[9], "fc1_resb": out[10], "fc2_resb": out[11],
                 "fc1_pair": out[16], "op5_unfused": out[19] & 1,
-                **({"run_plan": ("default", "ln_pair", "few_tile")[out[19] >> 1], "fc2_ksplit": out[13]}
+                **({"run_plan": ("default", "ln_pair", "few_tile", "one_launch")[out[19] >> 1], "fc2_ksplit": out[13]}
                    if T is not None else {})}
 
     def set_plan_hint(self, T_hint=0):

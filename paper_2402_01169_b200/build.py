@@ -17,7 +17,7 @@ SOURCES = [os.path.join(SRC_DIR, f) for f in ("swin_mlp_int8.cu", "fused_mlp.cu"
 UNITS = [(SOURCES[0], [], "swin_mlp_int8.o")] + \
     [(SOURCES[1], [f"-DFUSED_PART={k}"], f"fused_mlp_{k}.o") for k in (0, 1, 2, 3)]
 DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("mlp_kernels.cuh", "sm100_ptx.cuh", "fused_mlp.cuh", "op5_unfused.cuh",
-                                               "attn_kernels.cuh")] + \
+                                               "attn_kernels.cuh", "small_mlp.cuh")] + \
     [os.path.join(ROOT, "include", f) for f in ("swin_mlp_int8.h", "swin_attn_int8.h")]
 LIB = os.path.join(HERE, "libswin_mlp_int8.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

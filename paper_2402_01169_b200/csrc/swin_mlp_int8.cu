@@ -23,6 +23,7 @@
 #include "../../include/swin_attn_int8.h"
 #include "mlp_kernels.cuh"
 #include "attn_kernels.cuh"
+#include "small_mlp.cuh"
 #include "fused_mlp.cuh"
 #include "op5_unfused.cuh"
 
@@ -524,6 +525,13 @@ struct swin_mlp_int8_s {
     Plan p1s, p2s;
     bool has_small = false;
     CUtensorMap tm_w1s, tm_w2s;
+    // one-launch plan for runs of at most kSMaxT tokens (small_mlp.cuh): P = H / 128 CTAs
+    bool has_tiny = false;
+    int tiny_P = 0, tiny_NP = 0, tiny_PR = 0;
+    CUtensorMap tm_w1t, tm_w2t;
+    int32_t* tiny_cnt = nullptr;   // [2] arrival / departure counters (zero between runs)
+    int32_t* tiny_acc = nullptr;   // [64][C] int32 FC2 sums (zero between runs)
+    void (*tiny_fn)(CUtensorMap, CUtensorMap, CUtensorMap, SmallArgs) = nullptr;
     std::vector<void*> allocs;
     // native profiling (bench roofline): event triples per recorded run
     bool prof_on = false;
@@ -564,6 +572,7 @@ struct swin_mlp_int8_s {
 // 1 = the CTA-pair op #6 (p2b, at most one wave of pairs), 2 = the few-tile plans
 // (p1s/p2s: the defaults would put both GEMMs on fewer than num_sms / 4 CTAs).
 static int plan_choice(const swin_mlp_int8_s* h, int64_t T) {
+    if (h->has_tiny && T <= kSMaxT) return 3;   // one launch (small_mlp.cuh)
     const int64_t m_tiles = (T + kBM - 1) / kBM;
     const int64_t units1 = (h->p1.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p1.n_groups;
     const int64_t units2 = (h->p2.pair ? (m_tiles + 1) / 2 * 2 : m_tiles) * h->p2.CS;
@@ -811,6 +820,39 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
             h->has_small = true;
         }
     }
+    {
+        // one-launch plan for T <= 64: fp32 LayerNorm, C % 128 == 0 (the row's float4 groups per
+        // lane), H / 128 CTAs all co-resident, FC2 output in pieces of <= 256 columns
+        const char* te = std::getenv("SWIN_MLP_TINY");   // '0': never (A/B switch, read per create)
+        const int P = H / 128;
+        int NP = (C + 255) / 256;   // the fewest FC2 pieces of <= 256 columns, a multiple of 16 each
+        while (NP <= C / 16 && (C % NP || (C / NP) % 16)) ++NP;
+        const int PR = NP > 0 ? C / NP : 0;
+        void (*tfn)(CUtensorMap, CUtensorMap, CUtensorMap, SmallArgs) = nullptr;
+        const bool gl = d.act == SWIN_MLP_ACT_GELU_ERF;
+        switch (C / 128) {   // the LayerNorm row groups per lane (C % 128 == 0)
+#define TINY(g) case g: tfn = gl ? small_mlp_kernel<g, 1> : small_mlp_kernel<g, 0>; break;
+            TINY(3) TINY(4) TINY(5) TINY(6) TINY(8) TINY(10) TINY(12)
+#undef TINY
+            default: break;
+        }
+        if (!(te && *te == '0') && tfn && !h->unfused && !d.ln_fp64 && C >= 384 && C % 128 == 0 && H % 128 == 0 &&
+            P <= h->num_sms && PR * NP == C && PR % 16 == 0 && PR <= 256) {
+            h->tiny_fn = tfn;
+            H_TRY(encode_2d(&h->tm_w1t, h->w1, H, C, C, 128));
+            H_TRY(encode_2d(&h->tm_w2t, h->w2, C, H, H, (uint32_t)PR));
+            void* cp = nullptr;
+            const size_t acc_bytes = (size_t)kSMaxT * C * 4;
+            CUDA_TRY(cudaMalloc(&cp, acc_bytes + 256));
+            h->allocs.push_back(cp);
+            CUDA_TRY(cudaMemset(cp, 0, acc_bytes + 256));
+            h->tiny_acc = static_cast<int32_t*>(cp);
+            h->tiny_cnt = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(cp) + acc_bytes);
+            CUDA_TRY(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSSmem));
+            h->tiny_P = P; h->tiny_NP = NP; h->tiny_PR = PR;
+            h->has_tiny = true;
+        }
+    }
     if (h->unfused && d.act == SWIN_MLP_ACT_SHIFT_GELU) {
         static void (*const sgt[4])(ShiftGeluArgs) = {op5_shiftgelu_kernel<false, false>, op5_shiftgelu_kernel<false, true>,
                                                       op5_shiftgelu_kernel<true, false>, op5_shiftgelu_kernel<true, true>};
@@ -882,7 +924,8 @@ size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T) {
     if (h->fp.on) return 0;   // one kernel: the hidden tile never leaves the SM
     const size_t hq = (size_t)(((T * h->d.H) + 127) / 128 * 128);
     if (h->unfused) return hq + (size_t)T * h->d.H * 4;   // unfused plan: + A1 int32 [T][H]
-    return hq + split_region_bytes(h, T);                  // + op #6 split-K partials (small T)
+    const size_t two = hq + split_region_bytes(h, T);      // + op #6 split-K partials (small T)
+    return two;   // (the one-launch plan, T <= 64, uses handle-owned buffers only)
 }
 
 // plan_T: the token count the launch plans are chosen for (the run's own T, the handle's plan
@@ -963,6 +1006,40 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
 
     const int64_t m_tiles = (T + kBM - 1) / kBM;
     const int run_plan = plan_choice(h, plan_T > 0 ? plan_T : h->plan_hint > 0 ? h->plan_hint : T);
+    if (run_plan == 3 && T <= kSMaxT) {   // one launch for the whole layer (small_mlp.cuh)
+        CUtensorMap tmx;
+        ST_TRY(encode_cached(h, &tmx, x, T, C, C, (uint32_t)kSMaxT));
+        SmallArgs a = {};
+        a.T = (int32_t)T; a.C = C; a.H = H; a.P = h->tiny_P; a.NP = h->tiny_NP; a.PR = h->tiny_PR;
+        a.act = h->d.act == SWIN_MLP_ACT_GELU_ERF ? 1 : 0;
+        a.m1 = h->m1; a.b1 = h->b1; a.zc1 = h->zc1; a.m2 = h->m2; a.b2 = h->b2; a.zc2 = h->zc2;
+        a.gamma = h->gamma; a.beta = h->beta;
+        a.inv_h = h->inv_h; a.z_h = h->d.h_zero_point; a.inv_y = h->inv_y; a.z_y = h->d.y_zero_point;
+        a.s_x = h->d.x_scale; a.z_x = h->d.x_zero_point; a.eps = h->d.ln_eps;
+        a.x = x; a.y = y; a.resid = residual; a.resid_out = residual_out;
+        a.acc = h->tiny_acc; a.cnt = h->tiny_cnt;
+        if (dbg) { a.acc1_tap = acc1; a.hid_tap = hidden; a.acc2_tap = acc2; a.ln_tap = ln_out; }
+        a.trace = h->trace;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)h->tiny_P);
+        cfg.blockDim = dim3((unsigned)kSThreads);
+        cfg.dynamicSmemBytes = kSSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaEvent_t* ev = nullptr;
+        if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
+        if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, h->tiny_fn, tmx, h->tm_w1t, h->tm_w2t, a));
+        if (ev) {
+            CUDA_TRY(cudaEventRecord(ev[1], s));
+            CUDA_TRY(cudaEventRecord(ev[2], s));
+        }
+        return SWIN_MLP_OK;
+    }
     const bool use_s = run_plan == 2, use_b = run_plan == 1;
     const Plan& P1 = use_s ? h->p1s : h->p1;
     const CUtensorMap& tmw1 = use_s ? h->tm_w1s : h->tm_w1;
@@ -1481,6 +1558,12 @@ int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20) {
     swin_mlp_int8_plan(h, out20);
     if (h->fp.on) return 0;   // the one-kernel plan: the same launch for every T
     const int c = plan_choice(h, h->plan_hint > 0 ? h->plan_hint : T);
+    if (c == 3) {   // the one-launch plan: out20[0] = CTAs, [4] = FC2 piece columns, [5] = pieces
+        for (int i = 0; i < 12; ++i) out20[i] = 0;
+        out20[0] = h->tiny_P; out20[4] = h->tiny_PR; out20[5] = h->tiny_NP; out20[13] = 1; out20[16] = 0;
+        out20[19] = (h->unfused ? 1 : 0) | (c << 1);
+        return 0;
+    }
     const Plan& P1 = c == 2 ? h->p1s : h->p1;
     const Plan& P2 = c == 2 ? h->p2s : c == 1 ? h->p2b : h->p2;
     out20[0] = P1.BN; out20[1] = P1.CS; out20[2] = P1.stages; out20[3] = P1.max_clusters;

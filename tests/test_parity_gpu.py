@@ -255,11 +255,28 @@ def test_shard_concat_across_plan_switch(dev, ln_fp64):
 
 @pytest.mark.parametrize("C,T", [(384, 49), (512, 49), (768, 49), (768, 128), (768, 200), (1024, 49),
                                  (1536, 49), (384, 1), (768, 17)])
-def test_parity_few_tile_plans(dev, C, T):
-    """The few-tile plans chosen per run for one or two m-tiles (configs[0]: one 7x7
-    window, T = 49, C = 768) against the oracle, every output element."""
+def test_parity_few_tile_plans(dev, C, T, monkeypatch):
+    """The few-tile plans chosen per run for one or two m-tiles against the oracle, every output
+    element (runs of <= 64 tokens take the one-launch plan unless SWIN_MLP_TINY=0)."""
+    monkeypatch.setenv("SWIN_MLP_TINY", "0")
     _run_and_check(dev, _layer(C, 7100 + C + T), T, x_seed=T)
     _run_and_check(dev, _layer(C, 7200 + C + T, act=1, bias=True, zx=-5, zh=3, zy=2), T, x_seed=T + 1,
+                   resid=True, e2e=False)
+
+
+@pytest.mark.parametrize("C,T", [(384, 49), (512, 64), (768, 49), (768, 1), (768, 17), (1024, 33), (1536, 49),
+                                 (640, 49)])
+def test_parity_one_launch_plan(dev, C, T):
+    """The one-launch plan for runs of <= 64 tokens (small_mlp.cuh; configs[0]: one 7x7 window,
+    T = 49, C = 768): H/128 CTAs each own 128 hidden columns, FC2 partials summed exactly, op #6
+    per row by one warp.  A1, Hq, A2, z bit-exact; Y within the tier; GELU, bias, zero points and
+    the fp32 residual on the second case.  Back-to-back runs exercise the counter reset."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    L = _layer(C, 7500 + C + T)
+    assert SwinMlpInt8Layer(L, device=0).plan(T)["run_plan"] == "one_launch"
+    for rep in range(2):
+        _run_and_check(dev, L, T, x_seed=T + rep)
+    _run_and_check(dev, _layer(C, 7600 + C + T, act=1, bias=True, zx=-5, zh=3, zy=2), T, x_seed=T + 1,
                    resid=True, e2e=False)
 
 
@@ -532,7 +549,8 @@ def test_plan_for_reports_the_run_plan(dev):
     (FC1 BN = 64 single-CTA tiles, op #6 on an 8-CTA cluster), a full-stage run the defaults."""
     from paper_2402_01169_b200 import SwinMlpInt8Layer
     layer = SwinMlpInt8Layer(_layer(768, 7300), device=0)
-    small, big = layer.plan(49), layer.plan(200704)
+    window, small, big = layer.plan(49), layer.plan(100), layer.plan(200704)
+    assert window["run_plan"] == "one_launch" and window["fc1_bn"] == 3072 // 128   # CTAs
     assert small["run_plan"] == "few_tile" and small["fc1_bn"] == 64 and small["fc1_pair"] == 0
     assert small["fc2_cs"] == 8 and small["fc2_bn"] == 96
     assert big["run_plan"] == "default"
