@@ -113,3 +113,40 @@ def test_attn_errors(dev):
     A = synth.make_attn_layer(96, 15, 15, 3, M=5)
     with pytest.raises(SwinMlpError):
         SwinAttnInt8Layer(A, device=0)
+
+
+@pytest.mark.parametrize("C,S,M,shift,B", [(96, 14, 7, 3, 2), (384, 14, 7, 0, 2)])
+def test_whole_block_chain(dev, C, S, M, shift, B):
+    """One quantized Swin block through the C ABI (Fig. 1, all six fused ops): op #1 ->
+    QKV + op #2 -> Q.K + op #3 -> V.att -> Proj + op #4 (+LN2, residual = the block input) -> the
+    MLP (FC1 + op #5 ReLU -> FC2 + op #6, fp32 residual = op #4's z).  Each stage is checked
+    against the oracle applied to the GPU's own previous output (so the tiers do not compound),
+    which also pins the hand-offs: window order out of op #1, raster order out of V.att."""
+    from paper_2402_01169_b200 import SwinAttnInt8Layer, SwinMlpInt8Layer, SwinOp1Int8, SwinProjInt8Layer
+    A = synth.make_attn_layer(C, S, S, 8800 + C, M=M, shift=shift)
+    P = synth.make_proj(C, 8900 + C)
+    P.s_a, P.z_a = A.s_a, A.z_a                       # the proj GEMM reads the V.att output grid
+    L = synth.make_layer(C, 9000 + C)
+    L.s_x, L.z_x = P.s_y, P.z_y                       # the MLP reads op #4's output grid
+    x = synth.make_block_input(B, S, S, C, 9100 + C)
+    xd = torch.from_numpy(x).to(dev)
+    T = B * S * S
+    xw = SwinOp1Int8(A, device=0)(xd)
+    a = SwinAttnInt8Layer(A, device=0)(xw, B)
+    R = xd.reshape(T, C).contiguous()                 # the residual stream, raster order
+    z = torch.empty((T, C), dtype=torch.float32, device=dev)
+    y4 = SwinProjInt8Layer(P, device=0)(a, R, residual_out=z)
+    y = SwinMlpInt8Layer(L, device=0)(y4, residual=z)
+    torch.cuda.synchronize()
+    xw_n, a_n, y4_n, z_n, y_n = (t.cpu().numpy() for t in (xw, a, y4, z, y))
+    mx, rate = _flip_stats(xw_n, oracle.op1(x, A.gamma1, A.beta1, A.eps, A.s_x, A.z_x, M, shift))
+    assert mx <= 1 and rate <= 1e-4, ("op1", mx, rate)
+    qkv_ref = oracle.qkv(xw_n, A.w_qkv, A.s_wqkv, A.b_qkv, A.s_x, A.z_x, A.s_q, A.s_k, A.s_v)
+    mx, rate = _flip_stats(a_n, oracle.attn(qkv_ref, A, B))
+    assert mx <= 1 and rate <= 5e-4, ("attn", mx, rate)
+    Y4, _, Z4, _ = oracle.proj_op4(P, a_n, x.reshape(T, C))
+    np.testing.assert_array_equal(z_n, Z4, err_msg="op #4 residual stream z")
+    mx, rate = _flip_stats(y4_n, Y4)
+    assert mx <= 1 and rate <= 1e-4, ("op4 Y", mx, rate)
+    mx, rate = _flip_stats(y_n, oracle.mlp(L, y4_n, R=z_n))
+    assert mx <= 1 and rate <= 1e-4, ("mlp Y", mx, rate)
