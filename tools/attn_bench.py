@@ -15,7 +15,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
-from paper_2402_01169_b200 import SwinAttnInt8Layer, SwinOp1Int8  # noqa: E402
+from paper_2402_01169_b200 import SwinAttnInt8Layer, SwinMlpInt8Layer, SwinOp1Int8, SwinProjInt8Layer  # noqa: E402
 
 # (name, batch, C0, img, window): the per-GPU shapes of BASELINE configs[1], [3] (b128 per GPU), [4]
 MODELS = {"swin_t": ("Swin-T b64", 64, 96, 224, 7), "swin_b": ("Swin-B b128", 128, 128, 224, 7),
@@ -60,6 +60,28 @@ def run(model="swin_t", steps=20):
 
         us_op1 = timed(lambda: op1(x, y=xw))
         us_attn = timed(lambda: attn(xw, B, a=a, workspace=ws))
+        # the rest of the block: Proj + op #4 (+LN2) on the residual stream, then the MLP (ReLU)
+        P = synth.make_proj(C, synth.layer_seed(9, s, 1))
+        P.s_a, P.z_a = A.s_a, A.z_a
+        Lm = synth.make_layer(C, synth.layer_seed(9, s, 2))
+        Lm.s_x, Lm.z_x = P.s_y, P.z_y
+        proj, mlp = SwinProjInt8Layer(P, device=0), SwinMlpInt8Layer(Lm, device=0)
+        R = x.reshape(T, C)
+        zb = torch.empty((T, C), dtype=torch.float32, device="cuda")
+        y4 = torch.empty((T, C), dtype=torch.int8, device="cuda")
+        yb = torch.empty((T, C), dtype=torch.int8, device="cuda")
+        mws = torch.empty(max(mlp.workspace(T).numel(), 128), dtype=torch.uint8, device="cuda")
+
+        def block():
+            op1(x, y=xw)
+            attn(xw, B, a=a, workspace=ws)
+            proj(a, R, y=y4, residual_out=zb)
+            mlp(y4, y=yb, residual=zb, workspace=mws)
+
+        for _ in range(2):
+            block()
+        torch.cuda.synchronize()
+        us_block = timed(block)
         attn.profile_begin(steps)
         for k in range(steps):
             flush.fill_(k & 0xff)
@@ -77,10 +99,12 @@ def run(model="swin_t", steps=20):
                      "qkv_tops": round(ops_qkv / us_qkv / 1e6, 1), "qkv_tensor_frac": round(ops_qkv / us_qkv / 1e6 / int8_peak, 3),
                      "core_gbs": round(b_core / us_core / 1e3, 1), "core_hbm_frac": round(b_core / us_core / 1e3 / hbm, 3),
                      "core_gops": round(4.0 * N * C * T / us_core / 1e3, 1),
-                     "tokens_per_s_attn_half": T / ((us_op1 + us_attn) * 1e-6)})
-        del op1, attn, x, xw, a
+                     "tokens_per_s_attn_half": T / ((us_op1 + us_attn) * 1e-6),
+                     "block_us": round(us_block, 2), "block_tokens_per_s": T / (us_block * 1e-6),
+                     "block": "op #1 -> QKV/op #2 -> attention core -> Proj/op #4 (+LN2) -> MLP (ReLU), 7 launches"})
+        del op1, attn, x, xw, a, proj, mlp
         torch.cuda.empty_cache()
-    return {"what": "attention half: op #1 + QKV GEMM/op #2 + attention core (NEXT-4 / NEXT-3)",
+    return {"what": "attention half: op #1 + QKV GEMM/op #2 + attention core (NEXT-4 / NEXT-3), and the whole block",
             "bytes_per_token": {"op1": "4C read (fp32) + C write", "core": "3C read (qkv) + C write"},
             "hbm_peak_gbs": hbm, "int8_peak_tops": int8_peak, "l2": "flushed before every run", "rows": rows}
 
