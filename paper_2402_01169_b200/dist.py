@@ -19,7 +19,10 @@ def shard_range(n_items: int, rank: int, world: int) -> Tuple[int, int]:
 
 def shard_tokens(batch: int, tokens_per_image: int, rank: int, world: int) -> Tuple[int, int]:
     """Token rows [t0, t1) of this rank when a batch is split by whole images
-    (rows are independent, so any split gives the unsharded result bit-exactly)."""
+    (rows are independent: with the handles' plan hint set to the whole batch's T --
+    swin_mlp_int8_set_plan_hint, R20 -- every shard runs the batch's launch plans and
+    concat(shards) equals the unsharded run bit for bit; without it a shard small enough to take
+    another plan moves Y only inside the R15 tier)."""
     lo, hi = shard_range(batch, rank, world)
     return lo * tokens_per_image, hi * tokens_per_image
 

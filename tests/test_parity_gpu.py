@@ -253,12 +253,17 @@ def test_shard_concat_across_plan_switch(dev, ln_fp64):
         _tier_int8(y, full["y"].cpu().numpy(), what="Y across plans")
 
 
-@pytest.mark.parametrize("C,T", [(384, 49), (512, 49), (768, 49), (768, 128), (768, 200), (1024, 49),
-                                 (1536, 49), (384, 1), (768, 17)])
-def test_parity_few_tile_plans(dev, C, T, monkeypatch):
+@pytest.mark.parametrize("C,T,plan", [(384, 49, "few_tile"), (512, 49, "few_tile"), (768, 49, "few_tile"),
+                                      (768, 128, "few_tile"), (768, 200, "few_tile"), (1024, 49, "few_tile"),
+                                      (1536, 49, "default"), (384, 1, "few_tile"), (768, 17, "few_tile")])
+def test_parity_few_tile_plans(dev, C, T, plan, monkeypatch):
     """The few-tile plans chosen per run for one or two m-tiles against the oracle, every output
-    element (runs of <= 64 tokens take the one-launch plan unless SWIN_MLP_TINY=0)."""
+    element (runs of <= 64 tokens take the one-launch plan unless SWIN_MLP_TINY=0).  The plan each
+    case runs is asserted: at C = 1536 the default FC1 CTA-pair plan already spreads one m-tile
+    over 48 CTAs (>= num_sms / 4), so that case is the default plan (with split-K op #6) at T = 49."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
     monkeypatch.setenv("SWIN_MLP_TINY", "0")
+    assert SwinMlpInt8Layer(_layer(C, 7100 + C + T), device=0).plan(T)["run_plan"] == plan
     _run_and_check(dev, _layer(C, 7100 + C + T), T, x_seed=T)
     _run_and_check(dev, _layer(C, 7200 + C + T, act=1, bias=True, zx=-5, zh=3, zy=2), T, x_seed=T + 1,
                    resid=True, e2e=False)
