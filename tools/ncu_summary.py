@@ -89,7 +89,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "launch__grid_size", "launch__cluster_dim_x"]
 traffic = {}
 lines.append("\n## `ncu --set full` captures (tools/prof_layer.py <stage>, 2nd run; one launch each)\n")
-lines.append("| kernel | us | DRAM read MB | DRAM write MB | L2 bytes MB | tensor(imma) % active | issue % | L2 % | regs | grid | cluster |")
+lines.append("| kernel | us | DRAM read MB | DRAM write MB | L2 bytes MB (32 x lts__t_sectors) | tensor(imma) % active | issue % | L2 % | regs | grid | cluster |")
 lines.append("|---|---|---|---|---|---|---|---|---|---|---|")
 specs = synth.swin_t_batch64_layers()
 for st in range(4):
@@ -130,7 +130,7 @@ for st in range(4):
         rd, wr = val("dram__bytes_read.sum", "MB"), val("dram__bytes_write.sum", "MB")
         traffic[name] = (rd + wr) * 1e6
         lines.append(f"| {name} | {val('gpu__time_duration.sum', 'us'):.1f} | {rd:.1f} | {wr:.1f} | "
-                     f"{val('lts__t_bytes.sum', 'MB'):.1f} | "
+                     f"{val('lts__t_sectors.sum') * 32e-6:.1f} | "
                      f"{val('sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{val('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{val('lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
