@@ -325,8 +325,11 @@ __global__ void __launch_bounds__(32 * kAttnWarps) attn_core_kernel(const AttnAr
                     creg[e][nt / 8] |= (uint32_t)(jj < N ? region(jj) : 15) << (4 * (nt % 8));
                 }
         }
+        // N = 16 k + 1 (M = 7: 49 tokens): the last token row is done on its own below (dp4a,
+        // lane-parallel over keys), not as an m-tile of 15 empty rows
+        constexpr int MTM = (N % 16 == 1) ? MT - 1 : MT;
 #pragma unroll 1
-        for (int mt = 0; mt < MT; ++mt) {
+        for (int mt = 0; mt < MTM; ++mt) {
             const int i0 = mt * 16 + g, i1 = i0 + 8;
             uint32_t af[4];
             af[0] = *reinterpret_cast<const uint32_t*>(sQ + i0 * 32 + tq * 4);
@@ -450,6 +453,57 @@ __global__ void __launch_bounds__(32 * kAttnWarps) attn_core_kernel(const AttnAr
                         *reinterpret_cast<const int4*>(sP + r * 32 + (lane & 1) * 16);
             }
             __syncwarp();   // (the P tile is rewritten by the next m-tile)
+        }
+        if constexpr (N % 16 == 1) {
+            // ---- the last token row r = N - 1: S[r][j] by dp4a for keys j = lane, lane + 32, the
+            // same fp32 softmax steps as the m-tiles (one fma per logit and per exponent,
+            // e * fl(inv_p * rcp(sum))), Pq into smem, O[r][n] = Pq . v^T[n] by dp4a for n = lane
+            constexpr int r = N - 1;
+            uint32_t qw[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) qw[k] = reinterpret_cast<const uint32_t*>(sQ + r * 32)[k];
+            const int rr = masked ? region(r) : 0;
+            float lv[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int j = (int)lane + 32 * t;
+                float l = -INFINITY;
+                if (j < N) {
+                    const uint32_t* kr = reinterpret_cast<const uint32_t*>(sK + j * 32);
+                    int acc = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) acc = __dp4a((int)qw[k], (int)kr[k], acc);
+                    l = __fmaf_rn((float)acc, a.m3, bias_h[r * NP + j]);
+                    if (masked && region(j) != rr) l = __fadd_rn(l, -100.0f);
+                }
+                lv[t] = l;
+            }
+            float mx = fmaxf(lv[0], lv[1]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float nm = -__fmul_rn(mx, L2E);
+            const float e0 = ex2_approx(__fmaf_rn(lv[0], L2E, nm)), e1 = ex2_approx(__fmaf_rn(lv[1], L2E, nm));
+            float sm = __fadd_rn(e0, e1);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sm = __fadd_rn(sm, __shfl_xor_sync(0xffffffffu, sm, o));
+            const float qs = __fmul_rn(a.inv_p, rcp_approx(sm));
+            const uint32_t p0 = f2u8_rn_sat(__fmul_rn(e0, qs)), p1 = f2u8_rn_sat(__fmul_rn(e1, qs));
+            sP[lane] = (uint8_t)p0;
+            if ((int)lane + 32 < KP) sP[lane + 32] = (int)lane + 32 < N ? (uint8_t)p1 : (uint8_t)0;
+            if (a.p_tap) {
+                int8_t* pt = a.p_tap + (win * a.heads + h) * (int64_t)N * N + (int64_t)r * N;
+                pt[lane] = (int8_t)p0;
+                if ((int)lane + 32 < N) pt[lane + 32] = (int8_t)p1;
+            }
+            __syncwarp();
+            const uint32_t* pw = reinterpret_cast<const uint32_t*>(sP);
+            const uint32_t* vw = reinterpret_cast<const uint32_t*>(sVt + lane * KP);
+            int ov = 0;
+#pragma unroll
+            for (int w = 0; w < KP / 4; ++w) ov = __dp4a((int)pw[w], (int)vw[w], ov);
+            const int qo = min(max(__float2int_rn(__fmul_rn((float)ov, a.m_o)) + a.z_a, -128), 127);
+            a.out[raster(r) * C + h * 32 + lane] = (int8_t)qo;
+            __syncwarp();   // (the P row is rewritten by the next window)
         }
         __syncwarp();   // (q / k / v^T are restaged by the next window)
     }
