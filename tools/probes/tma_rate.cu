@@ -136,6 +136,45 @@ __global__ void __launch_bounds__(64, 1) ring_rot(const __grid_constant__ CUtens
     }
 }
 
+// Row-strided source: a [rows][ld] int8 matrix read as {128 B x box_rows} boxes (the GEMM operand
+// pattern: K-blocks of 128 B out of rows of C or H bytes), one ring, one box per stage.
+__global__ void __launch_bounds__(64, 1) ring_ld(const __grid_constant__ CUtensorMap tm, int S, int items, int rows_total,
+                                                  int box_rows, int nkb) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t box = (uint32_t)box_rows * 128u;
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t bars = base + (uint32_t)S * box;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { mbar_init(bars + 8u * s, 1); mbar_init(bars + 8u * (S + s), 1); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int s = 0; uint32_t ph = 0;
+        for (int it = 0; it < items; ++it) {
+            mbar_wait(bars + 8u * (S + s), ph ^ 1u);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(bars + 8u * s, box);
+                const int kb = it % nkb;
+                const int row = (int)(((unsigned)(it / nkb) * (unsigned)box_rows + blockIdx.x * 512u) % (unsigned)rows_total);
+                tma_load_2d(&tm, base + (uint32_t)s * box, bars + 8u * s, kb * 128, row);
+            }
+            __syncwarp();
+            if (++s == S) { s = 0; ph ^= 1u; }
+        }
+    } else {
+        int s = 0; uint32_t ph = 0;
+        for (int it = 0; it < items; ++it) {
+            mbar_wait(bars + 8u * s, ph);
+            __syncwarp();
+            if (elect_one()) mbar_arrive(bars + 8u * (S + s));
+            __syncwarp();
+            if (++s == S) { s = 0; ph ^= 1u; }
+        }
+    }
+}
+
 int main() {
     const int rows_total = 8192;   // 1 MB, L2 resident
     int8_t* w; cudaMalloc(&w, (size_t)rows_total * 128);
@@ -169,6 +208,35 @@ int main() {
                 const double bytes = (double)items * box * P;
                 printf("box %3d rows (%2d KB) rings %d S %d grid %3d: %.1f B/ns per SM, %.0f GB/s total\n", box_rows,
                        box / 1024, P, S, grid, bytes / (ms * 1e6), bytes * grid / (ms * 1e6));
+            }
+        }
+    }
+    {
+        cudaFuncSetAttribute(ring_ld, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        int8_t* w2; cudaMalloc(&w2, (size_t)16 << 20);
+        cudaMemset(w2, 1, (size_t)16 << 20);
+        for (int ld : {128, 512, 2048}) for (int box_rows : {128, 256}) {
+            const int rows = (8 << 20) / ld;   // 8 MB matrix, L2 resident
+            CUtensorMap tm;
+            cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows}; cuuint64_t str[1] = {(cuuint64_t)ld};
+            cuuint32_t bx[2] = {128, (cuuint32_t)box_rows}; cuuint32_t es[2] = {1, 1};
+            enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, w2, dims, str, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            const int box = box_rows * 128, S = box_rows == 128 ? 8 : 6, items = (64 << 20) / box / 8;
+            const int smem = S * box + 1024 + 16 * S + 64;
+            for (int grid : {1, 148}) {
+                int a0 = S, a1 = items, a2 = rows, a3 = box_rows, a4 = ld / 128;
+                void* args[] = {(void*)&tm, (void*)&a0, (void*)&a1, (void*)&a2, (void*)&a3, (void*)&a4};
+                cudaLaunchKernel((const void*)ring_ld, dim3(grid), dim3(64), args, smem, 0);
+                if (cudaDeviceSynchronize() != cudaSuccess) { printf("error\n"); return 1; }
+                cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                cudaLaunchKernel((const void*)ring_ld, dim3(grid), dim3(64), args, smem, 0);
+                cudaEventRecord(e1); cudaEventSynchronize(e1);
+                float ms; cudaEventElapsedTime(&ms, e0, e1);
+                const double bytes = (double)items * box;
+                printf("STRIDE ld %4d box %3d rows S %d grid %3d: %.1f B/ns per SM, %.0f GB/s total\n", ld, box_rows, S,
+                       grid, bytes / (ms * 1e6), bytes * grid / (ms * 1e6));
             }
         }
     }
