@@ -175,6 +175,50 @@ __global__ void __launch_bounds__(64, 1) ring_ld(const __grid_constant__ CUtenso
     }
 }
 
+// 3-D boxes: {128 B of K, 128 rows, KB K-blocks} of a [rows][ld] matrix seen as dims {128, rows, ld/128}
+// (strides ld, 128): one TMA op lands KB consecutive K-blocks as [KB][128 rows][128 B] (SW128 K-major)
+__device__ __forceinline__ void tma_load_3d(const void* tmap, uint32_t dst, uint32_t bar, int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__global__ void __launch_bounds__(64, 1) ring_3d(const __grid_constant__ CUtensorMap tm, int S, int items, int rows_total,
+                                                  int KB, int nkb) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t box = 128u * 128u * (uint32_t)KB;
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t bars = base + (uint32_t)S * box;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { mbar_init(bars + 8u * s, 1); mbar_init(bars + 8u * (S + s), 1); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int s = 0; uint32_t ph = 0;
+        for (int it = 0; it < items; ++it) {
+            mbar_wait(bars + 8u * (S + s), ph ^ 1u);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(bars + 8u * s, box);
+                const int kb = (it * KB) % nkb;
+                const int row = (int)(((unsigned)(it * KB / nkb) * 128u + blockIdx.x * 512u) % (unsigned)rows_total);
+                tma_load_3d(&tm, base + (uint32_t)s * box, bars + 8u * s, 0, row, kb);
+            }
+            __syncwarp();
+            if (++s == S) { s = 0; ph ^= 1u; }
+        }
+    } else {
+        int s = 0; uint32_t ph = 0;
+        for (int it = 0; it < items; ++it) {
+            mbar_wait(bars + 8u * s, ph);
+            __syncwarp();
+            if (elect_one()) mbar_arrive(bars + 8u * (S + s));
+            __syncwarp();
+            if (++s == S) { s = 0; ph ^= 1u; }
+        }
+    }
+}
+
 int main() {
     const int rows_total = 8192;   // 1 MB, L2 resident
     int8_t* w; cudaMalloc(&w, (size_t)rows_total * 128);
@@ -237,6 +281,37 @@ int main() {
                 const double bytes = (double)items * box;
                 printf("STRIDE ld %4d box %3d rows S %d grid %3d: %.1f B/ns per SM, %.0f GB/s total\n", ld, box_rows, S,
                        grid, bytes / (ms * 1e6), bytes * grid / (ms * 1e6));
+            }
+        }
+    }
+    {
+        cudaFuncSetAttribute(ring_3d, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        int8_t* w3; cudaMalloc(&w3, (size_t)16 << 20);
+        cudaMemset(w3, 1, (size_t)16 << 20);
+        const int ld = 2048, rows = (8 << 20) / ld, nkb = ld / 128;
+        for (int KB : {1, 2, 4}) {
+            CUtensorMap tm;
+            cuuint64_t dims[3] = {128, (cuuint64_t)rows, (cuuint64_t)nkb};
+            cuuint64_t str[2] = {(cuuint64_t)ld, 128};
+            cuuint32_t bx[3] = {128, 128, (cuuint32_t)KB}; cuuint32_t es[3] = {1, 1, 1};
+            CUresult er = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, w3, dims, str, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (er != CUDA_SUCCESS) { printf("3D encode failed %d (KB %d)\n", (int)er, KB); continue; }
+            const int box = 16384 * KB, S = KB == 1 ? 8 : KB == 2 ? 6 : 3, items = (64 << 20) / box / 8;
+            const int smem = S * box + 1024 + 16 * S + 64;
+            for (int grid : {1, 148}) {
+                int a0 = S, a1 = items, a2 = rows, a3 = KB, a4 = nkb;
+                void* args[] = {(void*)&tm, (void*)&a0, (void*)&a1, (void*)&a2, (void*)&a3, (void*)&a4};
+                cudaLaunchKernel((const void*)ring_3d, dim3(grid), dim3(64), args, smem, 0);
+                if (cudaDeviceSynchronize() != cudaSuccess) { printf("error 3d\n"); return 1; }
+                cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                cudaLaunchKernel((const void*)ring_3d, dim3(grid), dim3(64), args, smem, 0);
+                cudaEventRecord(e1); cudaEventSynchronize(e1);
+                float ms; cudaEventElapsedTime(&ms, e0, e1);
+                const double bytes = (double)items * box;
+                printf("BOX3D 128 rows x %d K-blocks (%d KB) S %d grid %3d: %.1f B/ns per SM, %.0f GB/s total\n", KB, box / 1024,
+                       S, grid, bytes / (ms * 1e6), bytes * grid / (ms * 1e6));
             }
         }
     }
