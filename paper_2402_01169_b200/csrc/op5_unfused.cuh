@@ -20,6 +20,7 @@
 #include <cstdint>
 
 #include "mlp_kernels.cuh"
+#include "attn_kernels.cuh"   // (FastDiv)
 
 namespace swinmlp {
 
@@ -108,6 +109,7 @@ struct ShiftGeluArgs {
     float inv_g;         // fl(1/s_g)
     float k_g;           // fl(fl(s_g * inv_h) * 2^-7)
     int32_t x0;          // floor(-1 / fl(1.702 s_g)) < 0
+    FastDiv divx0;       // by |x0| (ShiftExp's q = floor(p / x0) = |p| / |x0| for p <= 0)
     int32_t z_h;
     int32_t H;
     int64_t T;
@@ -119,10 +121,10 @@ __device__ __forceinline__ int32_t sg_quant_in(int32_t a, float m, float b, floa
 }
 
 // ShiftExp(x <= 0) with n = 15 (see swin_mlp_int8.h): 2^(x S log2 e) on the scale 2^15 |x0|.
-__device__ __forceinline__ int64_t sg_shift_exp(int32_t x, int32_t x0) {
+__device__ __forceinline__ int64_t sg_shift_exp(int32_t x, int32_t x0, const FastDiv& dx0) {
     int32_t p = x + (x >> 1) - (x >> 4);             // arithmetic shifts: floor(x/2), floor(x/16)
     p = max(p, 15 * x0);
-    const int32_t q = p / x0;                        // p <= 0, x0 < 0: truncation == floor
+    const int32_t q = (int32_t)fdiv((uint32_t)(-p), dx0);   // p <= 0, x0 < 0: floor(p / x0) = |p| / |x0|
     const int32_t m = p - q * x0 - 2 * x0;           // r - 2 x0 > 0
     const int64_t e = 14 - q >= 0 ? (int64_t)m << (14 - q) : (int64_t)(m >> 1);
     return e > 0 ? e : 0;
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(kOp5Threads) op5_shiftgelu_kernel(const __grid
     for (int64_t t = warp; t < p.T; t += nwarps) {
         const int4* row = reinterpret_cast<const int4*>(p.a1 + t * p.H);
         int32_t im = -32768;
+#pragma unroll 2
         for (int k = lane; k < H4; k += 32) {   // pass 1: the row max of I
             const int4 a = __ldg(row + k);
             const float4 mv = __ldg(reinterpret_cast<const float4*>(p.m1) + k);
@@ -148,8 +151,9 @@ __global__ void __launch_bounds__(kOp5Threads) op5_shiftgelu_kernel(const __grid
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) im = max(im, __shfl_xor_sync(0xffffffffu, im, o));
-        const int64_t e_m = sg_shift_exp(im > 0 ? -im : 0, p.x0);
+        const int64_t e_m = sg_shift_exp(im > 0 ? -im : 0, p.x0, p.divx0);
         uint32_t* out = reinterpret_cast<uint32_t*>(p.hq + t * p.H);
+#pragma unroll 2
         for (int k = lane; k < H4; k += 32) {   // pass 2 (A1 from L2)
             const int4 a = __ldg(row + k);
             const float4 mv = __ldg(reinterpret_cast<const float4*>(p.m1) + k);
@@ -159,11 +163,17 @@ __global__ void __launch_bounds__(kOp5Threads) op5_shiftgelu_kernel(const __grid
             int32_t qv[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int64_t e_x = sg_shift_exp(I[j] - im, p.x0);
+                const int64_t e_x = sg_shift_exp(I[j] - im, p.x0, p.divx0);
                 const int64_t sum = min(e_x + e_m, (int64_t)2147483647);
-                // floor((2^31 - 1) / sum): the double quotient, corrected to the exact floor
+                // floor((2^31 - 1) / sum): an fp32 reciprocal estimate (relative error < 2^-21, so
+                // off by at most 2^10 / sum + 1), corrected to the exact floor with integer products;
+                // small sums (rare: both exponentials tiny) take the double quotient
                 int64_t f = 0;
-                if (sum > 0) {
+                if (sum >= 4096) {
+                    f = (int64_t)__fmul_rn(2147483647.0f, __frcp_rn((float)sum));
+                    while (f * sum > 2147483647LL) --f;
+                    while ((f + 1) * sum <= 2147483647LL) ++f;
+                } else if (sum > 0) {
                     f = (int64_t)(2147483647.0 / (double)sum);
                     if (f * sum > 2147483647LL) --f;
                     else if ((f + 1) * sum <= 2147483647LL) ++f;

@@ -864,6 +864,7 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
         volatile float k_g = sgih * 0.0078125f;
         h->sg.inv_g = inv_g; h->sg.k_g = k_g;
         h->sg.x0 = (int32_t)std::floor(-1.0 / (double)S);
+        h->sg.divx0 = make_fastdiv((uint32_t)(-h->sg.x0));
         h->sg.z_h = d.h_zero_point;
         int per_sm = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->sg_fn, kOp5Threads, 0));

@@ -2,7 +2,7 @@
 CUDA events on the launching stream, back-to-back runs, L2 flushed before each run) and its plan.
 Plan switches are the SWIN_MLP_* environment variables read at create time (see swin_mlp_int8.cu).
 
-usage: python tools/layer_sweep.py C T [iters]   -> one JSON line"""
+usage: python tools/layer_sweep.py C T [iters] [relu|gelu|shiftgelu]   -> one JSON line"""
 import json
 import os
 import sys
@@ -15,7 +15,8 @@ from paper_2402_01169_b200 import SwinMlpInt8Layer, swin_mlp_int8_workspace_byte
 
 C, T = int(sys.argv[1]), int(sys.argv[2])
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-L = synth.make_layer(C, synth.layer_seed(4, 2, 0), act=synth.ACT_RELU)
+act = {"relu": synth.ACT_RELU, "gelu": synth.ACT_GELU, "shiftgelu": synth.ACT_SHIFT_GELU}[sys.argv[4] if len(sys.argv) > 4 else "relu"]
+L = synth.make_layer(C, synth.layer_seed(4, 2, 0), act=act)
 h = SwinMlpInt8Layer(L, device=0)
 x = torch.from_numpy(synth.make_activations(L, T, 7)).cuda()
 y = torch.empty_like(x)
