@@ -136,7 +136,11 @@ size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T);
  *   T >= 0 (T == 0: no launch, SWIN_MLP_OK)
  *   workspace    >= swin_mlp_int8_workspace_bytes(h, T) bytes, device, 128-byte aligned
  *   stream       cudaStream_t (NULL = legacy default stream)
- * Ownership: all buffers are the caller's; nothing is retained after return. */
+ * Ownership: all buffers are the caller's; nothing is retained after return.
+ * Concurrency: for T <= 64 (the one-launch plan) the kernel reduces FC2 into a
+ * handle-owned int32 scratch [64][C] and counter, which it leaves zeroed on exit; two runs of ONE
+ * handle must therefore be ordered (same stream, or an event between streams).  Distinct handles
+ * never share scratch, and runs with T > 64 use only the caller's workspace. */
 swin_mlp_status_t swin_mlp_int8_run(swin_mlp_int8_t h, const int8_t* x, const float* residual,
                                     int8_t* y, float* residual_out, int64_t T,
                                     void* workspace, size_t workspace_bytes, void* stream);

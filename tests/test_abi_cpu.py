@@ -62,6 +62,8 @@ def test_sm100a_code_only():
             assert "LDG" in f and "STG" in f and "SHFL" in f, name
         elif "attn_core_kernel" in name:   # op #3 core: warp mma.sync (IMMA) on 49 / 144-token windows
             assert "IMMA" in f and "MUFU.EX2" in f and "LDS" in f, name
+        elif "small_mlp_kernel" in name:   # one-launch plan: FC2 partials by bulk reduce-add, op #6 by STG
+            assert "UTCIMMA" in f and "LDTM" in f and "UTMALDG" in f and "UBLKRED" in f, name
         elif "mlp_gemm_kernelILi3E" in name:   # EP_ACC: FC1 storing int32 A1 from registers
             assert "UTCIMMA" in f and "LDTM" in f and "STG" in f, name
         else:
