@@ -11,6 +11,8 @@
 //           part_j = Hq_j . W2[:, 128 j .. 128 j + 127]^T     (tcgen05, 256-col pieces,
 //                                                              2 TMEM buffers), staged in smem
 //                    and bulk-reduce-added (cp.reduce.async.bulk .add.s32) into acc[T][C]
+//                    (the L2's reduction throughput, ~0.65 TB/s for these 24-way sums, sets the
+//                    pace; one TMA tensor reduce-add per 32-column group measured no faster)
 //   all:    arrival counter == P (release / acquire at gpu scope)
 //           rows r = j, j + P, ...: A2 = acc[r] - z_h wsum2 (int32 sums: exact in any order),
 //           then op #6 (dQ, bias, residual, LayerNorm, Q) with the row in registers of one
@@ -218,11 +220,25 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 const int ch = (int)half * 4 + c4, cl = ch * 16, n0 = (int)j * 128 + cl;
                 float v[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int32_t a = (int32_t)r[c4][e] - __float_as_int(cm[256 + cl + e]);
-                    if (p.acc1_tap && valid) p.acc1_tap[(int64_t)row * p.H + n0 + e] = a;
-                    const float yv = __fmaf_rn(__int2float_rn(a), cm[cl + e], cm[128 + cl + e]);
-                    v[e] = __fmul_rn(ACT ? gelu_erf_f32(yv) : yv, p.inv_h);   // (ReLU: the max folds into Q)
+                for (int e4 = 0; e4 < 4; ++e4) {   // four columns per 16-B constant load
+                    const float4 mv = *reinterpret_cast<const float4*>(cm + cl + 4 * e4);
+                    const float4 bv = *reinterpret_cast<const float4*>(cm + 128 + cl + 4 * e4);
+                    const int4 zv = *reinterpret_cast<const int4*>(cm + 256 + cl + 4 * e4);
+                    const int32_t a[4] = {(int32_t)r[c4][4 * e4] - zv.x, (int32_t)r[c4][4 * e4 + 1] - zv.y,
+                                          (int32_t)r[c4][4 * e4 + 2] - zv.z, (int32_t)r[c4][4 * e4 + 3] - zv.w};
+                    if (p.acc1_tap && valid)
+                        *reinterpret_cast<int4*>(p.acc1_tap + (int64_t)row * p.H + n0 + 4 * e4) = make_int4(a[0], a[1], a[2], a[3]);
+                    float2 y0 = f2_fma(make_float2(__int2float_rn(a[0]), __int2float_rn(a[1])), make_float2(mv.x, mv.y),
+                                       make_float2(bv.x, bv.y));
+                    float2 y1 = f2_fma(make_float2(__int2float_rn(a[2]), __int2float_rn(a[3])), make_float2(mv.z, mv.w),
+                                       make_float2(bv.z, bv.w));
+                    if (ACT) {
+                        y0 = make_float2(gelu_erf_f32(y0.x), gelu_erf_f32(y0.y));
+                        y1 = make_float2(gelu_erf_f32(y1.x), gelu_erf_f32(y1.y));
+                    }
+                    const float2 ih = make_float2(p.inv_h, p.inv_h);   // (ReLU: the max folds into Q)
+                    const float2 t0 = f2_mul(y0, ih), t1 = f2_mul(y1, ih);
+                    v[4 * e4] = t0.x; v[4 * e4 + 1] = t0.y; v[4 * e4 + 2] = t1.x; v[4 * e4 + 3] = t1.y;
                 }
                 uint32_t w[4];
                 if (ACT) {
@@ -300,17 +316,24 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             int4 a4[G];
             uint32_t xw[G];
             float4 m4[G], b4[G], r4[G];
+            constexpr bool PRE = G <= 8;   // gamma / beta in the same round trip (register budget)
+            float4 g4[PRE ? G : 1], t4[PRE ? G : 1];
 #pragma unroll
             for (int v = 0; v < G; ++v) {
                 const int c = 4 * (int)lane + 128 * v;
-                int4* ap = reinterpret_cast<int4*>(p.acc + (int64_t)r * C + c);
-                a4[v] = __ldcg(ap);                   // the P partials' exact int32 sum
-                __stcg(ap, make_int4(0, 0, 0, 0));    // zero again for the next run
+                a4[v] = __ldcg(reinterpret_cast<const int4*>(p.acc + (int64_t)r * C + c));   // the P partials' exact sum
                 m4[v] = __ldg(reinterpret_cast<const float4*>(p.m2 + c));
                 b4[v] = p.b2 ? __ldg(reinterpret_cast<const float4*>(p.b2 + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
                 if (p.resid) r4[v] = __ldg(reinterpret_cast<const float4*>(p.resid + (int64_t)r * C + c));
                 else xw[v] = __ldg(reinterpret_cast<const uint32_t*>(p.x + (int64_t)r * C + c));
+                if constexpr (PRE) {
+                    g4[v] = __ldg(reinterpret_cast<const float4*>(p.gamma + c));
+                    t4[v] = __ldg(reinterpret_cast<const float4*>(p.beta + c));
+                }
             }
+#pragma unroll
+            for (int v = 0; v < G; ++v)   // zero again for the next run
+                __stcg(reinterpret_cast<int4*>(p.acc + (int64_t)r * C + 4 * (int)lane + 128 * v), make_int4(0, 0, 0, 0));
             float z[G][4];
             float s = 0.f;
 #pragma unroll
@@ -357,8 +380,13 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
 #pragma unroll
             for (int v = 0; v < G; ++v) {
                 const int c = 4 * (int)lane + 128 * v;
-                const float4 gv = __ldg(reinterpret_cast<const float4*>(p.gamma + c));
-                const float4 bv = __ldg(reinterpret_cast<const float4*>(p.beta + c));
+                float4 gv, bv;
+                if constexpr (PRE) {
+                    gv = g4[PRE ? v : 0]; bv = t4[PRE ? v : 0];
+                } else {
+                    gv = __ldg(reinterpret_cast<const float4*>(p.gamma + c));
+                    bv = __ldg(reinterpret_cast<const float4*>(p.beta + c));
+                }
                 const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};
                 float yh[4];
                 int q[4];

@@ -17,7 +17,7 @@ __device__ __forceinline__ void st16(uint32_t a, const uint32_t (&r)[16]) {
                    "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
 }
 
-template <int MODE>   // 0: ld + wait each, 1: 4 lds then wait, 2: st
+template <int MODE>   // 0: ld + wait each, 1: 4 lds then wait, 2: st, 3: 4 lds then wait, rotating over all 512 columns
 __global__ void __launch_bounds__(640, 1) probe(int iters, int nwarps, unsigned long long* out, uint32_t* sink) {
     __shared__ uint32_t slot;
     const uint32_t warp = threadIdx.x >> 5;
@@ -45,6 +45,12 @@ __global__ void __launch_bounds__(640, 1) probe(int iters, int nwarps, unsigned 
                 ld16(tb + col0, r); ld16(tb + col0 + 16, a); ld16(tb + col0 + 32, b); ld16(tb + col0 + 48, c);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 acc ^= r[0] ^ a[3] ^ b[7] ^ c[15];
+            } else if (MODE == 3) {
+                uint32_t a[16], b[16], c[16];
+                const uint32_t cb = ((uint32_t)(i * 64 + warp * 128)) & 511u;
+                ld16(tb + cb, r); ld16(tb + cb + 16, a); ld16(tb + cb + 32, b); ld16(tb + cb + 48, c);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                acc ^= r[0] ^ a[3] ^ b[7] ^ c[15] ^ r[9] ^ a[11];
             } else {
                 for (int k = 0; k < 16; ++k) r[k] = acc + k;
                 st16(tb + col0 + (i & 3) * 16, r);
@@ -66,17 +72,17 @@ int main() {
     unsigned long long* out; uint32_t* sink;
     cudaMalloc(&out, 8 * 148); cudaMalloc(&sink, 4 * 640);
     const int iters = 4096;
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
         for (int nw : {1, 4, 8, 16, 20}) {
-            auto k = mode == 0 ? probe<0> : mode == 1 ? probe<1> : probe<2>;
+            auto k = mode == 0 ? probe<0> : mode == 1 ? probe<1> : mode == 2 ? probe<2> : probe<3>;
             k<<<1, 640>>>(iters, nw, out, sink);
             cudaDeviceSynchronize();
             unsigned long long c = 0;
             cudaMemcpy(&c, out, 8, cudaMemcpyDeviceToHost);
-            const double per = mode == 1 ? 4.0 : 1.0;
+            const double per = (mode == 1 || mode == 3) ? 4.0 : 1.0;
             const double bytes = (double)iters * nw * 32 * 16 * 4 * per;
             printf("mode %d (%s) warps %2d: %8llu clk  %.1f B/clk  %.1f clk/instr/warp\n", mode,
-                   mode == 0 ? "ld16+wait" : mode == 1 ? "4xld16+wait" : "st16+wait", nw, c, bytes / c,
+                   mode == 0 ? "ld16+wait" : mode == 1 ? "4xld16+wait" : mode == 2 ? "st16+wait" : "4xld16 rot", nw, c, bytes / c,
                    (double)c / iters / per);
         }
     }
