@@ -137,10 +137,11 @@ size_t swin_mlp_int8_workspace_bytes(swin_mlp_int8_t h, int64_t T);
  *   workspace    >= swin_mlp_int8_workspace_bytes(h, T) bytes, device, 128-byte aligned
  *   stream       cudaStream_t (NULL = legacy default stream)
  * Ownership: all buffers are the caller's; nothing is retained after return.
- * Concurrency: for T <= 64 (the one-launch plan) the kernel reduces FC2 into a
- * handle-owned int32 scratch [64][C] and counter, which it leaves zeroed on exit; two runs of ONE
- * handle must therefore be ordered (same stream, or an event between streams).  Distinct handles
- * never share scratch, and runs with T > 64 use only the caller's workspace. */
+ * Concurrency: for T <= 64 (the one-launch plan; clusters of up to 8 CTAs) the
+ * kernel reduces FC2 into a handle-owned int32 scratch [64][C] and counter, which it leaves
+ * zeroed on exit; two runs of ONE handle must therefore be ordered (same stream, or an event
+ * between streams).  Distinct handles never share scratch, and runs with T > 64 use only the
+ * caller's workspace. */
 swin_mlp_status_t swin_mlp_int8_run(swin_mlp_int8_t h, const int8_t* x, const float* residual,
                                     int8_t* y, float* residual_out, int64_t T,
                                     void* workspace, size_t workspace_bytes, void* stream);
@@ -228,7 +229,8 @@ int32_t swin_mlp_int8_plan(swin_mlp_int8_t h, int32_t* out10);
  * chooses per run: the few-tile plans for one or two m-tiles, the CTA-pair op #6 for at
  * most one wave of pairs, else the defaults).  Same 20-entry layout as
  * swin_mlp_int8_plan with entries 0-11 and 16 describing the chosen plans, and entry 19 =
- * op5_unfused | (choice << 1), choice 0 = default, 1 = CTA-pair op #6, 2 = few-tile, and
+ * op5_unfused | (choice << 1), choice 0 = default, 1 = CTA-pair op #6, 2 = few-tile,
+ * 3 = one launch for T <= 64 (entries 0 = CTAs, 4 = FC2 columns per CTA, 5 = cluster size), and
  * entry 13 = the op #6 split-K factor S of this run (1 = none; S > 1 splits FC2's K = H
  * over S clusters per m-tile when the unsplit grid would fill at most half the SMs).
  * The plan hint (swin_mlp_int8_set_plan_hint), when set, replaces T.  For a one-kernel

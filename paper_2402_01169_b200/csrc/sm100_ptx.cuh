@@ -284,6 +284,15 @@ __device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uin
                  ::"r"(remote_addr), "l"(__double_as_longlong(v)), "r"(remote_bar) : "memory");
 }
 
+// Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory into a (possibly remote)
+// CTA's shared memory (cluster address), signalling complete_tx(bytes) on the mbarrier at
+// `remote_bar` in that CTA.
+__device__ __forceinline__ void bulk_copy_s2cluster(uint32_t remote_dst, uint32_t src, uint32_t bytes,
+                                                    uint32_t remote_bar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(remote_dst), "r"(src), "r"(bytes), "r"(remote_bar) : "memory");
+}
+
 __device__ __forceinline__ void st_async_val(uint32_t remote_addr, double v, uint32_t remote_bar) {
     st_async_f64(remote_addr, v, remote_bar);
 }

@@ -4,21 +4,24 @@
 // At T <= 64 the layer is a chain of latencies, not of bandwidth: the
 // two-kernel plan pays two launches, the programmatic-dependent hand-off, FC2's K = 4C on a
 // few SMs and a one-tile LayerNorm.  Here the hidden dimension is split over P = H / 128 CTAs
-// (one per SM, all co-resident) and nothing but the int32 FC2 partials leaves the SM:
+// (one per SM, all co-resident), in clusters of Q CTAs (S = P / Q slices of Q * 128 hidden
+// columns), and nothing but int32 FC2 partials leaves the cluster:
 //
-//   CTA j:  acc1_j = X . W1[128 j .. 128 j + 127]^T          (tcgen05, TMEM cols [0, 128))
-//           Hq_j   = op #5(acc1_j)                            (smem, SW128 K-major: FC2's A)
-//           part_j = Hq_j . W2[:, 128 j .. 128 j + 127]^T     (tcgen05, 256-col pieces,
-//                                                              2 TMEM buffers), staged in smem
-//                    and bulk-reduce-added (cp.reduce.async.bulk .add.s32) into acc[T][C]
-//                    (the L2's reduction throughput, ~0.65 TB/s for these 24-way sums, sets the
-//                    pace; one TMA tensor reduce-add per 32-column group measured no faster)
+//   CTA j = Q s + g (cluster s, rank g):
+//           acc1_j = X . W1[128 j .. 128 j + 127]^T            (tcgen05, TMEM cols [0, 128))
+//           Hq_j   = op #5(acc1_j)                              (smem slot g of the cluster's Hq
+//                    tile, SW128 K-major; bulk-copied into slot g of the Q - 1 peers: DSMEM)
+//           part   = Hq_s . W2[g PR .. g PR + PR - 1, slice s]^T (tcgen05, PR = C / Q columns,
+//                    K = Q * 128), staged in smem and bulk-reduce-added (cp.reduce.async.bulk
+//                    .add.s32) into acc[T][C]: S-way sums instead of P-way ones
 //   all:    arrival counter == P (release / acquire at gpu scope)
 //           rows r = j, j + P, ...: A2 = acc[r] - z_h wsum2 (int32 sums: exact in any order),
 //           then op #6 (dQ, bias, residual, LayerNorm, Q) with the row in registers of one
 //           warp; the row of acc is zeroed again after it is read, and the last CTA to leave
 //           resets the counters: acc and the counters are all zero between runs (handle-owned,
 //           so runs of one handle must be stream-ordered).
+// The L2's reduction throughput (≈ 0.65 TB/s for these many-way int32 sums) set the pace of the
+// P-way version (3.6 MB at C = 768, T = 49); the cluster split divides those bytes by Q.
 //
 // Same arithmetic as the other plans: A1, Hq, A2 and z bit-exact; the LayerNorm statistics
 // are the fp32 two-pass of the row held by one warp (Y within the R15 tier).
@@ -37,17 +40,23 @@ namespace swinmlp {
 constexpr int kSThreads = 32 * 10;
 constexpr int kSMaxT = 64;
 constexpr int kSStages = 4;
-constexpr uint32_t kSSlot = 32768;                 // FC1 {A 16 KB (64 rows loaded), B 16 KB} | W2 piece
-constexpr uint32_t kSHq = kSStages * kSSlot;       // [128 rows][128 B] SW128 hidden tile
-constexpr uint32_t kSStageRow = 256 * 4 + 16;      // one int32 partial row of a piece (+16 B: bank shift)
-constexpr uint32_t kSStage = kSHq + 16384;         // [64 rows][kSStageRow] partial staging
-constexpr uint32_t kSConst = kSStage + kSMaxT * kSStageRow;   // m1, b1, zc1 of the CTA's 128 columns
+constexpr int kSMaxQ = 8;                          // cluster size (portable maximum)
+constexpr uint32_t kSSlot = 32768;                 // FC1 {A 16 KB (64 rows loaded), B 16 KB} | W2 K-block
+constexpr uint32_t kSHq = kSStages * kSSlot;       // Hq: Q K-blocks of [64 rows][128 B] SW128, 8 KB apart
+                                                   // (+ 8 KB: the M = 128 MMA's rows 64-127 of the last one,
+                                                   // which land in TMEM lanes that carry no tokens)
+constexpr uint32_t kSHqSlot = 8192;
+constexpr uint32_t kSStageRow = 256 * 4 + 16;      // one int32 partial row (+16 B: bank shift)
+constexpr uint32_t kSStage = 0;                    // [64 rows][kSStageRow] partial staging, over the
+                                                   // operand ring (free once FC2's MMAs completed)
+constexpr uint32_t kSConst = kSHq + (kSMaxQ + 1) * kSHqSlot;   // m1, b1, zc1 of the CTA's 128 columns
 constexpr uint32_t kSBars = kSConst + 3 * 128 * 4;
 constexpr uint32_t kSSmem = kSBars + 256 + 1024;   // + barriers/TMEM slot + alignment slack
 
 struct SmallArgs {
     int32_t T, C, H, P;    // tokens (<= 64), channels, hidden, CTAs (= H / 128)
-    int32_t NP, PR;        // FC2 pieces of PR output columns (NP * PR == C, PR <= 256, PR % 16 == 0)
+    int32_t Q, PR;         // cluster size (P % Q == 0) and FC2 columns per CTA (Q * PR == C, PR <= 256,
+                           // PR % 32 == 0)
     int32_t act;           // 0 ReLU, 1 GELU (exact erf)
     const float* m1; const float* b1; const int32_t* zc1;   // [H]
     const float* m2; const float* b2; const int32_t* zc2;   // [C]
@@ -79,9 +88,10 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t j = blockIdx.x;
     const uint32_t bar_full = base + kSBars, bar_empty = bar_full + 8u * kSStages;
     const uint32_t bar_acc1 = bar_empty + 8u * kSStages, bar_hq = bar_acc1 + 8u;
-    const uint32_t bar_tfull = bar_hq + 8u, bar_tempty = bar_tfull + 16u;
+    const uint32_t bar_tfull = bar_hq + 8u, bar_peer = bar_tfull + 8u;   // FC2 done; peers' Hq landed
     volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (base - raw) + kSBars + 128);
     const int C = p.C, NKB = (C + kBK - 1) / kBK;
+    const uint32_t Q = (uint32_t)p.Q, g = Q > 1 ? cluster_ctarank() : 0u, s_slice = j / Q;
     unsigned long long* trc = p.trace ? p.trace + 16 * blockIdx.x : nullptr;
     if (trc && threadIdx.x == 0) trc[0] = gtimer();
 
@@ -98,17 +108,17 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             }
             mbar_init(bar_acc1, 1);
             mbar_init(bar_hq, 8);
-            for (int b = 0; b < 2; ++b) {
-                mbar_init(bar_tfull + 8u * b, 1);
-                mbar_init(bar_tempty + 8u * b, 8);
-            }
+            mbar_init(bar_tfull, 1);
+            mbar_init(bar_peer, 1);
+            if (Q > 1) mbar_arrive_expect_tx(bar_peer, (Q - 1u) * kSHqSlot);   // the peers' Hq slots
             fence_mbar_init();
         }
         __syncwarp();
         tmem_alloc(smem_u32(const_cast<uint32_t*>(tmem_slot)), 512);
     }
     tc_fence_before();
-    __syncthreads();
+    if (Q > 1) cluster_sync_all();   // every peer's barriers exist before any copy signals them
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (trc && threadIdx.x == 0) trc[1] = gtimer();
@@ -138,11 +148,12 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 tma_load_2d(&tmX, slot, bar_full + 8u * s, kb * kBK, 0);
                 if (++s == kSStages) { s = 0; ph ^= 1u; }
             }
-            // FC2: W2 pieces [PR rows][128 B] of this CTA's hidden columns
-            for (int pc = 0; pc < p.NP; ++pc) {
+            // FC2: the W2 K-blocks [PR rows of group g][128 hidden columns] of the cluster's slice
+            for (uint32_t kk = 0; kk < Q; ++kk) {
                 mbar_wait(bar_empty + 8u * s, ph ^ 1u);
                 mbar_arrive_expect_tx(bar_full + 8u * s, (uint32_t)p.PR * kBK);
-                tma_load_2d(&tmW2, base + (uint32_t)s * kSSlot, bar_full + 8u * s, (int)(j * 128), pc * p.PR);
+                tma_load_2d(&tmW2, base + (uint32_t)s * kSSlot, bar_full + 8u * s, (int)((s_slice * Q + kk) * 128),
+                            (int)g * p.PR);
                 if (++s == kSStages) { s = 0; ph ^= 1u; }
             }
         }
@@ -167,21 +178,20 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             __syncwarp();
             if (++s == kSStages) { s = 0; ph ^= 1u; }
         }
-        mbar_wait(bar_hq, 0);   // Hq staged (and acc1 drained: FC2 piece 0 reuses its columns)
+        mbar_wait(bar_hq, 0);                // this CTA's Hq slot staged
+        if (Q > 1) mbar_wait(bar_peer, 0);   // ... and the peers' (DSMEM bulk copies)
         tc_fence_after();
         if (trc && lane == 0) trc[4] = gtimer();
-        for (int pc = 0; pc < p.NP; ++pc) {
-            const uint32_t b = pc & 1u;
-            mbar_wait(bar_tempty + 8u * b, ((pc >> 1) & 1) ^ 1u);
+        for (uint32_t kk = 0; kk < Q; ++kk) {   // K = Q * 128: the cluster's hidden slice
             mbar_wait(bar_full + 8u * s, ph);
             tc_fence_after();
             const uint32_t slot = base + (uint32_t)s * kSSlot;
             if (elect_one()) {
                 for (int k = 0; k < 4; ++k)
-                    mma_i8(tmem + b * 256u, umma_desc_k128(base + kSHq) + 2u * k, umma_desc_k128(slot) + 2u * k, id2,
-                           k != 0);
+                    mma_i8(tmem + 256u, umma_desc_k128(base + kSHq + kk * kSHqSlot) + 2u * k,
+                           umma_desc_k128(slot) + 2u * k, id2, (kk | (uint32_t)k) != 0u);
                 mma_commit(bar_empty + 8u * s);
-                mma_commit(bar_tfull + 8u * b);
+                if (kk + 1u == Q) mma_commit(bar_tfull);
             }
             __syncwarp();
             if (++s == kSStages) { s = 0; ph ^= 1u; }
@@ -207,7 +217,7 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         tc_fence_after();
         if (trc && ew == 0 && lane == 0) trc[3] = gtimer();
         if (live) {
-            const uint32_t hrow = base + kSHq + row * 128u;
+            const uint32_t hrow = base + kSHq + g * kSHqSlot + row * 128u;   // slot g, rows 0-63
             uint32_t r[4][16];
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4)   // this warp's 64 columns in one round trip
@@ -255,47 +265,50 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             }
         }
         if (trc && ew == 0 && lane == 0) trc[11] = gtimer();
-        fence_proxy_async_smem();   // Hq visible to the tensor core (async proxy)
+        fence_proxy_async_smem();   // Hq visible to the tensor core and the bulk copies (async proxy)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_hq);
-        // ---- FC2 pieces: TMEM -> smem staging -> bulk reduce-add into acc (rows < T)
-        const int hc = p.PR / 2;   // columns per warp half
-        const uint32_t srow = base + kSStage + row * kSStageRow;
-        for (int pc = 0; pc < p.NP; ++pc) {
-            const uint32_t b = pc & 1u;
-            mbar_wait(bar_tfull + 8u * b, (pc >> 1) & 1);
-            tc_fence_after();
-            if (live) {
-                uint32_t r[8][16];   // the warp half's <= 128 columns of the piece, one round trip
-                const int nch = hc / 16;
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (k < nch) tmem_ld16(tmem + ((quad * 32u) << 16) + b * 256u + (uint32_t)((int)half * hc + 16 * k), r[k]);
-                tmem_wait_ld();
-                bulk_wait_read<0>();   // the previous piece's reduce has read this thread's staging
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if (k >= nch) break;
-                    reg_fence16(r[k]);
-                    const int c0 = (int)half * hc + 16 * k;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        st_shared_v4(srow + (uint32_t)(c0 + 4 * q) * 4u, r[k][4 * q], r[k][4 * q + 1], r[k][4 * q + 2],
-                                     r[k][4 * q + 3]);
-                }
-                fence_proxy_async_smem();
-                if (valid) {
-                    bulk_reduce_add_s32(p.acc + (int64_t)row * C + pc * p.PR + (int)half * hc,
-                                        srow + (uint32_t)((int)half * hc) * 4u, (uint32_t)hc * 4u);
-                    bulk_commit();
+        if (Q > 1) {   // the slot to the Q - 1 peers (rows 0-63; their MMA waits on bar_peer)
+            named_bar_sync(2, 256);
+            if (ew == 0 && lane == 0) {
+                const uint32_t src = base + kSHq + g * kSHqSlot;
+                for (uint32_t r = 1; r < Q; ++r) {
+                    const uint32_t peer = (g + r) % Q;
+                    bulk_copy_s2cluster(mapa(src, peer), src, kSHqSlot, mapa(bar_peer, peer));
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty + 8u * b);
-            if (trc && ew == 0 && lane == 0 && pc < 3) trc[6 + pc] = gtimer();
         }
+        // ---- FC2: TMEM -> smem staging -> bulk reduce-add into acc[rows < T][g PR .. g PR + PR)
+        const int hc = p.PR / 2;   // columns per warp half
+        const uint32_t srow = base + kSStage + row * kSStageRow;
+        mbar_wait(bar_tfull, 0);
+        tc_fence_after();
+        if (live) {
+            uint32_t r[8][16];   // the warp half's <= 128 columns, one round trip
+            const int nch = hc / 16;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < nch) tmem_ld16(tmem + ((quad * 32u) << 16) + 256u + (uint32_t)((int)half * hc + 16 * k), r[k]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k >= nch) break;
+                reg_fence16(r[k]);
+                const int c0 = (int)half * hc + 16 * k;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    st_shared_v4(srow + (uint32_t)(c0 + 4 * q) * 4u, r[k][4 * q], r[k][4 * q + 1], r[k][4 * q + 2],
+                                 r[k][4 * q + 3]);
+            }
+            fence_proxy_async_smem();
+            if (valid) {
+                bulk_reduce_add_s32(p.acc + (int64_t)row * C + (int)g * p.PR + (int)half * hc,
+                                    srow + (uint32_t)((int)half * hc) * 4u, (uint32_t)hc * 4u);
+                bulk_commit();
+            }
+        }
+        if (trc && ew == 0 && lane == 0) trc[6] = gtimer();
         if (live && valid) {
             bulk_wait_all();             // this thread's reduce-adds have been performed
             fence_proxy_async_global();  // ... and are ordered before its generic-proxy release below
@@ -414,7 +427,8 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     }
     if (trc && warp == 2 && lane == 0) trc[14] = gtimer();
     tc_fence_before();
-    __syncthreads();
+    if (Q > 1) cluster_sync_all();   // no CTA leaves while a peer's copy may still read its Hq slot
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);

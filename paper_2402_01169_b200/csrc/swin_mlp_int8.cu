@@ -313,6 +313,32 @@ static int one_group_env() {
     return (e && *e == '0') ? 0 : 1;
 }
 
+// The one-launch plan's P / Q clusters must all be co-resident (its CTAs wait on each other).
+template <class F>
+static bool tiny_clusters_fit(F fn, int P, int Q) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSSmem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)P);
+    cfg.blockDim = dim3((unsigned)kSThreads);
+    cfg.dynamicSmemBytes = kSSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)Q;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return n >= P / Q;
+}
+
 // ln_pair: -1 = the SWIN_MLP_LN_PAIR switch, 1 = only the CTA-pair op #6 plan, 0 = never it
 // small_bn > 0: the few-tile plan for runs of one or two m-tiles (a 7x7 window, T = 49):
 // FC1 single-CTA tiles of small_bn columns (more CTAs on the same few rows), op #6 the
@@ -527,7 +553,7 @@ struct swin_mlp_int8_s {
     CUtensorMap tm_w1s, tm_w2s;
     // one-launch plan for runs of at most kSMaxT tokens (small_mlp.cuh): P = H / 128 CTAs
     bool has_tiny = false;
-    int tiny_P = 0, tiny_NP = 0, tiny_PR = 0;
+    int tiny_P = 0, tiny_Q = 0, tiny_PR = 0;   // CTAs, cluster size, FC2 columns per CTA (Q * PR == C)
     CUtensorMap tm_w1t, tm_w2t;
     int32_t* tiny_cnt = nullptr;   // [2] arrival / departure counters (zero between runs)
     int32_t* tiny_acc = nullptr;   // [64][C] int32 FC2 sums (zero between runs)
@@ -825,9 +851,12 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
         // lane), H / 128 CTAs all co-resident, FC2 output in pieces of <= 256 columns
         const char* te = std::getenv("SWIN_MLP_TINY");   // '0': never (A/B switch, read per create)
         const int P = H / 128;
-        int NP = (C + 255) / 256;   // the fewest FC2 pieces of <= 256 columns, a multiple of 16 each
-        while (NP <= C / 16 && (C % NP || (C / NP) % 16)) ++NP;
-        const int PR = NP > 0 ? C / NP : 0;
+        // the smallest cluster size Q (P % Q == 0, Q <= 8) whose column group PR = C / Q fits one
+        // MMA (<= 256) and splits into two warp halves of 16-column chunks
+        const char* qe = std::getenv("SWIN_MLP_TINY_Q");   // A/B: the smallest valid Q >= this (read per create)
+        int Q = (qe && *qe) ? std::max(1, std::atoi(qe)) : 1;
+        while (Q <= kSMaxQ && (P % Q || C % Q || C / Q > 256 || (C / Q) % 32)) ++Q;
+        const int PR = Q <= kSMaxQ ? C / Q : 0;
         void (*tfn)(CUtensorMap, CUtensorMap, CUtensorMap, SmallArgs) = nullptr;
         const bool gl = d.act == SWIN_MLP_ACT_GELU_ERF;
         switch (C / 128) {   // the LayerNorm row groups per lane (C % 128 == 0)
@@ -837,7 +866,8 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
             default: break;
         }
         if (!(te && *te == '0') && tfn && !h->unfused && !d.ln_fp64 && C >= 384 && C % 128 == 0 && H % 128 == 0 &&
-            P <= h->num_sms && PR * NP == C && PR % 16 == 0 && PR <= 256) {
+            P <= h->num_sms && Q <= kSMaxQ && PR * Q == C && PR % 32 == 0 && PR <= 256 &&
+            tiny_clusters_fit(tfn, P, Q)) {
             h->tiny_fn = tfn;
             H_TRY(encode_2d(&h->tm_w1t, h->w1, H, C, C, 128));
             H_TRY(encode_2d(&h->tm_w2t, h->w2, C, H, H, (uint32_t)PR));
@@ -849,7 +879,7 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
             h->tiny_acc = static_cast<int32_t*>(cp);
             h->tiny_cnt = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(cp) + acc_bytes);
             CUDA_TRY(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSSmem));
-            h->tiny_P = P; h->tiny_NP = NP; h->tiny_PR = PR;
+            h->tiny_P = P; h->tiny_Q = Q; h->tiny_PR = PR;
             h->has_tiny = true;
         }
     }
@@ -1011,7 +1041,7 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         CUtensorMap tmx;
         ST_TRY(encode_cached(h, &tmx, x, T, C, C, (uint32_t)kSMaxT));
         SmallArgs a = {};
-        a.T = (int32_t)T; a.C = C; a.H = H; a.P = h->tiny_P; a.NP = h->tiny_NP; a.PR = h->tiny_PR;
+        a.T = (int32_t)T; a.C = C; a.H = H; a.P = h->tiny_P; a.Q = h->tiny_Q; a.PR = h->tiny_PR;
         a.act = h->d.act == SWIN_MLP_ACT_GELU_ERF ? 1 : 0;
         a.m1 = h->m1; a.b1 = h->b1; a.zc1 = h->zc1; a.m2 = h->m2; a.b2 = h->b2; a.zc2 = h->zc2;
         a.gamma = h->gamma; a.beta = h->beta;
@@ -1026,11 +1056,15 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
         cfg.blockDim = dim3((unsigned)kSThreads);
         cfg.dynamicSmemBytes = kSSmem;
         cfg.stream = s;
-        cudaLaunchAttribute at[1];
+        cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = (unsigned)h->tiny_Q;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = 2;
         cudaEvent_t* ev = nullptr;
         if (h->prof_on && h->prof_n < h->prof_max) ev = &h->prof_ev[3 * (size_t)h->prof_n++];
         if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
@@ -1561,7 +1595,7 @@ int32_t swin_mlp_int8_plan_for(swin_mlp_int8_t h, int64_t T, int32_t* out20) {
     const int c = plan_choice(h, h->plan_hint > 0 ? h->plan_hint : T);
     if (c == 3) {   // the one-launch plan: out20[0] = CTAs, [4] = FC2 piece columns, [5] = pieces
         for (int i = 0; i < 12; ++i) out20[i] = 0;
-        out20[0] = h->tiny_P; out20[4] = h->tiny_PR; out20[5] = h->tiny_NP; out20[13] = 1; out20[16] = 0;
+        out20[0] = h->tiny_P; out20[4] = h->tiny_PR; out20[5] = h->tiny_Q; out20[13] = 1; out20[16] = 0;
         out20[19] = (h->unfused ? 1 : 0) | (c << 1);
         return 0;
     }
