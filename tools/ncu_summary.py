@@ -138,7 +138,8 @@ for st in range(4):
                      f"{d.get('launch__cluster_dim_x', '')} |")
 # extra captures: the north-star stage (Swin-B b128 stage 3, C = 512) and the attention half
 extra = {"swinb3": ("Swin-B b128 stage 3 layer (C=512, T=25088)", ["fc1_relu_q", "fc2_ln_q"]),
-         "attn0": ("attention half, Swin-T b64 stage 0 (C=96, T=200704)", ["op1", "qkv_op2", "attn_core"])}
+         "attn0": ("attention half, Swin-T b64 stage 0 (C=96, T=200704)", ["op1", "qkv_op2", "attn_core"]),
+         "config0": ("configs[0]: one 7x7 window (C=768, T=49), the one-launch plan", ["small_mlp (one launch)"])}
 for key, (what, names) in extra.items():
     raw_csv = os.path.join(ROOT, "gpurun_out", f"full_stage{key}_raw.csv")
     if not os.path.exists(raw_csv):

@@ -33,9 +33,14 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 python tools/attn_one.py 0 2 > $o/plain_attn_$tag.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"attn_core|op1_kernel|mlp_gemm_kernel" -s 3 -c 3 \
     -o $o/full_attn0 -f python tools/attn_one.py 0 2 > $o/ncu_full_attn_$tag.log 2>&1
+# configs[0]: one 7x7 window, the one-launch plan (small_mlp.cuh)
+python tools/prof_layer.py 768x49 3 > $o/plain_config0_$tag.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:small_mlp -s 2 -c 1 -o $o/full_config0 -f \
+    python tools/prof_layer.py 768x49 3 > $o/ncu_full_config0_$tag.log 2>&1
+python tools/trace_small.py 768 49 > $o/trace_${tag}_config0.log 2>&1
 # bring-back budget (gpurun merges <= 64 MiB): raw + source CSV exports of every capture,
 # the .ncu-rep only for the dominant stage-0 kernel
-for s in 0 1 2 3 swinb3 attn0; do
+for s in 0 1 2 3 swinb3 attn0 config0; do
   [ -f $o/full_stage$s.ncu-rep ] || [ -f $o/full_$s.ncu-rep ] || continue
   [ -f $o/full_$s.ncu-rep ] && mv $o/full_$s.ncu-rep $o/full_stage$s.ncu-rep
   ncu -i $o/full_stage$s.ncu-rep --page raw --csv > $o/full_stage${s}_raw.csv 2>/dev/null
