@@ -88,8 +88,8 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     const uint32_t j = blockIdx.x;
     const uint32_t bar_full = base + kSBars, bar_empty = bar_full + 8u * kSStages;
     const uint32_t bar_acc1 = bar_empty + 8u * kSStages, bar_hq = bar_acc1 + 8u;
-    const uint32_t bar_tfull = bar_hq + 8u, bar_peer = bar_tfull + 8u;   // FC2 done; peers' Hq landed
-    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (base - raw) + kSBars + 128);
+    const uint32_t bar_tfull = bar_hq + 8u, bar_peer = bar_tfull + 8u;   // FC2 done; [Q] slot kk landed
+    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (base - raw) + kSBars + 192);
     const int C = p.C, NKB = (C + kBK - 1) / kBK;
     const uint32_t Q = (uint32_t)p.Q, g = Q > 1 ? cluster_ctarank() : 0u, s_slice = j / Q;
     unsigned long long* trc = p.trace ? p.trace + 16 * blockIdx.x : nullptr;
@@ -109,8 +109,11 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             mbar_init(bar_acc1, 1);
             mbar_init(bar_hq, 8);
             mbar_init(bar_tfull, 1);
-            mbar_init(bar_peer, 1);
-            if (Q > 1) mbar_arrive_expect_tx(bar_peer, (Q - 1u) * kSHqSlot);   // the peers' Hq slots
+            for (uint32_t r = 0; r < Q; ++r) {   // one barrier per peer's Hq slot
+                if (r == g) continue;
+                mbar_init(bar_peer + 8u * r, 1);
+                mbar_arrive_expect_tx(bar_peer + 8u * r, kSHqSlot);
+            }
             fence_mbar_init();
         }
         __syncwarp();
@@ -149,7 +152,8 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 if (++s == kSStages) { s = 0; ph ^= 1u; }
             }
             // FC2: the W2 K-blocks [PR rows of group g][128 hidden columns] of the cluster's slice
-            for (uint32_t kk = 0; kk < Q; ++kk) {
+            for (uint32_t i = 0; i < Q; ++i) {   // the MMA's order: own slot first, then the peers'
+                const uint32_t kk = (g + i) % Q;
                 mbar_wait(bar_empty + 8u * s, ph ^ 1u);
                 mbar_arrive_expect_tx(bar_full + 8u * s, (uint32_t)p.PR * kBK);
                 tma_load_2d(&tmW2, base + (uint32_t)s * kSSlot, bar_full + 8u * s, (int)((s_slice * Q + kk) * 128),
@@ -179,19 +183,20 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
             if (++s == kSStages) { s = 0; ph ^= 1u; }
         }
         mbar_wait(bar_hq, 0);                // this CTA's Hq slot staged
-        if (Q > 1) mbar_wait(bar_peer, 0);   // ... and the peers' (DSMEM bulk copies)
         tc_fence_after();
         if (trc && lane == 0) trc[4] = gtimer();
-        for (uint32_t kk = 0; kk < Q; ++kk) {   // K = Q * 128: the cluster's hidden slice
+        for (uint32_t i = 0; i < Q; ++i) {   // K = Q * 128: own slot, then each peer's as it lands
+            const uint32_t kk = (g + i) % Q;
+            if (i > 0) mbar_wait(bar_peer + 8u * kk, 0);   // (DSMEM bulk copy from peer kk)
             mbar_wait(bar_full + 8u * s, ph);
             tc_fence_after();
             const uint32_t slot = base + (uint32_t)s * kSSlot;
             if (elect_one()) {
                 for (int k = 0; k < 4; ++k)
                     mma_i8(tmem + 256u, umma_desc_k128(base + kSHq + kk * kSHqSlot) + 2u * k,
-                           umma_desc_k128(slot) + 2u * k, id2, (kk | (uint32_t)k) != 0u);
+                           umma_desc_k128(slot) + 2u * k, id2, (i | (uint32_t)k) != 0u);
                 mma_commit(bar_empty + 8u * s);
-                if (kk + 1u == Q) mma_commit(bar_tfull);
+                if (i + 1u == Q) mma_commit(bar_tfull);
             }
             __syncwarp();
             if (++s == kSStages) { s = 0; ph ^= 1u; }
@@ -275,7 +280,7 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
                 const uint32_t src = base + kSHq + g * kSHqSlot;
                 for (uint32_t r = 1; r < Q; ++r) {
                     const uint32_t peer = (g + r) % Q;
-                    bulk_copy_s2cluster(mapa(src, peer), src, kSHqSlot, mapa(bar_peer, peer));
+                    bulk_copy_s2cluster(mapa(src, peer), src, kSHqSlot, mapa(bar_peer + 8u * g, peer));
                 }
             }
         }
