@@ -335,6 +335,14 @@ __device__ __forceinline__ void reg_fence16(uint32_t (&r)[16]) {
                  :: "memory");
 }
 // TMA bulk tensor store smem -> global (2-D), bulk-group completion.
+// 3-D tile {c0 innermost, c1, c2}: with a map {128 B of K, rows, K-blocks} (strides ld, 128) one op
+// lands consecutive K-blocks as [K-blocks][rows][128 B] (SW128 K-major)
+__device__ __forceinline__ void tma_load_3d(const void* tmap, uint32_t dst, uint32_t bar, int32_t c0, int32_t c1,
+                                            int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int32_t c0, int32_t c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
                  ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(src), "r"(c0), "r"(c1) : "memory");

@@ -42,7 +42,16 @@ constexpr int kSMaxT = 64;
 constexpr int kSStages = 4;
 constexpr int kSMaxQ = 8;                          // cluster size (portable maximum)
 constexpr uint32_t kSSlot = 32768;                 // FC1 {A 16 KB (64 rows loaded), B 16 KB} | W2 K-block
-constexpr uint32_t kSHq = kSStages * kSSlot;       // Hq: Q K-blocks of [64 rows][128 B] SW128, 8 KB apart
+// C <= 768 (at most 6 K-blocks): FC1's operands resident at once, each landed by ONE 3-D TMA op
+// (the per-op cost of the TMA unit, not the bytes, paces small boxes):
+//   A  [K-blocks][64 rows][128 B] at 8 KB steps (+ 8 KB: the M = 128 MMA's rows 64-127 of a K-block
+//      are the next one's rows, TMEM lanes without tokens)            base .. base + 56 KB
+//   W1 [K-blocks][128 rows][128 B]                                    base + 56 KB .. base + 152 KB
+// and after FC1 the cluster slice's W2 K-blocks [Q][PR rows][128 B] (C * 128 bytes) over W1, again
+// one op.
+constexpr int kSResKB = 6;
+constexpr uint32_t kSResW1 = 57344;
+constexpr uint32_t kSHq = kSResW1 + kSResKB * 16384;   // Hq: Q K-blocks of [64 rows][128 B] SW128, 8 KB apart
                                                    // (+ 8 KB: the M = 128 MMA's rows 64-127 of the last one,
                                                    // which land in TMEM lanes that carry no tokens)
 constexpr uint32_t kSHqSlot = 8192;
@@ -80,16 +89,19 @@ template <int G, int ACT>
 __global__ void __launch_bounds__(kSThreads, 1)
 small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                  const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ SmallArgs p) {
+    // (resident mode, G <= kSResKB: tmX / tmW1 / tmW2 are the 3-D maps {128 B, rows, K-blocks})
     using namespace sm100;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t j = blockIdx.x;
-    const uint32_t bar_full = base + kSBars, bar_empty = bar_full + 8u * kSStages;
+    constexpr bool RES = G <= kSResKB;   // (G = C / 128 = FC1's K-blocks)
+    const uint32_t bar_full = base + kSBars, bar_empty = bar_full + 8u * 8u;   // [8] FC1 K-block / ring slot
     const uint32_t bar_acc1 = bar_empty + 8u * kSStages, bar_hq = bar_acc1 + 8u;
     const uint32_t bar_tfull = bar_hq + 8u, bar_peer = bar_tfull + 8u;   // FC2 done; [Q] slot kk landed
-    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (base - raw) + kSBars + 192);
+    const uint32_t bar_w2 = bar_peer + 8u * kSMaxQ;                     // [Q] resident mode: W2 K-block i landed
+    volatile uint32_t* tmem_slot = reinterpret_cast<volatile uint32_t*>(smem_raw + (base - raw) + kSBars + 248);
     const int C = p.C, NKB = (C + kBK - 1) / kBK;
     const uint32_t Q = (uint32_t)p.Q, g = Q > 1 ? cluster_ctarank() : 0u, s_slice = j / Q;
     unsigned long long* trc = p.trace ? p.trace + 16 * blockIdx.x : nullptr;
@@ -102,9 +114,10 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
     }
     if (warp == 1) {
         if (lane == 0) {
-            for (int s = 0; s < kSStages; ++s) {
+            for (int s = 0; s < 8; ++s) {
                 mbar_init(bar_full + 8u * s, 1);
-                mbar_init(bar_empty + 8u * s, 1);
+                mbar_init(bar_w2 + 8u * s, 1);
+                if (s < kSStages) mbar_init(bar_empty + 8u * s, 1);
             }
             mbar_init(bar_acc1, 1);
             mbar_init(bar_hq, 8);
@@ -129,7 +142,18 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
 
     if (warp == 0) {
         // ============================ TMA producer ============================
-        if (elect_one()) {
+        if (RES && elect_one()) {
+            // the W1 slice before the wait (a constant), X after it; one op each
+            mbar_arrive_expect_tx(bar_full, (uint32_t)NKB * 128u * kBK);
+            tma_load_3d(&tmW1, base + kSResW1, bar_full, 0, (int)(j * 128), 0);
+            pdl_wait();   // X: the previous kernel's output
+            if (trc) trc[2] = gtimer();
+            mbar_arrive_expect_tx(bar_full + 8u, (uint32_t)NKB * 64u * kBK);
+            tma_load_3d(&tmX, base, bar_full + 8u, 0, 0, 0);
+            mbar_wait(bar_acc1, 0);   // FC1's MMAs have read W1: the slice's W2 K-blocks replace it
+            mbar_arrive_expect_tx(bar_w2, (uint32_t)C * kBK);
+            tma_load_3d(&tmW2, base + kSResW1, bar_w2, 0, (int)g * p.PR, (int)(s_slice * Q));
+        } else if (!RES && elect_one()) {
             const int n_pre = NKB < kSStages ? NKB : kSStages;
             // W1 K-blocks of the first slots: constants, issued before the wait on the previous kernel
             for (int kb = 0; kb < n_pre; ++kb) {
@@ -167,7 +191,22 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         int s = 0;
         uint32_t ph = 0;
         const uint32_t id1 = idesc_i8(kBM, 128), id2 = idesc_i8(kBM, (uint32_t)p.PR);
-        for (int kb = 0; kb < NKB; ++kb) {
+        if constexpr (RES) {
+            mbar_wait(bar_full, 0);        // W1
+            mbar_wait(bar_full + 8u, 0);   // X
+            tc_fence_after();
+            for (int kb = 0; kb < NKB; ++kb) {
+                const uint32_t xa = base + (uint32_t)kb * 8192u, wb = base + kSResW1 + (uint32_t)kb * 16384u;
+                const int rem = C - kb * kBK, nk = rem >= kBK ? 4 : rem / 32;
+                if (elect_one()) {
+                    for (int k = 0; k < nk; ++k)
+                        mma_i8(tmem, umma_desc_k128(xa) + 2u * k, umma_desc_k128(wb) + 2u * k, id1, (kb | k) != 0);
+                    if (kb == NKB - 1) mma_commit(bar_acc1);
+                }
+                __syncwarp();
+            }
+        }
+        for (int kb = 0; kb < (RES ? 0 : NKB); ++kb) {
             mbar_wait(bar_full + 8u * s, ph);
             tc_fence_after();
             const uint32_t slot = base + (uint32_t)s * kSSlot;
@@ -188,18 +227,19 @@ small_mlp_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant_
         for (uint32_t i = 0; i < Q; ++i) {   // K = Q * 128: own slot, then each peer's as it lands
             const uint32_t kk = (g + i) % Q;
             if (i > 0) mbar_wait(bar_peer + 8u * kk, 0);   // (DSMEM bulk copy from peer kk)
-            mbar_wait(bar_full + 8u * s, ph);
+            if constexpr (RES) mbar_wait(bar_w2, 0);
+            else mbar_wait(bar_full + 8u * s, ph);
             tc_fence_after();
-            const uint32_t slot = base + (uint32_t)s * kSSlot;
+            const uint32_t slot = RES ? base + kSResW1 + kk * (uint32_t)p.PR * kBK : base + (uint32_t)s * kSSlot;
             if (elect_one()) {
                 for (int k = 0; k < 4; ++k)
                     mma_i8(tmem + 256u, umma_desc_k128(base + kSHq + kk * kSHqSlot) + 2u * k,
                            umma_desc_k128(slot) + 2u * k, id2, (i | (uint32_t)k) != 0u);
-                mma_commit(bar_empty + 8u * s);
+                if (!RES) mma_commit(bar_empty + 8u * s);
                 if (i + 1u == Q) mma_commit(bar_tfull);
             }
             __syncwarp();
-            if (++s == kSStages) { s = 0; ph ^= 1u; }
+            if (!RES && ++s == kSStages) { s = 0; ph ^= 1u; }
         }
     } else {
         // ============================ epilogue ================================

@@ -134,6 +134,25 @@ swin_mlp_status_t encode_2d(CUtensorMap* map, const void* ptr, int64_t rows, int
     return SWIN_MLP_OK;
 }
 
+// 3-D view {128 B of K, rows, K-blocks} (strides ld, 128) of an int8 [rows][ld] matrix, 128-byte
+// swizzle: one box {128, box_rows, box_kb} lands box_kb consecutive K-blocks as [box_kb][box_rows][128 B]
+swin_mlp_status_t encode_3dk(CUtensorMap* map, const void* ptr, int64_t rows, int64_t ld, int64_t nkb, uint32_t box_rows,
+                             uint32_t box_kb) {
+    auto fn = encode_fn();
+    if (!fn) return fail(SWIN_MLP_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)rows, (cuuint64_t)nkb};
+    cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)kBK};
+    cuuint32_t box[3] = {(cuuint32_t)kBK, box_rows, box_kb};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(SWIN_MLP_ECUDA, "cuTensorMapEncodeTiled (3-D) failed (%d) rows=%lld nkb=%lld box=%u x %u", (int)r,
+                    (long long)rows, (long long)nkb, box_rows, box_kb);
+    return SWIN_MLP_OK;
+}
+
 constexpr uint32_t kSmemBudget = 227 * 1024;
 
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
@@ -619,7 +638,8 @@ swin_mlp_status_t encode_cached(swin_mlp_int8_s* h, CUtensorMap* map, const void
         for (auto& e : h->map_cache)
             if (e.first == key) { *map = e.second; return SWIN_MLP_OK; }
     }
-    const swin_mlp_status_t st = encode_2d(map, ptr, rows, cols, ld, box_rows, box_cols, swz);
+    const swin_mlp_status_t st = (int)swz < 0 ? encode_3dk(map, ptr, rows, ld, cols, box_rows, box_cols)
+                                              : encode_2d(map, ptr, rows, cols, ld, box_rows, box_cols, swz);
     if (st != SWIN_MLP_OK) return st;
     std::lock_guard<std::mutex> lk(h->map_mu);
     constexpr size_t kCap = 64;
@@ -869,8 +889,13 @@ swin_mlp_status_t swin_mlp_int8_create(const swin_mlp_int8_desc_t* desc, swin_ml
             P <= h->num_sms && Q <= kSMaxQ && PR * Q == C && PR % 32 == 0 && PR <= 256 &&
             tiny_clusters_fit(tfn, P, Q)) {
             h->tiny_fn = tfn;
-            H_TRY(encode_2d(&h->tm_w1t, h->w1, H, C, C, 128));
-            H_TRY(encode_2d(&h->tm_w2t, h->w2, C, H, H, (uint32_t)PR));
+            if (C / 128 <= kSResKB) {   // resident mode: one 3-D op per operand (small_mlp.cuh)
+                H_TRY(encode_3dk(&h->tm_w1t, h->w1, H, C, C / 128, 128, (uint32_t)(C / 128)));
+                H_TRY(encode_3dk(&h->tm_w2t, h->w2, C, H, H / 128, (uint32_t)PR, (uint32_t)Q));
+            } else {
+                H_TRY(encode_2d(&h->tm_w1t, h->w1, H, C, C, 128));
+                H_TRY(encode_2d(&h->tm_w2t, h->w2, C, H, H, (uint32_t)PR));
+            }
             void* cp = nullptr;
             const size_t acc_bytes = (size_t)kSMaxT * C * 4;
             CUDA_TRY(cudaMalloc(&cp, acc_bytes + 256));
@@ -1039,7 +1064,11 @@ static swin_mlp_status_t run_impl(swin_mlp_int8_t h, const int8_t* x, const floa
     const int run_plan = plan_choice(h, plan_T > 0 ? plan_T : h->plan_hint > 0 ? h->plan_hint : T);
     if (run_plan == 3 && T <= kSMaxT) {   // one launch for the whole layer (small_mlp.cuh)
         CUtensorMap tmx;
-        ST_TRY(encode_cached(h, &tmx, x, T, C, C, (uint32_t)kSMaxT));
+        if (C / 128 <= kSResKB)   // 3-D: all K-blocks of the <= 64 rows in one op (a negative swizzle tags it)
+            ST_TRY(encode_cached(h, &tmx, x, T, C / 128, C, (uint32_t)kSMaxT, (uint32_t)(C / 128),
+                                 (CUtensorMapSwizzle)-1));
+        else
+            ST_TRY(encode_cached(h, &tmx, x, T, C, C, (uint32_t)kSMaxT));
         SmallArgs a = {};
         a.T = (int32_t)T; a.C = C; a.H = H; a.P = h->tiny_P; a.Q = h->tiny_Q; a.PR = h->tiny_PR;
         a.act = h->d.act == SWIN_MLP_ACT_GELU_ERF ? 1 : 0;
