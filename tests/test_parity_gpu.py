@@ -285,6 +285,19 @@ def test_parity_one_launch_plan(dev, C, T):
                    resid=True, e2e=False)
 
 
+@pytest.mark.parametrize("C,T,q", [(768, 49, 4), (768, 64, 6), (768, 33, 8), (1024, 49, 8), (384, 17, 4)])
+def test_one_launch_cluster_sizes(dev, C, T, q, monkeypatch):
+    """The one-launch plan's cluster split at other cluster sizes (SWIN_MLP_TINY_Q: the smallest
+    valid Q >= q): more peers per Hq exchange (DSMEM bulk copies into up to 7 peers), narrower
+    column groups per CTA, fewer-way L2 sums.  A1, Hq, A2, z bit-exact, Y in tier."""
+    from paper_2402_01169_b200 import SwinMlpInt8Layer
+    monkeypatch.setenv("SWIN_MLP_TINY_Q", str(q))
+    L = _layer(C, 7700 + C + T + q)
+    plan = SwinMlpInt8Layer(L, device=0).plan(T)
+    assert plan["run_plan"] == "one_launch" and plan["fc2_cs"] >= q and C % plan["fc2_cs"] == 0
+    _run_and_check(dev, L, T, x_seed=T + q, e2e=False)
+
+
 def test_run_host_matches_device(dev):
     """The end-to-end host-buffer entry point (H2D, run, D2H inside the library)."""
     from paper_2402_01169_b200 import SwinMlpInt8Layer
